@@ -1,0 +1,139 @@
+/* dapple-b200 C-ABI (libdapple.so).
+ *
+ * The reference (proj/, C++20 namespace pipeplan) exposes its planner and
+ * simulator as C++ value types and free functions (proj/include/pipeplan/
+ * *.hpp) and has no FFI and no executor.  This header is the drop-in
+ * boundary a non-C++ host binds:
+ *
+ *  1. dpl_host_call      -- the whole pipeplan surface as JSON requests:
+ *       "plan"                 planner.hpp:71-73   (planner.cpp:306-421)
+ *       "brute_force_plan"     planner.hpp:78-79   (planner.cpp:423-489)
+ *       "simulate_plan"        planner.hpp:87-90   (planner.cpp:491-514)
+ *       "build_stage_sequence" estimator.hpp:25-27 (estimator.cpp:13-37)
+ *       "estimate"             estimator.hpp:35/41 (estimator.cpp:56-107)
+ *       "schedule"             simulator.hpp:46-58 (simulator.cpp:153-179)
+ *       "optimize_phi"         simulator.hpp:71-72 (simulator.cpp:233-286)
+ *       "expand_plan_phi", "apply_recompute", "allreduce_time",
+ *       "splitconcat_time", "aggregate_stage", "enumerate_placements",
+ *       "memory_feasible", "load_profile", "load_cluster", "stage_chain",
+ *       "timeline_svg"
+ *     Errors come back as {"error":{"type":..., "what":...}} using the
+ *     reference's exception classes (invalid_argument / out_of_range /
+ *     logic_error / runtime_error) and messages.
+ *
+ *  2. dpl_exec_*         -- the executor entry point that mirrors
+ *     simulate_plan (planner.hpp:87-90) but runs the step on B200s and
+ *     returns a *measured* Timeline (one process per GPU; see
+ *     include/pipeplan/executor.hpp for the C++ form).
+ *
+ *  3. dpl_k_*            -- the individual stage kernels, exported so tests
+ *     can check each against the CPU oracle.
+ *
+ * Conventions: int status (0 = ok), dpl_last_error() for the message,
+ * opaque handles, no C++ exceptions cross the ABI, bf16 tensors as void*.
+ */
+#ifndef DAPPLE_H_
+#define DAPPLE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------- host */
+const char* dpl_host_call(const char* request_json);
+const char* dpl_last_error(void);
+const char* dpl_version(void);
+
+/* ---------------------------------------------------------------- kernels */
+/* C[z,m,n] = epi(alpha * sum_k A[z,m,k] B[z,n,k]); see csrc/kernels/gemm.h */
+typedef struct dpl_gemm_desc {
+  int M, N, K, batch;
+  const void* A;
+  long long lda, a_batch_stride;
+  int a_mn_major;
+  const void* B;
+  long long ldb, b_batch_stride;
+  int b_mn_major;
+  void* C;
+  long long ldc;
+  int zdiv;
+  long long s_zo, s_zi;
+  int ndiv;
+  long long s_no;
+  uint32_t epi; /* DPL_EPI_* flags */
+  float alpha;
+  const float* bias;
+  const void* aux_in;
+  const void* resid;
+  void* aux_out;
+  int force_bn;
+} dpl_gemm_desc;
+
+#define DPL_EPI_OUT_BF16 0u
+#define DPL_EPI_OUT_F32 1u
+#define DPL_EPI_OUT_F32_ACC 2u
+#define DPL_EPI_BIAS (1u << 2)
+#define DPL_EPI_GELU (1u << 3)
+#define DPL_EPI_RELU (1u << 4)
+#define DPL_EPI_AUX_OUT (1u << 5)
+#define DPL_EPI_DGELU (1u << 6)
+#define DPL_EPI_DRELU (1u << 7)
+#define DPL_EPI_RESID (1u << 8)
+
+int dpl_k_gemm(const dpl_gemm_desc* desc, void* stream);
+int dpl_k_layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y, float* mean, float* rstd,
+                        int rows, int h, float eps, void* stream);
+int dpl_k_layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd, const float* gamma,
+                        const void* dresid, void* dx, float* dgamma, float* dbeta, int rows, int h, void* stream);
+int dpl_k_softmax_fwd(const float* s, void* p, int rows, int len, int q_len, int causal, void* stream);
+int dpl_k_softmax_bwd(const void* p, const float* dp, void* ds, int rows, int len, void* stream);
+int dpl_k_colsum_acc(const void* dy, float* db, int rows, int cols, void* stream);
+int dpl_k_mse_loss(const void* y, const void* t, void* dy, float* loss_acc, long long n, float grad_scale,
+                   void* stream);
+int dpl_k_sgd_apply(float* w32, float* g, void* w16, long long n, float lr, void* stream);
+int dpl_k_fill_uniform_bf16(void* dst, long long n, uint64_t seed, uint64_t tensor, long long idx0, float scale,
+                            void* stream);
+int dpl_k_fill_uniform_f32(float* dst, long long n, uint64_t seed, uint64_t tensor, long long idx0, float scale,
+                           void* stream);
+/* Kernel launches issued by this library since load (smoke/bench evidence). */
+long long dpl_k_launch_count(void);
+
+/* ---------------------------------------------------------------- executor */
+typedef struct dpl_exec dpl_exec; /* one per process / GPU */
+
+/* Creates the executor for this rank.  `config_json` carries the model
+ * ({"model": "mlp"|"bert"|"gpt", dims...}), the plan (plan JSON as written
+ * by plan_to_json), the profile and cluster JSON, M, GBS, lr, seed, rank and
+ * world size.  Allocates parameters, gradients, activation stash and
+ * Split-Concat receive buffers on `device`. */
+int dpl_exec_create(const char* config_json, int device, dpl_exec** out);
+/* Opaque blob this rank must share with every other rank (CUDA IPC handles
+ * of its receive buffers and flag words); dpl_exec_connect takes the blobs
+ * of all ranks, concatenated in rank order. */
+int dpl_exec_export(dpl_exec* ex, void* blob, size_t cap, size_t* len);
+int dpl_exec_connect(dpl_exec* ex, const void* blobs, size_t blob_len, int world);
+/* NCCL: rank 0 of each stage group creates the id (128 bytes), the group
+ * shares it, then every member initialises its communicator. */
+int dpl_exec_nccl_id(void* id128);
+int dpl_exec_nccl_init(dpl_exec* ex, const void* id128);
+/* One synchronous DAPPLE step: phi warm-up forwards, 1F1B steady state,
+ * drain, per-layer AllReduce, SGD apply.  Host inputs may be NULL (inputs
+ * generated on device from the seed).  *loss gets the global-batch loss on
+ * last-stage ranks (NaN elsewhere). */
+int dpl_exec_step(dpl_exec* ex, const void* host_input, const void* host_target, float* loss);
+/* Measured timeline of the last step as JSON (same layout as the
+ * simulator's Timeline, seconds), plus per-block kernel times. */
+const char* dpl_exec_timeline(dpl_exec* ex);
+/* Copies a parameter / gradient tensor (by name) to host, for parity. */
+int dpl_exec_read_tensor(dpl_exec* ex, const char* name, int grad, void* host, size_t bytes);
+int dpl_exec_info(dpl_exec* ex, char* buf, size_t cap);
+void dpl_exec_destroy(dpl_exec* ex);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DAPPLE_H_ */

@@ -1,0 +1,101 @@
+// extern "C" shims over the stage kernels (include/dapple.h, section 3).
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <exception>
+#include <string>
+
+#include "dapple.h"
+#include "kernels/elementwise.h"
+#include "kernels/gemm.h"
+
+namespace dpl {
+thread_local std::string g_last_error;
+std::atomic<long long> g_launches{0};
+
+int fail(const std::string& what) {
+  g_last_error = what;
+  return 1;
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(std::string("CUDA: ") + cudaGetErrorString(e));
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e.what());
+  }
+}
+}  // namespace dpl
+
+using dpl::guarded;
+
+extern "C" {
+
+const char* dpl_last_error(void) { return dpl::g_last_error.c_str(); }
+const char* dpl_version(void) { return "dapple-b200 0.1 (sm_100a)"; }
+long long dpl_k_launch_count(void) { return dpl::g_launches.load(); }
+
+int dpl_k_gemm(const dpl_gemm_desc* d, void* stream) {
+  return guarded([&] {
+    dpl::GemmDesc g;
+    g.M = d->M; g.N = d->N; g.K = d->K; g.batch = d->batch;
+    g.A = d->A; g.lda = d->lda; g.a_batch_stride = d->a_batch_stride; g.a_mn_major = d->a_mn_major;
+    g.B = d->B; g.ldb = d->ldb; g.b_batch_stride = d->b_batch_stride; g.b_mn_major = d->b_mn_major;
+    g.C = d->C; g.ldc = d->ldc; g.zdiv = d->zdiv; g.s_zo = d->s_zo; g.s_zi = d->s_zi;
+    g.ndiv = d->ndiv; g.s_no = d->s_no; g.epi = d->epi; g.alpha = d->alpha; g.bias = d->bias;
+    g.aux_in = d->aux_in; g.resid = d->resid; g.aux_out = d->aux_out; g.force_bn = d->force_bn;
+    dpl::GemmOp op;
+    op.prepare(g);
+    op.launch(static_cast<cudaStream_t>(stream));
+  });
+}
+
+int dpl_k_layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y, float* mean, float* rstd,
+                        int rows, int h, float eps, void* stream) {
+  return guarded([&] { dpl::layernorm_fwd(x, gamma, beta, y, mean, rstd, rows, h, eps, static_cast<cudaStream_t>(stream)); });
+}
+
+int dpl_k_layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd, const float* gamma,
+                        const void* dresid, void* dx, float* dgamma, float* dbeta, int rows, int h, void* stream) {
+  return guarded([&] {
+    dpl::layernorm_bwd(dy, x, mean, rstd, gamma, dresid, dx, dgamma, dbeta, rows, h, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int dpl_k_softmax_fwd(const float* s, void* p, int rows, int len, int q_len, int causal, void* stream) {
+  return guarded([&] { dpl::softmax_fwd(s, p, rows, len, q_len, causal, static_cast<cudaStream_t>(stream)); });
+}
+
+int dpl_k_softmax_bwd(const void* p, const float* dp, void* ds, int rows, int len, void* stream) {
+  return guarded([&] { dpl::softmax_bwd(p, dp, ds, rows, len, static_cast<cudaStream_t>(stream)); });
+}
+
+int dpl_k_colsum_acc(const void* dy, float* db, int rows, int cols, void* stream) {
+  return guarded([&] { dpl::colsum_acc(dy, db, rows, cols, static_cast<cudaStream_t>(stream)); });
+}
+
+int dpl_k_mse_loss(const void* y, const void* t, void* dy, float* loss_acc, long long n, float grad_scale,
+                   void* stream) {
+  return guarded([&] { dpl::mse_loss(y, t, dy, loss_acc, n, grad_scale, static_cast<cudaStream_t>(stream)); });
+}
+
+int dpl_k_sgd_apply(float* w32, float* g, void* w16, long long n, float lr, void* stream) {
+  return guarded([&] { dpl::sgd_apply(w32, g, w16, n, lr, static_cast<cudaStream_t>(stream)); });
+}
+
+int dpl_k_fill_uniform_bf16(void* dst, long long n, uint64_t seed, uint64_t tensor, long long idx0, float scale,
+                            void* stream) {
+  return guarded([&] { dpl::fill_uniform_bf16(dst, n, seed, tensor, idx0, scale, static_cast<cudaStream_t>(stream)); });
+}
+
+int dpl_k_fill_uniform_f32(float* dst, long long n, uint64_t seed, uint64_t tensor, long long idx0, float scale,
+                           void* stream) {
+  return guarded([&] { dpl::fill_uniform_f32(dst, n, seed, tensor, idx0, scale, static_cast<cudaStream_t>(stream)); });
+}
+
+}  // extern "C"

@@ -1,0 +1,508 @@
+// HBM-bound stage kernels (N1/N2/N6): LayerNorm fwd/bwd, attention softmax
+// fwd/bwd, bias-gradient column sums, MSE loss, SGD apply, and the seeded
+// synthetic-data generator.  One warp per row, 16-byte vector accesses,
+// warp-shuffle reductions; per-column gradient partials are reduced in
+// shared memory and folded into fp32 gradient buffers with one atomic per
+// column per block.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <type_traits>
+
+#include "elementwise.h"
+
+namespace dpl {
+
+namespace {
+
+// Rows are processed one per warp with kMaxVec 8-element vectors per lane
+// held in registers (kMaxVec in {1,2,4,8}: rows up to 2048 elements).
+template <typename F>
+void dispatch_vec(int len, F&& f) {
+  const int v = (len / 8 + 31) / 32;
+  if (v <= 1) f(std::integral_constant<int, 1>{});
+  else if (v <= 2) f(std::integral_constant<int, 2>{});
+  else if (v <= 4) f(std::integral_constant<int, 4>{});
+  else f(std::integral_constant<int, 8>{});
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&f)[8]) {
+  const uint4 r = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 x = __bfloat1622float2(h[e]);
+    f[2 * e] = x.x;
+    f[2 * e + 1] = x.y;
+  }
+}
+__device__ __forceinline__ void load8(const float* p, float (&f)[8]) {
+  const float4 a = *reinterpret_cast<const float4*>(p);
+  const float4 b = *reinterpret_cast<const float4*>(p + 4);
+  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+  f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
+__device__ __forceinline__ void store8(__nv_bfloat16* p, const float (&f)[8]) {
+  uint4 r;
+  uint32_t* w = reinterpret_cast<uint32_t*>(&r);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * e], f[2 * e + 1]);
+    w[e] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  *reinterpret_cast<uint4*>(p) = r;
+}
+
+// ------------------------------------------------------------ LayerNorm
+template <int kMaxVec>
+__global__ void layernorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ gamma,
+                                     const float* __restrict__ beta, __nv_bfloat16* __restrict__ y,
+                                     float* __restrict__ mean_out, float* __restrict__ rstd_out, int rows, int h,
+                                     float eps) {
+  const int warps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nvec = h / 8;
+  for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < rows; row += gridDim.x * warps) {
+    const __nv_bfloat16* xr = x + static_cast<long long>(row) * h;
+    float v[kMaxVec][8];
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < kMaxVec; ++i) {
+      const int vi = lane + 32 * i;
+      if (vi < nvec) {
+        load8(xr + vi * 8, v[i]);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) s += v[i][e];
+      }
+    }
+    const float mean = warp_sum(s) / h;
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < kMaxVec; ++i) {
+      if (lane + 32 * i < nvec) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float d = v[i][e] - mean;
+          q += d * d;
+        }
+      }
+    }
+    const float rstd = rsqrtf(warp_sum(q) / h + eps);
+    __nv_bfloat16* yr = y + static_cast<long long>(row) * h;
+#pragma unroll
+    for (int i = 0; i < kMaxVec; ++i) {
+      const int vi = lane + 32 * i;
+      if (vi < nvec) {
+        float g[8], b[8], o[8];
+        load8(gamma + vi * 8, g);
+        load8(beta + vi * 8, b);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = (v[i][e] - mean) * rstd * g[e] + b[e];
+        store8(yr + vi * 8, o);
+      }
+    }
+    if (lane == 0) {
+      mean_out[row] = mean;
+      rstd_out[row] = rstd;
+    }
+  }
+}
+
+// dx = rstd * (g*dy - mean(g*dy) - xhat * mean(g*dy*xhat)) [+ dresid]
+// dgamma += sum_rows dy*xhat, dbeta += sum_rows dy
+template <int kMaxVec>
+__global__ void layernorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+                                     const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
+                                     const float* __restrict__ gamma, const __nv_bfloat16* __restrict__ dresid,
+                                     __nv_bfloat16* __restrict__ dx, float* __restrict__ dgamma,
+                                     float* __restrict__ dbeta, int rows, int h) {
+  extern __shared__ float red[];  // [warps][2][h]
+  const int warps = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nvec = h / 8;
+  float dg[kMaxVec][8], db[kMaxVec][8];
+#pragma unroll
+  for (int i = 0; i < kMaxVec; ++i)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) dg[i][e] = db[i][e] = 0.f;
+
+  for (int row = blockIdx.x * warps + warp; row < rows; row += gridDim.x * warps) {
+    const long long base = static_cast<long long>(row) * h;
+    const float mean = mean_in[row];
+    const float rstd = rstd_in[row];
+    float xh[kMaxVec][8], gd[kMaxVec][8];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < kMaxVec; ++i) {
+      const int vi = lane + 32 * i;
+      if (vi < nvec) {
+        float xv[8], dv[8], g[8];
+        load8(x + base + vi * 8, xv);
+        load8(dy + base + vi * 8, dv);
+        load8(gamma + vi * 8, g);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          xh[i][e] = (xv[e] - mean) * rstd;
+          gd[i][e] = dv[e] * g[e];
+          s1 += gd[i][e];
+          s2 += gd[i][e] * xh[i][e];
+          dg[i][e] += dv[e] * xh[i][e];
+          db[i][e] += dv[e];
+        }
+      }
+    }
+    const float m1 = warp_sum(s1) / h;
+    const float m2 = warp_sum(s2) / h;
+#pragma unroll
+    for (int i = 0; i < kMaxVec; ++i) {
+      const int vi = lane + 32 * i;
+      if (vi < nvec) {
+        float o[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = rstd * (gd[i][e] - m1 - xh[i][e] * m2);
+        if (dresid) {
+          float r[8];
+          load8(dresid + base + vi * 8, r);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) o[e] += r[e];
+        }
+        store8(dx + base + vi * 8, o);
+      }
+    }
+  }
+  // block reduction of the column partials, then one atomic per column
+#pragma unroll
+  for (int i = 0; i < kMaxVec; ++i) {
+    const int vi = lane + 32 * i;
+    if (vi < nvec) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        red[(warp * 2) * h + vi * 8 + e] = dg[i][e];
+        red[(warp * 2 + 1) * h + vi * 8 + e] = db[i][e];
+      }
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < h; c += blockDim.x) {
+    float a = 0.f, b = 0.f;
+    for (int w = 0; w < warps; ++w) {
+      a += red[(w * 2) * h + c];
+      b += red[(w * 2 + 1) * h + c];
+    }
+    atomicAdd(dgamma + c, a);
+    atomicAdd(dbeta + c, b);
+  }
+}
+
+// ------------------------------------------------------------ softmax
+// S fp32 [rows][L] (already scaled), P bf16.  Causal: row r is query
+// (r % q_len) and keys k > q are masked.
+template <int kMaxVec>
+__global__ void softmax_fwd_kernel(const float* __restrict__ s, __nv_bfloat16* __restrict__ p, int rows, int len,
+                                   int q_len, int causal) {
+  const int warps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nvec = len / 8;
+  for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < rows; row += gridDim.x * warps) {
+    const float* sr = s + static_cast<long long>(row) * len;
+    const int q = row % q_len;
+    float v[kMaxVec][8];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < kMaxVec; ++i) {
+      const int vi = lane + 32 * i;
+      if (vi < nvec) {
+        load8(sr + vi * 8, v[i]);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          if (causal && vi * 8 + e > q) v[i][e] = -INFINITY;
+          mx = fmaxf(mx, v[i][e]);
+        }
+      }
+    }
+    mx = warp_max(mx);
+    float sum = 0.f;
+#pragma unroll
+    for (int i = 0; i < kMaxVec; ++i) {
+      if (lane + 32 * i < nvec) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          v[i][e] = __expf(v[i][e] - mx);
+          sum += v[i][e];
+        }
+      }
+    }
+    const float inv = 1.f / warp_sum(sum);
+    __nv_bfloat16* pr = p + static_cast<long long>(row) * len;
+#pragma unroll
+    for (int i = 0; i < kMaxVec; ++i) {
+      const int vi = lane + 32 * i;
+      if (vi < nvec) {
+        float o[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = v[i][e] * inv;
+        store8(pr + vi * 8, o);
+      }
+    }
+  }
+}
+
+// dS = P * (dP - sum(P * dP))   (P bf16, dP fp32 -> dS bf16)
+template <int kMaxVec>
+__global__ void softmax_bwd_kernel(const __nv_bfloat16* __restrict__ p, const float* __restrict__ dp,
+                                   __nv_bfloat16* __restrict__ ds, int rows, int len) {
+  const int warps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nvec = len / 8;
+  for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < rows; row += gridDim.x * warps) {
+    const long long base = static_cast<long long>(row) * len;
+    float pv[kMaxVec][8], gv[kMaxVec][8];
+    float dot = 0.f;
+#pragma unroll
+    for (int i = 0; i < kMaxVec; ++i) {
+      const int vi = lane + 32 * i;
+      if (vi < nvec) {
+        load8(p + base + vi * 8, pv[i]);
+        load8(dp + base + vi * 8, gv[i]);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) dot += pv[i][e] * gv[i][e];
+      }
+    }
+    dot = warp_sum(dot);
+#pragma unroll
+    for (int i = 0; i < kMaxVec; ++i) {
+      const int vi = lane + 32 * i;
+      if (vi < nvec) {
+        float o[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = pv[i][e] * (gv[i][e] - dot);
+        store8(ds + base + vi * 8, o);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ bias grads
+// db[c] += sum_r dy[r][c]; each block owns a slab of rows, threads own
+// 8-column vectors; one atomic per column per block.
+__global__ void colsum_acc_kernel(const __nv_bfloat16* __restrict__ dy, float* __restrict__ db, int rows, int cols,
+                                  int rows_per_block) {
+  const int nvec = cols / 8;
+  const int r0 = blockIdx.y * rows_per_block;
+  const int r1 = min(rows, r0 + rows_per_block);
+  for (int vi = blockIdx.x * blockDim.x + threadIdx.x; vi < nvec; vi += gridDim.x * blockDim.x) {
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int r = r0; r < r1; ++r) {
+      float f[8];
+      load8(dy + static_cast<long long>(r) * cols + vi * 8, f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += f[e];
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) atomicAdd(db + vi * 8 + e, acc[e]);
+  }
+}
+
+// ------------------------------------------------------------ loss
+// loss_acc += sum (y - t)^2 ; dy = (y - t) * grad_scale  (grad_scale = 2/numel)
+__global__ void mse_kernel(const __nv_bfloat16* __restrict__ y, const __nv_bfloat16* __restrict__ t,
+                           __nv_bfloat16* __restrict__ dy, float* __restrict__ loss_acc, long long n,
+                           float grad_scale) {
+  float local = 0.f;
+  const long long nvec = n / 8;
+  for (long long vi = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; vi < nvec;
+       vi += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float a[8], b[8], o[8];
+    load8(y + vi * 8, a);
+    load8(t + vi * 8, b);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float d = a[e] - b[e];
+      local += d * d;
+      o[e] = d * grad_scale;
+    }
+    store8(dy + vi * 8, o);
+  }
+  local = warp_sum(local);
+  __shared__ float part[32];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = local;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? part[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) atomicAdd(loss_acc, v);
+  }
+}
+
+// ------------------------------------------------------------ optimizer
+// w32 -= lr * g ; w16 = bf16(w32) ; g = 0   (fp32 master weights)
+__global__ void sgd_kernel(float* __restrict__ w32, float* __restrict__ g, __nv_bfloat16* __restrict__ w16,
+                           long long n, float lr) {
+  const long long nvec = n / 4;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < nvec;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float4 w = reinterpret_cast<float4*>(w32)[i];
+    const float4 gg = reinterpret_cast<float4*>(g)[i];
+    w.x -= lr * gg.x;
+    w.y -= lr * gg.y;
+    w.z -= lr * gg.z;
+    w.w -= lr * gg.w;
+    reinterpret_cast<float4*>(w32)[i] = w;
+    reinterpret_cast<float4*>(g)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (w16) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(w.x, w.y);
+      __nv_bfloat162 hi = __floats2bfloat162_rn(w.z, w.w);
+      uint2 pk;
+      pk.x = *reinterpret_cast<uint32_t*>(&lo);
+      pk.y = *reinterpret_cast<uint32_t*>(&hi);
+      reinterpret_cast<uint2*>(w16)[i] = pk;
+    }
+  }
+  // scalar tail
+  for (long long i = nvec * 4 + blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    w32[i] -= lr * g[i];
+    g[i] = 0.f;
+    if (w16) w16[i] = __float2bfloat16_rn(w32[i]);
+  }
+}
+
+// ------------------------------------------------------------ synthetic data
+__device__ __forceinline__ float hash_uniform(uint64_t seed, uint64_t tensor, uint64_t idx) {
+  uint64_t z = seed + tensor * 0xD1B54A32D192ED03ull + idx * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D649BB133111EBull;
+  z ^= z >> 31;
+  return static_cast<float>(z >> 40) * (1.0f / 16777216.0f) * 2.0f - 1.0f;
+}
+
+// dst[r][c] = scale * U(-1,1) keyed by (seed, tensor, (row0 + r) * cols + c)
+__global__ void fill_uniform_bf16_kernel(__nv_bfloat16* dst, long long n, uint64_t seed, uint64_t tensor,
+                                         long long idx0, float scale) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    dst[i] = __float2bfloat16_rn(scale * hash_uniform(seed, tensor, static_cast<uint64_t>(idx0 + i)));
+}
+__global__ void fill_uniform_f32_kernel(float* dst, long long n, uint64_t seed, uint64_t tensor, long long idx0,
+                                        float scale) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    dst[i] = scale * hash_uniform(seed, tensor, static_cast<uint64_t>(idx0 + i));
+}
+__global__ void fill_const_f32_kernel(float* dst, long long n, float v) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    dst[i] = v;
+}
+__global__ void cast_f32_bf16_kernel(const float* src, __nv_bfloat16* dst, long long n) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    dst[i] = __float2bfloat16_rn(src[i]);
+}
+
+int grid_for(long long work, int threads) {
+  long long g = (work + threads - 1) / threads;
+  const long long cap = 148LL * 16;
+  return static_cast<int>(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+}  // namespace
+
+void layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y, float* mean, float* rstd, int rows,
+                   int h, float eps, cudaStream_t s) {
+  const int warps = 8;
+  const int grid = std::max(1, std::min((rows + warps - 1) / warps, 148 * 8));
+  dispatch_vec(h, [&](auto v) {
+    layernorm_fwd_kernel<decltype(v)::value><<<grid, warps * 32, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(x), gamma, beta, static_cast<__nv_bfloat16*>(y), mean, rstd, rows, h, eps);
+  });
+}
+
+void layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd, const float* gamma,
+                   const void* dresid, void* dx, float* dgamma, float* dbeta, int rows, int h, cudaStream_t s) {
+  const int warps = 8;
+  const int grid = std::max(1, std::min((rows + warps - 1) / warps, 148 * 2));
+  const size_t smem = static_cast<size_t>(warps) * 2 * h * sizeof(float);
+  dispatch_vec(h, [&](auto v) {
+    auto* k = layernorm_bwd_kernel<decltype(v)::value>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    k<<<grid, warps * 32, smem, s>>>(static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), mean,
+                                     rstd, gamma, static_cast<const __nv_bfloat16*>(dresid),
+                                     static_cast<__nv_bfloat16*>(dx), dgamma, dbeta, rows, h);
+  });
+}
+
+void softmax_fwd(const float* s, void* p, int rows, int len, int q_len, int causal, cudaStream_t st) {
+  const int warps = 8;
+  const int grid = std::max(1, std::min((rows + warps - 1) / warps, 148 * 16));
+  dispatch_vec(len, [&](auto v) {
+    softmax_fwd_kernel<decltype(v)::value><<<grid, warps * 32, 0, st>>>(s, static_cast<__nv_bfloat16*>(p), rows, len,
+                                                                        q_len, causal);
+  });
+}
+
+void softmax_bwd(const void* p, const float* dp, void* ds, int rows, int len, cudaStream_t st) {
+  const int warps = 8;
+  const int grid = std::max(1, std::min((rows + warps - 1) / warps, 148 * 16));
+  dispatch_vec(len, [&](auto v) {
+    softmax_bwd_kernel<decltype(v)::value><<<grid, warps * 32, 0, st>>>(static_cast<const __nv_bfloat16*>(p), dp,
+                                                                        static_cast<__nv_bfloat16*>(ds), rows, len);
+  });
+}
+
+void colsum_acc(const void* dy, float* db, int rows, int cols, cudaStream_t s) {
+  const int threads = 128;
+  const int nvec = cols / 8;
+  const int gx = (nvec + threads - 1) / threads;
+  // enough row slabs to put ~4 blocks on every SM
+  int gy = std::max(1, (148 * 4) / std::max(gx, 1));
+  gy = std::min(gy, rows);
+  const int rpb = (rows + gy - 1) / gy;
+  gy = (rows + rpb - 1) / rpb;
+  colsum_acc_kernel<<<dim3(gx, gy), threads, 0, s>>>(static_cast<const __nv_bfloat16*>(dy), db, rows, cols, rpb);
+}
+
+void mse_loss(const void* y, const void* t, void* dy, float* loss_acc, long long n, float grad_scale, cudaStream_t s) {
+  mse_kernel<<<grid_for(n / 8, 256), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(y),
+                                                   static_cast<const __nv_bfloat16*>(t),
+                                                   static_cast<__nv_bfloat16*>(dy), loss_acc, n, grad_scale);
+}
+
+void sgd_apply(float* w32, float* g, void* w16, long long n, float lr, cudaStream_t s) {
+  sgd_kernel<<<grid_for(n / 4, 256), 256, 0, s>>>(w32, g, static_cast<__nv_bfloat16*>(w16), n, lr);
+}
+
+void fill_uniform_bf16(void* dst, long long n, uint64_t seed, uint64_t tensor, long long idx0, float scale,
+                       cudaStream_t s) {
+  fill_uniform_bf16_kernel<<<grid_for(n, 256), 256, 0, s>>>(static_cast<__nv_bfloat16*>(dst), n, seed, tensor, idx0,
+                                                            scale);
+}
+
+void fill_uniform_f32(float* dst, long long n, uint64_t seed, uint64_t tensor, long long idx0, float scale,
+                      cudaStream_t s) {
+  fill_uniform_f32_kernel<<<grid_for(n, 256), 256, 0, s>>>(dst, n, seed, tensor, idx0, scale);
+}
+
+void fill_const_f32(float* dst, long long n, float v, cudaStream_t s) {
+  fill_const_f32_kernel<<<grid_for(n, 256), 256, 0, s>>>(dst, n, v);
+}
+
+void cast_f32_bf16(const float* src, void* dst, long long n, cudaStream_t s) {
+  cast_f32_bf16_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, static_cast<__nv_bfloat16*>(dst), n);
+}
+
+}  // namespace dpl

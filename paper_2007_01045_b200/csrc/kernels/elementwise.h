@@ -1,0 +1,28 @@
+// Host launchers for the HBM-bound stage kernels (elementwise.cu).
+// All tensors are row-major; bf16 tensors are passed as void*.  Row lengths
+// must be multiples of 8 elements (16-byte vectors).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace dpl {
+
+void layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y, float* mean, float* rstd, int rows,
+                   int h, float eps, cudaStream_t s);
+void layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd, const float* gamma,
+                   const void* dresid, void* dx, float* dgamma, float* dbeta, int rows, int h, cudaStream_t s);
+void softmax_fwd(const float* s, void* p, int rows, int len, int q_len, int causal, cudaStream_t st);
+void softmax_bwd(const void* p, const float* dp, void* ds, int rows, int len, cudaStream_t st);
+void colsum_acc(const void* dy, float* db, int rows, int cols, cudaStream_t s);
+void mse_loss(const void* y, const void* t, void* dy, float* loss_acc, long long n, float grad_scale, cudaStream_t s);
+void sgd_apply(float* w32, float* g, void* w16, long long n, float lr, cudaStream_t s);
+void fill_uniform_bf16(void* dst, long long n, uint64_t seed, uint64_t tensor, long long idx0, float scale,
+                       cudaStream_t s);
+void fill_uniform_f32(float* dst, long long n, uint64_t seed, uint64_t tensor, long long idx0, float scale,
+                      cudaStream_t s);
+void fill_const_f32(float* dst, long long n, float v, cudaStream_t s);
+void cast_f32_bf16(const float* src, void* dst, long long n, cudaStream_t s);
+
+}  // namespace dpl

@@ -1,0 +1,100 @@
+// Host-side interface of the tcgen05 GEMM (gemm_tcgen05.cu).
+//
+//   C[z, m, n] = epilogue( alpha * sum_k A[z, m, k] * B[z, n, k] )
+//
+// A is stored K-major ([M][lda], k contiguous) or M-major ([K][lda], m
+// contiguous); B likewise with N.  Output addressing is general enough to
+// express the attention head split / merge without separate transpose
+// kernels:
+//   off(z, m, n) = (z / zdiv) * s_zo + (z % zdiv) * s_zi + m * ldc
+//                + (n / ndiv) * s_no + (n % ndiv)
+// aux_in / resid / aux_out share C's addressing.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace dpl {
+
+enum GemmEpilogue : uint32_t {
+  kOutBf16 = 0,      // C bf16 = result
+  kOutF32 = 1,       // C fp32 = result
+  kOutF32Acc = 2,    // C fp32 += result   (micro-batch gradient accumulation)
+  kOutMask = 3,
+  kBias = 1u << 2,   // + bias[n] (fp32)
+  kGelu = 1u << 3,   // gelu(.)
+  kRelu = 1u << 4,   // relu(.)
+  kAuxOut = 1u << 5, // also store the pre-activation (bf16) to aux_out
+  kDGelu = 1u << 6,  // * gelu'(aux_in)
+  kDRelu = 1u << 7,  // * relu'(aux_in)
+  kResid = 1u << 8,  // + resid (bf16), added after bias, before activation
+};
+
+struct GemmDesc {
+  int M = 0, N = 0, K = 0, batch = 1;
+  const void* A = nullptr;
+  long long lda = 0, a_batch_stride = 0;
+  int a_mn_major = 0;
+  const void* B = nullptr;
+  long long ldb = 0, b_batch_stride = 0;
+  int b_mn_major = 0;
+  void* C = nullptr;
+  long long ldc = 0;
+  int zdiv = 1;
+  long long s_zo = 0, s_zi = 0;
+  int ndiv = 1 << 30;
+  long long s_no = 0;
+  uint32_t epi = kOutBf16;
+  float alpha = 1.0f;
+  const float* bias = nullptr;
+  const void* aux_in = nullptr;
+  const void* resid = nullptr;
+  void* aux_out = nullptr;
+  int force_bn = 0;  // 0 = heuristic; else 64/128/256
+};
+
+// Device-visible launch parameters (one per prepared GEMM).
+struct alignas(64) GemmParams {
+  CUtensorMap tma_a;
+  CUtensorMap tma_b;
+  int M, N, K, batch;
+  int a_mn_major, b_mn_major;
+  int num_m_blocks, num_n_blocks, num_k_blocks, num_tiles;
+  uint32_t epi;
+  float alpha;
+  void* C;
+  long long ldc;
+  int zdiv, ndiv;
+  long long s_zo, s_zi, s_no;
+  const float* bias;
+  const __nv_bfloat16* aux_in;
+  const __nv_bfloat16* resid;
+  __nv_bfloat16* aux_out;
+  int vec_ok;
+};
+
+// A prepared GEMM: tensor maps encoded once, launched many times (the
+// executor prepares every layer's GEMMs at setup, so steps pay no host cost).
+class GemmOp {
+ public:
+  GemmOp() = default;
+  void prepare(const GemmDesc& d);
+  void launch(cudaStream_t stream) const;
+  int bn() const { return bn_; }
+  int grid() const { return grid_; }
+  double flops() const { return 2.0 * params_.M * params_.N * static_cast<double>(params_.K) * params_.batch; }
+  bool ready() const { return bn_ != 0; }
+
+ private:
+  GemmParams params_{};
+  int bn_ = 0;
+  int grid_ = 0;
+  size_t smem_ = 0;
+};
+
+int num_sms();
+
+}  // namespace dpl

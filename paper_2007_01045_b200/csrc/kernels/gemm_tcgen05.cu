@@ -1,0 +1,488 @@
+// Persistent warp-specialised bf16 GEMM for sm_100a (stage kernels N1/N2).
+//
+//   warp 0      TMA producer: A/B tiles -> smem ring (SWIZZLE_128B)
+//   warp 1      MMA issuer: tcgen05.mma (M=128, N=BN, K=16) into TMEM
+//   warp 2      TMEM allocator (2 x BN fp32 columns: double-buffered accumulator)
+//   warps 4-7   epilogue: tcgen05.ld -> bias / residual / activation /
+//               activation-derivative / fp32 gradient accumulation -> global
+//
+// The accumulator is double buffered in TMEM so the epilogue of tile i
+// overlaps the MMAs of tile i+1.  Operands may be K-major or MN-major (the
+// backward GEMMs dX = dY W and dW += dY^T X read transposed operands straight
+// from their forward layouts; no transpose kernels).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "gemm.h"
+#include "ptx.cuh"
+
+namespace dpl {
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;  // one 128-byte swizzle atom of bf16
+constexpr int kThreads = 256;
+constexpr int kSmemBudget = 227 * 1024;
+
+template <int BN>
+struct Cfg {
+  static constexpr int kABytes = kBM * kBK * 2;
+  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = std::min(8, (kSmemBudget - 2048) / kStageBytes);
+  static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int kSmem = 1024 /*align slack*/ + kStages * kStageBytes + 1024 /*barriers*/;
+};
+
+__device__ __forceinline__ float gelu_f(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
+__device__ __forceinline__ float dgelu_f(float x) {
+  const float cdf = 0.5f * (1.0f + erff(x * 0.70710678118654752f));
+  const float pdf = 0.39894228040143268f * __expf(-0.5f * x * x);
+  return cdf + x * pdf;
+}
+
+__device__ __forceinline__ long long out_offset(const GemmParams& p, int z, int m, int n) {
+  return static_cast<long long>(z / p.zdiv) * p.s_zo + static_cast<long long>(z % p.zdiv) * p.s_zi +
+         static_cast<long long>(m) * p.ldc + static_cast<long long>(n / p.ndiv) * p.s_no + (n % p.ndiv);
+}
+
+// Apply the epilogue to one thread's 32 consecutive columns of one row.
+__device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int z, int row, int n0, const uint32_t (&raw)[32]) {
+  if (row >= p.M || n0 >= p.N) return;
+  const long long off = out_offset(p, z, row, n0);
+  const int ncols = min(32, p.N - n0);
+  const bool full = (ncols == 32) && p.vec_ok;
+  const uint32_t epi = p.epi;
+
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(raw[j]) * p.alpha;
+
+  if (epi & kBias) {
+    if (full) {
+      const float4* b4 = reinterpret_cast<const float4*>(p.bias + n0);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 b = __ldg(b4 + q);
+        v[4 * q] += b.x;
+        v[4 * q + 1] += b.y;
+        v[4 * q + 2] += b.z;
+        v[4 * q + 3] += b.w;
+      }
+    } else {
+      for (int j = 0; j < ncols; ++j) v[j] += p.bias[n0 + j];
+    }
+  }
+  if (epi & kResid) {
+    if (full) {
+      const uint4* r4 = reinterpret_cast<const uint4*>(p.resid + off);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 r = r4[q];
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(h[e]);
+          v[8 * q + 2 * e] += f.x;
+          v[8 * q + 2 * e + 1] += f.y;
+        }
+      }
+    } else {
+      for (int j = 0; j < ncols; ++j) v[j] += __bfloat162float(p.resid[off + j]);
+    }
+  }
+  if (epi & (kDGelu | kDRelu)) {
+    float z[32];
+    if (full) {
+      const uint4* a4 = reinterpret_cast<const uint4*>(p.aux_in + off);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 r = a4[q];
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(h[e]);
+          z[8 * q + 2 * e] = f.x;
+          z[8 * q + 2 * e + 1] = f.y;
+        }
+      }
+    } else {
+      for (int j = 0; j < 32; ++j) z[j] = j < ncols ? __bfloat162float(p.aux_in[off + j]) : 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] *= (epi & kDGelu) ? dgelu_f(z[j]) : (z[j] > 0.f ? 1.f : 0.f);
+  }
+  if (epi & kAuxOut) {
+    if (full) {
+      uint4* o4 = reinterpret_cast<uint4*>(p.aux_out + off);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 w;
+        uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          __nv_bfloat162 h = __floats2bfloat162_rn(v[8 * q + 2 * e], v[8 * q + 2 * e + 1]);
+          wp[e] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        o4[q] = w;
+      }
+    } else {
+      for (int j = 0; j < ncols; ++j) p.aux_out[off + j] = __float2bfloat16_rn(v[j]);
+    }
+  }
+  if (epi & kGelu) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
+  } else if (epi & kRelu) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
+  }
+
+  const uint32_t kind = epi & kOutMask;
+  if (kind == kOutBf16) {
+    __nv_bfloat16* c = static_cast<__nv_bfloat16*>(p.C) + off;
+    if (full) {
+      uint4* c4 = reinterpret_cast<uint4*>(c);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 w;
+        uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          __nv_bfloat162 h = __floats2bfloat162_rn(v[8 * q + 2 * e], v[8 * q + 2 * e + 1]);
+          wp[e] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        c4[q] = w;
+      }
+    } else {
+      for (int j = 0; j < ncols; ++j) c[j] = __float2bfloat16_rn(v[j]);
+    }
+  } else {
+    float* c = static_cast<float*>(p.C) + off;
+    const bool acc = kind == kOutF32Acc;
+    if (full) {
+      float4* c4 = reinterpret_cast<float4*>(c);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4 w = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        if (acc) {
+          const float4 o = c4[q];
+          w.x += o.x;
+          w.y += o.y;
+          w.z += o.z;
+          w.w += o.w;
+        }
+        c4[q] = w;
+      }
+    } else {
+      for (int j = 0; j < ncols; ++j) c[j] = acc ? c[j] + v[j] : v[j];
+    }
+  }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_constant__ GemmParams p) {
+  using C = Cfg<BN>;
+  constexpr int S = C::kStages;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + S * C::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes);
+  uint64_t* empty = full + S;
+  uint64_t* tmem_full = empty + S;
+  uint64_t* tmem_empty = tmem_full + 2;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+  const uint32_t warp = ptx::warp_id();
+  const uint32_t lane = ptx::lane_id();
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&p.tma_a);
+    ptx::tma_prefetch_desc(&p.tma_b);
+    for (int s = 0; s < S; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tmem_full[a], 1);
+      ptx::mbar_init(&tmem_empty[a], 128);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<C::kTmemCols>(tmem_base_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_slot;
+
+  const int tiles_per_z = p.num_m_blocks * p.num_n_blocks;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        const int z = t / tiles_per_z;
+        const int r = t % tiles_per_z;
+        const int mb = r % p.num_m_blocks;
+        const int nb = r / p.num_m_blocks;
+        for (int kb = 0; kb < p.num_k_blocks; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+          uint8_t* sa = smem_a + stage * C::kABytes;
+          uint8_t* sb = smem_b + stage * C::kBBytes;
+          if (!p.a_mn_major) {
+            ptx::tma_load_3d(sa, &p.tma_a, &full[stage], kb * kBK, mb * kBM, z);
+          } else {
+#pragma unroll
+            for (int j = 0; j < kBM / 64; ++j)
+              ptx::tma_load_3d(sa + j * 64 * kBK * 2, &p.tma_a, &full[stage], mb * kBM + j * 64, kb * kBK, z);
+          }
+          if (!p.b_mn_major) {
+            ptx::tma_load_3d(sb, &p.tma_b, &full[stage], kb * kBK, nb * BN, z);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              ptx::tma_load_3d(sb + j * 64 * kBK * 2, &p.tma_b, &full[stage], nb * BN + j * 64, kb * kBK, z);
+          }
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = ptx::idesc_bf16_f32(kBM, BN, p.a_mn_major != 0, p.b_mn_major != 0);
+      // K-major: 8-row groups 1024 B apart, advance 32 B per K=16 step.
+      // MN-major: 64-wide MN chunks 8 KB apart (LBO), 8-row K groups 1 KB
+      // apart (SBO), advance 16 rows = 2 KB per K=16 step.
+      const uint32_t a_lbo = p.a_mn_major ? 64 * kBK * 2 : 16;
+      const uint32_t b_lbo = p.b_mn_major ? 64 * kBK * 2 : 16;
+      const uint32_t a_step = p.a_mn_major ? 16 * 128 : 32;
+      const uint32_t b_step = p.b_mn_major ? 16 * 128 : 32;
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = 0; kb < p.num_k_blocks; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t sa = ptx::smem_addr(smem_a + stage * C::kABytes);
+          const uint32_t sb = ptx::smem_addr(smem_b + stage * C::kBBytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            const uint64_t ad = ptx::smem_desc_sw128(sa + k * a_step, a_lbo, 1024);
+            const uint64_t bd = ptx::smem_desc_sw128(sb + k * b_step, b_lbo, 1024);
+            ptx::mma_bf16(tmem_d, ad, bd, idesc, (kb | k) != 0);
+          }
+          ptx::mma_commit(&empty[stage]);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::mma_commit(&tmem_full[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const uint32_t quad = warp & 3;  // TMEM lane quadrant this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      const int z = t / tiles_per_z;
+      const int r = t % tiles_per_z;
+      const int mb = r % p.num_m_blocks;
+      const int nb = r / p.num_m_blocks;
+      ptx::mbar_wait(&tmem_full[acc], acc_phase);
+      ptx::tc_fence_after();
+      const int row = mb * kBM + quad * 32 + lane;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t raw[32];
+        ptx::tmem_ld_32x32b_x32(tmem_base + ((quad * 32) << 16) + acc * BN + c * 32, raw);
+        ptx::tmem_wait_ld();
+        epilogue_chunk(p, z, row, nb * BN + c * 32, raw);
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tmem_empty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !ptr) {
+      throw std::runtime_error("dpl: cuTensorMapEncodeTiled unavailable");
+    }
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+// 3-D bf16 tensor map over [batch][outer][inner] with a (64 x box_outer)
+// SWIZZLE_128B box.
+CUtensorMap make_map(const void* base, long long inner, long long outer, long long ld, int batch,
+                     long long batch_stride, int box_outer) {
+  if (reinterpret_cast<uintptr_t>(base) % 16 != 0) throw std::invalid_argument("dpl gemm: operand not 16B aligned");
+  if ((ld * 2) % 16 != 0) throw std::invalid_argument("dpl gemm: leading dimension must be a multiple of 8");
+  if (batch > 1 && (batch_stride * 2) % 16 != 0) throw std::invalid_argument("dpl gemm: batch stride alignment");
+  CUtensorMap map;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer),
+                        static_cast<cuuint64_t>(batch)};
+  const long long bs = batch > 1 ? batch_stride : ld * outer;
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld * 2), static_cast<cuuint64_t>(bs * 2)};
+  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_outer), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult rc = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (rc != CUDA_SUCCESS) throw std::runtime_error("dpl gemm: cuTensorMapEncodeTiled failed (" + std::to_string(rc) + ")");
+  return map;
+}
+
+template <int BN>
+void configure_kernel() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(gemm_bf16_tcgen05<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::kSmem);
+  });
+}
+
+int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
+
+}  // namespace
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+void GemmOp::prepare(const GemmDesc& d) {
+  if (d.M <= 0 || d.N <= 0 || d.K <= 0 || d.batch <= 0) throw std::invalid_argument("dpl gemm: empty problem");
+  if (d.ndiv % 32 != 0) throw std::invalid_argument("dpl gemm: ndiv must be a multiple of 32");
+  int bn = d.force_bn;
+  if (bn == 0) {
+    if (d.N <= 64) {
+      bn = 64;
+    } else {
+      // minimise (waves x tile width); ties prefer the wider tile
+      const int sms = num_sms();
+      long long best = -1;
+      for (int cand : {256, 128}) {
+        const long long tiles = static_cast<long long>(ceil_div(d.M, kBM)) * ceil_div(d.N, cand) * d.batch;
+        const long long cost = ((tiles + sms - 1) / sms) * cand;
+        if (best < 0 || cost < best) {
+          best = cost;
+          bn = cand;
+        }
+      }
+    }
+  }
+  GemmParams& p = params_;
+  p = GemmParams{};
+  p.M = d.M;
+  p.N = d.N;
+  p.K = d.K;
+  p.batch = d.batch;
+  p.a_mn_major = d.a_mn_major;
+  p.b_mn_major = d.b_mn_major;
+  p.tma_a = d.a_mn_major ? make_map(d.A, d.M, d.K, d.lda, d.batch, d.a_batch_stride, kBK)
+                         : make_map(d.A, d.K, d.M, d.lda, d.batch, d.a_batch_stride, kBM);
+  p.tma_b = d.b_mn_major ? make_map(d.B, d.N, d.K, d.ldb, d.batch, d.b_batch_stride, kBK)
+                         : make_map(d.B, d.K, d.N, d.ldb, d.batch, d.b_batch_stride, bn);
+  p.num_m_blocks = ceil_div(d.M, kBM);
+  p.num_n_blocks = ceil_div(d.N, bn);
+  p.num_k_blocks = ceil_div(d.K, kBK);
+  p.num_tiles = p.num_m_blocks * p.num_n_blocks * d.batch;
+  p.epi = d.epi;
+  p.alpha = d.alpha;
+  p.C = d.C;
+  p.ldc = d.ldc;
+  p.zdiv = d.zdiv;
+  p.ndiv = d.ndiv;
+  p.s_zo = d.s_zo;
+  p.s_zi = d.s_zi;
+  p.s_no = d.s_no;
+  p.bias = d.bias;
+  p.aux_in = static_cast<const __nv_bfloat16*>(d.aux_in);
+  p.resid = static_cast<const __nv_bfloat16*>(d.resid);
+  p.aux_out = static_cast<__nv_bfloat16*>(d.aux_out);
+  // 16-byte vector epilogue needs every row/segment start 16B aligned
+  const int esz = (d.epi & kOutMask) == kOutBf16 ? 2 : 4;
+  const bool aligned = reinterpret_cast<uintptr_t>(d.C) % 16 == 0 && (d.ldc * esz) % 16 == 0 &&
+                       (d.s_zo * esz) % 16 == 0 && (d.s_zi * esz) % 16 == 0 && (d.s_no * esz) % 16 == 0 &&
+                       (!d.bias || reinterpret_cast<uintptr_t>(d.bias) % 16 == 0) &&
+                       (!d.aux_in || reinterpret_cast<uintptr_t>(d.aux_in) % 16 == 0) &&
+                       (!d.resid || reinterpret_cast<uintptr_t>(d.resid) % 16 == 0) &&
+                       (!d.aux_out || reinterpret_cast<uintptr_t>(d.aux_out) % 16 == 0) &&
+                       ((d.epi & kOutMask) == kOutBf16 || (d.ldc * 2) % 16 == 0);
+  const bool aux_aligned = !(d.aux_in || d.resid || d.aux_out) || ((d.ldc * 2) % 16 == 0 && (d.s_zo * 2) % 16 == 0 &&
+                                                                   (d.s_zi * 2) % 16 == 0 && (d.s_no * 2) % 16 == 0);
+  p.vec_ok = aligned && aux_aligned;
+  bn_ = bn;
+  grid_ = std::min(p.num_tiles, num_sms());
+  switch (bn) {
+    case 64: smem_ = Cfg<64>::kSmem; configure_kernel<64>(); break;
+    case 128: smem_ = Cfg<128>::kSmem; configure_kernel<128>(); break;
+    case 256: smem_ = Cfg<256>::kSmem; configure_kernel<256>(); break;
+    default: throw std::invalid_argument("dpl gemm: BN must be 64, 128 or 256");
+  }
+}
+
+void GemmOp::launch(cudaStream_t stream) const {
+  switch (bn_) {
+    case 64: gemm_bf16_tcgen05<64><<<grid_, kThreads, smem_, stream>>>(params_); break;
+    case 128: gemm_bf16_tcgen05<128><<<grid_, kThreads, smem_, stream>>>(params_); break;
+    case 256: gemm_bf16_tcgen05<256><<<grid_, kThreads, smem_, stream>>>(params_); break;
+    default: throw std::logic_error("dpl gemm: launch before prepare");
+  }
+}
+
+}  // namespace dpl

@@ -1,0 +1,76 @@
+"""Python front for the individual sm_100a stage kernels (dpl_k_* in
+include/dapple.h).  torch tensors are used only as device allocations; every
+call goes straight to libdapple.so on the tensor's current CUDA stream."""
+from __future__ import annotations
+
+import ctypes
+
+from ._lib import (EPI_AUX_OUT, EPI_BIAS, EPI_DGELU, EPI_DRELU, EPI_GELU, EPI_OUT_BF16, EPI_OUT_F32,  # noqa: F401
+                   EPI_OUT_F32_ACC, EPI_RELU, EPI_RESID, GemmDesc, check, lib)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    import torch
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def gemm(A, B, C, M, N, K, *, lda, ldb, ldc, a_mn_major=False, b_mn_major=False, batch=1, a_batch_stride=0,
+         b_batch_stride=0, epi=EPI_OUT_BF16, alpha=1.0, bias=None, aux_in=None, resid=None, aux_out=None, zdiv=1,
+         s_zo=None, s_zi=0, ndiv=1 << 30, s_no=0, force_bn=0):
+    """C[z,m,n] = epi(alpha * sum_k A[z,m,k] * B[z,n,k]) (see csrc/kernels/gemm.h)."""
+    d = GemmDesc()
+    d.M, d.N, d.K, d.batch = M, N, K, batch
+    d.A, d.lda, d.a_batch_stride, d.a_mn_major = A.data_ptr(), lda, a_batch_stride, int(a_mn_major)
+    d.B, d.ldb, d.b_batch_stride, d.b_mn_major = B.data_ptr(), ldb, b_batch_stride, int(b_mn_major)
+    d.C, d.ldc, d.zdiv = C.data_ptr(), ldc, zdiv
+    d.s_zo = M * ldc if s_zo is None else s_zo
+    d.s_zi, d.ndiv, d.s_no = s_zi, ndiv, s_no
+    d.epi, d.alpha = epi, alpha
+    d.bias = None if bias is None else bias.data_ptr()
+    d.aux_in = None if aux_in is None else aux_in.data_ptr()
+    d.resid = None if resid is None else resid.data_ptr()
+    d.aux_out = None if aux_out is None else aux_out.data_ptr()
+    d.force_bn = force_bn
+    check(lib().dpl_k_gemm(ctypes.byref(d), _stream()))
+
+
+def layernorm_fwd(x, gamma, beta, y, mean, rstd, rows, h, eps=1e-5):
+    check(lib().dpl_k_layernorm_fwd(_ptr(x), _ptr(gamma), _ptr(beta), _ptr(y), _ptr(mean), _ptr(rstd), rows, h, eps,
+                                    _stream()))
+
+
+def layernorm_bwd(dy, x, mean, rstd, gamma, dresid, dx, dgamma, dbeta, rows, h):
+    check(lib().dpl_k_layernorm_bwd(_ptr(dy), _ptr(x), _ptr(mean), _ptr(rstd), _ptr(gamma), _ptr(dresid), _ptr(dx),
+                                    _ptr(dgamma), _ptr(dbeta), rows, h, _stream()))
+
+
+def softmax_fwd(s, p, rows, length, q_len, causal=False):
+    check(lib().dpl_k_softmax_fwd(_ptr(s), _ptr(p), rows, length, q_len, int(causal), _stream()))
+
+
+def softmax_bwd(p, dp, ds, rows, length):
+    check(lib().dpl_k_softmax_bwd(_ptr(p), _ptr(dp), _ptr(ds), rows, length, _stream()))
+
+
+def colsum_acc(dy, db, rows, cols):
+    check(lib().dpl_k_colsum_acc(_ptr(dy), _ptr(db), rows, cols, _stream()))
+
+
+def mse_loss(y, t, dy, loss_acc, n, grad_scale):
+    check(lib().dpl_k_mse_loss(_ptr(y), _ptr(t), _ptr(dy), _ptr(loss_acc), n, grad_scale, _stream()))
+
+
+def sgd_apply(w32, g, w16, n, lr):
+    check(lib().dpl_k_sgd_apply(_ptr(w32), _ptr(g), _ptr(w16), n, lr, _stream()))
+
+
+def fill_uniform_bf16(dst, n, seed, tensor, idx0=0, scale=1.0):
+    check(lib().dpl_k_fill_uniform_bf16(_ptr(dst), n, seed, tensor, idx0, scale, _stream()))
+
+
+def fill_uniform_f32(dst, n, seed, tensor, idx0=0, scale=1.0):
+    check(lib().dpl_k_fill_uniform_f32(_ptr(dst), n, seed, tensor, idx0, scale, _stream()))

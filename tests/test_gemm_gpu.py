@@ -1,0 +1,121 @@
+"""tcgen05 GEMM vs a plain torch fp32 reference on the same bf16 operands."""
+import pytest
+import torch
+
+from paper_2007_01045_b200 import kernels as K
+
+pytestmark = pytest.mark.gpu
+
+
+def _rand(*shape, dev, scale=1.0, dtype=torch.bfloat16, seed=0):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    return ((torch.rand(*shape, generator=g) * 2 - 1) * scale).to(dtype).to(dev)
+
+
+def _close(out, ref, tol):
+    err = (out.float() - ref).abs().max().item()
+    scale = ref.abs().max().item() + 1e-6
+    assert err <= tol * scale, f"max err {err:.4g} vs scale {scale:.4g}"
+
+
+@pytest.mark.parametrize("M,N,Kd", [(128, 256, 64), (256, 512, 1024), (300, 200, 136), (1024, 3072, 1024),
+                                    (64, 64, 16), (513, 1000, 520)])
+@pytest.mark.parametrize("bn", [0, 64, 128, 256])
+def test_gemm_kk(cuda, M, N, Kd, bn):
+    A = _rand(M, Kd, dev=cuda, seed=1)
+    B = _rand(N, Kd, dev=cuda, seed=2)
+    C = torch.zeros(M, N, dtype=torch.bfloat16, device=cuda)
+    K.gemm(A, B, C, M, N, Kd, lda=Kd, ldb=Kd, ldc=N, force_bn=bn)
+    torch.cuda.synchronize()
+    _close(C, A.float() @ B.float().T, 2e-2)
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(True, False), (False, True), (True, True)])
+@pytest.mark.parametrize("M,N,Kd", [(256, 256, 128), (384, 640, 1024), (200, 136, 72)])
+@pytest.mark.parametrize("bn", [64, 128, 256])
+def test_gemm_mn_major(cuda, a_mn, b_mn, M, N, Kd, bn):
+    At = _rand(Kd, M, dev=cuda, seed=3) if a_mn else _rand(M, Kd, dev=cuda, seed=3)
+    Bt = _rand(Kd, N, dev=cuda, seed=4) if b_mn else _rand(N, Kd, dev=cuda, seed=4)
+    A = At.T if a_mn else At
+    B = Bt.T if b_mn else Bt
+    C = torch.zeros(M, N, dtype=torch.float32, device=cuda)
+    K.gemm(At, Bt, C, M, N, Kd, lda=(M if a_mn else Kd), ldb=(N if b_mn else Kd), ldc=N, a_mn_major=a_mn,
+           b_mn_major=b_mn, epi=K.EPI_OUT_F32, force_bn=bn)
+    torch.cuda.synchronize()
+    _close(C, A.float() @ B.float().T, 1e-3)
+
+
+def test_gemm_wgrad_accumulates(cuda):
+    # dW[N_out, K_in] += dY^T X over two micro-batches (both operands MN-major)
+    T, n_out, k_in = 1024, 768, 512
+    dW = torch.zeros(n_out, k_in, dtype=torch.float32, device=cuda)
+    ref = torch.zeros_like(dW)
+    for mb in range(2):
+        dY = _rand(T, n_out, dev=cuda, seed=10 + mb)
+        X = _rand(T, k_in, dev=cuda, seed=20 + mb)
+        K.gemm(dY, X, dW, n_out, k_in, T, lda=n_out, ldb=k_in, ldc=k_in, a_mn_major=True, b_mn_major=True,
+               epi=K.EPI_OUT_F32_ACC)
+        ref += dY.float().T @ X.float()
+    torch.cuda.synchronize()
+    _close(dW, ref, 1e-3)
+
+
+def test_gemm_bias_gelu_aux(cuda):
+    M, N, Kd = 512, 1024, 256
+    A = _rand(M, Kd, dev=cuda, seed=5)
+    B = _rand(N, Kd, dev=cuda, seed=6, scale=0.1)
+    bias = _rand(N, dev=cuda, seed=7, dtype=torch.float32)
+    C = torch.empty(M, N, dtype=torch.bfloat16, device=cuda)
+    Z = torch.empty(M, N, dtype=torch.bfloat16, device=cuda)
+    K.gemm(A, B, C, M, N, Kd, lda=Kd, ldb=Kd, ldc=N, epi=K.EPI_BIAS | K.EPI_GELU | K.EPI_AUX_OUT, bias=bias,
+           aux_out=Z)
+    torch.cuda.synchronize()
+    z = A.float() @ B.float().T + bias
+    _close(Z, z, 2e-2)
+    _close(C, torch.nn.functional.gelu(z), 2e-2)
+
+
+def test_gemm_dgelu_and_resid(cuda):
+    M, N, Kd = 256, 512, 384
+    A = _rand(M, Kd, dev=cuda, seed=8)
+    B = _rand(N, Kd, dev=cuda, seed=9, scale=0.1)
+    Z = _rand(M, N, dev=cuda, seed=11, scale=2.0)
+    R = _rand(M, N, dev=cuda, seed=12)
+    C = torch.empty(M, N, dtype=torch.bfloat16, device=cuda)
+    K.gemm(A, B, C, M, N, Kd, lda=Kd, ldb=Kd, ldc=N, epi=K.EPI_DGELU, aux_in=Z)
+    torch.cuda.synchronize()
+    z = Z.float().requires_grad_(True)
+    g = torch.autograd.grad(torch.nn.functional.gelu(z).sum(), z)[0]
+    _close(C, (A.float() @ B.float().T) * g, 2e-2)
+    K.gemm(A, B, C, M, N, Kd, lda=Kd, ldb=Kd, ldc=N, epi=K.EPI_RESID, resid=R, alpha=0.5)
+    torch.cuda.synchronize()
+    _close(C, 0.5 * (A.float() @ B.float().T) + R.float(), 2e-2)
+
+
+def test_gemm_attention_head_split_merge(cuda):
+    # QKV projection with head-split store, then batched S = Q K^T and
+    # ctx = P V with head-merge store, as the transformer stage uses them.
+    B_, S, H, nh = 2, 256, 256, 4
+    d = H // nh
+    T = B_ * S
+    X = _rand(T, H, dev=cuda, seed=13)
+    W = _rand(3 * H, H, dev=cuda, seed=14, scale=0.1)
+    qkv = torch.empty(3, nh, B_, S, d, dtype=torch.bfloat16, device=cuda)
+    K.gemm(X, W, qkv, T, 3 * H, H, lda=H, ldb=H, ldc=d, ndiv=d, s_no=T * d)
+    ref = (X.float() @ W.float().T).view(B_, S, 3, nh, d).permute(2, 3, 0, 1, 4)
+    torch.cuda.synchronize()
+    _close(qkv, ref, 2e-2)
+    q, k, v = qkv[0].reshape(nh * B_, S, d), qkv[1].reshape(nh * B_, S, d), qkv[2].reshape(nh * B_, S, d)
+    Sc = torch.empty(nh * B_, S, S, dtype=torch.float32, device=cuda)
+    K.gemm(q, k, Sc, S, S, d, lda=d, ldb=d, ldc=S, batch=nh * B_, a_batch_stride=S * d, b_batch_stride=S * d,
+           epi=K.EPI_OUT_F32, alpha=0.125)
+    torch.cuda.synchronize()
+    _close(Sc, 0.125 * q.float() @ k.float().transpose(1, 2), 1e-3)
+    P = torch.softmax(Sc, -1).to(torch.bfloat16)
+    ctx = torch.empty(T, H, dtype=torch.bfloat16, device=cuda)
+    # z = h*B + b ; row = b*S + s ; col = h*d + j
+    K.gemm(P, v, ctx, S, d, S, lda=S, ldb=d, ldc=H, batch=nh * B_, a_batch_stride=S * S, b_batch_stride=S * d,
+           b_mn_major=True, zdiv=B_, s_zo=d, s_zi=S * H)
+    torch.cuda.synchronize()
+    ref_ctx = (P.float() @ v.float()).view(nh, B_, S, d).permute(1, 2, 0, 3).reshape(T, H)
+    _close(ctx, ref_ctx, 2e-2)
