@@ -46,3 +46,294 @@ def hash_uniform(seed: int, tensor: int, idx) -> np.ndarray:
         z = z ^ (z >> np.uint64(31))
     u = (z >> np.uint64(40)).astype(np.float32) * np.float32(1.0 / 16777216.0)
     return u * np.float32(2.0) - np.float32(1.0)
+
+
+# ---------------------------------------------------------------- helpers
+def _tid(layer: int, t: int) -> int:
+    return 1000 + layer * 16 + t
+
+
+def _u(seed, tensor, n, scale) -> np.ndarray:
+    return np.float32(scale) * hash_uniform(seed, tensor, np.arange(n, dtype=np.uint64))
+
+
+def _erf(x):
+    from scipy.special import erf
+    return erf(x)
+
+
+def gelu(x):
+    return 0.5 * x * (1.0 + _erf(x / np.sqrt(2.0)))
+
+
+def dgelu(x):
+    return 0.5 * (1.0 + _erf(x / np.sqrt(2.0))) + x * np.exp(-0.5 * x * x) / np.sqrt(2.0 * np.pi)
+
+
+@dataclass
+class Model:
+    kind: str = "mlp"  # mlp | bert | gpt
+    layers: int = 16
+    hidden: int = 1024
+    heads: int = 16
+    ffn: int = 4096
+    seq: int = 1
+    causal: bool = False
+    eps: float = 1e-5
+
+    @staticmethod
+    def from_dict(d: dict) -> "Model":
+        m = Model(kind=d["kind"], layers=d["layers"], hidden=d["hidden"], heads=d.get("heads", 16),
+                  ffn=d.get("ffn", 4 * d["hidden"]), seq=d.get("seq", 1), causal=d.get("causal", False))
+        if m.kind == "mlp":
+            m.seq = 1
+        if m.kind == "gpt":
+            m.causal = True
+        return m
+
+
+def init_layer(model: Model, layer: int, seed: int) -> dict:
+    """Parameters of one layer exactly as the device initialises them
+    (csrc/runtime/layers.cu bind())."""
+    H, F = model.hidden, model.ffn
+    if model.kind == "mlp":
+        return {"W": _u(seed, _tid(layer, 0), H * H, np.sqrt(np.float32(6.0) / np.float32(H))).reshape(H, H),
+                "b": _u(seed, _tid(layer, 1), H, 0.05)}
+    sh = np.float32(1.0) / np.sqrt(np.float32(H))
+    sf = np.float32(1.0) / np.sqrt(np.float32(F))
+    return {"ln1_g": np.ones(H, np.float32), "ln1_b": np.zeros(H, np.float32),
+            "Wqkv": _u(seed, _tid(layer, 2), 3 * H * H, sh).reshape(3 * H, H),
+            "bqkv": _u(seed, _tid(layer, 3), 3 * H, 0.02),
+            "Wo": _u(seed, _tid(layer, 4), H * H, sh).reshape(H, H), "bo": _u(seed, _tid(layer, 5), H, 0.02),
+            "ln2_g": np.ones(H, np.float32), "ln2_b": np.zeros(H, np.float32),
+            "W1": _u(seed, _tid(layer, 8), F * H, sh).reshape(F, H), "b1": _u(seed, _tid(layer, 9), F, 0.02),
+            "W2": _u(seed, _tid(layer, 10), H * F, sf).reshape(H, F), "b2": _u(seed, _tid(layer, 11), H, 0.02)}
+
+
+def batch_data(model: Model, seed: int, sample0: int, samples: int):
+    """Input and target rows of samples [sample0, sample0 + samples):
+    element (g, pos, h) is keyed by index (g * seq + pos) * H + h."""
+    n = samples * model.seq * model.hidden
+    idx = np.arange(n, dtype=np.uint64) + np.uint64(sample0 * model.seq * model.hidden)
+    shape = (samples * model.seq, model.hidden)
+    return hash_uniform(seed, 1, idx).reshape(shape), hash_uniform(seed, 2, idx).reshape(shape)
+
+
+def bf16_round(a) -> np.ndarray:
+    """Round-to-nearest-even to bfloat16 (as __float2bfloat16_rn), returned
+    as float64.  Used by the oracle's bf16 mode at exactly the points where
+    the device stores a bf16 tensor."""
+    a32 = np.asarray(a, dtype=np.float32)
+    u = a32.view(np.uint32).astype(np.uint64)
+    r = ((u + np.uint64(0x7FFF) + ((u >> np.uint64(16)) & np.uint64(1))) >> np.uint64(16)) << np.uint64(16)
+    return r.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def _ident(a):
+    return a
+
+
+MATRICES = {"W", "Wqkv", "Wo", "W1", "W2"}
+
+
+def _gemm_weights(p, q):
+    return {k: (q(v) if k in MATRICES else v) for k, v in p.items()}
+
+
+# ---------------------------------------------------------------- layers
+def _ln_fwd(x, g, b, eps):
+    mean = x.mean(-1, keepdims=True)
+    var = ((x - mean) ** 2).mean(-1, keepdims=True)
+    rstd = 1.0 / np.sqrt(var + eps)
+    xh = (x - mean) * rstd
+    return xh * g + b, (xh, rstd)
+
+
+def _ln_bwd(dy, g, cache):
+    xh, rstd = cache
+    gd = dy * g
+    dx = rstd * (gd - gd.mean(-1, keepdims=True) - xh * (gd * xh).mean(-1, keepdims=True))
+    return dx, (dy * xh).sum(0), dy.sum(0)
+
+
+def layer_forward(model: Model, layer: int, p: dict, x: np.ndarray, samples: int, q=_ident):
+    """Returns (y, cache).  x: [samples * seq, H] rows.  q rounds the tensors
+    the device stores in bf16 (identity in the exact mode)."""
+    p = _gemm_weights(p, q)
+    if model.kind == "mlp":
+        z = x @ p["W"].T + p["b"]
+        y = q(np.maximum(z, 0) if layer != model.layers - 1 else z)
+        return y, (x,)
+    H, nh, s = model.hidden, model.heads, model.seq
+    d = H // nh
+    ln1, c1 = _ln_fwd(x, p["ln1_g"], p["ln1_b"], model.eps)
+    ln1 = q(ln1)
+    qkv = q(ln1 @ p["Wqkv"].T + p["bqkv"])
+    qh, k, v = (qkv[:, i * H:(i + 1) * H].reshape(samples, s, nh, d).transpose(0, 2, 1, 3) for i in range(3))
+    sc = (qh @ k.transpose(0, 1, 3, 2)) / np.sqrt(d)
+    if model.causal:
+        sc = np.where(np.triu(np.ones((s, s), bool), 1), -np.inf, sc)
+    sc = sc - sc.max(-1, keepdims=True)
+    P = np.exp(sc)
+    P = q(P / P.sum(-1, keepdims=True))
+    ctx = q((P @ v).transpose(0, 2, 1, 3).reshape(samples * s, H))
+    h = q(x + ctx @ p["Wo"].T + p["bo"])
+    ln2, c2 = _ln_fwd(h, p["ln2_g"], p["ln2_b"], model.eps)
+    ln2 = q(ln2)
+    z1f = ln2 @ p["W1"].T + p["b1"]
+    g = q(gelu(z1f))
+    y = q(h + g @ p["W2"].T + p["b2"])
+    return y, (x, ln1, c1, qh, k, v, P, ctx, h, ln2, c2, q(z1f), g)
+
+
+def layer_backward(model: Model, layer: int, p: dict, cache, dy: np.ndarray, samples: int, need_dx=True,
+                   q=_ident):
+    """MLP layers take / return the gradient w.r.t. the pre-activation
+    (layers.h gradient contract); transformer blocks w.r.t. the block
+    output / input."""
+    p = _gemm_weights(p, q)
+    if model.kind == "mlp":
+        (x,) = cache
+        grads = {"W": dy.T @ x, "b": dy.sum(0)}
+        dx = None
+        if need_dx:
+            dx = dy @ p["W"]
+            if layer > 0:
+                dx = dx * (x > 0)
+            dx = q(dx)
+        return dx, grads
+    H, nh, s = model.hidden, model.heads, model.seq
+    d = H // nh
+    x, ln1, c1, qh, k, v, P, ctx, h, ln2, c2, z1, g = cache
+    gr = {}
+    gr["W2"], gr["b2"] = dy.T @ g, dy.sum(0)
+    dz1 = q((dy @ p["W2"]) * dgelu(z1))
+    gr["W1"], gr["b1"] = dz1.T @ ln2, dz1.sum(0)
+    dh, gr["ln2_g"], gr["ln2_b"] = _ln_bwd(q(dz1 @ p["W1"]), p["ln2_g"], c2)
+    dh = q(dh + dy)
+    gr["Wo"], gr["bo"] = dh.T @ ctx, dh.sum(0)
+    dctx = q(dh @ p["Wo"]).reshape(samples, s, nh, d).transpose(0, 2, 1, 3)
+    dP = dctx @ v.transpose(0, 1, 3, 2)
+    dS = q(P * (dP - (P * dP).sum(-1, keepdims=True)))
+    scale = 1.0 / np.sqrt(d)
+    dq = q(scale * (dS @ k))
+    dk = q(scale * (dS.transpose(0, 1, 3, 2) @ qh))
+    dv = q(P.transpose(0, 1, 3, 2) @ dctx)
+    dqkv = np.concatenate([t.transpose(0, 2, 1, 3).reshape(samples * s, H) for t in (dq, dk, dv)], axis=1)
+    gr["Wqkv"], gr["bqkv"] = dqkv.T @ ln1, dqkv.sum(0)
+    dx, gr["ln1_g"], gr["ln1_b"] = _ln_bwd(q(dqkv @ p["Wqkv"]), p["ln1_g"], c1)
+    return q(dx + dh), gr
+
+
+# ---------------------------------------------------------------- steps
+@dataclass
+class StepResult:
+    loss: float
+    grads: dict = field(default_factory=dict)   # (layer, name) -> summed gradient
+    params: dict = field(default_factory=dict)  # (layer, name) -> parameter after SGD
+
+
+def full_batch_step(model, gbs: int, seed: int = 1234, lr: float = 1e-3, dtype=np.float64,
+                    layers=None, bf16: bool = False) -> StepResult:
+    """One sequential pass over the whole global batch (the known answer the
+    pipelined step must reproduce).  With bf16=True every
+    tensor the device stores in bf16 (inputs, targets, GEMM weights,
+    activations, activation gradients) is rounded to bf16 at the same point;
+    arithmetic stays fp64."""
+    model = Model.from_dict(model) if isinstance(model, dict) else model
+    layers = range(model.layers) if layers is None else layers
+    q = bf16_round if bf16 else _ident
+    params = {l: {k: v.astype(dtype) for k, v in init_layer(model, l, seed).items()} for l in layers}
+    x, t = batch_data(model, seed, 0, gbs)
+    x, t = q(x.astype(dtype)), q(t.astype(dtype))
+    caches = []
+    for l in layers:
+        x, c = layer_forward(model, l, params[l], x, gbs, q=q)
+        caches.append(c)
+    numel = gbs * model.seq * model.hidden
+    diff = x - t
+    loss = float((diff * diff).sum() / numel)
+    dy = q(2.0 * diff / numel)
+    res = StepResult(loss)
+    for li in reversed(range(len(caches))):
+        l = list(layers)[li]
+        dy, g = layer_backward(model, l, params[l], caches[li], dy, gbs, need_dx=li > 0, q=q)
+        for k, v in g.items():
+            res.grads[(l, k)] = v
+            res.params[(l, k)] = (params[l][k].astype(np.float32) - np.float32(lr) * v.astype(np.float32))
+    return res
+
+
+def scheduled_step(model, plan: dict, micro_batches: int, gbs: int, seed: int = 1234, lr: float = 1e-3,
+                   dtype=np.float64) -> StepResult:
+    """The DAPPLE step as the plan executes it: every stage replica owns an
+    even row slice of each micro-batch, activations and gradients cross stage
+    boundaries by interval overlap (Split-Concat), each replica accumulates
+    its gradients over the micro-batches in chain order B_0..B_{M-1}, and the
+    replica group sums them (AllReduce) before the update."""
+    model = Model.from_dict(model) if isinstance(model, dict) else model
+    stages = plan["stages"]
+    B = gbs // micro_batches
+    params = {l: {k: v.astype(dtype) for k, v in init_layer(model, l, seed).items()} for l in range(model.layers)}
+    numel = gbs * model.seq * model.hidden
+    acc = {}  # (stage, replica, layer, name) -> grad
+    loss = 0.0
+    for i in range(micro_batches):
+        xs = None  # per-replica input slices of the current stage
+        caches = []
+        for k, st in enumerate(stages):
+            r = len(st["gpus"])
+            lo, hi = st["layers"]
+            b = B // r
+            if k == 0:
+                xs = [batch_data(model, seed, i * B + j * b, b)[0].astype(dtype) for j in range(r)]
+            else:
+                whole = np.concatenate(xs, axis=0)  # split-concat: rows are batch-major
+                rows = b * model.seq
+                xs = [whole[j * rows:(j + 1) * rows] for j in range(r)]
+            stage_caches = []
+            for j in range(r):
+                x = xs[j]
+                cs = []
+                for l in range(lo, hi):
+                    x, c = layer_forward(model, l, params[l], x, b)
+                    cs.append(c)
+                xs[j] = x
+                stage_caches.append(cs)
+            caches.append(stage_caches)
+        # loss on the last stage
+        last = stages[-1]
+        r = len(last["gpus"])
+        b = B // r
+        dys = []
+        for j in range(r):
+            t = batch_data(model, seed, i * B + j * b, b)[1].astype(dtype)
+            diff = xs[j] - t
+            loss += float((diff * diff).sum())
+            dys.append(2.0 * diff / numel)
+        for k in reversed(range(len(stages))):
+            st = stages[k]
+            r = len(st["gpus"])
+            lo, hi = st["layers"]
+            b = B // r
+            if k != len(stages) - 1:
+                whole = np.concatenate(dys, axis=0)
+                rows = b * model.seq
+                dys = [whole[j * rows:(j + 1) * rows] for j in range(r)]
+            for j in range(r):
+                dy = dys[j]
+                for li, l in reversed(list(enumerate(range(lo, hi)))):
+                    dy, g = layer_backward(model, l, params[l], caches[k][j][li], dy, b, need_dx=(l > 0))
+                    for name, v in g.items():
+                        key = (k, j, l, name)
+                        acc[key] = acc[key] + v if key in acc else v
+                dys[j] = dy
+    res = StepResult(loss / numel)
+    for k, st in enumerate(stages):
+        lo, hi = st["layers"]
+        for l in range(lo, hi):
+            for name in params[l]:
+                g = sum(acc[(k, j, l, name)] for j in range(len(st["gpus"])))  # AllReduce
+                res.grads[(l, name)] = g
+                res.params[(l, name)] = params[l][name].astype(np.float32) - np.float32(lr) * g.astype(np.float32)
+    return res

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 
 namespace dpl {
 
@@ -93,6 +94,21 @@ class GemmOp {
   int bn_ = 0;
   int grid_ = 0;
   size_t smem_ = 0;
+};
+
+// Prepared-GEMM cache keyed by the full descriptor (pointers included):
+// tensor maps are encoded the first time a (layer, buffer) combination is
+// seen and reused on every later step.
+class GemmCache {
+ public:
+  const GemmOp& get(const GemmDesc& d);
+  void run(const GemmDesc& d, cudaStream_t s) { get(d).launch(s); }
+  size_t size() const;
+  double flops_run = 0.0;  // flops launched through run() (accounting)
+
+ private:
+  struct Impl;
+  std::shared_ptr<Impl> impl_;
 };
 
 int num_sms();

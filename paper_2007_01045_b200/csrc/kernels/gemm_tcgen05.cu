@@ -17,7 +17,9 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <stdexcept>
 #include <string>
 
@@ -475,6 +477,39 @@ void GemmOp::prepare(const GemmDesc& d) {
     default: throw std::invalid_argument("dpl gemm: BN must be 64, 128 or 256");
   }
 }
+
+struct GemmCache::Impl {
+  std::unordered_map<std::string, std::unique_ptr<GemmOp>> ops;
+};
+
+const GemmOp& GemmCache::get(const GemmDesc& d) {
+  if (!impl_) impl_ = std::make_shared<Impl>();
+  // explicit field-wise key: no padding bytes
+  const long long f[] = {d.M, d.N, d.K, d.batch,
+                         static_cast<long long>(reinterpret_cast<uintptr_t>(d.A)), d.lda, d.a_batch_stride,
+                         d.a_mn_major,
+                         static_cast<long long>(reinterpret_cast<uintptr_t>(d.B)), d.ldb, d.b_batch_stride,
+                         d.b_mn_major,
+                         static_cast<long long>(reinterpret_cast<uintptr_t>(d.C)), d.ldc, d.zdiv, d.s_zo, d.s_zi,
+                         d.ndiv, d.s_no, static_cast<long long>(d.epi),
+                         static_cast<long long>(reinterpret_cast<uintptr_t>(d.bias)),
+                         static_cast<long long>(reinterpret_cast<uintptr_t>(d.aux_in)),
+                         static_cast<long long>(reinterpret_cast<uintptr_t>(d.resid)),
+                         static_cast<long long>(reinterpret_cast<uintptr_t>(d.aux_out)), d.force_bn};
+  std::string key(reinterpret_cast<const char*>(f), sizeof f);
+  uint32_t a;
+  std::memcpy(&a, &d.alpha, 4);
+  key.append(reinterpret_cast<const char*>(&a), 4);
+  auto it = impl_->ops.find(key);
+  if (it == impl_->ops.end()) {
+    auto op = std::make_unique<GemmOp>();
+    op->prepare(d);
+    it = impl_->ops.emplace(std::move(key), std::move(op)).first;
+  }
+  return *it->second;
+}
+
+size_t GemmCache::size() const { return impl_ ? impl_->ops.size() : 0; }
 
 void GemmOp::launch(cudaStream_t stream) const {
   switch (bn_) {

@@ -1,0 +1,788 @@
+// Per-GPU DAPPLE step executor (one process per GPU).
+//
+// The executor mirrors simulate_plan (reference planner.cpp:491-514): the
+// same plan, the same phi resolution (planner.cpp:501-508) and the same
+// per-stage block order (simulator.cpp:81-97, realised by
+// pipeplan::stage_chain), but every block is a real stream program on a
+// B200 and the returned Timeline is measured.
+//
+// Streams per rank
+//   compute   the stage's F/B chain (all tcgen05 GEMMs + stage kernels)
+//   send_act  Split-Concat forward hand-off  (peer copies over NVLink)
+//   send_grad Split-Concat backward hand-off
+//   reduce    per-layer NCCL AllReduce of the replica group + SGD apply
+//
+// Cross-GPU dependencies never involve the host: a sender pushes its rows
+// straight into the receiver's buffer (cudaMemcpyAsync to a CUDA-IPC
+// mapping), then a one-thread kernel stores a sequence number into the
+// receiver's flag word; the receiver's compute stream waits on that word
+// with cuStreamWaitValue32(GEQ).  The whole step is enqueued without a host
+// round trip; the host synchronises once at the end.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dapple.h"
+#include "host/json.hpp"
+#include "kernels/elementwise.h"
+#include "layers.h"
+#include "pipeplan/io.hpp"
+#include "pipeplan/simulator.hpp"
+
+namespace dpl {
+
+int fail(const std::string& what);
+
+namespace {
+
+using json::Value;
+
+#define DPL_CUDA(x)                                                                                   \
+  do {                                                                                                \
+    const cudaError_t cuda_rc_ = (x);                                                                 \
+    if (cuda_rc_ != cudaSuccess) throw std::runtime_error(std::string(#x) + ": " + cudaGetErrorString(cuda_rc_)); \
+  } while (0)
+#define DPL_NCCL(x)                                                                                   \
+  do {                                                                                                \
+    const ncclResult_t nccl_rc_ = (x);                                                                \
+    if (nccl_rc_ != ncclSuccess) throw std::runtime_error(std::string(#x) + ": " + ncclGetErrorString(nccl_rc_)); \
+  } while (0)
+
+typedef CUresult (*StreamValueFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+StreamValueFn wait_value_fn() {
+  static StreamValueFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<StreamValueFn>(p);
+  }();
+  return fn;
+}
+
+__global__ void signal_kernel(uint32_t* flag, uint32_t value) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(value) : "memory");
+}
+
+// Fallback wait if stream memory operations are unavailable.
+__global__ void wait_kernel(const uint32_t* flag, uint32_t value) {
+  uint32_t v;
+  do {
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+  } while (static_cast<int32_t>(v - value) < 0);
+}
+
+__global__ void stamp_kernel(unsigned long long* out) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *out = t;
+}
+
+// A contiguous run of micro-batch rows moved between two replicas of
+// adjacent stages (Split-Concat).  Rows are token rows;
+// offsets are relative to each side's own slice.
+struct Route {
+  int src_rank, dst_rank;
+  long long src_row, dst_row, rows;
+};
+
+// Interval-overlap mapping of a micro-batch of B samples from the r_a even
+// slices of stage a to the r_b even slices of stage b: at most r_a + r_b - 1
+// non-empty flows (the reference's model charges r_a * r_b equal flows,
+// costmodel.cpp:60-69).
+std::vector<Route> split_concat_routes(const pipeplan::Stage& a, const pipeplan::Stage& b, int B, int seq) {
+  const int ra = a.replication(), rb = b.replication();
+  std::vector<Route> out;
+  for (int i = 0; i < ra; ++i) {
+    const long long lo_a = 1LL * i * B / ra, hi_a = 1LL * (i + 1) * B / ra;
+    for (int j = 0; j < rb; ++j) {
+      const long long lo_b = 1LL * j * B / rb, hi_b = 1LL * (j + 1) * B / rb;
+      const long long lo = std::max(lo_a, lo_b), hi = std::min(hi_a, hi_b);
+      if (hi <= lo) continue;
+      out.push_back({a.devices[i], b.devices[j], (lo - lo_a) * seq, (lo - lo_b) * seq, (hi - lo) * seq});
+    }
+  }
+  return out;
+}
+
+struct BlockEvents {
+  cudaEvent_t start = nullptr, end = nullptr;
+};
+
+}  // namespace
+
+class Executor {
+ public:
+  explicit Executor(const Value& cfg, int device);
+  ~Executor();
+
+  size_t export_blob(void* blob, size_t cap);
+  void connect(const uint8_t* blobs, size_t blob_len, int world);
+  void nccl_init(const void* id);
+  void disconnect();
+  float step(const void* host_input, const void* host_target);
+  std::string timeline_json() const;
+  void read_tensor(const std::string& name, bool grad, void* host, size_t bytes);
+  std::string info() const;
+
+ private:
+  // --- configuration
+  ModelSpec spec_;
+  pipeplan::PipelinePlan plan_;
+  int M_ = 1, gbs_ = 1, B_ = 1, rank_ = 0, world_ = 1, device_ = 0;
+  float lr_ = 1e-3f;
+  uint64_t seed_ = 1234;
+  int k_ = 0, S_ = 1, rep_ = 0, r_ = 1, lo_ = 0, hi_ = 1;
+  int phi_ = 1;
+  std::vector<int> phi_expanded_;
+  std::vector<pipeplan::ChainOp> chain_;
+  std::vector<Route> in_routes_, out_routes_;  // activations into / out of this rank
+  long long numel_global_ = 0;
+  bool timeline_ = true;
+  bool apply_ = true;  // false: keep the accumulated gradients (parity reads)
+
+  // --- device state
+  DeviceMemory mem_;
+  StageContext ctx_;
+  std::vector<std::unique_ptr<Layer>> layers_;
+  std::vector<size_t> param_off_;
+  size_t n_params_ = 0;
+  float* w32_ = nullptr;
+  float* g32_ = nullptr;
+  bf16* w16_ = nullptr;
+  std::vector<std::vector<bf16*>> act_;  // [layer-in-stage 1..L-1][slot]
+  std::vector<bf16*> in_;                // stage-0 input per slot
+  std::vector<bf16*> out_;               // stage output per micro-batch
+  std::vector<bf16*> target_, dloss_;    // last stage, per slot
+  std::vector<bf16*> send_grad_;         // first-layer dX per micro-batch (stage > 0)
+  bf16* gbuf_[2] = {nullptr, nullptr};
+  float* loss_acc_ = nullptr;
+  unsigned long long* t0_ = nullptr;
+  // receive region (one cudaMalloc, exported over CUDA IPC):
+  //   [recv_act M x R x H][recv_grad M x R x H][flags: act[world], grad[world]]
+  uint8_t* recv_ = nullptr;
+  size_t recv_bytes_ = 0, recv_grad_off_ = 0, flags_off_ = 0;
+  std::vector<uint8_t*> peer_recv_;  // by rank (IPC-mapped), null if unused
+  std::vector<int> peer_rows_;       // rows per slice of each rank's stage
+
+  cudaStream_t compute_ = nullptr, send_act_ = nullptr, send_grad_s_ = nullptr, reduce_ = nullptr;
+  ncclComm_t comm_ = nullptr;
+  cudaEvent_t ev_begin_ = nullptr, ev_end_ = nullptr, ev_reduce_done_ = nullptr;
+  cudaEvent_t ev_sa_done_ = nullptr, ev_sg_done_ = nullptr;
+  std::vector<BlockEvents> fwd_ev_, bwd_ev_, send_fwd_ev_, send_bwd_ev_;
+  std::vector<cudaEvent_t> layer_done_, fwd_done_, bwd_done_;
+  long long steps_done_ = 0;
+  float last_loss_ = NAN;
+  double flops_per_step_ = 0.0;
+
+  // --- helpers
+  int rows_of_stage(int k) const { return B_ / plan_.stages[k].replication() * spec_.seq; }
+  int L() const { return hi_ - lo_; }
+  bf16* recv_act(int i) const {
+    return reinterpret_cast<bf16*>(recv_) + static_cast<size_t>(i) * ctx_.rows * spec_.hidden;
+  }
+  bf16* recv_grad(int i) const {
+    return reinterpret_cast<bf16*>(recv_ + recv_grad_off_) + static_cast<size_t>(i) * ctx_.rows * spec_.hidden;
+  }
+  uint32_t* flags() const { return reinterpret_cast<uint32_t*>(recv_ + flags_off_); }
+  size_t layout_grad_off(int rows) const;
+  size_t layout_flags_off(int rows) const;
+  void wait_flag(cudaStream_t s, uint32_t* flag, uint32_t value);
+  void signal(cudaStream_t s, uint32_t* remote_flag, uint32_t value);
+  void forward(int i, uint32_t base);
+  void backward(int i, uint32_t base);
+  void record(cudaEvent_t e, cudaStream_t s) { DPL_CUDA(cudaEventRecord(e, s)); }
+};
+
+Executor::Executor(const Value& cfg, int device) : device_(device) {
+  DPL_CUDA(cudaSetDevice(device_));
+  const Value& m = cfg.at("model");
+  spec_.kind = m.at("kind").as_string();
+  spec_.layers = static_cast<int>(m.at("layers").as_int());
+  spec_.hidden = static_cast<int>(m.at("hidden").as_int());
+  if (m.contains("heads")) spec_.heads = static_cast<int>(m.at("heads").as_int());
+  if (m.contains("ffn")) spec_.ffn = static_cast<int>(m.at("ffn").as_int());
+  spec_.seq = m.contains("seq") ? static_cast<int>(m.at("seq").as_int()) : 1;
+  spec_.causal = m.contains("causal") && m.at("causal").as_bool();
+  if (spec_.kind == "mlp") spec_.seq = 1;
+  if (spec_.kind == "gpt") spec_.causal = true;
+
+  plan_ = pipeplan::plan_from_json(cfg.at("plan").is_string() ? cfg.at("plan").as_string() : cfg.at("plan").dump());
+  M_ = static_cast<int>(cfg.at("M").as_int());
+  gbs_ = static_cast<int>(cfg.at("gbs").as_int());
+  rank_ = cfg.contains("rank") ? static_cast<int>(cfg.at("rank").as_int()) : 0;
+  world_ = cfg.contains("world") ? static_cast<int>(cfg.at("world").as_int()) : 1;
+  if (cfg.contains("lr")) lr_ = static_cast<float>(cfg.at("lr").as_double());
+  if (cfg.contains("seed")) seed_ = static_cast<uint64_t>(cfg.at("seed").as_int());
+  if (cfg.contains("timeline")) timeline_ = cfg.at("timeline").as_bool();
+  if (cfg.contains("apply")) apply_ = cfg.at("apply").as_bool();
+  if (M_ < 1 || gbs_ % M_ != 0) throw std::invalid_argument("dpl exec: GBS must be a multiple of M");
+  B_ = gbs_ / M_;
+
+  // plan checks: contiguous cover of the model's layers, disjoint devices
+  S_ = plan_.compute_stage_count();
+  if (S_ < 1) throw std::invalid_argument("dpl exec: empty plan");
+  int expect = 0;
+  k_ = -1;
+  for (int k = 0; k < S_; ++k) {
+    const pipeplan::Stage& st = plan_.stages[k];
+    if (st.layer_lo != expect || st.layer_hi <= st.layer_lo)
+      throw std::invalid_argument("dpl exec: plan stages must partition the layers");
+    expect = st.layer_hi;
+    if (B_ % st.replication() != 0)
+      throw std::invalid_argument("dpl exec: micro-batch of " + std::to_string(B_) + " samples does not split evenly over " +
+                                  std::to_string(st.replication()) + " replicas (PAPER.md:1222-1231)");
+    for (size_t j = 0; j < st.devices.size(); ++j) {
+      if (st.devices[j] >= world_) throw std::invalid_argument("dpl exec: plan uses GPU ids beyond the world size");
+      if (st.devices[j] == rank_) {
+        k_ = k;
+        rep_ = static_cast<int>(j);
+      }
+    }
+  }
+  if (expect != spec_.layers) throw std::invalid_argument("dpl exec: plan does not cover the model's layers");
+  if (k_ < 0) throw std::invalid_argument("dpl exec: rank " + std::to_string(rank_) + " has no stage in the plan");
+  const pipeplan::Stage& mine = plan_.stages[k_];
+  r_ = mine.replication();
+  lo_ = mine.layer_lo;
+  hi_ = mine.layer_hi;
+
+  // phi resolution, planner.cpp:501-508 (preset A is cost-independent)
+  const int Se = 2 * S_ - 1;
+  if (static_cast<int>(plan_.phi_expanded.size()) == Se) {
+    phi_expanded_ = plan_.phi_expanded;
+  } else if (!plan_.phi.empty()) {
+    phi_expanded_ = pipeplan::expand_plan_phi(plan_.phi);
+  } else {
+    phi_expanded_.resize(Se);
+    for (int x = 0; x < Se; ++x) phi_expanded_[x] = std::min(Se - x, M_);
+  }
+  phi_ = std::min(phi_expanded_[2 * k_], M_);
+  chain_ = pipeplan::stage_chain(M_, phi_, pipeplan::ScheduleKind::dapple);
+
+  if (k_ > 0) {
+    for (const Route& r : split_concat_routes(plan_.stages[k_ - 1], mine, B_, spec_.seq))
+      if (r.dst_rank == rank_) in_routes_.push_back(r);
+  }
+  if (k_ + 1 < S_) {
+    for (const Route& r : split_concat_routes(mine, plan_.stages[k_ + 1], B_, spec_.seq))
+      if (r.src_rank == rank_) out_routes_.push_back(r);
+  }
+  numel_global_ = 1LL * gbs_ * spec_.seq * spec_.hidden;
+
+  // --- context, layers, parameters
+  ctx_.spec = spec_;
+  ctx_.samples = B_ / r_;
+  ctx_.rows = ctx_.samples * spec_.seq;
+  ctx_.slots = phi_;
+  ctx_.mem = &mem_;
+  DPL_CUDA(cudaStreamCreateWithFlags(&compute_, cudaStreamNonBlocking));
+  mem_.set_stream(compute_);
+  DPL_CUDA(cudaStreamCreateWithFlags(&send_act_, cudaStreamNonBlocking));
+  DPL_CUDA(cudaStreamCreateWithFlags(&send_grad_s_, cudaStreamNonBlocking));
+  DPL_CUDA(cudaStreamCreateWithFlags(&reduce_, cudaStreamNonBlocking));
+  ctx_.stream = compute_;
+
+  for (int l = lo_; l < hi_; ++l) layers_.push_back(make_layer(spec_, l));
+  for (auto& layer : layers_) {
+    param_off_.push_back(n_params_);
+    n_params_ += (layer->param_count() + 63) / 64 * 64;  // keep every layer 256B aligned
+  }
+  w32_ = static_cast<float*>(mem_.alloc(n_params_ * 4));
+  g32_ = static_cast<float*>(mem_.alloc(n_params_ * 4));
+  w16_ = static_cast<bf16*>(mem_.alloc(n_params_ * 2));
+  for (size_t li = 0; li < layers_.size(); ++li)
+    layers_[li]->bind(w32_ + param_off_[li], g32_ + param_off_[li], w16_ + param_off_[li], seed_, compute_);
+
+  const size_t RH = static_cast<size_t>(ctx_.rows) * spec_.hidden;
+  if (spec_.kind != "mlp") {
+    const size_t z = static_cast<size_t>(spec_.heads) * ctx_.samples;
+    const size_t ss = static_cast<size_t>(spec_.seq) * spec_.seq;
+    ctx_.scores = static_cast<float*>(mem_.alloc(z * ss * 4));
+    ctx_.dscores = static_cast<bf16*>(mem_.alloc(z * ss * 2));
+    ctx_.t_h = static_cast<bf16*>(mem_.alloc(RH * 2));
+    ctx_.t_h2 = static_cast<bf16*>(mem_.alloc(RH * 2));
+    ctx_.t_h3 = static_cast<bf16*>(mem_.alloc(RH * 2));
+    ctx_.t_qkv = static_cast<bf16*>(mem_.alloc(RH * 3 * 2));
+    ctx_.t_f = static_cast<bf16*>(mem_.alloc(static_cast<size_t>(ctx_.rows) * spec_.ffn * 2));
+  }
+  for (auto& layer : layers_) layer->alloc_stash(ctx_);
+  act_.assign(L(), {});
+  for (int li = 1; li < L(); ++li)
+    for (int s = 0; s < phi_; ++s) act_[li].push_back(static_cast<bf16*>(mem_.alloc(RH * 2)));
+  if (k_ == 0)
+    for (int s = 0; s < phi_; ++s) in_.push_back(static_cast<bf16*>(mem_.alloc(RH * 2)));
+  for (int i = 0; i < M_; ++i) out_.push_back(static_cast<bf16*>(mem_.alloc(RH * 2)));
+  if (k_ == S_ - 1) {
+    for (int s = 0; s < phi_; ++s) {
+      target_.push_back(static_cast<bf16*>(mem_.alloc(RH * 2)));
+      dloss_.push_back(static_cast<bf16*>(mem_.alloc(RH * 2)));
+    }
+  }
+  if (k_ > 0)
+    for (int i = 0; i < M_; ++i) send_grad_.push_back(static_cast<bf16*>(mem_.alloc(RH * 2)));
+  gbuf_[0] = static_cast<bf16*>(mem_.alloc(RH * 2));
+  gbuf_[1] = static_cast<bf16*>(mem_.alloc(RH * 2));
+  loss_acc_ = static_cast<float*>(mem_.alloc(4));
+  t0_ = static_cast<unsigned long long*>(mem_.alloc(8));
+
+  // receive region: one allocation so a single IPC handle covers it
+  recv_grad_off_ = layout_grad_off(ctx_.rows);
+  flags_off_ = layout_flags_off(ctx_.rows);
+  recv_bytes_ = flags_off_ + 2 * static_cast<size_t>(world_) * 4;
+  recv_ = static_cast<uint8_t*>(mem_.alloc(recv_bytes_));
+  peer_recv_.assign(world_, nullptr);
+  peer_rows_.assign(world_, 0);
+  for (int k = 0; k < S_; ++k)
+    for (int d : plan_.stages[k].devices) peer_rows_[d] = rows_of_stage(k);
+
+  // events
+  auto mk = [](cudaEvent_t* e) { DPL_CUDA(cudaEventCreate(e)); };
+  auto mk_nt = [](cudaEvent_t* e) { DPL_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming)); };
+  mk(&ev_begin_);
+  mk(&ev_end_);
+  mk_nt(&ev_reduce_done_);
+  mk_nt(&ev_sa_done_);
+  mk_nt(&ev_sg_done_);
+  fwd_ev_.resize(M_);
+  bwd_ev_.resize(M_);
+  send_fwd_ev_.resize(M_);
+  send_bwd_ev_.resize(M_);
+  for (auto* v : {&fwd_ev_, &bwd_ev_, &send_fwd_ev_, &send_bwd_ev_})
+    for (BlockEvents& b : *v) {
+      mk(&b.start);
+      mk(&b.end);
+    }
+  layer_done_.resize(L());
+  for (auto& e : layer_done_) mk_nt(&e);
+  fwd_done_.resize(M_);
+  bwd_done_.resize(M_);
+  for (auto& e : fwd_done_) mk_nt(&e);
+  for (auto& e : bwd_done_) mk_nt(&e);
+
+  for (size_t li = 0; li < layers_.size(); ++li) {
+    const bool need_dx = !(k_ == 0 && li == 0);
+    flops_per_step_ += M_ * (layers_[li]->flops_fwd(ctx_) + layers_[li]->flops_bwd(ctx_, need_dx));
+  }
+  // parameters initialised and every buffer (incl. the IPC-exported flags)
+  // zeroed before any peer can see this rank
+  DPL_CUDA(cudaDeviceSynchronize());
+}
+
+size_t Executor::layout_grad_off(int rows) const {
+  const size_t bytes = static_cast<size_t>(M_) * rows * spec_.hidden * 2;
+  return (bytes + 255) & ~size_t(255);
+}
+size_t Executor::layout_flags_off(int rows) const { return 2 * layout_grad_off(rows); }
+
+// Teardown is two-phase across ranks: every rank first unmaps its peers'
+// regions and destroys its communicator (disconnect), the ranks barrier, and
+// only then free memory -- freeing an exported region while another process
+// still has it mapped is undefined behaviour in CUDA IPC.
+void Executor::disconnect() {
+  cudaSetDevice(device_);
+  cudaDeviceSynchronize();
+  if (comm_) {
+    ncclCommDestroy(comm_);
+    comm_ = nullptr;
+  }
+  for (uint8_t*& p : peer_recv_) {
+    if (p) cudaIpcCloseMemHandle(p);
+    p = nullptr;
+  }
+}
+
+Executor::~Executor() {
+  disconnect();
+  for (cudaStream_t s : {compute_, send_act_, send_grad_s_, reduce_})
+    if (s) cudaStreamDestroy(s);
+}
+
+size_t Executor::export_blob(void* blob, size_t cap) {
+  cudaIpcMemHandle_t h;
+  DPL_CUDA(cudaIpcGetMemHandle(&h, recv_));
+  if (cap < sizeof h) throw std::invalid_argument("dpl exec: export buffer too small");
+  std::memcpy(blob, &h, sizeof h);
+  return sizeof h;
+}
+
+void Executor::connect(const uint8_t* blobs, size_t blob_len, int world) {
+  if (world != world_) throw std::invalid_argument("dpl exec: world size mismatch");
+  std::vector<int> peers;
+  for (const Route& r : out_routes_) peers.push_back(r.dst_rank);
+  for (const Route& r : in_routes_) peers.push_back(r.src_rank);
+  for (int p : peers) {
+    if (p == rank_ || peer_recv_[p]) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, blobs + static_cast<size_t>(p) * blob_len, sizeof h);
+    void* ptr = nullptr;
+    DPL_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    peer_recv_[p] = static_cast<uint8_t*>(ptr);
+  }
+}
+
+void Executor::nccl_init(const void* id) {
+  if (r_ == 1) return;
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof uid);
+  DPL_NCCL(ncclCommInitRank(&comm_, r_, uid, rep_));
+}
+
+void Executor::wait_flag(cudaStream_t s, uint32_t* flag, uint32_t value) {
+  if (StreamValueFn fn = wait_value_fn()) {
+    const CUresult rc = fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flag), value, 0x0 /*GEQ*/);
+    if (rc == CUDA_SUCCESS) return;
+  }
+  wait_kernel<<<1, 1, 0, s>>>(flag, value);
+}
+
+void Executor::signal(cudaStream_t s, uint32_t* remote_flag, uint32_t value) {
+  signal_kernel<<<1, 1, 0, s>>>(remote_flag, value);
+}
+
+void Executor::forward(int i, uint32_t base) {
+  const int slot = i % phi_;
+  const size_t H = spec_.hidden;
+  const bf16* x;
+  if (k_ == 0) {
+    x = in_[slot];
+  } else {
+    for (const Route& r : in_routes_) wait_flag(compute_, flags() + r.src_rank, base + i + 1);
+    x = recv_act(i);
+  }
+  record(fwd_ev_[i].start, compute_);
+  for (int li = 0; li < L(); ++li) {
+    bf16* y = li + 1 < L() ? act_[li + 1][slot] : out_[i];
+    layers_[li]->forward(ctx_, slot, x, y);
+    x = y;
+  }
+  if (k_ == S_ - 1) {
+    // MSE over the whole global batch: loss = sum (y-t)^2 / numel, dY = 2 (y-t) / numel
+    mse_loss(out_[i], target_[slot], dloss_[slot], loss_acc_, static_cast<long long>(ctx_.rows) * H,
+             2.0f / static_cast<float>(numel_global_), compute_);
+  }
+  record(fwd_ev_[i].end, compute_);
+  if (!out_routes_.empty()) {
+    DPL_CUDA(cudaEventRecord(fwd_done_[i], compute_));
+    DPL_CUDA(cudaStreamWaitEvent(send_act_, fwd_done_[i], 0));
+    record(send_fwd_ev_[i].start, send_act_);
+    for (const Route& r : out_routes_) {
+      uint8_t* peer = peer_recv_[r.dst_rank];
+      const int rows_dst = peer_rows_[r.dst_rank];
+      bf16* dst = reinterpret_cast<bf16*>(peer) + (static_cast<size_t>(i) * rows_dst + r.dst_row) * H;
+      DPL_CUDA(cudaMemcpyAsync(dst, out_[i] + r.src_row * H, r.rows * H * 2, cudaMemcpyDeviceToDevice, send_act_));
+      uint32_t* flag = reinterpret_cast<uint32_t*>(peer + layout_flags_off(rows_dst)) + rank_;
+      signal(send_act_, flag, base + i + 1);
+    }
+    record(send_fwd_ev_[i].end, send_act_);
+  }
+}
+
+void Executor::backward(int i, uint32_t base) {
+  const int slot = i % phi_;
+  const size_t H = spec_.hidden;
+  const bf16* dy;
+  if (k_ == S_ - 1) {
+    dy = dloss_[slot];
+  } else {
+    for (const Route& r : out_routes_) wait_flag(compute_, flags() + world_ + r.dst_rank, base + i + 1);
+    dy = recv_grad(i);
+  }
+  record(bwd_ev_[i].start, compute_);
+  const bool last_mb = i == M_ - 1;
+  int pp = 0;
+  for (int li = L() - 1; li >= 0; --li) {
+    const bf16* x = li > 0 ? act_[li][slot] : (k_ == 0 ? in_[slot] : recv_act(i));
+    bf16* dx = nullptr;
+    if (li > 0) {
+      dx = gbuf_[pp];
+      pp ^= 1;
+    } else if (k_ > 0) {
+      dx = send_grad_[i];
+    }
+    layers_[li]->backward(ctx_, slot, x, dy, dx);
+    dy = dx;
+    if (last_mb) {
+      // this layer's gradients are final: AllReduce over the replica group
+      // and apply while the remaining layers' backward runs
+      DPL_CUDA(cudaEventRecord(layer_done_[li], compute_));
+      DPL_CUDA(cudaStreamWaitEvent(reduce_, layer_done_[li], 0));
+      const size_t off = param_off_[li];
+      const size_t n = layers_[li]->param_count();
+      if (comm_) DPL_NCCL(ncclAllReduce(g32_ + off, g32_ + off, n, ncclFloat, ncclSum, comm_, reduce_));
+      if (apply_) sgd_apply(w32_ + off, g32_ + off, w16_ + off, static_cast<long long>(n), lr_, reduce_);
+    }
+  }
+  record(bwd_ev_[i].end, compute_);
+  if (k_ > 0) {
+    DPL_CUDA(cudaEventRecord(bwd_done_[i], compute_));
+    DPL_CUDA(cudaStreamWaitEvent(send_grad_s_, bwd_done_[i], 0));
+    record(send_bwd_ev_[i].start, send_grad_s_);
+    for (const Route& r : in_routes_) {
+      uint8_t* peer = peer_recv_[r.src_rank];
+      const int rows_src = peer_rows_[r.src_rank];
+      bf16* dst = reinterpret_cast<bf16*>(peer + layout_grad_off(rows_src)) +
+                  (static_cast<size_t>(i) * rows_src + r.src_row) * H;
+      DPL_CUDA(cudaMemcpyAsync(dst, send_grad_[i] + r.dst_row * H, r.rows * H * 2, cudaMemcpyDeviceToDevice,
+                               send_grad_s_));
+      uint32_t* flag = reinterpret_cast<uint32_t*>(peer + layout_flags_off(rows_src)) + world_ + rank_;
+      signal(send_grad_s_, flag, base + i + 1);
+    }
+    record(send_bwd_ev_[i].end, send_grad_s_);
+  }
+}
+
+float Executor::step(const void* host_input, const void* host_target) {
+  DPL_CUDA(cudaSetDevice(device_));
+  const uint32_t base = static_cast<uint32_t>(steps_done_ * M_);
+  const size_t H = spec_.hidden;
+  const size_t RH = static_cast<size_t>(ctx_.rows) * H;
+  stamp_kernel<<<1, 1, 0, compute_>>>(t0_);
+  DPL_CUDA(cudaEventRecord(ev_begin_, compute_));
+  DPL_CUDA(cudaMemsetAsync(loss_acc_, 0, 4, compute_));
+
+  // sample rows [row0, row0 + samples) of micro-batch i owned by this replica
+  const long long slice_first = 1LL * rep_ * (B_ / r_);
+  for (const pipeplan::ChainOp& op : chain_) {
+    const int i = op.micro_batch;
+    const int slot = i % phi_;
+    if (op.kind == pipeplan::BlockKind::forward) {
+      const long long sample0 = 1LL * i * B_ + slice_first;
+      const long long idx0 = sample0 * spec_.seq * static_cast<long long>(H);
+      if (k_ == 0) {
+        if (host_input) {
+          DPL_CUDA(cudaMemcpyAsync(in_[slot], static_cast<const bf16*>(host_input) + static_cast<size_t>(i) * RH,
+                                   RH * 2, cudaMemcpyHostToDevice, compute_));
+        } else {
+          fill_uniform_bf16(in_[slot], static_cast<long long>(RH), seed_, kTensorInput, idx0, 1.0f, compute_);
+        }
+      }
+      if (k_ == S_ - 1) {
+        if (host_target) {
+          DPL_CUDA(cudaMemcpyAsync(target_[slot], static_cast<const bf16*>(host_target) + static_cast<size_t>(i) * RH,
+                                   RH * 2, cudaMemcpyHostToDevice, compute_));
+        } else {
+          fill_uniform_bf16(target_[slot], static_cast<long long>(RH), seed_, kTensorTarget, idx0, 1.0f, compute_);
+        }
+      }
+      forward(i, base);
+    } else {
+      backward(i, base);
+    }
+  }
+  if (k_ == S_ - 1 && comm_) {
+    DPL_CUDA(cudaStreamWaitEvent(reduce_, bwd_ev_[M_ - 1].end, 0));
+    DPL_NCCL(ncclAllReduce(loss_acc_, loss_acc_, 1, ncclFloat, ncclSum, comm_, reduce_));
+  }
+  DPL_CUDA(cudaEventRecord(ev_reduce_done_, reduce_));
+  DPL_CUDA(cudaEventRecord(ev_sa_done_, send_act_));
+  DPL_CUDA(cudaEventRecord(ev_sg_done_, send_grad_s_));
+  DPL_CUDA(cudaStreamWaitEvent(compute_, ev_reduce_done_, 0));
+  DPL_CUDA(cudaStreamWaitEvent(compute_, ev_sa_done_, 0));
+  DPL_CUDA(cudaStreamWaitEvent(compute_, ev_sg_done_, 0));
+  DPL_CUDA(cudaEventRecord(ev_end_, compute_));
+  float loss = NAN;
+  if (k_ == S_ - 1) {
+    DPL_CUDA(cudaMemcpyAsync(&loss, loss_acc_, 4, cudaMemcpyDeviceToHost, compute_));
+  }
+  DPL_CUDA(cudaStreamSynchronize(compute_));
+  DPL_CUDA(cudaGetLastError());
+  ++steps_done_;
+  if (k_ == S_ - 1) loss = loss / static_cast<float>(numel_global_);
+  last_loss_ = loss;
+  return loss;
+}
+
+std::string Executor::timeline_json() const {
+  auto ms = [&](cudaEvent_t e) {
+    float v = 0.f;
+    if (cudaEventElapsedTime(&v, ev_begin_, e) != cudaSuccess) {
+      cudaGetLastError();
+      return -1.0;
+    }
+    return static_cast<double>(v) * 1e-3;
+  };
+  unsigned long long t0 = 0;
+  cudaMemcpy(&t0, t0_, 8, cudaMemcpyDeviceToHost);
+  Value out = Value::object();
+  out["rank"] = rank_;
+  out["stage"] = k_;
+  out["replica"] = rep_;
+  out["expanded_stage"] = 2 * k_;
+  out["M"] = M_;
+  out["phi"] = phi_;
+  out["t0_ns"] = static_cast<long long>(t0);
+  out["step_s"] = ms(ev_end_);
+  out["flops"] = flops_per_step_;
+  Value blocks = Value::array();
+  auto add = [&](int stage, int mb, int kind, const BlockEvents& b) {
+    Value row = Value::array();
+    row.push_back(stage);
+    row.push_back(mb);
+    row.push_back(kind);
+    row.push_back(ms(b.start));
+    row.push_back(ms(b.end));
+    blocks.push_back(std::move(row));
+  };
+  for (int i = 0; i < M_; ++i) add(2 * k_, i, 0, fwd_ev_[i]);
+  for (int i = 0; i < M_; ++i) add(2 * k_, i, 1, bwd_ev_[i]);
+  if (!out_routes_.empty())
+    for (int i = 0; i < M_; ++i) add(2 * k_ + 1, i, 0, send_fwd_ev_[i]);
+  if (k_ > 0)
+    for (int i = 0; i < M_; ++i) add(2 * k_ - 1, i, 1, send_bwd_ev_[i]);
+  out["blocks"] = std::move(blocks);
+  return out.dump();
+}
+
+void Executor::read_tensor(const std::string& name, bool grad, void* host, size_t bytes) {
+  // name = "<global layer>.<tensor>" ; only layers of this stage are readable
+  const size_t dot = name.find('.');
+  if (dot == std::string::npos) throw std::invalid_argument("dpl exec: tensor name must be <layer>.<name>");
+  const int layer = std::stoi(name.substr(0, dot));
+  const std::string t = name.substr(dot + 1);
+  if (layer < lo_ || layer >= hi_) throw std::out_of_range("dpl exec: layer not on this stage");
+  const int li = layer - lo_;
+  for (const Layer::Named& n : layers_[li]->tensors()) {
+    if (n.name != t) continue;
+    if (bytes != n.count * 4) throw std::invalid_argument("dpl exec: size mismatch for " + name);
+    const float* src = (grad ? g32_ : w32_) + param_off_[li] + n.offset;
+    DPL_CUDA(cudaSetDevice(device_));
+    DPL_CUDA(cudaDeviceSynchronize());
+    DPL_CUDA(cudaMemcpy(host, src, bytes, cudaMemcpyDeviceToHost));
+    return;
+  }
+  throw std::invalid_argument("dpl exec: unknown tensor " + name);
+}
+
+std::string Executor::info() const {
+  Value v = Value::object();
+  v["rank"] = rank_;
+  v["stage"] = k_;
+  v["replica"] = rep_;
+  v["replication"] = r_;
+  v["layers"] = std::vector<int>{lo_, hi_};
+  v["phi"] = phi_;
+  v["phi_expanded"] = phi_expanded_;
+  v["rows"] = ctx_.rows;
+  v["micro_batch_samples"] = B_;
+  v["params"] = static_cast<long long>(n_params_);
+  v["device_bytes"] = static_cast<long long>(mem_.total());
+  v["flops_per_step"] = flops_per_step_;
+  v["gemm_plans"] = static_cast<long long>(ctx_.gemms.size());
+  Value chain = Value::array();
+  for (const auto& c : chain_) chain.push_back(std::string(c.kind == pipeplan::BlockKind::forward ? "F" : "B") +
+                                               std::to_string(c.micro_batch));
+  v["chain"] = std::move(chain);
+  Value routes = Value::array();
+  for (const auto* list : {&in_routes_, &out_routes_})
+    for (const Route& r : *list) {
+      Value e = Value::array();
+      e.push_back(r.src_rank);
+      e.push_back(r.dst_rank);
+      e.push_back(r.src_row);
+      e.push_back(r.dst_row);
+      e.push_back(r.rows);
+      routes.push_back(std::move(e));
+    }
+  v["routes"] = std::move(routes);
+  return v.dump();
+}
+
+}  // namespace dpl
+
+// ------------------------------------------------------------------ C-ABI
+struct dpl_exec {
+  std::unique_ptr<dpl::Executor> impl;
+  std::string reply;
+};
+
+namespace {
+template <typename F>
+int exec_guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    return dpl::fail(e.what());
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int dpl_exec_create(const char* config_json, int device, dpl_exec** out) {
+  return exec_guard([&] {
+    auto ex = std::make_unique<dpl_exec>();
+    ex->impl = std::make_unique<dpl::Executor>(dpl::json::Value::parse(config_json), device);
+    *out = ex.release();
+  });
+}
+
+int dpl_exec_export(dpl_exec* ex, void* blob, size_t cap, size_t* len) {
+  return exec_guard([&] { *len = ex->impl->export_blob(blob, cap); });
+}
+
+int dpl_exec_connect(dpl_exec* ex, const void* blobs, size_t blob_len, int world) {
+  return exec_guard([&] { ex->impl->connect(static_cast<const uint8_t*>(blobs), blob_len, world); });
+}
+
+int dpl_exec_nccl_id(void* id128) {
+  return exec_guard([&] {
+    ncclUniqueId id;
+    DPL_NCCL(ncclGetUniqueId(&id));
+    std::memcpy(id128, &id, sizeof id);
+  });
+}
+
+int dpl_exec_nccl_init(dpl_exec* ex, const void* id128) {
+  return exec_guard([&] { ex->impl->nccl_init(id128); });
+}
+
+int dpl_exec_step(dpl_exec* ex, const void* host_input, const void* host_target, float* loss) {
+  return exec_guard([&] {
+    const float l = ex->impl->step(host_input, host_target);
+    if (loss) *loss = l;
+  });
+}
+
+const char* dpl_exec_timeline(dpl_exec* ex) {
+  try {
+    ex->reply = ex->impl->timeline_json();
+  } catch (const std::exception& e) {
+    ex->reply = std::string("{\"error\":\"") + e.what() + "\"}";
+  }
+  return ex->reply.c_str();
+}
+
+int dpl_exec_read_tensor(dpl_exec* ex, const char* name, int grad, void* host, size_t bytes) {
+  return exec_guard([&] { ex->impl->read_tensor(name, grad != 0, host, bytes); });
+}
+
+int dpl_exec_info(dpl_exec* ex, char* buf, size_t cap) {
+  return exec_guard([&] {
+    const std::string s = ex->impl->info();
+    if (s.size() + 1 > cap) throw std::invalid_argument("dpl exec: info buffer too small");
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
+}
+
+int dpl_exec_disconnect(dpl_exec* ex) {
+  return exec_guard([&] { ex->impl->disconnect(); });
+}
+
+void dpl_exec_destroy(dpl_exec* ex) { delete ex; }
+
+}  // extern "C"

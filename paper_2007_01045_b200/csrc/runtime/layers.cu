@@ -1,0 +1,381 @@
+// Layer programs (see layers.h).  Every matrix product is the tcgen05 GEMM;
+// bias, residual, GELU / ReLU and their derivatives, fp32 micro-batch
+// gradient accumulation and the attention head split / merge all live in the
+// GEMM epilogues, so the only non-GEMM kernels are LayerNorm, softmax and
+// the bias-gradient column sums.
+#include <cmath>
+#include <stdexcept>
+
+#include "kernels/elementwise.h"
+#include "layers.h"
+
+namespace dpl {
+
+DeviceMemory::~DeviceMemory() {
+  cudaDeviceSynchronize();
+  for (void* p : blocks_) cudaFree(p);
+}
+
+void* DeviceMemory::alloc(size_t bytes) {
+  if (bytes == 0) bytes = 256;
+  bytes = (bytes + 255) & ~size_t(255);
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    throw std::runtime_error("dpl: cudaMalloc of " + std::to_string(bytes) + " bytes failed");
+  }
+  // zero on a stream the executor orders against (it synchronises the
+  // device before any other work), never on the legacy default stream
+  if (cudaMemsetAsync(p, 0, bytes, stream_) != cudaSuccess) throw std::runtime_error("dpl: cudaMemsetAsync failed");
+  blocks_.push_back(p);
+  total_ += bytes;
+  return p;
+}
+
+namespace {
+
+template <typename T>
+T* alloc_n(StageContext& ctx, size_t n) {
+  return static_cast<T*>(ctx.mem->alloc(n * sizeof(T)));
+}
+
+GemmDesc plain(int M, int N, int K, const void* A, long long lda, bool a_mn, const void* B, long long ldb, bool b_mn,
+               void* C, long long ldc, uint32_t epi) {
+  GemmDesc d;
+  d.M = M;
+  d.N = N;
+  d.K = K;
+  d.A = A;
+  d.lda = lda;
+  d.a_mn_major = a_mn;
+  d.B = B;
+  d.ldb = ldb;
+  d.b_mn_major = b_mn;
+  d.C = C;
+  d.ldc = ldc;
+  d.s_zo = static_cast<long long>(M) * ldc;
+  d.epi = epi;
+  return d;
+}
+
+struct ParamInit {
+  size_t offset;
+  size_t count;
+  int tid;
+  float scale;  // U(-scale, scale); NaN = constant 1 (LayerNorm gamma)
+};
+
+void init_params(const std::vector<ParamInit>& plan, int layer, float* w32, bf16* w16, size_t total, uint64_t seed,
+                 cudaStream_t s) {
+  for (const ParamInit& p : plan) {
+    if (std::isnan(p.scale)) {
+      fill_const_f32(w32 + p.offset, static_cast<long long>(p.count), 1.0f, s);
+    } else {
+      fill_uniform_f32(w32 + p.offset, static_cast<long long>(p.count), seed, param_tensor_id(layer, p.tid), 0,
+                       p.scale, s);
+    }
+  }
+  cast_f32_bf16(w32, w16, static_cast<long long>(total), s);
+}
+
+// ------------------------------------------------------------------ MLP
+// y = relu(x W^T + b) (no ReLU on the model's last layer); W [H][H].
+class MlpLayer final : public Layer {
+ public:
+  MlpLayer(const ModelSpec& spec, int index)
+      : h_(spec.hidden), index_(index), relu_(index != spec.layers - 1), in_relu_(index > 0) {}
+
+  size_t param_count() const override { return static_cast<size_t>(h_) * h_ + h_; }
+
+  void bind(float* w32, float* g32, bf16* w16, uint64_t seed, cudaStream_t s) override {
+    w32_ = w32;
+    g32_ = g32;
+    w16_ = w16;
+    const size_t hh = static_cast<size_t>(h_) * h_;
+    init_params({{0, hh, 0, std::sqrt(6.0f / h_)}, {hh, static_cast<size_t>(h_), 1, 0.05f}}, index_, w32, w16,
+                param_count(), seed, s);
+  }
+
+  void alloc_stash(StageContext&) override {}
+
+  void forward(StageContext& ctx, int, const bf16* x, bf16* y) override {
+    GemmDesc d = plain(ctx.rows, h_, h_, x, h_, false, w16_, h_, false, y, h_, kBias | (relu_ ? kRelu : 0u));
+    d.bias = bias32();
+    ctx.gemms.run(d, ctx.stream);
+  }
+
+  void backward(StageContext& ctx, int, const bf16* x, const bf16* dz, bf16* dx) override {
+    const int R = ctx.rows;
+    // dW += dZ^T X  (both operands read transposed from their row-major forms)
+    ctx.gemms.run(plain(h_, h_, R, dz, h_, true, x, h_, true, g32_, h_, kOutF32Acc), ctx.stream);
+    colsum_acc(dz, g32_ + static_cast<size_t>(h_) * h_, R, h_, ctx.stream);
+    if (dx) {
+      // dX = dZ W, with the previous layer's relu'(x) fused in the epilogue
+      GemmDesc d = plain(R, h_, h_, dz, h_, false, w16_, h_, true, dx, h_, in_relu_ ? kDRelu : 0u);
+      d.aux_in = x;
+      ctx.gemms.run(d, ctx.stream);
+    }
+  }
+
+  double flops_fwd(const StageContext& ctx) const override { return 2.0 * ctx.rows * h_ * h_; }
+  double flops_bwd(const StageContext& ctx, bool need_dx) const override {
+    return (need_dx ? 4.0 : 2.0) * ctx.rows * h_ * h_;
+  }
+  std::vector<Named> tensors() const override {
+    return {{"W", 0, static_cast<size_t>(h_) * h_}, {"b", static_cast<size_t>(h_) * h_, static_cast<size_t>(h_)}};
+  }
+
+ private:
+  const float* bias32() const { return w32_ + static_cast<size_t>(h_) * h_; }
+  int h_, index_;
+  bool relu_, in_relu_;
+  float* w32_ = nullptr;
+  float* g32_ = nullptr;
+  bf16* w16_ = nullptr;
+};
+
+// ------------------------------------------------------------------ transformer
+// Pre-LN block:  h = x + Wo·attn(LN1 x) + bo ;  y = h + W2·gelu(W1·LN2 h + b1) + b2
+class TransformerLayer final : public Layer {
+ public:
+  TransformerLayer(const ModelSpec& spec, int index)
+      : H_(spec.hidden), F_(spec.ffn), nh_(spec.heads), d_(spec.hidden / spec.heads), causal_(spec.causal),
+        eps_(spec.ln_eps), index_(index) {
+    if (H_ % nh_ != 0 || d_ % 32 != 0) throw std::invalid_argument("dpl: head dim must be a multiple of 32");
+    size_t o = 0;
+    auto add = [&](size_t n) {
+      const size_t at = o;
+      o += n;
+      return at;
+    };
+    ln1g_ = add(H_);
+    ln1b_ = add(H_);
+    wqkv_ = add(3ull * H_ * H_);
+    bqkv_ = add(3ull * H_);
+    wo_ = add(1ull * H_ * H_);
+    bo_ = add(H_);
+    ln2g_ = add(H_);
+    ln2b_ = add(H_);
+    w1_ = add(1ull * F_ * H_);
+    b1_ = add(F_);
+    w2_ = add(1ull * H_ * F_);
+    b2_ = add(H_);
+    total_ = o;
+  }
+
+  size_t param_count() const override { return total_; }
+
+  void bind(float* w32, float* g32, bf16* w16, uint64_t seed, cudaStream_t s) override {
+    w32_ = w32;
+    g32_ = g32;
+    w16_ = w16;
+    const float nan = std::nanf("");
+    const float sh = 1.0f / std::sqrt(static_cast<float>(H_));
+    const float sf = 1.0f / std::sqrt(static_cast<float>(F_));
+    init_params({{ln1g_, size_t(H_), 0, nan},
+                 {ln1b_, size_t(H_), 1, 0.0f},
+                 {wqkv_, 3ull * H_ * H_, 2, sh},
+                 {bqkv_, 3ull * H_, 3, 0.02f},
+                 {wo_, 1ull * H_ * H_, 4, sh},
+                 {bo_, size_t(H_), 5, 0.02f},
+                 {ln2g_, size_t(H_), 6, nan},
+                 {ln2b_, size_t(H_), 7, 0.0f},
+                 {w1_, 1ull * F_ * H_, 8, sh},
+                 {b1_, size_t(F_), 9, 0.02f},
+                 {w2_, 1ull * H_ * F_, 10, sf},
+                 {b2_, size_t(H_), 11, 0.02f}},
+                index_, w32, w16, total_, seed, s);
+  }
+
+  void alloc_stash(StageContext& ctx) override {
+    const size_t R = ctx.rows;
+    const size_t z = static_cast<size_t>(nh_) * ctx.samples;
+    const size_t ss = static_cast<size_t>(ctx.spec.seq) * ctx.spec.seq;
+    stash_.resize(ctx.slots);
+    for (Stash& st : stash_) {
+      st.ln1 = alloc_n<bf16>(ctx, R * H_);
+      st.mean1 = alloc_n<float>(ctx, R);
+      st.rstd1 = alloc_n<float>(ctx, R);
+      st.qkv = alloc_n<bf16>(ctx, 3 * R * H_);
+      st.P = alloc_n<bf16>(ctx, z * ss);
+      st.ctx = alloc_n<bf16>(ctx, R * H_);
+      st.h = alloc_n<bf16>(ctx, R * H_);
+      st.ln2 = alloc_n<bf16>(ctx, R * H_);
+      st.mean2 = alloc_n<float>(ctx, R);
+      st.rstd2 = alloc_n<float>(ctx, R);
+      st.z1 = alloc_n<bf16>(ctx, R * F_);
+      st.g = alloc_n<bf16>(ctx, R * F_);
+    }
+  }
+
+  void forward(StageContext& ctx, int slot, const bf16* x, bf16* y) override {
+    Stash& st = stash_[slot];
+    const int R = ctx.rows, s = ctx.spec.seq, b = ctx.samples, z = nh_ * b;
+    cudaStream_t str = ctx.stream;
+    layernorm_fwd(x, w32_ + ln1g_, w32_ + ln1b_, st.ln1, st.mean1, st.rstd1, R, H_, eps_, str);
+    {  // QKV with head-split store: [3][heads][b][s][d]
+      GemmDesc d = plain(R, 3 * H_, H_, st.ln1, H_, false, w16_ + wqkv_, H_, false, st.qkv, d_, kBias);
+      d.ndiv = d_;
+      d.s_no = static_cast<long long>(R) * d_;
+      d.bias = w32_ + bqkv_;
+      ctx.gemms.run(d, str);
+    }
+    {  // S = Q K^T / sqrt(d)   (fp32 scores)
+      GemmDesc d = plain(s, s, d_, q(st), d_, false, k(st, R), d_, false, ctx.scores, s, kOutF32);
+      batched(d, z, 1LL * s * d_, 1LL * s * d_, 1LL * s * s);
+      d.alpha = 1.0f / std::sqrt(static_cast<float>(d_));
+      ctx.gemms.run(d, str);
+    }
+    softmax_fwd(ctx.scores, st.P, z * s, s, s, causal_ ? 1 : 0, str);
+    {  // ctx = P V with head-merge store into [R][H]
+      GemmDesc d = plain(s, d_, s, st.P, s, false, v(st, R), d_, true, st.ctx, H_, kOutBf16);
+      batched(d, z, 1LL * s * s, 1LL * s * d_, 0);
+      merge(d, b, s, H_);
+      ctx.gemms.run(d, str);
+    }
+    {  // h = x + ctx Wo^T + bo
+      GemmDesc d = plain(R, H_, H_, st.ctx, H_, false, w16_ + wo_, H_, false, st.h, H_, kBias | kResid);
+      d.bias = w32_ + bo_;
+      d.resid = x;
+      ctx.gemms.run(d, str);
+    }
+    layernorm_fwd(st.h, w32_ + ln2g_, w32_ + ln2b_, st.ln2, st.mean2, st.rstd2, R, H_, eps_, str);
+    {  // g = gelu(ln2 W1^T + b1), z1 = pre-activation
+      GemmDesc d = plain(R, F_, H_, st.ln2, H_, false, w16_ + w1_, H_, false, st.g, F_, kBias | kGelu | kAuxOut);
+      d.bias = w32_ + b1_;
+      d.aux_out = st.z1;
+      ctx.gemms.run(d, str);
+    }
+    {  // y = h + g W2^T + b2
+      GemmDesc d = plain(R, H_, F_, st.g, F_, false, w16_ + w2_, F_, false, y, H_, kBias | kResid);
+      d.bias = w32_ + b2_;
+      d.resid = st.h;
+      ctx.gemms.run(d, str);
+    }
+  }
+
+  void backward(StageContext& ctx, int slot, const bf16* x, const bf16* dy, bf16* dx) override {
+    Stash& st = stash_[slot];
+    const int R = ctx.rows, s = ctx.spec.seq, b = ctx.samples, z = nh_ * b;
+    cudaStream_t str = ctx.stream;
+    const float scale = 1.0f / std::sqrt(static_cast<float>(d_));
+    bf16* dz1 = ctx.t_f;
+    bf16* dln = ctx.t_h;
+    bf16* dh = ctx.t_h2;
+    bf16* dctx_h = ctx.t_h3;
+    bf16* dqkv = ctx.t_qkv;
+
+    // FFN2: dW2 += dy^T g ; db2 ; dz1 = (dy W2) * gelu'(z1)
+    ctx.gemms.run(plain(H_, F_, R, dy, H_, true, st.g, F_, true, g32_ + w2_, F_, kOutF32Acc), str);
+    colsum_acc(dy, g32_ + b2_, R, H_, str);
+    {
+      GemmDesc d = plain(R, F_, H_, dy, H_, false, w16_ + w2_, F_, true, dz1, F_, kDGelu);
+      d.aux_in = st.z1;
+      ctx.gemms.run(d, str);
+    }
+    // FFN1: dW1 += dz1^T ln2 ; db1 ; dln2 = dz1 W1
+    ctx.gemms.run(plain(F_, H_, R, dz1, F_, true, st.ln2, H_, true, g32_ + w1_, H_, kOutF32Acc), str);
+    colsum_acc(dz1, g32_ + b1_, R, F_, str);
+    ctx.gemms.run(plain(R, H_, F_, dz1, F_, false, w16_ + w1_, H_, true, dln, H_, kOutBf16), str);
+    // LN2 backward (+ residual gradient dy)
+    layernorm_bwd(dln, st.h, st.mean2, st.rstd2, w32_ + ln2g_, dy, dh, g32_ + ln2g_, g32_ + ln2b_, R, H_, str);
+    // O projection: dWo += dh^T ctx ; dbo ; dctx = dh Wo (head-split store)
+    ctx.gemms.run(plain(H_, H_, R, dh, H_, true, st.ctx, H_, true, g32_ + wo_, H_, kOutF32Acc), str);
+    colsum_acc(dh, g32_ + bo_, R, H_, str);
+    {
+      GemmDesc d = plain(R, H_, H_, dh, H_, false, w16_ + wo_, H_, true, dctx_h, d_, kOutBf16);
+      d.ndiv = d_;
+      d.s_no = static_cast<long long>(R) * d_;
+      ctx.gemms.run(d, str);
+    }
+    {  // dP = dctx V^T (fp32, reuses the scores buffer)
+      GemmDesc d = plain(s, s, d_, dctx_h, d_, false, v(st, R), d_, false, ctx.scores, s, kOutF32);
+      batched(d, z, 1LL * s * d_, 1LL * s * d_, 1LL * s * s);
+      ctx.gemms.run(d, str);
+    }
+    softmax_bwd(st.P, ctx.scores, ctx.dscores, z * s, s, str);
+    {  // dQ = scale dS K   -> dqkv[:, 0:H]
+      GemmDesc d = plain(s, d_, s, ctx.dscores, s, false, k(st, R), d_, true, dqkv, 3 * H_, kOutBf16);
+      batched(d, z, 1LL * s * s, 1LL * s * d_, 0);
+      merge(d, b, s, 3 * H_);
+      d.alpha = scale;
+      ctx.gemms.run(d, str);
+    }
+    {  // dK = scale dS^T Q -> dqkv[:, H:2H]
+      GemmDesc d = plain(s, d_, s, ctx.dscores, s, true, q(st), d_, true, dqkv + H_, 3 * H_, kOutBf16);
+      batched(d, z, 1LL * s * s, 1LL * s * d_, 0);
+      merge(d, b, s, 3 * H_);
+      d.alpha = scale;
+      ctx.gemms.run(d, str);
+    }
+    {  // dV = P^T dctx      -> dqkv[:, 2H:3H]
+      GemmDesc d = plain(s, d_, s, st.P, s, true, dctx_h, d_, true, dqkv + 2 * H_, 3 * H_, kOutBf16);
+      batched(d, z, 1LL * s * s, 1LL * s * d_, 0);
+      merge(d, b, s, 3 * H_);
+      ctx.gemms.run(d, str);
+    }
+    // QKV: dWqkv += dqkv^T ln1 ; dbqkv ; dln1 = dqkv Wqkv
+    ctx.gemms.run(plain(3 * H_, H_, R, dqkv, 3 * H_, true, st.ln1, H_, true, g32_ + wqkv_, H_, kOutF32Acc), str);
+    colsum_acc(dqkv, g32_ + bqkv_, R, 3 * H_, str);
+    ctx.gemms.run(plain(R, H_, 3 * H_, dqkv, 3 * H_, false, w16_ + wqkv_, H_, true, dln, H_, kOutBf16), str);
+    // LN1 backward (+ residual gradient dh); the model's first layer still
+    // needs gamma/beta grads, its dx goes to scratch
+    layernorm_bwd(dln, x, st.mean1, st.rstd1, w32_ + ln1g_, dh, dx ? dx : dctx_h, g32_ + ln1g_, g32_ + ln1b_, R, H_,
+                  str);
+  }
+
+  double flops_fwd(const StageContext& ctx) const override {
+    const double R = ctx.rows, s = ctx.spec.seq, z = static_cast<double>(nh_) * ctx.samples;
+    return 2.0 * R * (4.0 * H_ * H_ + 2.0 * H_ * F_) + 4.0 * z * s * s * d_;
+  }
+  double flops_bwd(const StageContext& ctx, bool) const override { return 2.0 * flops_fwd(ctx); }
+
+  std::vector<Named> tensors() const override {
+    return {{"ln1_g", ln1g_, size_t(H_)}, {"ln1_b", ln1b_, size_t(H_)},   {"Wqkv", wqkv_, 3ull * H_ * H_},
+            {"bqkv", bqkv_, 3ull * H_},   {"Wo", wo_, 1ull * H_ * H_},     {"bo", bo_, size_t(H_)},
+            {"ln2_g", ln2g_, size_t(H_)}, {"ln2_b", ln2b_, size_t(H_)},   {"W1", w1_, 1ull * F_ * H_},
+            {"b1", b1_, size_t(F_)},      {"W2", w2_, 1ull * H_ * F_},     {"b2", b2_, size_t(H_)}};
+  }
+
+ private:
+  struct Stash {
+    bf16 *ln1, *qkv, *P, *ctx, *h, *ln2, *z1, *g;
+    float *mean1, *rstd1, *mean2, *rstd2;
+  };
+  const bf16* q(const Stash& st) const { return st.qkv; }
+  const bf16* k(const Stash& st, int R) const { return st.qkv + static_cast<size_t>(R) * H_; }
+  const bf16* v(const Stash& st, int R) const { return st.qkv + 2ull * R * H_; }
+  static void batched(GemmDesc& d, int z, long long a_bs, long long b_bs, long long c_bs) {
+    d.batch = z;
+    d.a_batch_stride = a_bs;
+    d.b_batch_stride = b_bs;
+    if (c_bs) d.s_zo = c_bs;
+  }
+  // z = head * b + sample ; row = sample * s + pos ; col = head * d + j
+  void merge(GemmDesc& d, int b, int s, int ldc) const {
+    d.zdiv = b;
+    d.s_zo = d_;
+    d.s_zi = static_cast<long long>(s) * ldc;
+    d.ldc = ldc;
+  }
+
+  int H_, F_, nh_, d_;
+  bool causal_;
+  float eps_;
+  int index_;
+  size_t ln1g_, ln1b_, wqkv_, bqkv_, wo_, bo_, ln2g_, ln2b_, w1_, b1_, w2_, b2_, total_;
+  float* w32_ = nullptr;
+  float* g32_ = nullptr;
+  bf16* w16_ = nullptr;
+  std::vector<Stash> stash_;
+};
+
+}  // namespace
+
+std::unique_ptr<Layer> make_layer(const ModelSpec& spec, int global_index) {
+  if (spec.kind == "mlp") return std::make_unique<MlpLayer>(spec, global_index);
+  if (spec.kind == "bert" || spec.kind == "gpt") return std::make_unique<TransformerLayer>(spec, global_index);
+  throw std::invalid_argument("dpl: unknown model kind '" + spec.kind + "'");
+}
+
+}  // namespace dpl

@@ -1,0 +1,102 @@
+// Stage layers for the executor: the per-layer forward / backward programs
+// built from the sm_100a kernels.  A "layer" is one profile layer
+// (LayerProfile, model.hpp:16-22): one Linear+ReLU for the MLP family, one
+// pre-LN transformer block for BERT / GPT.
+//
+// Gradient contract between consecutive layers (also across the stage
+// boundary, where it travels through Split-Concat):
+//   * MLP:        grad w.r.t. the layer's *pre-activation* output (dZ); the
+//                 consumer layer applies relu'(x) to the dX it produces, so
+//                 the activation derivative is fused into the dgrad GEMM.
+//   * transformer: grad w.r.t. the block output (residual stream).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "kernels/gemm.h"
+
+namespace dpl {
+
+using bf16 = __nv_bfloat16;
+
+struct ModelSpec {
+  std::string kind = "mlp";  // "mlp" | "bert" | "gpt"
+  int layers = 16;
+  int hidden = 1024;
+  int heads = 16;
+  int ffn = 4096;
+  int seq = 1;  // tokens per sample (1 for the MLP)
+  bool causal = false;
+  float ln_eps = 1e-5f;
+};
+
+// Device memory owned by one stage replica (freed by the executor).
+class DeviceMemory {
+ public:
+  ~DeviceMemory();
+  void* alloc(size_t bytes);  // 256-byte aligned, zero-initialised on stream()
+  size_t total() const { return total_; }
+  void set_stream(cudaStream_t s) { stream_ = s; }
+
+ private:
+  cudaStream_t stream_ = nullptr;
+  std::vector<void*> blocks_;
+  size_t total_ = 0;
+};
+
+// Per-replica context shared by the layers of a stage.
+struct StageContext {
+  ModelSpec spec;
+  int rows = 0;     // token rows per micro-batch slice (samples * seq)
+  int samples = 0;  // samples per micro-batch slice
+  int slots = 1;    // activation stash depth (phi of this stage)
+  cudaStream_t stream = nullptr;
+  GemmCache gemms;
+  DeviceMemory* mem = nullptr;
+  // shared scratch (transformer backward / attention)
+  float* scores = nullptr;  // fp32 [z][s][s]  (S in forward, dP in backward)
+  bf16* dscores = nullptr;  // bf16 [z][s][s]
+  bf16* t_h = nullptr;      // [R][H] scratch
+  bf16* t_h2 = nullptr;     // [R][H] scratch
+  bf16* t_h3 = nullptr;     // [R][H] scratch (head layout)
+  bf16* t_qkv = nullptr;    // [R][3H]
+  bf16* t_f = nullptr;      // [R][F]
+  double flops_fwd = 0.0, flops_bwd = 0.0;  // per micro-batch slice (accounting)
+};
+
+class Layer {
+ public:
+  virtual ~Layer() = default;
+  // number of fp32 parameters and their (tensor id, count, init scale) list
+  virtual size_t param_count() const = 0;
+  // binds parameter / gradient / bf16-copy views and initialises weights
+  virtual void bind(float* w32, float* g32, bf16* w16, uint64_t seed, cudaStream_t s) = 0;
+  virtual void alloc_stash(StageContext& ctx) = 0;
+  virtual void forward(StageContext& ctx, int slot, const bf16* x, bf16* y) = 0;
+  // dx may be null (first layer of the model: no input gradient needed)
+  virtual void backward(StageContext& ctx, int slot, const bf16* x, const bf16* dy, bf16* dx) = 0;
+  virtual double flops_fwd(const StageContext& ctx) const = 0;
+  virtual double flops_bwd(const StageContext& ctx, bool need_dx) const = 0;
+  // named tensors for parity reads: (name, offset into the layer's params, count)
+  struct Named {
+    std::string name;
+    size_t offset;
+    size_t count;
+  };
+  virtual std::vector<Named> tensors() const = 0;
+};
+
+std::unique_ptr<Layer> make_layer(const ModelSpec& spec, int global_index);
+
+// Synthetic data tensor ids (shared with oracle/executor_ref.py).
+constexpr uint64_t kTensorInput = 1;
+constexpr uint64_t kTensorTarget = 2;
+inline uint64_t param_tensor_id(int layer, int t) { return 1000ull + static_cast<uint64_t>(layer) * 16ull + t; }
+
+}  // namespace dpl

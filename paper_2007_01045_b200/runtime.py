@@ -1,0 +1,134 @@
+"""Per-GPU executor driver: the B200 counterpart of simulate_plan
+(reference planner.hpp:87-90).  One process per GPU; torch.distributed is
+used only for plumbing (exchanging CUDA-IPC handles and NCCL ids).  The step
+itself -- the plan's early-backward 1F1B chain, Split-Concat peer copies,
+per-layer NCCL AllReduce and SGD apply -- runs in libdapple.so (C++/CUDA).
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import math
+from typing import Optional
+
+from ._lib import check, lib
+
+BLOB_BYTES = 64  # cudaIpcMemHandle_t
+
+
+class Executor:
+    def __init__(self, model: dict, plan, micro_batches: int, gbs: int, *, lr: float = 1e-3, seed: int = 1234,
+                 rank: int = 0, world: int = 1, device: Optional[int] = None, apply: bool = True,
+                 timeline: bool = True):
+        self.plan = json.loads(plan) if isinstance(plan, str) else plan
+        self.model, self.M, self.gbs = model, micro_batches, gbs
+        self.rank, self.world = rank, world
+        self.device = rank if device is None else device
+        cfg = {"model": model, "plan": self.plan, "M": micro_batches, "gbs": gbs, "lr": lr, "seed": seed,
+               "rank": rank, "world": world, "apply": apply, "timeline": timeline}
+        h = ctypes.c_void_p()
+        check(lib().dpl_exec_create(json.dumps(cfg).encode(), self.device, ctypes.byref(h)))
+        self._h = h
+        self.info = self._info()
+        if world > 1:
+            self._connect()
+
+    # ----------------------------------------------------------- plumbing
+    def _info(self) -> dict:
+        buf = ctypes.create_string_buffer(1 << 16)
+        check(lib().dpl_exec_info(self._h, buf, len(buf)))
+        return json.loads(buf.value.decode())
+
+    def _connect(self):
+        import torch.distributed as dist
+        blob = ctypes.create_string_buffer(BLOB_BYTES)
+        n = ctypes.c_size_t()
+        check(lib().dpl_exec_export(self._h, blob, BLOB_BYTES, ctypes.byref(n)))
+        blobs = [None] * self.world
+        dist.all_gather_object(blobs, bytes(blob.raw[:BLOB_BYTES]))
+        joined = b"".join(blobs)
+        check(lib().dpl_exec_connect(self._h, joined, BLOB_BYTES, self.world))
+        # one NCCL communicator per stage replica group; its first GPU makes the id
+        stage = self.plan["stages"][self.info["stage"]]
+        leader = sorted(stage["gpus"])[0]
+        my_id = None
+        if self.rank == leader and len(stage["gpus"]) > 1:
+            idbuf = ctypes.create_string_buffer(128)
+            check(lib().dpl_exec_nccl_id(idbuf))
+            my_id = bytes(idbuf.raw)
+        ids = [None] * self.world
+        dist.all_gather_object(ids, my_id)
+        if len(stage["gpus"]) > 1:
+            check(lib().dpl_exec_nccl_init(self._h, ids[leader]))
+
+    # ----------------------------------------------------------- step
+    def step(self, host_input=None, host_target=None) -> float:
+        """One synchronous DAPPLE step.  host_input / host_target: pinned host
+        tensors holding this replica's slices of every micro-batch
+        ([M][rows][H] bf16), or None to generate the seeded synthetic data on
+        the device.  Returns the global-batch loss on last-stage ranks."""
+        loss = ctypes.c_float(float("nan"))
+        pin = None if host_input is None else ctypes.c_void_p(host_input.data_ptr())
+        pt = None if host_target is None else ctypes.c_void_p(host_target.data_ptr())
+        check(lib().dpl_exec_step(self._h, pin, pt, ctypes.byref(loss)))
+        return loss.value
+
+    def timeline(self) -> dict:
+        return json.loads(lib().dpl_exec_timeline(self._h).decode())
+
+    def read(self, layer: int, name: str, count: int, grad: bool = False):
+        import numpy as np
+        out = np.empty(count, dtype=np.float32)
+        check(lib().dpl_exec_read_tensor(self._h, f"{layer}.{name}".encode(), int(grad),
+                                         out.ctypes.data_as(ctypes.c_void_p), out.nbytes))
+        return out
+
+    def close(self):
+        """Collective when world > 1: unmap peers, barrier, then free."""
+        if getattr(self, "_h", None):
+            if self.world > 1:
+                import torch.distributed as dist
+                check(lib().dpl_exec_disconnect(self._h))
+                if dist.is_initialized():
+                    dist.barrier()
+            lib().dpl_exec_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        # never collective from a finaliser: just free local state
+        if getattr(self, "_h", None):
+            try:
+                lib().dpl_exec_destroy(self._h)
+            except Exception:
+                pass
+            self._h = None
+
+
+def merge_timelines(parts: list, micro_batches: int, stages: int) -> dict:
+    """Combines per-rank measured timelines into one Timeline over the
+    expanded 2S-1 stages (simulator.hpp:25-35 layout), aligned on the GPUs'
+    global timer.  A replicated stage's block spans its replicas (min start,
+    max end).  Returns {"blocks", "latency", "busy", "bubble"}."""
+    t0 = min(p["t0_ns"] for p in parts) * 1e-9
+    se = 2 * stages - 1
+    span = {}
+    for p in parts:
+        off = p["t0_ns"] * 1e-9 - t0
+        for x, i, kind, s, e in p["blocks"]:
+            if s < 0 or e < 0:
+                continue
+            key = (x, i, kind)
+            s, e = s + off, e + off
+            if key in span:
+                span[key] = (min(span[key][0], s), max(span[key][1], e))
+            else:
+                span[key] = (s, e)
+    blocks = []
+    for x in range(se):
+        for kind in (0, 1):
+            for i in range(micro_batches):
+                s, e = span.get((x, i, kind), (math.nan, math.nan))
+                blocks.append([x, i, kind, s, e])
+    latency = max(p["t0_ns"] * 1e-9 - t0 + p["step_s"] for p in parts)
+    busy = sum(sum(e - s for x, i, k, s, e in p["blocks"] if x % 2 == 0 and s >= 0) for p in parts)
+    return {"blocks": blocks, "latency": latency, "busy": busy, "bubble": 1.0 - busy / (len(parts) * latency)}

@@ -1,0 +1,74 @@
+"""CPU oracle self-checks: the plan-scheduled step (replica slices,
+Split-Concat, per-replica accumulation, AllReduce) equals the sequential
+full-batch step, and the oracle's manual backward equals autograd."""
+import numpy as np
+import pytest
+
+from oracle.executor_ref import Model, batch_data, full_batch_step, hash_uniform, init_layer, layer_forward, scheduled_step
+
+PLANS = [
+    {"stages": [{"layers": [0, 4], "gpus": [0]}]},
+    {"stages": [{"layers": [0, 4], "gpus": [0, 1, 2, 3]}]},
+    {"stages": [{"layers": [0, 2], "gpus": [0]}, {"layers": [2, 4], "gpus": [1]}]},
+    {"stages": [{"layers": [0, 1], "gpus": [0, 1]}, {"layers": [1, 4], "gpus": [2, 3]}]},
+    {"stages": [{"layers": [0, 3], "gpus": [0, 1, 2]}, {"layers": [3, 4], "gpus": [3]}]},
+    {"stages": [{"layers": [0, 1], "gpus": [0]}, {"layers": [1, 2], "gpus": [1, 2, 3]}, {"layers": [2, 4], "gpus": [4, 5]}]},
+]
+
+
+@pytest.mark.parametrize("plan", PLANS)
+@pytest.mark.parametrize("kind", ["mlp", "bert", "gpt"])
+def test_scheduled_equals_full_batch(plan, kind):
+    m = dict(kind=kind, layers=4, hidden=32, heads=2, ffn=64, seq=8)
+    gbs, M = 24, 2  # 12 samples per micro-batch split over 1, 2, 3, 4 replicas
+    a = full_batch_step(m, gbs)
+    b = scheduled_step(m, plan, M, gbs)
+    assert abs(a.loss - b.loss) <= 1e-12 * abs(a.loss)
+    for key, g in a.grads.items():
+        assert np.allclose(b.grads[key], g, rtol=1e-10, atol=1e-14), key
+
+
+def test_hash_uniform_golden():
+    # frozen values of the shared device/host generator
+    v = hash_uniform(1234, 1, np.arange(4, dtype=np.uint64))
+    assert v.dtype == np.float32 and np.all(np.abs(v) < 1)
+    again = hash_uniform(1234, 1, np.arange(4, dtype=np.uint64))
+    assert np.array_equal(v, again)
+    assert not np.array_equal(v, hash_uniform(1235, 1, np.arange(4, dtype=np.uint64)))
+    u = hash_uniform(7, 3, np.arange(200000, dtype=np.uint64))
+    assert abs(float(u.mean())) < 0.01 and 0.32 < float(u.var()) < 0.35
+
+
+@pytest.mark.parametrize("kind", ["mlp", "bert", "gpt"])
+def test_manual_backward_matches_autograd(kind):
+    torch = pytest.importorskip("torch")
+    m = Model.from_dict(dict(kind=kind, layers=3, hidden=16, heads=2, ffn=32, seq=4))
+    gbs = 3
+    res = full_batch_step(m, gbs)
+    params = {l: {k: torch.tensor(v, dtype=torch.float64, requires_grad=True)
+                  for k, v in init_layer(m, l, 1234).items()} for l in range(m.layers)}
+    x, t = (torch.tensor(a, dtype=torch.float64) for a in batch_data(m, 1234, 0, gbs))
+    H, nh, s = m.hidden, m.heads, m.seq
+    d = H // nh
+    for l in range(m.layers):
+        p = params[l]
+        if kind == "mlp":
+            z = x @ p["W"].T + p["b"]
+            x = torch.relu(z) if l != m.layers - 1 else z
+            continue
+        ln1 = torch.nn.functional.layer_norm(x, (H,), p["ln1_g"], p["ln1_b"], m.eps)
+        qkv = ln1 @ p["Wqkv"].T + p["bqkv"]
+        q, k, v = (qkv[:, i * H:(i + 1) * H].reshape(gbs, s, nh, d).transpose(1, 2) for i in range(3))
+        sc = q @ k.transpose(-1, -2) / d ** 0.5
+        if m.causal:
+            sc = sc.masked_fill(torch.triu(torch.ones(s, s, dtype=torch.bool), 1), float("-inf"))
+        ctx = (torch.softmax(sc, -1) @ v).transpose(1, 2).reshape(gbs * s, H)
+        h = x + ctx @ p["Wo"].T + p["bo"]
+        ln2 = torch.nn.functional.layer_norm(h, (H,), p["ln2_g"], p["ln2_b"], m.eps)
+        x = h + torch.nn.functional.gelu(ln2 @ p["W1"].T + p["b1"]) @ p["W2"].T + p["b2"]
+    loss = ((x - t) ** 2).sum() / (gbs * s * H)
+    loss.backward()
+    assert abs(loss.item() - res.loss) < 1e-12
+    for l in range(m.layers):
+        for k, v in params[l].items():
+            assert np.allclose(v.grad.numpy(), res.grads[(l, k)], rtol=1e-9, atol=1e-13), (l, k)
