@@ -1,0 +1,407 @@
+#!/usr/bin/env python
+"""bench.py -- DAPPLE synchronous pipelined-DP training step on B200.
+
+Workload (BASELINE.json configs[1]): BERT-48 encoder, hidden 1024, seq 512,
+16 heads, FFN 4096, bf16, MSE regression head, synthetic data, M = 8
+micro-batches, each stage replica owning an 8-sample (4096-token) slice of
+every micro-batch.  Plans:
+  N = 1   [0,48) x1                         (the step: 8 micro-batches accumulated)
+  N >= 2  [0,24) x N/2 | [24,48) x N/2      (BASELINE's 2-stage shape; 2 x 4 at N = 8)
+so the global batch is 64 samples per replica group (GBS = 64 * N / S).
+
+Metric: training samples/s of the whole job (value: device-timed, inputs
+generated in HBM; e2e: through the public API with pinned host inputs /
+targets copied in and the loss read back every step), plus the measured
+pipeline bubble and the planner-predicted vs measured batch latency L.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl dapple|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MODELS = {
+    "bert48": dict(kind="bert", layers=48, hidden=1024, heads=16, ffn=4096, seq=512),
+    "gpt2-1.5b": dict(kind="gpt", layers=48, hidden=1600, heads=25, ffn=6400, seq=1024),
+    "mlp16": dict(kind="mlp", layers=16, hidden=1024),
+}
+METRIC = "training samples/sec at 1/2/4/8 B200; pipeline bubble %; predicted-vs-measured L"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def flops_per_sample(m: dict) -> float:
+    """GEMM + attention-matmul FLOPs of one sample, fwd + dgrad + wgrad
+    (24h^2 + 4sh per token per layer, x3)."""
+    if m["kind"] == "mlp":
+        return 6.0 * m["hidden"] ** 2 * m["layers"]
+    h, s, f = m["hidden"], m["seq"], m["ffn"]
+    per_token = 2 * (4 * h * h + 2 * h * f) + 4 * s * h
+    return 3.0 * per_token * s * m["layers"]
+
+
+def make_plan(n: int, layers: int) -> dict:
+    if n == 1:
+        return {"stages": [{"layers": [0, layers], "gpus": [0], "replication": 1}]}
+    half = n // 2
+    cut = layers // 2
+    return {"stages": [{"layers": [0, cut], "gpus": list(range(half)), "replication": half},
+                       {"layers": [cut, layers], "gpus": list(range(half, n)), "replication": n - half}]}
+
+
+def load_peaks() -> tuple[dict, str]:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return PEAKS_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    FIELDS = ["index", "clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self):
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "--query-gpu=" + ",".join(self.FIELDS),
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < len(self.FIELDS):
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    return rank, world
+
+
+def gather(obj, world):
+    if world == 1:
+        return [obj]
+    import torch.distributed as dist
+    out = [None] * world
+    dist.all_gather_object(out, obj)
+    return out
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def host_batches(model: dict, plan: dict, rank: int, m: int, slice_samples: int, seed: int):
+    """Pinned host copies of this rank's input / target slices of every
+    micro-batch (the e2e leg's H2D sources), same values the device
+    generator would produce."""
+    import numpy as np
+    import torch
+    from oracle.executor_ref import Model, batch_data  # data generator shared with the device
+    mm = Model.from_dict(model)
+    stages = plan["stages"]
+    k = next(i for i, s in enumerate(stages) if rank in s["gpus"])
+    rep = stages[k]["gpus"].index(rank)
+    r = len(stages[k]["gpus"])
+    B = slice_samples * r
+    ins, tgts = [], []
+    for i in range(m):
+        x, t = batch_data(mm, seed, i * B + rep * slice_samples, slice_samples)
+        ins.append(x)
+        tgts.append(t)
+    def pinned(arrs):
+        a = torch.from_numpy(np.stack(arrs)).to(torch.bfloat16)
+        return a.pin_memory()
+    inp = pinned(ins) if k == 0 else None
+    tgt = pinned(tgts) if k == len(stages) - 1 else None
+    return inp, tgt
+
+
+def predicted_latency(model, plan, timelines, m, n):
+    """Builds a B200 layer profile from the measured blocks (per-layer F/B of
+    the full micro-batch = block time x r / layers on the stage) and asks the
+    host planner for est_latency (estimator.cpp:56-86) and sim_latency
+    (simulate_plan, planner.cpp:491-514) of the executed plan."""
+    from paper_2007_01045_b200 import pipeplan
+    stages = plan["stages"]
+    per_layer = {}
+    for k, st in enumerate(stages):
+        f_times, b_times = [], []
+        for tl in timelines:
+            if tl["stage"] != k:
+                continue
+            for x, i, kind, s, e in tl["blocks"]:
+                if x == 2 * k and s >= 0:
+                    (f_times if kind == 0 else b_times).append(e - s)
+        lo, hi = st["layers"]
+        r = len(st["gpus"])
+        f = statistics.median(f_times) * r / (hi - lo)
+        b = statistics.median(b_times) * r / (hi - lo)
+        for l in range(lo, hi):
+            per_layer[l] = (f, b)
+    h = model["hidden"]
+    act = 8 * len(stages[0]["gpus"]) * model.get("seq", 1) * h * 2  # one micro-batch's boundary activation
+    params = (12 * h * h + 13 * h) * 4 if model["kind"] != "mlp" else (h * h + h) * 4
+    profile = {"profile_batch_size": 8, "layers": [
+        {"fwd_time_us": per_layer[l][0] * 1e6, "bwd_time_us": per_layer[l][1] * 1e6, "activation_bytes": act,
+         "param_bytes": params} for l in range(model["layers"])]}
+    # NVLink 5 through NVSwitch: measured 770 GB/s peer copy, AR bus bw 725 GB/s (B200_PROFILING.md)
+    cluster = {"seps": [n], "intra_bw_gbps": 770.0, "inter_bw_gbps": 50.0, "intra_latency_us": 5.0,
+               "inter_latency_us": 10.0, "per_gpu_memory_gb": 180.0}
+    seq = pipeplan.build_stage_sequence(plan, profile, cluster)
+    est = pipeplan.estimate_latency(seq, m)
+    sim = pipeplan.simulate_plan(plan, profile, cluster, m)
+    blocks = sim["timeline"]["blocks"]
+    busy = 0.0
+    for x, i, kind, s, e in blocks:
+        if x % 2 == 0:
+            busy += (e - s) * len(stages[x // 2]["gpus"])
+    sim_bubble = 1.0 - busy / (n * sim["latency"])
+    return {"est_ms": est["total"] * 1e3, "sim_ms": sim["latency"] * 1e3, "sim_bubble": sim_bubble,
+            "pivot": est["pivot"], "profile": profile, "cluster": cluster}
+
+
+def cpu_baseline(model: dict, budget_layers: int | None = None) -> dict:
+    """The oracle's CPU step (numpy, all host cores) on a bounded sample:
+    one sample through `budget_layers` layers, fwd + bwd + SGD."""
+    from oracle.executor_ref import CpuTrainer
+    sub = dict(model)
+    if budget_layers:
+        sub["layers"] = budget_layers
+    tr = CpuTrainer(sub)
+    tr.step(0, 1)  # warm (BLAS threads, page-in)
+    t0 = time.perf_counter()
+    tr.step(1, 1)
+    dt = time.perf_counter() - t0
+    frac = sub["layers"] / model["layers"]
+    return {"value": frac / dt, "unit": "samples/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"1 sample x {sub['layers']}/{model['layers']} layers fwd+bwd+SGD, fp32 numpy "
+                      f"(oracle/executor_ref.py CpuTrainer), {dt:.2f}s"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU implementation of the step on this host."""
+    if rank != 0:
+        return
+    model = MODELS[args.model]
+    layers = min(model["layers"], args.ref_layers)
+    from oracle.executor_ref import CpuTrainer
+    sub = dict(model, layers=layers)
+    tr = CpuTrainer(sub)
+    for w in range(args.warmup):
+        tr.step(w, 1)
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        tr.step(args.warmup + k, 1)
+    dt = time.perf_counter() - t0
+    frac = layers / model["layers"]
+    value = args.steps * frac / dt
+    unit = "samples/s"
+    line = {"metric": METRIC, "value": value, "unit": unit, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+            "config": {"workload": args.model, **model},
+            "cpu_baseline": {"value": value, "unit": unit, "cores": os.cpu_count(), "kind": "port",
+                             "sample": f"each step: 1 sample x {layers}/{model['layers']} layers fwd+bwd+SGD, "
+                                       "fp32 numpy oracle (the reference has no numerical executor)"},
+            "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="dapple", choices=["dapple", "reference"])
+    ap.add_argument("--model", default="bert48", choices=sorted(MODELS))
+    ap.add_argument("--micro-batches", type=int, default=8)
+    ap.add_argument("--slice", type=int, default=8, help="samples per replica slice of a micro-batch")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-layers", type=int, default=8)
+    ap.add_argument("--seed", type=int, default=1234)
+    args = ap.parse_args()
+    rank, world = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+
+    import torch
+    torch.cuda.set_device(rank)
+    from paper_2007_01045_b200 import _lib
+    from paper_2007_01045_b200.runtime import Executor, merge_timelines
+
+    model = MODELS[args.model]
+    plan = make_plan(world, model["layers"])
+    S = len(plan["stages"])
+    r0 = len(plan["stages"][0]["gpus"])
+    M = args.micro_batches
+    gbs = M * args.slice * r0
+    lib = _lib.lib()
+
+    ex = Executor(model, plan, M, gbs, lr=1e-4, seed=args.seed, rank=rank, world=world, device=rank)
+    for _ in range(args.warmup):
+        ex.step()
+    torch.cuda.synchronize()
+
+    # ------------------------------------------------------------ timed (device)
+    clocks = ClockSampler() if rank == 0 else None
+    barrier(world)
+    if clocks:
+        clocks.start()
+    launches0 = lib.dpl_k_launch_count()
+    t_wall0 = time.perf_counter()
+    tls = []
+    for _ in range(args.steps):
+        ex.step()
+        tls.append(ex.timeline())
+    torch.cuda.synchronize()
+    barrier(world)
+    t_wall = time.perf_counter() - t_wall0
+    launches = lib.dpl_k_launch_count() - launches0
+    clk = clocks.stop() if clocks else None
+
+    all_tls = gather(tls, world)  # [rank][step]
+    lat, bub = [], []
+    for k in range(args.steps):
+        merged = merge_timelines([all_tls[r][k] for r in range(world)], M, S)
+        lat.append(merged["latency"])
+        bub.append(merged["bubble"])
+    total_launches = sum(gather(launches, world))
+    device_s = sum(lat)
+    value = args.steps * gbs / device_s
+
+    # ------------------------------------------------------------ GEMM roofline (one profiled step)
+    ex.gemm_profile(True)
+    ex.step()
+    prof = ex.gemm_profile_report()
+    step_tl = ex.timeline()
+    ex.gemm_profile(False)
+    profs = gather({"prof": prof, "step_s": step_tl["step_s"]}, world)
+
+    # ------------------------------------------------------------ e2e (public API, host buffers)
+    e2e = None
+    if not args.no_e2e:
+        inp, tgt = host_batches(model, plan, rank, M, args.slice, args.seed)
+        ex.step(inp, tgt)  # warm the H2D path
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            ex.step(inp, tgt)  # H2D of the step's inputs/targets, D2H of the loss
+        torch.cuda.synchronize()
+        barrier(world)
+        t_e2e = time.perf_counter() - t0
+        h2d = (inp.numel() * 2 if inp is not None else 0) + (tgt.numel() * 2 if tgt is not None else 0)
+        d2h = 4 if rank in plan["stages"][-1]["gpus"] else 0
+        sums = gather((h2d, d2h, t_e2e), world)
+        e2e = {"value": args.steps * gbs / max(s[2] for s in sums), "unit": "samples/s",
+               "h2d_bytes_per_step": sum(s[0] for s in sums), "d2h_bytes_per_step": sum(s[1] for s in sums),
+               "timing": "wall clock between barriers, pinned host buffers"}
+
+    info = ex.info
+    ex.close()
+    if rank != 0:
+        return
+
+    # ------------------------------------------------------------ report
+    peaks, peaks_src = load_peaks()
+    g_flops = sum(p["prof"]["flops"] for p in profs)
+    g_secs = sum(p["prof"]["seconds"] for p in profs)
+    achieved = g_flops / g_secs / 1e12 if g_secs > 0 else 0.0
+    peak = peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"])
+    gemm_share = g_secs / sum(p["step_s"] for p in profs)
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
+            traffic = json.load(f).get("bytes_per_launch")
+    except Exception:
+        pass
+    pred = predicted_latency(model, plan, [all_tls[r][-1] for r in range(world)], M, world)
+    measured_ms = statistics.mean(lat) * 1e3
+    fps = flops_per_sample(model)
+    line = {
+        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": measured_ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded splitmix64 inputs/targets, random-init "
+                                                      "weights)",
+        "config": {"workload": args.model, **model, "global_batch": gbs, "micro_batches": M,
+                   "slice_samples": args.slice, "plan": [[s["layers"], s["gpus"]] for s in plan["stages"]],
+                   "phi": info["phi_expanded"], "parallelism": f"{S} stages x {r0} replicas",
+                   "l2": "working set (GBs of activations) far larger than the 126 MB L2"},
+        "bubble": statistics.mean(bub),
+        "latency": {"measured_ms": measured_ms, "est_ms": pred["est_ms"], "sim_ms": pred["sim_ms"],
+                    "sim_bubble": pred["sim_bubble"], "pivot": pred["pivot"],
+                    "measured_over_sim": measured_ms / pred["sim_ms"],
+                    "profile": "per-layer F/B calibrated from this run's measured blocks"},
+        "tflops_per_gpu": fps * value / world / 1e12,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "gemm_bf16_tcgen05 (all launches of one step, CUDA events per launch)",
+                     "peak_source": f"bf16_tflops_sustained of {peaks_src}", "gemm_share_of_step": gemm_share,
+                     "shapes": prof["shapes"][:16]},
+        "clocks": clk,
+        "gpu_launches": total_launches,
+        "wall_s": t_wall,
+        "e2e": e2e,
+    }
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(model, budget_layers=min(model["layers"], 48))
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -130,6 +130,10 @@ const char* dpl_exec_timeline(dpl_exec* ex);
 /* Copies a parameter / gradient tensor (by name) to host, for parity. */
 int dpl_exec_read_tensor(dpl_exec* ex, const char* name, int grad, void* host, size_t bytes);
 int dpl_exec_info(dpl_exec* ex, char* buf, size_t cap);
+/* Per-launch GEMM timing (CUDA events around every GEMM launch of the next
+ * steps) and its summary as JSON {launches, seconds, flops, shapes[]}. */
+int dpl_exec_gemm_profile(dpl_exec* ex, int enable);
+const char* dpl_exec_gemm_profile_json(dpl_exec* ex);
 /* Multi-rank teardown: disconnect on every rank (unmaps peers' IPC regions,
  * destroys the NCCL communicator), barrier, then destroy. */
 int dpl_exec_disconnect(dpl_exec* ex);

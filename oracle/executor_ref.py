@@ -62,12 +62,16 @@ def _erf(x):
     return erf(x)
 
 
+_SQRT2 = math.sqrt(2.0)
+_INV_SQRT_2PI = 1.0 / math.sqrt(2.0 * math.pi)
+
+
 def gelu(x):
-    return 0.5 * x * (1.0 + _erf(x / np.sqrt(2.0)))
+    return 0.5 * x * (1.0 + _erf(x / _SQRT2))
 
 
 def dgelu(x):
-    return 0.5 * (1.0 + _erf(x / np.sqrt(2.0))) + x * np.exp(-0.5 * x * x) / np.sqrt(2.0 * np.pi)
+    return 0.5 * (1.0 + _erf(x / _SQRT2)) + x * np.exp(-0.5 * x * x) * _INV_SQRT_2PI
 
 
 @dataclass
@@ -144,7 +148,7 @@ def _gemm_weights(p, q):
 def _ln_fwd(x, g, b, eps):
     mean = x.mean(-1, keepdims=True)
     var = ((x - mean) ** 2).mean(-1, keepdims=True)
-    rstd = 1.0 / np.sqrt(var + eps)
+    rstd = 1.0 / np.sqrt(var + float(eps))
     xh = (x - mean) * rstd
     return xh * g + b, (xh, rstd)
 
@@ -170,7 +174,7 @@ def layer_forward(model: Model, layer: int, p: dict, x: np.ndarray, samples: int
     ln1 = q(ln1)
     qkv = q(ln1 @ p["Wqkv"].T + p["bqkv"])
     qh, k, v = (qkv[:, i * H:(i + 1) * H].reshape(samples, s, nh, d).transpose(0, 2, 1, 3) for i in range(3))
-    sc = (qh @ k.transpose(0, 1, 3, 2)) / np.sqrt(d)
+    sc = (qh @ k.transpose(0, 1, 3, 2)) * (1.0 / math.sqrt(d))
     if model.causal:
         sc = np.where(np.triu(np.ones((s, s), bool), 1), -np.inf, sc)
     sc = sc - sc.max(-1, keepdims=True)
@@ -215,7 +219,7 @@ def layer_backward(model: Model, layer: int, p: dict, cache, dy: np.ndarray, sam
     dctx = q(dh @ p["Wo"]).reshape(samples, s, nh, d).transpose(0, 2, 1, 3)
     dP = dctx @ v.transpose(0, 1, 3, 2)
     dS = q(P * (dP - (P * dP).sum(-1, keepdims=True)))
-    scale = 1.0 / np.sqrt(d)
+    scale = 1.0 / math.sqrt(d)
     dq = q(scale * (dS @ k))
     dk = q(scale * (dS.transpose(0, 1, 3, 2) @ qh))
     dv = q(P.transpose(0, 1, 3, 2) @ dctx)
@@ -337,3 +341,34 @@ def scheduled_step(model, plan: dict, micro_batches: int, gbs: int, seed: int = 
                 res.grads[(l, name)] = g
                 res.params[(l, name)] = params[l][name].astype(np.float32) - np.float32(lr) * g.astype(np.float32)
     return res
+
+
+class CpuTrainer:
+    """The oracle's training step as a reusable CPU trainer (parameters kept
+    across steps, in-place SGD) -- the CPU path bench.py times beside the GPU
+    (cpu_baseline, and the `--impl reference` arm).  numpy dispatches the
+    matrix products to its multithreaded BLAS, so it uses all host cores."""
+
+    def __init__(self, model, seed: int = 1234, dtype=np.float32):
+        self.model = Model.from_dict(model) if isinstance(model, dict) else model
+        self.seed, self.dtype = seed, dtype
+        self.params = {l: {k: v.astype(dtype) for k, v in init_layer(self.model, l, seed).items()}
+                       for l in range(self.model.layers)}
+
+    def step(self, sample0: int, samples: int, lr: float = 1e-3) -> float:
+        m = self.model
+        x, t = batch_data(m, self.seed, sample0, samples)
+        x, t = x.astype(self.dtype), t.astype(self.dtype)
+        caches = []
+        for l in range(m.layers):
+            x, c = layer_forward(m, l, self.params[l], x, samples)
+            caches.append(c)
+        numel = samples * m.seq * m.hidden
+        diff = x - t
+        loss = float((diff * diff).sum() / numel)
+        dy = (2.0 / numel) * diff
+        for l in reversed(range(m.layers)):
+            dy, g = layer_backward(m, l, self.params[l], caches[l], dy, samples, need_dx=l > 0)
+            for k, v in g.items():
+                self.params[l][k] -= self.dtype(lr) * v.astype(self.dtype)
+        return loss

@@ -12,6 +12,8 @@
 namespace dpl {
 thread_local std::string g_last_error;
 std::atomic<long long> g_launches{0};
+void count_launch(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 int fail(const std::string& what) {
   g_last_error = what;
@@ -22,7 +24,6 @@ template <typename F>
 int guarded(F&& f) {
   try {
     f();
-    g_launches.fetch_add(1, std::memory_order_relaxed);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(std::string("CUDA: ") + cudaGetErrorString(e));
     return 0;

@@ -12,6 +12,7 @@
 #include <type_traits>
 
 #include "elementwise.h"
+#include "gemm.h"
 
 namespace dpl {
 
@@ -424,6 +425,7 @@ int grid_for(long long work, int threads) {
 
 void layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y, float* mean, float* rstd, int rows,
                    int h, float eps, cudaStream_t s) {
+  count_launch();
   const int warps = 8;
   const int grid = std::max(1, std::min((rows + warps - 1) / warps, 148 * 8));
   dispatch_vec(h, [&](auto v) {
@@ -434,6 +436,7 @@ void layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y
 
 void layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd, const float* gamma,
                    const void* dresid, void* dx, float* dgamma, float* dbeta, int rows, int h, cudaStream_t s) {
+  count_launch();
   const int warps = 8;
   const int grid = std::max(1, std::min((rows + warps - 1) / warps, 148 * 2));
   const size_t smem = static_cast<size_t>(warps) * 2 * h * sizeof(float);
@@ -447,6 +450,7 @@ void layernorm_bwd(const void* dy, const void* x, const float* mean, const float
 }
 
 void softmax_fwd(const float* s, void* p, int rows, int len, int q_len, int causal, cudaStream_t st) {
+  count_launch();
   const int warps = 8;
   const int grid = std::max(1, std::min((rows + warps - 1) / warps, 148 * 16));
   dispatch_vec(len, [&](auto v) {
@@ -456,6 +460,7 @@ void softmax_fwd(const float* s, void* p, int rows, int len, int q_len, int caus
 }
 
 void softmax_bwd(const void* p, const float* dp, void* ds, int rows, int len, cudaStream_t st) {
+  count_launch();
   const int warps = 8;
   const int grid = std::max(1, std::min((rows + warps - 1) / warps, 148 * 16));
   dispatch_vec(len, [&](auto v) {
@@ -465,6 +470,7 @@ void softmax_bwd(const void* p, const float* dp, void* ds, int rows, int len, cu
 }
 
 void colsum_acc(const void* dy, float* db, int rows, int cols, cudaStream_t s) {
+  count_launch();
   const int threads = 128;
   const int nvec = cols / 8;
   const int gx = (nvec + threads - 1) / threads;
@@ -477,31 +483,37 @@ void colsum_acc(const void* dy, float* db, int rows, int cols, cudaStream_t s) {
 }
 
 void mse_loss(const void* y, const void* t, void* dy, float* loss_acc, long long n, float grad_scale, cudaStream_t s) {
+  count_launch();
   mse_kernel<<<grid_for(n / 8, 256), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(y),
                                                    static_cast<const __nv_bfloat16*>(t),
                                                    static_cast<__nv_bfloat16*>(dy), loss_acc, n, grad_scale);
 }
 
 void sgd_apply(float* w32, float* g, void* w16, long long n, float lr, cudaStream_t s) {
+  count_launch();
   sgd_kernel<<<grid_for(n / 4, 256), 256, 0, s>>>(w32, g, static_cast<__nv_bfloat16*>(w16), n, lr);
 }
 
 void fill_uniform_bf16(void* dst, long long n, uint64_t seed, uint64_t tensor, long long idx0, float scale,
                        cudaStream_t s) {
+  count_launch();
   fill_uniform_bf16_kernel<<<grid_for(n, 256), 256, 0, s>>>(static_cast<__nv_bfloat16*>(dst), n, seed, tensor, idx0,
                                                             scale);
 }
 
 void fill_uniform_f32(float* dst, long long n, uint64_t seed, uint64_t tensor, long long idx0, float scale,
                       cudaStream_t s) {
+  count_launch();
   fill_uniform_f32_kernel<<<grid_for(n, 256), 256, 0, s>>>(dst, n, seed, tensor, idx0, scale);
 }
 
 void fill_const_f32(float* dst, long long n, float v, cudaStream_t s) {
+  count_launch();
   fill_const_f32_kernel<<<grid_for(n, 256), 256, 0, s>>>(dst, n, v);
 }
 
 void cast_f32_bf16(const float* src, void* dst, long long n, cudaStream_t s) {
+  count_launch();
   cast_f32_bf16_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, static_cast<__nv_bfloat16*>(dst), n);
 }
 

@@ -17,6 +17,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <vector>
 
 namespace dpl {
 
@@ -87,6 +88,7 @@ class GemmOp {
   int bn() const { return bn_; }
   int grid() const { return grid_; }
   double flops() const { return 2.0 * params_.M * params_.N * static_cast<double>(params_.K) * params_.batch; }
+  const GemmParams& params() const { return params_; }
   bool ready() const { return bn_ != 0; }
 
  private:
@@ -96,13 +98,34 @@ class GemmOp {
   size_t smem_ = 0;
 };
 
+// Kernel launches issued by libdapple (all kernels); bench/smoke evidence.
+void count_launch(long long n = 1);
+long long launch_count();
+
+// Optional per-launch timing of GEMMs (CUDA events around each launch on the
+// launching stream) used by bench.py for the live roofline number.
+struct GemmProfile {
+  bool enabled = false;
+  struct Rec {
+    cudaEvent_t start, end;
+    double flops;
+    int M, N, K, batch, bn;
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  cudaEvent_t take();
+  void reset() { recs.clear(); used = 0; }
+};
+
 // Prepared-GEMM cache keyed by the full descriptor (pointers included):
 // tensor maps are encoded the first time a (layer, buffer) combination is
 // seen and reused on every later step.
 class GemmCache {
  public:
   const GemmOp& get(const GemmDesc& d);
-  void run(const GemmDesc& d, cudaStream_t s) { get(d).launch(s); }
+  void run(const GemmDesc& d, cudaStream_t s);
+  GemmProfile profile;
   size_t size() const;
   double flops_run = 0.0;  // flops launched through run() (accounting)
 

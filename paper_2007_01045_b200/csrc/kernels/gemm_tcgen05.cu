@@ -511,7 +511,38 @@ const GemmOp& GemmCache::get(const GemmDesc& d) {
 
 size_t GemmCache::size() const { return impl_ ? impl_->ops.size() : 0; }
 
+cudaEvent_t GemmProfile::take() {
+  if (used == pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    pool.push_back(e);
+  }
+  return pool[used++];
+}
+
+void GemmCache::run(const GemmDesc& d, cudaStream_t s) {
+  const GemmOp& op = get(d);
+  if (!profile.enabled) {
+    op.launch(s);
+    return;
+  }
+  GemmProfile::Rec r;
+  r.start = profile.take();
+  r.end = profile.take();
+  r.flops = op.flops();
+  r.M = d.M;
+  r.N = d.N;
+  r.K = d.K;
+  r.batch = d.batch;
+  r.bn = op.bn();
+  cudaEventRecord(r.start, s);
+  op.launch(s);
+  cudaEventRecord(r.end, s);
+  profile.recs.push_back(r);
+}
+
 void GemmOp::launch(cudaStream_t stream) const {
+  count_launch();
   switch (bn_) {
     case 64: gemm_bf16_tcgen05<64><<<grid_, kThreads, smem_, stream>>>(params_); break;
     case 128: gemm_bf16_tcgen05<128><<<grid_, kThreads, smem_, stream>>>(params_); break;

@@ -134,6 +134,11 @@ class Executor {
   void nccl_init(const void* id);
   void disconnect();
   float step(const void* host_input, const void* host_target);
+  void set_gemm_profile(bool on) {
+    ctx_.gemms.profile.enabled = on;
+    ctx_.gemms.profile.reset();
+  }
+  std::string gemm_profile_json() const;
   std::string timeline_json() const;
   void read_tensor(const std::string& name, bool grad, void* host, size_t bytes);
   std::string info() const;
@@ -446,10 +451,12 @@ void Executor::wait_flag(cudaStream_t s, uint32_t* flag, uint32_t value) {
     const CUresult rc = fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flag), value, 0x0 /*GEQ*/);
     if (rc == CUDA_SUCCESS) return;
   }
+  count_launch();
   wait_kernel<<<1, 1, 0, s>>>(flag, value);
 }
 
 void Executor::signal(cudaStream_t s, uint32_t* remote_flag, uint32_t value) {
+  count_launch();
   signal_kernel<<<1, 1, 0, s>>>(remote_flag, value);
 }
 
@@ -550,6 +557,7 @@ float Executor::step(const void* host_input, const void* host_target) {
   const uint32_t base = static_cast<uint32_t>(steps_done_ * M_);
   const size_t H = spec_.hidden;
   const size_t RH = static_cast<size_t>(ctx_.rows) * H;
+  count_launch();
   stamp_kernel<<<1, 1, 0, compute_>>>(t0_);
   DPL_CUDA(cudaEventRecord(ev_begin_, compute_));
   DPL_CUDA(cudaMemsetAsync(loss_acc_, 0, 4, compute_));
@@ -667,6 +675,54 @@ void Executor::read_tensor(const std::string& name, bool grad, void* host, size_
   throw std::invalid_argument("dpl exec: unknown tensor " + name);
 }
 
+std::string Executor::gemm_profile_json() const {
+  // per-launch durations of the GEMMs of the last profiled step, grouped by shape
+  struct Agg {
+    int M, N, K, batch, bn;
+    long long launches = 0;
+    double flops = 0, seconds = 0;
+  };
+  std::vector<Agg> aggs;
+  double total_s = 0, total_f = 0;
+  for (const auto& r : ctx_.gemms.profile.recs) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.start, r.end);
+    const double sec = ms * 1e-3;
+    total_s += sec;
+    total_f += r.flops;
+    auto it = std::find_if(aggs.begin(), aggs.end(), [&](const Agg& a) {
+      return a.M == r.M && a.N == r.N && a.K == r.K && a.batch == r.batch;
+    });
+    if (it == aggs.end()) {
+      aggs.push_back({r.M, r.N, r.K, r.batch, r.bn});
+      it = aggs.end() - 1;
+    }
+    it->launches++;
+    it->flops += r.flops;
+    it->seconds += sec;
+  }
+  Value out = Value::object();
+  out["launches"] = static_cast<long long>(ctx_.gemms.profile.recs.size());
+  out["seconds"] = total_s;
+  out["flops"] = total_f;
+  Value shapes = Value::array();
+  for (const Agg& a : aggs) {
+    Value e = Value::object();
+    e["M"] = a.M;
+    e["N"] = a.N;
+    e["K"] = a.K;
+    e["batch"] = a.batch;
+    e["bn"] = a.bn;
+    e["launches"] = a.launches;
+    e["flops"] = a.flops;
+    e["seconds"] = a.seconds;
+    e["tflops"] = a.seconds > 0 ? a.flops / a.seconds * 1e-12 : 0.0;
+    shapes.push_back(std::move(e));
+  }
+  out["shapes"] = std::move(shapes);
+  return out.dump();
+}
+
 std::string Executor::info() const {
   Value v = Value::object();
   v["rank"] = rank_;
@@ -777,6 +833,19 @@ int dpl_exec_info(dpl_exec* ex, char* buf, size_t cap) {
     if (s.size() + 1 > cap) throw std::invalid_argument("dpl exec: info buffer too small");
     std::memcpy(buf, s.c_str(), s.size() + 1);
   });
+}
+
+int dpl_exec_gemm_profile(dpl_exec* ex, int enable) {
+  return exec_guard([&] { ex->impl->set_gemm_profile(enable != 0); });
+}
+
+const char* dpl_exec_gemm_profile_json(dpl_exec* ex) {
+  try {
+    ex->reply = ex->impl->gemm_profile_json();
+  } catch (const std::exception& e) {
+    ex->reply = std::string("{\"error\":\"") + e.what() + "\"}";
+  }
+  return ex->reply.c_str();
 }
 
 int dpl_exec_disconnect(dpl_exec* ex) {

@@ -73,6 +73,12 @@ class Executor:
         check(lib().dpl_exec_step(self._h, pin, pt, ctypes.byref(loss)))
         return loss.value
 
+    def gemm_profile(self, enable: bool):
+        check(lib().dpl_exec_gemm_profile(self._h, int(enable)))
+
+    def gemm_profile_report(self) -> dict:
+        return json.loads(lib().dpl_exec_gemm_profile_json(self._h).decode())
+
     def timeline(self) -> dict:
         return json.loads(lib().dpl_exec_timeline(self._h).decode())
 
