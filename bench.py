@@ -70,7 +70,7 @@ def load_peaks() -> tuple[dict, str]:
 
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
-    FIELDS = ["index", "clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
+    FIELDS = ["timestamp", "index", "clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
               "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
               "clocks_event_reasons.sw_power_cap"]
 
@@ -90,7 +90,10 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self, name):
+        setattr(self, name, time.time())
 
     def stop(self) -> dict:
         if not self.proc:
@@ -100,22 +103,26 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        sm, smax, reasons = [], [], set()
+        sm, smax, reasons, n_all = [], [], set(), 0
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
+        t0, t1 = getattr(self, "t_start", 0.0), getattr(self, "t_stop", float("inf"))
+        for ts, line in self.lines:
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) < len(self.FIELDS):
+            if len(parts) < len(self.FIELDS) or not (t0 <= ts <= t1):
                 continue
             try:
-                sm.append(float(parts[1]))
-                smax.append(float(parts[2]))
+                clk, cmax, power = float(parts[2]), float(parts[3]), float(parts[4])
             except ValueError:
                 continue
-            for name, v in zip(names, parts[4:8]):
+            n_all += 1
+            for name, v in zip(names, parts[5:9]):
                 if v.lower() == "active":
                     reasons.add(name)
+            if power >= 250.0:  # under load (idle B200 draws ~150 W)
+                sm.append(clk)
+                smax.append(cmax)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples_under_load": len(sm), "samples": n_all}
 
 
 def dist_setup():
@@ -294,15 +301,17 @@ def main():
     lib = _lib.lib()
 
     ex = Executor(model, plan, M, gbs, lr=1e-4, seed=args.seed, rank=rank, world=world, device=rank)
+    clocks = ClockSampler() if rank == 0 else None
+    if clocks:
+        clocks.start()
     for _ in range(args.warmup):
         ex.step()
     torch.cuda.synchronize()
 
     # ------------------------------------------------------------ timed (device)
-    clocks = ClockSampler() if rank == 0 else None
     barrier(world)
     if clocks:
-        clocks.start()
+        clocks.mark("t_start")
     launches0 = lib.dpl_k_launch_count()
     t_wall0 = time.perf_counter()
     tls = []
@@ -313,16 +322,21 @@ def main():
     barrier(world)
     t_wall = time.perf_counter() - t_wall0
     launches = lib.dpl_k_launch_count() - launches0
+    if clocks:
+        clocks.mark("t_stop")
     clk = clocks.stop() if clocks else None
 
     all_tls = gather(tls, world)  # [rank][step]
-    lat, bub = [], []
+    lat, bub, spans = [], [], []
     for k in range(args.steps):
         merged = merge_timelines([all_tls[r][k] for r in range(world)], M, S)
         lat.append(merged["latency"])
         bub.append(merged["bubble"])
+        spans.append((merged["start"], merged["end"]))
     total_launches = sum(gather(launches, world))
-    device_s = sum(lat)
+    # device-timed: first forward of the first timed step to the end of the
+    # last rank's last step, on the GPUs' global timer (max over ranks)
+    device_s = spans[-1][1] - spans[0][0]
     value = args.steps * gbs / device_s
 
     # ------------------------------------------------------------ GEMM roofline (one profiled step)
@@ -383,6 +397,7 @@ def main():
                    "phi": info["phi_expanded"], "parallelism": f"{S} stages x {r0} replicas",
                    "l2": "working set (GBs of activations) far larger than the 126 MB L2"},
         "bubble": statistics.mean(bub),
+        "device_s": device_s,
         "latency": {"measured_ms": measured_ms, "est_ms": pred["est_ms"], "sim_ms": pred["sim_ms"],
                     "sim_bubble": pred["sim_bubble"], "pivot": pred["pivot"],
                     "measured_over_sim": measured_ms / pred["sim_ms"],

@@ -135,6 +135,11 @@ def merge_timelines(parts: list, micro_batches: int, stages: int) -> dict:
             for i in range(micro_batches):
                 s, e = span.get((x, i, kind), (math.nan, math.nan))
                 blocks.append([x, i, kind, s, e])
-    latency = max(p["t0_ns"] * 1e-9 - t0 + p["step_s"] for p in parts)
+    # measured L: first forward start -> end of the last rank's step (apply,
+    # AllReduce and hand-offs drained), on the GPUs' global timer
+    first = min(s for x, i, k, s, e in blocks if k == 0 and x % 2 == 0 and not math.isnan(s))
+    end = max(p["t0_ns"] * 1e-9 - t0 + p["step_s"] for p in parts)
+    latency = end - first
     busy = sum(sum(e - s for x, i, k, s, e in p["blocks"] if x % 2 == 0 and s >= 0) for p in parts)
-    return {"blocks": blocks, "latency": latency, "busy": busy, "bubble": 1.0 - busy / (len(parts) * latency)}
+    return {"blocks": blocks, "latency": latency, "start": first + t0, "end": end + t0, "busy": busy,
+            "bubble": 1.0 - busy / (len(parts) * latency)}
