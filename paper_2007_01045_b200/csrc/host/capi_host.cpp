@@ -12,6 +12,7 @@
 #include "json.hpp"
 #include "pipeplan/costmodel.hpp"
 #include "pipeplan/estimator.hpp"
+#include "pipeplan/executor.hpp"
 #include "pipeplan/io.hpp"
 #include "pipeplan/model.hpp"
 #include "pipeplan/planner.hpp"
@@ -283,6 +284,24 @@ Value dispatch(const Value& req) {
       chain.push_back(std::move(e));
     }
     out["chain"] = std::move(chain);
+    return out;
+  }
+  if (op == "splitconcat_routes") {
+    const PipelinePlan p = plan_of(req.at("plan"));
+    const int k = int_of(req, "boundary", 0);
+    if (k < 0 || k + 1 >= p.compute_stage_count()) throw std::out_of_range("splitconcat_routes: bad boundary");
+    Value routes = Value::array();
+    for (const SplitConcatRoute& r :
+         splitconcat_routes(p.stages[k], p.stages[k + 1], int_of(req, "micro_batch", 1), int_of(req, "rows_per_sample", 1))) {
+      Value e = Value::array();
+      e.push_back(r.src_gpu);
+      e.push_back(r.dst_gpu);
+      e.push_back(static_cast<long long>(r.src_row));
+      e.push_back(static_cast<long long>(r.dst_row));
+      e.push_back(static_cast<long long>(r.rows));
+      routes.push_back(std::move(e));
+    }
+    out["routes"] = std::move(routes);
     return out;
   }
   if (op == "timeline_svg") {

@@ -6,6 +6,7 @@
 // (model.cpp:30-42): a number token without '.', 'e' or 'E' is an integer.
 #pragma once
 
+#include <algorithm>
 #include <cerrno>
 #include <cmath>
 #include <cstdint>
@@ -171,18 +172,24 @@ class Value {
         if (!a_.empty()) newline(depth);
         out += ']';
         break;
-      case Type::object:
+      case Type::object: {
+        // keys in lexicographic order, as nlohmann::json (std::map) writes
+        // them, so files round-trip byte-identically with the reference
+        std::vector<const std::pair<std::string, Value>*> order;
+        for (const auto& kv : o_) order.push_back(&kv);
+        std::sort(order.begin(), order.end(), [](const auto* a, const auto* b) { return a->first < b->first; });
         out += '{';
-        for (std::size_t k = 0; k < o_.size(); ++k) {
+        for (std::size_t k = 0; k < order.size(); ++k) {
           if (k) out += ',';
           newline(depth + 1);
-          write_string(out, o_[k].first);
+          write_string(out, order[k]->first);
           out += indent < 0 ? ":" : ": ";
-          o_[k].second.write(out, indent, depth + 1);
+          order[k]->second.write(out, indent, depth + 1);
         }
         if (!o_.empty()) newline(depth);
         out += '}';
         break;
+      }
     }
   }
 

@@ -36,6 +36,7 @@
 #include "host/json.hpp"
 #include "kernels/elementwise.h"
 #include "layers.h"
+#include "pipeplan/executor.hpp"
 #include "pipeplan/io.hpp"
 #include "pipeplan/simulator.hpp"
 
@@ -91,32 +92,7 @@ __global__ void stamp_kernel(unsigned long long* out) {
   *out = t;
 }
 
-// A contiguous run of micro-batch rows moved between two replicas of
-// adjacent stages (Split-Concat).  Rows are token rows;
-// offsets are relative to each side's own slice.
-struct Route {
-  int src_rank, dst_rank;
-  long long src_row, dst_row, rows;
-};
-
-// Interval-overlap mapping of a micro-batch of B samples from the r_a even
-// slices of stage a to the r_b even slices of stage b: at most r_a + r_b - 1
-// non-empty flows (the reference's model charges r_a * r_b equal flows,
-// costmodel.cpp:60-69).
-std::vector<Route> split_concat_routes(const pipeplan::Stage& a, const pipeplan::Stage& b, int B, int seq) {
-  const int ra = a.replication(), rb = b.replication();
-  std::vector<Route> out;
-  for (int i = 0; i < ra; ++i) {
-    const long long lo_a = 1LL * i * B / ra, hi_a = 1LL * (i + 1) * B / ra;
-    for (int j = 0; j < rb; ++j) {
-      const long long lo_b = 1LL * j * B / rb, hi_b = 1LL * (j + 1) * B / rb;
-      const long long lo = std::max(lo_a, lo_b), hi = std::min(hi_a, hi_b);
-      if (hi <= lo) continue;
-      out.push_back({a.devices[i], b.devices[j], (lo - lo_a) * seq, (lo - lo_b) * seq, (hi - lo) * seq});
-    }
-  }
-  return out;
-}
+using Route = pipeplan::SplitConcatRoute;
 
 struct BlockEvents {
   cudaEvent_t start = nullptr, end = nullptr;
@@ -279,12 +255,12 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
   chain_ = pipeplan::stage_chain(M_, phi_, pipeplan::ScheduleKind::dapple);
 
   if (k_ > 0) {
-    for (const Route& r : split_concat_routes(plan_.stages[k_ - 1], mine, B_, spec_.seq))
-      if (r.dst_rank == rank_) in_routes_.push_back(r);
+    for (const Route& r : pipeplan::splitconcat_routes(plan_.stages[k_ - 1], mine, B_, spec_.seq))
+      if (r.dst_gpu == rank_) in_routes_.push_back(r);
   }
   if (k_ + 1 < S_) {
-    for (const Route& r : split_concat_routes(mine, plan_.stages[k_ + 1], B_, spec_.seq))
-      if (r.src_rank == rank_) out_routes_.push_back(r);
+    for (const Route& r : pipeplan::splitconcat_routes(mine, plan_.stages[k_ + 1], B_, spec_.seq))
+      if (r.src_gpu == rank_) out_routes_.push_back(r);
   }
   numel_global_ = 1LL * gbs_ * spec_.seq * spec_.hidden;
 
@@ -427,8 +403,8 @@ size_t Executor::export_blob(void* blob, size_t cap) {
 void Executor::connect(const uint8_t* blobs, size_t blob_len, int world) {
   if (world != world_) throw std::invalid_argument("dpl exec: world size mismatch");
   std::vector<int> peers;
-  for (const Route& r : out_routes_) peers.push_back(r.dst_rank);
-  for (const Route& r : in_routes_) peers.push_back(r.src_rank);
+  for (const Route& r : out_routes_) peers.push_back(r.dst_gpu);
+  for (const Route& r : in_routes_) peers.push_back(r.src_gpu);
   for (int p : peers) {
     if (p == rank_ || peer_recv_[p]) continue;
     cudaIpcMemHandle_t h;
@@ -467,7 +443,7 @@ void Executor::forward(int i, uint32_t base) {
   if (k_ == 0) {
     x = in_[slot];
   } else {
-    for (const Route& r : in_routes_) wait_flag(compute_, flags() + r.src_rank, base + i + 1);
+    for (const Route& r : in_routes_) wait_flag(compute_, flags() + r.src_gpu, base + i + 1);
     x = recv_act(i);
   }
   record(fwd_ev_[i].start, compute_);
@@ -487,8 +463,8 @@ void Executor::forward(int i, uint32_t base) {
     DPL_CUDA(cudaStreamWaitEvent(send_act_, fwd_done_[i], 0));
     record(send_fwd_ev_[i].start, send_act_);
     for (const Route& r : out_routes_) {
-      uint8_t* peer = peer_recv_[r.dst_rank];
-      const int rows_dst = peer_rows_[r.dst_rank];
+      uint8_t* peer = peer_recv_[r.dst_gpu];
+      const int rows_dst = peer_rows_[r.dst_gpu];
       bf16* dst = reinterpret_cast<bf16*>(peer) + (static_cast<size_t>(i) * rows_dst + r.dst_row) * H;
       DPL_CUDA(cudaMemcpyAsync(dst, out_[i] + r.src_row * H, r.rows * H * 2, cudaMemcpyDeviceToDevice, send_act_));
       uint32_t* flag = reinterpret_cast<uint32_t*>(peer + layout_flags_off(rows_dst)) + rank_;
@@ -505,7 +481,7 @@ void Executor::backward(int i, uint32_t base) {
   if (k_ == S_ - 1) {
     dy = dloss_[slot];
   } else {
-    for (const Route& r : out_routes_) wait_flag(compute_, flags() + world_ + r.dst_rank, base + i + 1);
+    for (const Route& r : out_routes_) wait_flag(compute_, flags() + world_ + r.dst_gpu, base + i + 1);
     dy = recv_grad(i);
   }
   record(bwd_ev_[i].start, compute_);
@@ -539,8 +515,8 @@ void Executor::backward(int i, uint32_t base) {
     DPL_CUDA(cudaStreamWaitEvent(send_grad_s_, bwd_done_[i], 0));
     record(send_bwd_ev_[i].start, send_grad_s_);
     for (const Route& r : in_routes_) {
-      uint8_t* peer = peer_recv_[r.src_rank];
-      const int rows_src = peer_rows_[r.src_rank];
+      uint8_t* peer = peer_recv_[r.src_gpu];
+      const int rows_src = peer_rows_[r.src_gpu];
       bf16* dst = reinterpret_cast<bf16*>(peer + layout_grad_off(rows_src)) +
                   (static_cast<size_t>(i) * rows_src + r.src_row) * H;
       DPL_CUDA(cudaMemcpyAsync(dst, send_grad_[i] + r.dst_row * H, r.rows * H * 2, cudaMemcpyDeviceToDevice,
@@ -635,6 +611,7 @@ std::string Executor::timeline_json() const {
   out["t0_ns"] = static_cast<long long>(t0);
   out["step_s"] = ms(ev_end_);
   out["flops"] = flops_per_step_;
+  out["loss"] = std::isnan(last_loss_) ? Value() : Value(static_cast<double>(last_loss_));
   Value blocks = Value::array();
   auto add = [&](int stage, int mb, int kind, const BlockEvents& b) {
     Value row = Value::array();
@@ -746,11 +723,11 @@ std::string Executor::info() const {
   for (const auto* list : {&in_routes_, &out_routes_})
     for (const Route& r : *list) {
       Value e = Value::array();
-      e.push_back(r.src_rank);
-      e.push_back(r.dst_rank);
-      e.push_back(r.src_row);
-      e.push_back(r.dst_row);
-      e.push_back(r.rows);
+      e.push_back(r.src_gpu);
+      e.push_back(r.dst_gpu);
+      e.push_back(static_cast<long long>(r.src_row));
+      e.push_back(static_cast<long long>(r.dst_row));
+      e.push_back(static_cast<long long>(r.rows));
       routes.push_back(std::move(e));
     }
   v["routes"] = std::move(routes);

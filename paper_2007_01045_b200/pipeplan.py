@@ -14,7 +14,7 @@ from __future__ import annotations
 import json
 from typing import Any
 
-from ._lib import lib
+from ._lib import lib  # noqa: F401  (re-exported for tests)
 
 _ERRORS = {"invalid_argument": ValueError, "out_of_range": IndexError, "runtime_error": RuntimeError,
            "logic_error": RuntimeError}
