@@ -62,16 +62,19 @@ def _erf(x):
     return erf(x)
 
 
-_SQRT2 = math.sqrt(2.0)
-_INV_SQRT_2PI = 1.0 / math.sqrt(2.0 * math.pi)
+# GELU in its tanh form, as the device computes it (gemm_tcgen05.cu gelu_f):
+#   gelu(x) = 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3)))
+_K0 = math.sqrt(2.0 / math.pi)
+_K1 = 0.044715
 
 
 def gelu(x):
-    return 0.5 * x * (1.0 + _erf(x / _SQRT2))
+    return 0.5 * x * (1.0 + np.tanh(_K0 * (x + _K1 * x * x * x)))
 
 
 def dgelu(x):
-    return 0.5 * (1.0 + _erf(x / _SQRT2)) + x * np.exp(-0.5 * x * x) * _INV_SQRT_2PI
+    t = np.tanh(_K0 * (x + _K1 * x * x * x))
+    return 0.5 * (1.0 + t) + 0.5 * x * (1.0 - t * t) * _K0 * (1.0 + 3.0 * _K1 * x * x)
 
 
 @dataclass

@@ -298,23 +298,36 @@ __global__ void softmax_bwd_kernel(const __nv_bfloat16* __restrict__ p, const fl
 }
 
 // ------------------------------------------------------------ bias grads
-// db[c] += sum_r dy[r][c]; each block owns a slab of rows, threads own
-// 8-column vectors; one atomic per column per block.
+// db[c] += sum_r dy[r][c].  Block = 32 column-vectors (256 columns) x 8 row
+// phases; a warp reads 512 contiguous bytes of a row; the 8 row phases are
+// reduced in shared memory, then one atomic per column per block.
 __global__ void colsum_acc_kernel(const __nv_bfloat16* __restrict__ dy, float* __restrict__ db, int rows, int cols,
                                   int rows_per_block) {
+  __shared__ float part[8][256 + 1];
+  const int vx = threadIdx.x & 31, ry = threadIdx.x >> 5;
+  const int vi = blockIdx.x * 32 + vx;
   const int nvec = cols / 8;
   const int r0 = blockIdx.y * rows_per_block;
   const int r1 = min(rows, r0 + rows_per_block);
-  for (int vi = blockIdx.x * blockDim.x + threadIdx.x; vi < nvec; vi += gridDim.x * blockDim.x) {
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int r = r0; r < r1; ++r) {
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (vi < nvec) {
+    for (int r = r0 + ry; r < r1; r += 8) {
       float f[8];
       load8(dy + static_cast<long long>(r) * cols + vi * 8, f);
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc[e] += f[e];
     }
+  }
 #pragma unroll
-    for (int e = 0; e < 8; ++e) atomicAdd(db + vi * 8 + e, acc[e]);
+  for (int e = 0; e < 8; ++e) part[ry][vx * 8 + e] = acc[e];
+  __syncthreads();
+  const int c = threadIdx.x;  // 256 threads, one column each
+  const int col = blockIdx.x * 256 + c;
+  if (col < cols) {
+    float s = 0.f;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) s += part[y][c];
+    atomicAdd(db + col, s);
   }
 }
 
@@ -471,15 +484,12 @@ void softmax_bwd(const void* p, const float* dp, void* ds, int rows, int len, cu
 
 void colsum_acc(const void* dy, float* db, int rows, int cols, cudaStream_t s) {
   count_launch();
-  const int threads = 128;
-  const int nvec = cols / 8;
-  const int gx = (nvec + threads - 1) / threads;
-  // enough row slabs to put ~4 blocks on every SM
-  int gy = std::max(1, (148 * 4) / std::max(gx, 1));
-  gy = std::min(gy, rows);
+  const int gx = (cols + 255) / 256;
+  // about two blocks per SM, at least 64 rows per block
+  int gy = std::max(1, std::min((rows + 63) / 64, (148 * 2 + gx - 1) / gx));
   const int rpb = (rows + gy - 1) / gy;
   gy = (rows + rpb - 1) / rpb;
-  colsum_acc_kernel<<<dim3(gx, gy), threads, 0, s>>>(static_cast<const __nv_bfloat16*>(dy), db, rows, cols, rpb);
+  colsum_acc_kernel<<<dim3(gx, gy), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(dy), db, rows, cols, rpb);
 }
 
 void mse_loss(const void* y, const void* t, void* dy, float* loss_acc, long long n, float grad_scale, cudaStream_t s) {
