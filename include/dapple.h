@@ -84,6 +84,16 @@ typedef struct dpl_gemm_desc {
 #define DPL_EPI_RESID (1u << 8)
 
 int dpl_k_gemm(const dpl_gemm_desc* desc, void* stream);
+/* Fused attention forward, head dim 64: qkv head-split [3][heads][B][S][64],
+ * ctx head-merged [B*S][ldc], lse [heads*B][S]. */
+int dpl_k_attention_fwd(const void* qkv, void* ctx, long long ldc, float* lse, int samples, int seq, int heads,
+                        int causal, void* stream);
+/* Fused attention backward: recomputes P from lse, dO head-split
+ * [heads][B][S][64]; writes dQ/dK/dV head-merged into dqkv [B*S][3H];
+ * workspaces dsum [heads*B][S] and dq_acc [heads*B][S][64] fp32. */
+int dpl_k_attention_bwd(const void* qkv, const void* ctx, long long ldc, const float* lse, const void* dout,
+                        void* dqkv, float* dsum, float* dq_acc, int samples, int seq, int heads, int causal,
+                        void* stream);
 int dpl_k_layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y, float* mean, float* rstd,
                         int rows, int h, float eps, void* stream);
 int dpl_k_layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd, const float* gamma,

@@ -180,10 +180,13 @@ def layer_forward(model: Model, layer: int, p: dict, x: np.ndarray, samples: int
     sc = (qh @ k.transpose(0, 1, 3, 2)) * (1.0 / math.sqrt(d))
     if model.causal:
         sc = np.where(np.triu(np.ones((s, s), bool), 1), -np.inf, sc)
-    sc = sc - sc.max(-1, keepdims=True)
-    P = np.exp(sc)
-    P = q(P / P.sum(-1, keepdims=True))
-    ctx = q((P @ v).transpose(0, 2, 1, 3).reshape(samples * s, H))
+    # flash-attention numerics (csrc/kernels/attention.cu): unnormalised
+    # exp(s - rowmax) is what gets rounded to bf16 for the PV product, the
+    # row sum l stays fp32, the context is divided by l at the end
+    e = np.exp(sc - sc.max(-1, keepdims=True))
+    l = e.sum(-1, keepdims=True)
+    P = e / l
+    ctx = q(((q(e) @ v) / l).transpose(0, 2, 1, 3).reshape(samples * s, H))
     h = q(x + ctx @ p["Wo"].T + p["bo"])
     ln2, c2 = _ln_fwd(h, p["ln2_g"], p["ln2_b"], model.eps)
     ln2 = q(ln2)
@@ -220,12 +223,16 @@ def layer_backward(model: Model, layer: int, p: dict, cache, dy: np.ndarray, sam
     dh = q(dh + dy)
     gr["Wo"], gr["bo"] = dh.T @ ctx, dh.sum(0)
     dctx = q(dh @ p["Wo"]).reshape(samples, s, nh, d).transpose(0, 2, 1, 3)
+    # flash-attention backward: D = rowsum(dO * O) from the stored context,
+    # dS from the fp32 probabilities, P and dS rounded to bf16 as MMA operands
+    ctx_h = ctx.reshape(samples, s, nh, d).transpose(0, 2, 1, 3)
+    D = (dctx * ctx_h).sum(-1, keepdims=True)
     dP = dctx @ v.transpose(0, 1, 3, 2)
-    dS = q(P * (dP - (P * dP).sum(-1, keepdims=True)))
+    dS = P * (dP - D)
     scale = 1.0 / math.sqrt(d)
-    dq = q(scale * (dS @ k))
-    dk = q(scale * (dS.transpose(0, 1, 3, 2) @ qh))
-    dv = q(P.transpose(0, 1, 3, 2) @ dctx)
+    dq = q(scale * (q(dS) @ k))
+    dk = q(scale * (q(dS).transpose(0, 1, 3, 2) @ qh))
+    dv = q(q(P).transpose(0, 1, 3, 2) @ dctx)
     dqkv = np.concatenate([t.transpose(0, 2, 1, 3).reshape(samples * s, H) for t in (dq, dk, dv)], axis=1)
     gr["Wqkv"], gr["bqkv"] = dqkv.T @ ln1, dqkv.sum(0)
     dx, gr["ln1_g"], gr["ln1_b"] = _ln_bwd(q(dqkv @ p["Wqkv"]), p["ln1_g"], c1)

@@ -6,6 +6,7 @@
 #include <string>
 
 #include "dapple.h"
+#include "kernels/attention.h"
 #include "kernels/elementwise.h"
 #include "kernels/gemm.h"
 
@@ -53,6 +54,47 @@ int dpl_k_gemm(const dpl_gemm_desc* d, void* stream) {
     dpl::GemmOp op;
     op.prepare(g);
     op.launch(static_cast<cudaStream_t>(stream));
+  });
+}
+
+int dpl_k_attention_fwd(const void* qkv, void* ctx, long long ldc, float* lse, int samples, int seq, int heads,
+                        int causal, void* stream) {
+  return guarded([&] {
+    dpl::AttentionDesc d;
+    d.qkv = qkv;
+    d.ctx = ctx;
+    d.ldc = ldc;
+    d.lse = lse;
+    d.samples = samples;
+    d.seq = seq;
+    d.heads = heads;
+    d.causal = causal;
+    dpl::AttentionOp op;
+    op.prepare(d);
+    op.forward(static_cast<cudaStream_t>(stream));
+  });
+}
+
+int dpl_k_attention_bwd(const void* qkv, const void* ctx, long long ldc, const float* lse, const void* dout,
+                        void* dqkv, float* dsum, float* dq_acc, int samples, int seq, int heads, int causal,
+                        void* stream) {
+  return guarded([&] {
+    dpl::AttentionDesc d;
+    d.qkv = qkv;
+    d.ctx = const_cast<void*>(ctx);
+    d.ldc = ldc;
+    d.lse = const_cast<float*>(lse);
+    d.dout = dout;
+    d.dqkv = dqkv;
+    d.dsum = dsum;
+    d.dq_acc = dq_acc;
+    d.samples = samples;
+    d.seq = seq;
+    d.heads = heads;
+    d.causal = causal;
+    dpl::AttentionOp op;
+    op.prepare(d);
+    op.backward(static_cast<cudaStream_t>(stream));
   });
 }
 

@@ -1,0 +1,649 @@
+// Fused attention (flash style) for head dim 64 on sm_100a.
+//
+// Forward, one CTA per (z = head * B + sample, 128-query tile):
+//   warp 0      TMA: Q tile once, K/V tiles (128 keys) through a 2-stage ring
+//   warp 1      MMA: S_j = Q K_j^T  (M=128, N=128, K=64)   -> TMEM (2 buffers)
+//                    O_j = P_j V_j   (M=128, N=64,  K=128)  -> TMEM (2 buffers)
+//   warp 2      TMEM allocator
+//   warps 4-7   softmax: one thread per query row reads its S row from TMEM
+//               (no cross-thread reductions), keeps the running max / sum
+//               (online softmax, exp2 on the SFU), writes P_j (bf16) into a
+//               SWIZZLE_128B smem tile for the PV MMA, and accumulates
+//               O = O * alpha + O_j in registers.
+// Output: context head-merged into [R][H] (row = b*S + q, col = h*64 + j),
+// and the per-row log-sum-exp (natural log of the scaled scores) for the
+// backward pass.  S and P never touch HBM.
+//
+// Layout: qkv is head-split [3][heads][B][S][64] (written that way by the QKV
+// GEMM epilogue), so one 3-D tensor map {64, S, 3*heads*B} serves Q, K and V.
+// Because a [128 x 64] bf16 tile is exactly 128 rows of one 128-byte swizzle
+// atom, the same smem bytes are a valid K-major operand (M/N = rows) and a
+// valid MN-major operand (K = rows); P is written once in that layout.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "attention.h"
+#include "gemm.h"
+#include "ptx.cuh"
+
+namespace dpl {
+
+namespace {
+
+constexpr int kT = 128;           // query / key tile
+constexpr int kD = 64;            // head dim
+constexpr int kTileBytes = kT * kD * 2;  // 16 KB
+constexpr int kFwdThreads = 256;
+
+struct AttnFwdParams {
+  CUtensorMap qkv;  // {64, S, 3*heads*B}
+  int S, B, heads, causal, z_count;
+  float scale_log2;  // (1/sqrt(d)) * log2(e)
+  __nv_bfloat16* ctx;
+  long long ldc;  // H
+  float* lse;     // [z][S]
+};
+
+__device__ __forceinline__ float exp2_fast(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// byte offset of 16-byte chunk `c` (0..7) of row `r` inside a SWIZZLE_128B
+// [rows x 64] bf16 tile (1024-byte aligned)
+__device__ __forceinline__ uint32_t sw128(int r, int c) { return r * 128 + ((c ^ (r & 7)) << 4); }
+
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// Two CTAs per SM (80 KB smem, 256 TMEM columns each): S single-buffered,
+// O double-buffered; K, V, P single-buffered -- the co-resident CTA fills the
+// gaps this CTA's dependency chain leaves.
+__global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_constant__ AttnFwdParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                // 16 KB
+  uint8_t* sK = sQ + kTileBytes;     // 16 KB
+  uint8_t* sV = sK + kTileBytes;     // 16 KB
+  uint8_t* sP = sV + kTileBytes;     // 32 KB (two 64-key halves)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * kTileBytes);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;
+  uint64_t* k_empty = bars + 2;
+  uint64_t* v_full = bars + 3;
+  uint64_t* v_empty = bars + 4;
+  uint64_t* s_full = bars + 5;
+  uint64_t* s_empty = bars + 6;
+  uint64_t* p_full = bars + 7;
+  uint64_t* p_empty = bars + 8;
+  uint64_t* o_full = bars + 9;    // [2]
+  uint64_t* o_empty = bars + 11;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+
+  const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
+  const int qt = blockIdx.x, z = blockIdx.y;
+  const int q0 = qt * kT;
+  const int n_kv = p.causal ? qt + 1 : p.S / kT;
+  const int zk = p.z_count + z, zv = 2 * p.z_count + z;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&p.qkv);
+    ptx::mbar_init(q_full, 1);
+    ptx::mbar_init(k_full, 1);
+    ptx::mbar_init(k_empty, 1);
+    ptx::mbar_init(v_full, 1);
+    ptx::mbar_init(v_empty, 1);
+    ptx::mbar_init(s_full, 1);
+    ptx::mbar_init(s_empty, 128);
+    ptx::mbar_init(p_full, 128);
+    ptx::mbar_init(p_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&o_full[i], 1);
+      ptx::mbar_init(&o_empty[i], 128);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<256>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // TMEM columns: S [0,128), O buffers [128,192) [192,256)
+
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::mbar_arrive_expect_tx(q_full, kTileBytes);
+      ptx::tma_load_3d(sQ, &p.qkv, q_full, 0, q0, z);
+      for (int j = 0; j < n_kv; ++j) {
+        const uint32_t ph = (j & 1) ^ 1;
+        ptx::mbar_wait(k_empty, ph);
+        ptx::mbar_arrive_expect_tx(k_full, kTileBytes);
+        ptx::tma_load_3d(sK, &p.qkv, k_full, 0, j * kT, zk);
+        ptx::mbar_wait(v_empty, ph);
+        ptx::mbar_arrive_expect_tx(v_full, kTileBytes);
+        ptx::tma_load_3d(sV, &p.qkv, v_full, 0, j * kT, zv);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc_s = ptx::idesc_bf16_f32(kT, kT, false, false);  // Q K-major, K K-major
+      const uint32_t idesc_o = ptx::idesc_bf16_f32(kT, kD, false, true);   // P K-major, V MN-major
+      const uint32_t aq = ptx::smem_addr(sQ), bk = ptx::smem_addr(sK), bv = ptx::smem_addr(sV);
+      const uint32_t ap = ptx::smem_addr(sP);
+      ptx::mbar_wait(q_full, 0);
+      for (int j = 0; j < n_kv; ++j) {
+        const uint32_t ph = j & 1;
+        // S_j = Q K_j^T once K_j landed and S_{j-1} was read
+        ptx::mbar_wait(k_full, ph);
+        ptx::mbar_wait(s_empty, ph ^ 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < kD / 16; ++k)
+          ptx::mma_bf16(tmem, ptx::smem_desc_sw128(aq + k * 32, 16, 1024), ptx::smem_desc_sw128(bk + k * 32, 16, 1024),
+                        idesc_s, k > 0);
+        ptx::mma_commit(s_full);
+        ptx::mma_commit(k_empty);
+        // O_j = P_j V_j
+        ptx::mbar_wait(v_full, ph);
+        ptx::mbar_wait(p_full, ph);
+        ptx::mbar_wait(&o_empty[j & 1], ((j >> 1) & 1) ^ 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < kT / 16; ++k) {
+          const uint32_t a_off = (k >> 2) * kTileBytes + (k & 3) * 32;  // 64-key halves 16 KB apart
+          ptx::mma_bf16(tmem + 128 + (j & 1) * kD, ptx::smem_desc_sw128(ap + a_off, 16, 1024),
+                        ptx::smem_desc_sw128(bv + k * 16 * 128, 16, 1024), idesc_o, k > 0);
+        }
+        ptx::mma_commit(&o_full[j & 1]);
+        ptx::mma_commit(v_empty);
+        ptx::mma_commit(p_empty);
+      }
+    }
+  } else if (warp >= 4) {
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;  // query row within the tile
+    const int q = q0 + r;
+    const uint32_t trow = (quad * 32) << 16;
+    const float c = p.scale_log2;
+    float o[kD];
+#pragma unroll
+    for (int i = 0; i < kD; ++i) o[i] = 0.f;
+    float m = -INFINITY, l = 0.f;
+    float alpha_prev = 0.f;
+    for (int j = 0; j <= n_kv; ++j) {
+      float alpha = 1.f;
+      if (j < n_kv) {
+        const uint32_t ph = j & 1;
+        ptx::mbar_wait(s_full, ph);
+        ptx::tc_fence_after();
+        const bool diag = p.causal && j == n_kv - 1;
+        const int lim = diag ? r : kT - 1;  // last unmasked key column of this row
+        // pass 1: row max of the raw scores (scale > 0 commutes with max)
+        float mx = -INFINITY;
+#pragma unroll 1
+        for (int cc = 0; cc < kT / 32; ++cc) {
+          uint32_t v[32];
+          ptx::tmem_ld_32x32b_x32(tmem + trow + cc * 32, v);
+          ptx::tmem_wait_ld();
+          if (!diag) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(v[e]));
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) mx = cc * 32 + e <= lim ? fmaxf(mx, __uint_as_float(v[e])) : mx;
+          }
+        }
+        const float m_new = fmaxf(m, mx * c);
+        alpha = exp2_fast(m - m_new);
+        m = m_new;
+        ptx::mbar_wait(p_empty, ph ^ 1);  // PV_{j-1} finished reading P
+        float rs = 0.f;
+#pragma unroll 1
+        for (int cc = 0; cc < kT / 32; ++cc) {
+          uint32_t v[32];
+          ptx::tmem_ld_32x32b_x32(tmem + trow + cc * 32, v);
+          ptx::tmem_wait_ld();
+          float pv[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const float x = exp2_fast(fmaf(__uint_as_float(v[e]), c, -m));
+            pv[e] = (!diag || cc * 32 + e <= lim) ? x : 0.f;
+            rs += pv[e];
+          }
+          uint8_t* half = sP + (cc >> 1) * kTileBytes;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            uint4 w;
+            w.x = pack_bf16(pv[8 * u + 0], pv[8 * u + 1]);
+            w.y = pack_bf16(pv[8 * u + 2], pv[8 * u + 3]);
+            w.z = pack_bf16(pv[8 * u + 4], pv[8 * u + 5]);
+            w.w = pack_bf16(pv[8 * u + 6], pv[8 * u + 7]);
+            *reinterpret_cast<uint4*>(half + sw128(r, (cc & 1) * 4 + u)) = w;
+          }
+        }
+        l = l * alpha + rs;
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(s_empty);
+        fence_async_smem();
+        ptx::mbar_arrive(p_full);
+      }
+      if (j > 0) {  // O = O * alpha_{j-1} + O_{j-1}
+        const int jj = j - 1;
+        ptx::mbar_wait(&o_full[jj & 1], (jj >> 1) & 1);
+        ptx::tc_fence_after();
+        const uint32_t to = tmem + trow + 128 + (jj & 1) * kD;
+#pragma unroll
+        for (int cc = 0; cc < kD / 32; ++cc) {
+          uint32_t v[32];
+          ptx::tmem_ld_32x32b_x32(to + cc * 32, v);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[cc * 32 + e] = fmaf(o[cc * 32 + e], alpha_prev, __uint_as_float(v[e]));
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&o_empty[jj & 1]);
+      }
+      alpha_prev = alpha;
+    }
+    const float inv = 1.f / l;
+    const int b = z % p.B, h = z / p.B;
+    __nv_bfloat16* out = p.ctx + static_cast<long long>(b * p.S + q) * p.ldc + h * kD;
+#pragma unroll
+    for (int u = 0; u < kD / 8; ++u) {
+      uint4 w;
+      w.x = pack_bf16(o[8 * u + 0] * inv, o[8 * u + 1] * inv);
+      w.y = pack_bf16(o[8 * u + 2] * inv, o[8 * u + 3] * inv);
+      w.z = pack_bf16(o[8 * u + 4] * inv, o[8 * u + 5] * inv);
+      w.w = pack_bf16(o[8 * u + 6] * inv, o[8 * u + 7] * inv);
+      reinterpret_cast<uint4*>(out)[u] = w;
+    }
+    p.lse[static_cast<long long>(z) * p.S + q] = (m + log2f(l)) * 0.69314718055994531f;
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<256>(tmem);
+  }
+}
+
+// ---------------------------------------------------------------- backward
+// One CTA per (z, 128-key tile j), looping over query tiles i:
+//   S  = Q_i K_j^T,  dP = dO_i V_j^T                      (TMEM, 128 x 128 each)
+//   P  = exp(scale*S - lse),  dS = P * (dP - D)           (softmax warps -> smem bf16)
+//   dV += P^T dO_i,  dK += dS^T Q_i                         (TMEM, accumulate over i)
+//   dQ_i = dS K_j  -> fp32 atomics into dq_acc[z][S][64]   (summed over the key tiles)
+// D = rowsum(dO * O) comes from attn_bwd_prep_kernel; dq_acc is turned into
+// bf16 by attn_bwd_dq_kernel.  dK, dV are written head-merged into dqkv.
+constexpr int kBwdThreads = 384;  // warps 4-11: two per TMEM lane quadrant
+
+struct AttnBwdParams {
+  CUtensorMap qkv;   // {64, S, 3*heads*B}
+  CUtensorMap dout;  // {64, S, heads*B}   dO head-split
+  int S, B, heads, causal, z_count;
+  float scale, scale_log2;
+  const float* lse;  // [z][S]
+  const float* dsum; // [z][S]  D
+  float* dq_acc;     // [z][S][64]
+  __nv_bfloat16* dqkv;  // [B*S][3H]
+  long long ld;         // 3H
+  int H;
+};
+
+__global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_constant__ AttnBwdParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem;                         // 16 KB
+  uint8_t* sV = sK + kTileBytes;              // 16 KB
+  uint8_t* sQ = sV + kTileBytes;              // 2 x 16 KB
+  uint8_t* sO = sQ + 2 * kTileBytes;          // 2 x 16 KB (dO)
+  uint8_t* sP = sO + 2 * kTileBytes;          // 32 KB (two 64-key halves)
+  uint8_t* sS = sP + 2 * kTileBytes;          // 32 KB (dS)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sS + 2 * kTileBytes);
+  uint64_t* kv_full = bars;
+  uint64_t* qdo_full = bars + 1;   // [2]
+  uint64_t* qdo_empty = bars + 3;  // [2]
+  uint64_t* sp_full = bars + 5;
+  uint64_t* sp_empty = bars + 6;
+  uint64_t* pds_full = bars + 7;
+  uint64_t* pds_empty = bars + 8;
+  uint64_t* dq_full = bars + 9;
+  uint64_t* dq_empty = bars + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+
+  const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
+  const int j = blockIdx.x, z = blockIdx.y;
+  const int k0 = j * kT;
+  const int n_q = p.S / kT;
+  const int i_first = p.causal ? j : 0;
+  const int n_iter = n_q - i_first;
+  const int zk = p.z_count + z, zv = 2 * p.z_count + z;
+  // TMEM: S [0,128), dP [128,256), dV [256,320), dK [320,384), dQ [384,448)
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&p.qkv);
+    ptx::tma_prefetch_desc(&p.dout);
+    ptx::mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&qdo_full[i], 1);
+      ptx::mbar_init(&qdo_empty[i], 1);
+    }
+    ptx::mbar_init(sp_full, 1);
+    ptx::mbar_init(sp_empty, 256);
+    ptx::mbar_init(pds_full, 256);
+    ptx::mbar_init(pds_empty, 1);
+    ptx::mbar_init(dq_full, 1);
+    ptx::mbar_init(dq_empty, 256);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::mbar_arrive_expect_tx(kv_full, 2 * kTileBytes);
+      ptx::tma_load_3d(sK, &p.qkv, kv_full, 0, k0, zk);
+      ptx::tma_load_3d(sV, &p.qkv, kv_full, 0, k0, zv);
+      for (int it = 0; it < n_iter; ++it) {
+        const int st = it & 1, q0 = (i_first + it) * kT;
+        ptx::mbar_wait(&qdo_empty[st], ((it >> 1) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&qdo_full[st], 2 * kTileBytes);
+        ptx::tma_load_3d(sQ + st * kTileBytes, &p.qkv, &qdo_full[st], 0, q0, z);
+        ptx::tma_load_3d(sO + st * kTileBytes, &p.dout, &qdo_full[st], 0, q0, z);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t id_sq = ptx::idesc_bf16_f32(kT, kT, false, false);  // S, dP: K-major A and B
+      const uint32_t id_tt = ptx::idesc_bf16_f32(kT, kD, true, true);    // dV, dK: A^T, B MN-major
+      const uint32_t id_dq = ptx::idesc_bf16_f32(kT, kD, false, true);   // dQ: dS K-major, K MN-major
+      const uint32_t ak = ptx::smem_addr(sK), av = ptx::smem_addr(sV);
+      const uint32_t ap = ptx::smem_addr(sP), as = ptx::smem_addr(sS);
+      ptx::mbar_wait(kv_full, 0);
+      for (int it = 0; it < n_iter; ++it) {
+        const int st = it & 1;
+        const uint32_t aq = ptx::smem_addr(sQ + st * kTileBytes), ao = ptx::smem_addr(sO + st * kTileBytes);
+        ptx::mbar_wait(&qdo_full[st], (it >> 1) & 1);
+        ptx::mbar_wait(sp_empty, (it & 1) ^ 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < kD / 16; ++k) {
+          ptx::mma_bf16(tmem, ptx::smem_desc_sw128(aq + k * 32, 16, 1024), ptx::smem_desc_sw128(ak + k * 32, 16, 1024),
+                        id_sq, k > 0);
+          ptx::mma_bf16(tmem + 128, ptx::smem_desc_sw128(ao + k * 32, 16, 1024),
+                        ptx::smem_desc_sw128(av + k * 32, 16, 1024), id_sq, k > 0);
+        }
+        ptx::mma_commit(sp_full);
+        ptx::mbar_wait(pds_full, it & 1);
+        ptx::mbar_wait(dq_empty, (it & 1) ^ 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < kT / 16; ++k) {
+          // A^T views: 64-key halves 16 KB apart (LBO), 16 query rows per K step
+          const uint32_t row_step = k * 16 * 128;
+          ptx::mma_bf16(tmem + 256, ptx::smem_desc_sw128(ap + row_step, kTileBytes, 1024),
+                        ptx::smem_desc_sw128(ao + row_step, 16, 1024), id_tt, (it | k) != 0);
+          ptx::mma_bf16(tmem + 320, ptx::smem_desc_sw128(as + row_step, kTileBytes, 1024),
+                        ptx::smem_desc_sw128(aq + row_step, 16, 1024), id_tt, (it | k) != 0);
+          const uint32_t a_off = (k >> 2) * kTileBytes + (k & 3) * 32;
+          ptx::mma_bf16(tmem + 384, ptx::smem_desc_sw128(as + a_off, 16, 1024),
+                        ptx::smem_desc_sw128(ak + row_step, 16, 1024), id_dq, k > 0);
+        }
+        ptx::mma_commit(&qdo_empty[st]);
+        ptx::mma_commit(pds_empty);
+        ptx::mma_commit(dq_full);
+      }
+    }
+  } else if (warp >= 4) {
+    const int quad = warp & 3;
+    const int half = (warp - 4) >> 2;  // key columns [64*half, 64*half + 64); dQ / dK-dV split likewise
+    const int r = quad * 32 + lane;
+    const uint32_t trow = (quad * 32) << 16;
+    const int b = z % p.B, h = z / p.B;
+    for (int it = 0; it < n_iter; ++it) {
+      const int i = i_first + it, q = i * kT + r;
+      const float lse2 = p.lse[static_cast<long long>(z) * p.S + q] * 1.4426950408889634f;
+      const float dsum = p.dsum[static_cast<long long>(z) * p.S + q];
+      const bool diag = p.causal && i == j;
+      ptx::mbar_wait(sp_full, it & 1);
+      ptx::tc_fence_after();
+      ptx::mbar_wait(pds_empty, (it & 1) ^ 1);  // previous P / dS consumed by the MMAs
+#pragma unroll 1
+      for (int c = 2 * half; c < 2 * half + 2; ++c) {
+        uint32_t vs[32], vp[32];
+        ptx::tmem_ld_32x32b_x32(tmem + trow + c * 32, vs);
+        ptx::tmem_ld_32x32b_x32(tmem + trow + 128 + c * 32, vp);
+        ptx::tmem_wait_ld();
+        float pv[32], dv[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const bool masked = diag && (k0 + c * 32 + e > q);
+          const float pe = masked ? 0.f : exp2_fast(__uint_as_float(vs[e]) * p.scale_log2 - lse2);
+          pv[e] = pe;
+          dv[e] = pe * (__uint_as_float(vp[e]) - dsum);
+        }
+        uint8_t* hp = sP + (c >> 1) * kTileBytes;
+        uint8_t* hs = sS + (c >> 1) * kTileBytes;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int chunk = (c & 1) * 4 + u;
+          uint4 w;
+          w.x = pack_bf16(pv[8 * u + 0], pv[8 * u + 1]);
+          w.y = pack_bf16(pv[8 * u + 2], pv[8 * u + 3]);
+          w.z = pack_bf16(pv[8 * u + 4], pv[8 * u + 5]);
+          w.w = pack_bf16(pv[8 * u + 6], pv[8 * u + 7]);
+          *reinterpret_cast<uint4*>(hp + sw128(r, chunk)) = w;
+          w.x = pack_bf16(dv[8 * u + 0], dv[8 * u + 1]);
+          w.y = pack_bf16(dv[8 * u + 2], dv[8 * u + 3]);
+          w.z = pack_bf16(dv[8 * u + 4], dv[8 * u + 5]);
+          w.w = pack_bf16(dv[8 * u + 6], dv[8 * u + 7]);
+          *reinterpret_cast<uint4*>(hs + sw128(r, chunk)) = w;
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(sp_empty);
+      fence_async_smem();
+      ptx::mbar_arrive(pds_full);
+      // dQ_i partial of this key tile -> fp32 atomics
+      ptx::mbar_wait(dq_full, it & 1);
+      ptx::tc_fence_after();
+      float4* dst = reinterpret_cast<float4*>(p.dq_acc + (static_cast<long long>(z) * p.S + q) * kD);
+      {
+        const int c = half;  // 32 of the 64 dQ columns
+        uint32_t v[32];
+        ptx::tmem_ld_32x32b_x32(tmem + trow + 384 + c * 32, v);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          atomicAdd(dst + c * 8 + u, make_float4(__uint_as_float(v[4 * u]), __uint_as_float(v[4 * u + 1]),
+                                                 __uint_as_float(v[4 * u + 2]), __uint_as_float(v[4 * u + 3])));
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(dq_empty);
+    }
+    // dV, dK of this key tile (all MMAs done once the last dQ arrived)
+    if (n_iter == 0) {
+      // causal tile with no queries: cannot happen (i_first = j < n_q)
+    }
+    const int key = k0 + r;
+    __nv_bfloat16* row = p.dqkv + static_cast<long long>(b * p.S + key) * p.ld + h * kD;
+    {
+      const int which = half;  // 0: dV (cols 2H..), 1: dK (cols H.., scaled)
+      const float f = which ? p.scale : 1.f;
+      __nv_bfloat16* out = row + (which ? p.H : 2 * p.H);
+#pragma unroll
+      for (int c = 0; c < kD / 32; ++c) {
+        uint32_t v[32];
+        ptx::tmem_ld_32x32b_x32(tmem + trow + (which ? 320 : 256) + c * 32, v);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          uint4 w;
+          w.x = pack_bf16(f * __uint_as_float(v[8 * u + 0]), f * __uint_as_float(v[8 * u + 1]));
+          w.y = pack_bf16(f * __uint_as_float(v[8 * u + 2]), f * __uint_as_float(v[8 * u + 3]));
+          w.z = pack_bf16(f * __uint_as_float(v[8 * u + 4]), f * __uint_as_float(v[8 * u + 5]));
+          w.w = pack_bf16(f * __uint_as_float(v[8 * u + 6]), f * __uint_as_float(v[8 * u + 7]));
+          reinterpret_cast<uint4*>(out + c * 32)[u] = w;
+        }
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+}
+
+// D[z][q] = sum_j dO[z][q][j] * O[b*S+q][h*64+j]; zeroes dq_acc.  One warp
+// per row, 8 lanes x 8 elements.
+__global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ dout, const __nv_bfloat16* __restrict__ out,
+                                     long long ldo, float* __restrict__ dsum, float* __restrict__ dq_acc, int S, int B,
+                                     int rows) {
+  const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
+  for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < rows; row += gridDim.x * warps) {
+    const int z = row / S, q = row % S, b = z % B, h = z / B;
+    float acc = 0.f;
+    if (lane < 8) {
+      const uint4 a = reinterpret_cast<const uint4*>(dout + static_cast<long long>(row) * kD)[lane];
+      const uint4 c = reinterpret_cast<const uint4*>(out + static_cast<long long>(b * S + q) * ldo + h * kD)[lane];
+      const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
+      const __nv_bfloat162* pc = reinterpret_cast<const __nv_bfloat162*>(&c);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 x = __bfloat1622float2(pa[e]), y = __bfloat1622float2(pc[e]);
+        acc += x.x * y.x + x.y * y.y;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) dsum[row] = acc;
+    reinterpret_cast<float2*>(dq_acc + static_cast<long long>(row) * kD)[lane] = make_float2(0.f, 0.f);
+  }
+}
+
+// dqkv[b*S+q][h*64+j] = bf16(scale * dq_acc[z][q][j])
+__global__ void attn_bwd_dq_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv, long long ld,
+                                   float scale, int S, int B, int rows) {
+  const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
+  for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < rows; row += gridDim.x * warps) {
+    const int z = row / S, q = row % S, b = z % B, h = z / B;
+    const float2 v = reinterpret_cast<const float2*>(dq_acc + static_cast<long long>(row) * kD)[lane];
+    reinterpret_cast<uint32_t*>(dqkv + static_cast<long long>(b * S + q) * ld + h * kD)[lane] =
+        pack_bf16(scale * v.x, scale * v.y);
+  }
+}
+
+constexpr int kBwdSmem = 1024 + 10 * kTileBytes + 256;
+
+PFN_cuTensorMapEncodeTiled_v12000 encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      throw std::runtime_error("dpl: cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }();
+  return fn;
+}
+
+CUtensorMap head_map(const void* base, int S, long long mats) {
+  CUtensorMap map;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(kD), static_cast<cuuint64_t>(S), static_cast<cuuint64_t>(mats)};
+  cuuint64_t strides[2] = {kD * 2, static_cast<cuuint64_t>(S) * kD * 2};
+  cuuint32_t box[3] = {kD, kT, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  const CUresult rc = encode()(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box,
+                               es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (rc != CUDA_SUCCESS) throw std::runtime_error("dpl attention: tensor map encode failed");
+  return map;
+}
+
+constexpr int kFwdSmem = 1024 + 5 * kTileBytes + 256;
+
+}  // namespace
+
+void AttentionOp::prepare(const AttentionDesc& d) {
+  if (d.head_dim != kD) throw std::invalid_argument("dpl attention: head dim must be 64");
+  if (d.seq % kT != 0) throw std::invalid_argument("dpl attention: sequence length must be a multiple of 128");
+  desc_ = d;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem);
+    cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem);
+  });
+  fwd_map_ = head_map(d.qkv, d.seq, 3LL * d.heads * d.samples);
+  if (d.dout) dout_map_ = head_map(d.dout, d.seq, 1LL * d.heads * d.samples);
+  ready_ = true;
+}
+
+void AttentionOp::forward(cudaStream_t s) const {
+  if (!ready_) throw std::logic_error("dpl attention: forward before prepare");
+  AttnFwdParams p;
+  p.qkv = fwd_map_;
+  p.S = desc_.seq;
+  p.B = desc_.samples;
+  p.heads = desc_.heads;
+  p.causal = desc_.causal;
+  p.z_count = desc_.heads * desc_.samples;
+  p.scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(kD));
+  p.ctx = static_cast<__nv_bfloat16*>(desc_.ctx);
+  p.ldc = desc_.ldc;
+  p.lse = desc_.lse;
+  count_launch();
+  attn_fwd_kernel<<<dim3(desc_.seq / kT, p.z_count), kFwdThreads, kFwdSmem, s>>>(p);
+}
+
+void AttentionOp::backward(cudaStream_t s) const {
+  if (!ready_ || !desc_.dout || !desc_.dqkv || !desc_.dsum || !desc_.dq_acc)
+    throw std::logic_error("dpl attention: backward needs dout, dqkv and workspaces");
+  const int z_count = desc_.heads * desc_.samples;
+  const int rows = z_count * desc_.seq;
+  const float scale = 1.0f / std::sqrt(static_cast<float>(kD));
+  count_launch(3);
+  attn_bwd_prep_kernel<<<std::min((rows + 7) / 8, 148 * 16), 256, 0, s>>>(
+      static_cast<const __nv_bfloat16*>(desc_.dout), static_cast<const __nv_bfloat16*>(desc_.ctx), desc_.ldc,
+      desc_.dsum, desc_.dq_acc, desc_.seq, desc_.samples, rows);
+  AttnBwdParams p;
+  p.qkv = fwd_map_;
+  p.dout = dout_map_;
+  p.S = desc_.seq;
+  p.B = desc_.samples;
+  p.heads = desc_.heads;
+  p.causal = desc_.causal;
+  p.z_count = z_count;
+  p.scale = scale;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.lse = desc_.lse;
+  p.dsum = desc_.dsum;
+  p.dq_acc = desc_.dq_acc;
+  p.dqkv = static_cast<__nv_bfloat16*>(desc_.dqkv);
+  p.ld = 3LL * desc_.heads * kD;
+  p.H = desc_.heads * kD;
+  attn_bwd_kernel<<<dim3(desc_.seq / kT, z_count), kBwdThreads, kBwdSmem, s>>>(p);
+  attn_bwd_dq_kernel<<<std::min((rows + 7) / 8, 148 * 16), 256, 0, s>>>(desc_.dq_acc, p.dqkv, p.ld, scale, desc_.seq,
+                                                                        desc_.samples, rows);
+}
+
+}  // namespace dpl

@@ -129,7 +129,7 @@ __global__ void layernorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const
                                      const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
                                      const float* __restrict__ gamma, const __nv_bfloat16* __restrict__ dresid,
                                      __nv_bfloat16* __restrict__ dx, float* __restrict__ dgamma,
-                                     float* __restrict__ dbeta, int rows, int h) {
+                                     float* __restrict__ dbeta, float* __restrict__ ws, int rows, int h) {
   extern __shared__ float red[];  // [warps][2][h]
   const int warps = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5;
@@ -204,9 +204,25 @@ __global__ void layernorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const
       a += red[(w * 2) * h + c];
       b += red[(w * 2 + 1) * h + c];
     }
-    atomicAdd(dgamma + c, a);
-    atomicAdd(dbeta + c, b);
+    if (ws) {  // per-block partials, summed by ln_param_reduce_kernel
+      ws[static_cast<long long>(blockIdx.x) * 2 * h + c] = a;
+      ws[static_cast<long long>(blockIdx.x) * 2 * h + h + c] = b;
+    } else {
+      atomicAdd(dgamma + c, a);
+      atomicAdd(dbeta + c, b);
+    }
   }
+}
+
+// dgamma[c] += sum_b ws[b][0][c]; dbeta[c] += sum_b ws[b][1][c]
+__global__ void ln_param_reduce_kernel(const float* __restrict__ ws, float* __restrict__ dgamma,
+                                       float* __restrict__ dbeta, int blocks, int h) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= 2 * h) return;
+  float s = 0.f;
+  for (int b = 0; b < blocks; ++b) s += ws[static_cast<long long>(b) * 2 * h + c];
+  if (c < h) dgamma[c] += s;
+  else dbeta[c - h] += s;
 }
 
 // ------------------------------------------------------------ softmax
@@ -448,18 +464,20 @@ void layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y
 }
 
 void layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd, const float* gamma,
-                   const void* dresid, void* dx, float* dgamma, float* dbeta, int rows, int h, cudaStream_t s) {
-  count_launch();
+                   const void* dresid, void* dx, float* dgamma, float* dbeta, int rows, int h, cudaStream_t s,
+                   float* ws) {
+  count_launch(ws ? 2 : 1);
   const int warps = 8;
-  const int grid = std::max(1, std::min((rows + warps - 1) / warps, 148 * 2));
+  const int grid = std::max(1, std::min((rows + warps - 1) / warps, kLnBwdBlocks));
   const size_t smem = static_cast<size_t>(warps) * 2 * h * sizeof(float);
   dispatch_vec(h, [&](auto v) {
     auto* k = layernorm_bwd_kernel<decltype(v)::value>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     k<<<grid, warps * 32, smem, s>>>(static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), mean,
                                      rstd, gamma, static_cast<const __nv_bfloat16*>(dresid),
-                                     static_cast<__nv_bfloat16*>(dx), dgamma, dbeta, rows, h);
+                                     static_cast<__nv_bfloat16*>(dx), dgamma, dbeta, ws, rows, h);
   });
+  if (ws) ln_param_reduce_kernel<<<(2 * h + 255) / 256, 256, 0, s>>>(ws, dgamma, dbeta, grid, h);
 }
 
 void softmax_fwd(const float* s, void* p, int rows, int len, int q_len, int causal, cudaStream_t st) {

@@ -291,9 +291,9 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
   const size_t RH = static_cast<size_t>(ctx_.rows) * spec_.hidden;
   if (spec_.kind != "mlp") {
     const size_t z = static_cast<size_t>(spec_.heads) * ctx_.samples;
-    const size_t ss = static_cast<size_t>(spec_.seq) * spec_.seq;
-    ctx_.scores = static_cast<float*>(mem_.alloc(z * ss * 4));
-    ctx_.dscores = static_cast<bf16*>(mem_.alloc(z * ss * 2));
+    ctx_.att_dsum = static_cast<float*>(mem_.alloc(z * spec_.seq * 4));
+    ctx_.att_dq = static_cast<float*>(mem_.alloc(RH * 4));
+    ctx_.ln_ws = static_cast<float*>(mem_.alloc(static_cast<size_t>(kLnBwdBlocks) * 2 * spec_.hidden * 4));
     ctx_.t_h = static_cast<bf16*>(mem_.alloc(RH * 2));
     ctx_.t_h2 = static_cast<bf16*>(mem_.alloc(RH * 2));
     ctx_.t_h3 = static_cast<bf16*>(mem_.alloc(RH * 2));

@@ -1,11 +1,12 @@
-// Layer programs (see layers.h).  Every matrix product is the tcgen05 GEMM;
+// Layer programs (see layers.h).  Every projection is the tcgen05 GEMM with
 // bias, residual, GELU / ReLU and their derivatives, fp32 micro-batch
-// gradient accumulation and the attention head split / merge all live in the
-// GEMM epilogues, so the only non-GEMM kernels are LayerNorm, softmax and
-// the bias-gradient column sums.
+// gradient accumulation and the attention head split in its epilogue;
+// attention itself is the fused flash kernel (kernels/attention.cu), so the
+// only other kernels are LayerNorm and the bias-gradient column sums.
 #include <cmath>
 #include <stdexcept>
 
+#include "kernels/attention.h"
 #include "kernels/elementwise.h"
 #include "layers.h"
 
@@ -190,14 +191,13 @@ class TransformerLayer final : public Layer {
   void alloc_stash(StageContext& ctx) override {
     const size_t R = ctx.rows;
     const size_t z = static_cast<size_t>(nh_) * ctx.samples;
-    const size_t ss = static_cast<size_t>(ctx.spec.seq) * ctx.spec.seq;
     stash_.resize(ctx.slots);
     for (Stash& st : stash_) {
       st.ln1 = alloc_n<bf16>(ctx, R * H_);
       st.mean1 = alloc_n<float>(ctx, R);
       st.rstd1 = alloc_n<float>(ctx, R);
       st.qkv = alloc_n<bf16>(ctx, 3 * R * H_);
-      st.P = alloc_n<bf16>(ctx, z * ss);
+      st.lse = alloc_n<float>(ctx, z * ctx.spec.seq);
       st.ctx = alloc_n<bf16>(ctx, R * H_);
       st.h = alloc_n<bf16>(ctx, R * H_);
       st.ln2 = alloc_n<bf16>(ctx, R * H_);
@@ -210,7 +210,7 @@ class TransformerLayer final : public Layer {
 
   void forward(StageContext& ctx, int slot, const bf16* x, bf16* y) override {
     Stash& st = stash_[slot];
-    const int R = ctx.rows, s = ctx.spec.seq, b = ctx.samples, z = nh_ * b;
+    const int R = ctx.rows;
     cudaStream_t str = ctx.stream;
     layernorm_fwd(x, w32_ + ln1g_, w32_ + ln1b_, st.ln1, st.mean1, st.rstd1, R, H_, eps_, str);
     {  // QKV with head-split store: [3][heads][b][s][d]
@@ -220,19 +220,8 @@ class TransformerLayer final : public Layer {
       d.bias = w32_ + bqkv_;
       ctx.gemms.run(d, str);
     }
-    {  // S = Q K^T / sqrt(d)   (fp32 scores)
-      GemmDesc d = plain(s, s, d_, q(st), d_, false, k(st, R), d_, false, ctx.scores, s, kOutF32);
-      batched(d, z, 1LL * s * d_, 1LL * s * d_, 1LL * s * s);
-      d.alpha = 1.0f / std::sqrt(static_cast<float>(d_));
-      ctx.gemms.run(d, str);
-    }
-    softmax_fwd(ctx.scores, st.P, z * s, s, s, causal_ ? 1 : 0, str);
-    {  // ctx = P V with head-merge store into [R][H]
-      GemmDesc d = plain(s, d_, s, st.P, s, false, v(st, R), d_, true, st.ctx, H_, kOutBf16);
-      batched(d, z, 1LL * s * s, 1LL * s * d_, 0);
-      merge(d, b, s, H_);
-      ctx.gemms.run(d, str);
-    }
+    // fused flash attention: context head-merged into [R][H], lse stashed
+    attention(ctx, slot).forward(str);
     {  // h = x + ctx Wo^T + bo
       GemmDesc d = plain(R, H_, H_, st.ctx, H_, false, w16_ + wo_, H_, false, st.h, H_, kBias | kResid);
       d.bias = w32_ + bo_;
@@ -256,9 +245,8 @@ class TransformerLayer final : public Layer {
 
   void backward(StageContext& ctx, int slot, const bf16* x, const bf16* dy, bf16* dx) override {
     Stash& st = stash_[slot];
-    const int R = ctx.rows, s = ctx.spec.seq, b = ctx.samples, z = nh_ * b;
+    const int R = ctx.rows;
     cudaStream_t str = ctx.stream;
-    const float scale = 1.0f / std::sqrt(static_cast<float>(d_));
     bf16* dz1 = ctx.t_f;
     bf16* dln = ctx.t_h;
     bf16* dh = ctx.t_h2;
@@ -278,7 +266,8 @@ class TransformerLayer final : public Layer {
     colsum_acc(dz1, g32_ + b1_, R, F_, str);
     ctx.gemms.run(plain(R, H_, F_, dz1, F_, false, w16_ + w1_, H_, true, dln, H_, kOutBf16), str);
     // LN2 backward (+ residual gradient dy)
-    layernorm_bwd(dln, st.h, st.mean2, st.rstd2, w32_ + ln2g_, dy, dh, g32_ + ln2g_, g32_ + ln2b_, R, H_, str);
+    layernorm_bwd(dln, st.h, st.mean2, st.rstd2, w32_ + ln2g_, dy, dh, g32_ + ln2g_, g32_ + ln2b_, R, H_, str,
+                  ctx.ln_ws);
     // O projection: dWo += dh^T ctx ; dbo ; dctx = dh Wo (head-split store)
     ctx.gemms.run(plain(H_, H_, R, dh, H_, true, st.ctx, H_, true, g32_ + wo_, H_, kOutF32Acc), str);
     colsum_acc(dh, g32_ + bo_, R, H_, str);
@@ -288,32 +277,8 @@ class TransformerLayer final : public Layer {
       d.s_no = static_cast<long long>(R) * d_;
       ctx.gemms.run(d, str);
     }
-    {  // dP = dctx V^T (fp32, reuses the scores buffer)
-      GemmDesc d = plain(s, s, d_, dctx_h, d_, false, v(st, R), d_, false, ctx.scores, s, kOutF32);
-      batched(d, z, 1LL * s * d_, 1LL * s * d_, 1LL * s * s);
-      ctx.gemms.run(d, str);
-    }
-    softmax_bwd(st.P, ctx.scores, ctx.dscores, z * s, s, str);
-    {  // dQ = scale dS K   -> dqkv[:, 0:H]
-      GemmDesc d = plain(s, d_, s, ctx.dscores, s, false, k(st, R), d_, true, dqkv, 3 * H_, kOutBf16);
-      batched(d, z, 1LL * s * s, 1LL * s * d_, 0);
-      merge(d, b, s, 3 * H_);
-      d.alpha = scale;
-      ctx.gemms.run(d, str);
-    }
-    {  // dK = scale dS^T Q -> dqkv[:, H:2H]
-      GemmDesc d = plain(s, d_, s, ctx.dscores, s, true, q(st), d_, true, dqkv + H_, 3 * H_, kOutBf16);
-      batched(d, z, 1LL * s * s, 1LL * s * d_, 0);
-      merge(d, b, s, 3 * H_);
-      d.alpha = scale;
-      ctx.gemms.run(d, str);
-    }
-    {  // dV = P^T dctx      -> dqkv[:, 2H:3H]
-      GemmDesc d = plain(s, d_, s, st.P, s, true, dctx_h, d_, true, dqkv + 2 * H_, 3 * H_, kOutBf16);
-      batched(d, z, 1LL * s * s, 1LL * s * d_, 0);
-      merge(d, b, s, 3 * H_);
-      ctx.gemms.run(d, str);
-    }
+    // fused flash attention backward -> dQ, dK, dV head-merged into dqkv
+    attention(ctx, slot).backward(str);
     // QKV: dWqkv += dqkv^T ln1 ; dbqkv ; dln1 = dqkv Wqkv
     ctx.gemms.run(plain(3 * H_, H_, R, dqkv, 3 * H_, true, st.ln1, H_, true, g32_ + wqkv_, H_, kOutF32Acc), str);
     colsum_acc(dqkv, g32_ + bqkv_, R, 3 * H_, str);
@@ -321,7 +286,7 @@ class TransformerLayer final : public Layer {
     // LN1 backward (+ residual gradient dh); the model's first layer still
     // needs gamma/beta grads, its dx goes to scratch
     layernorm_bwd(dln, x, st.mean1, st.rstd1, w32_ + ln1g_, dh, dx ? dx : dctx_h, g32_ + ln1g_, g32_ + ln1b_, R, H_,
-                  str);
+                  str, ctx.ln_ws);
   }
 
   double flops_fwd(const StageContext& ctx) const override {
@@ -339,26 +304,33 @@ class TransformerLayer final : public Layer {
 
  private:
   struct Stash {
-    bf16 *ln1, *qkv, *P, *ctx, *h, *ln2, *z1, *g;
-    float *mean1, *rstd1, *mean2, *rstd2;
+    bf16 *ln1, *qkv, *ctx, *h, *ln2, *z1, *g;
+    float *mean1, *rstd1, *mean2, *rstd2, *lse;
+    AttentionOp attn;
+    bool attn_ready = false;
   };
-  const bf16* q(const Stash& st) const { return st.qkv; }
-  const bf16* k(const Stash& st, int R) const { return st.qkv + static_cast<size_t>(R) * H_; }
-  const bf16* v(const Stash& st, int R) const { return st.qkv + 2ull * R * H_; }
-  static void batched(GemmDesc& d, int z, long long a_bs, long long b_bs, long long c_bs) {
-    d.batch = z;
-    d.a_batch_stride = a_bs;
-    d.b_batch_stride = b_bs;
-    if (c_bs) d.s_zo = c_bs;
+  AttentionOp& attention(StageContext& ctx, int slot) {
+    Stash& st = stash_[slot];
+    if (!st.attn_ready) {
+      AttentionDesc d;
+      d.qkv = st.qkv;
+      d.ctx = st.ctx;
+      d.ldc = H_;
+      d.lse = st.lse;
+      d.samples = ctx.samples;
+      d.seq = ctx.spec.seq;
+      d.heads = nh_;
+      d.head_dim = d_;
+      d.causal = causal_;
+      d.dout = ctx.t_h3;
+      d.dqkv = ctx.t_qkv;
+      d.dsum = ctx.att_dsum;
+      d.dq_acc = ctx.att_dq;
+      st.attn.prepare(d);
+      st.attn_ready = true;
+    }
+    return st.attn;
   }
-  // z = head * b + sample ; row = sample * s + pos ; col = head * d + j
-  void merge(GemmDesc& d, int b, int s, int ldc) const {
-    d.zdiv = b;
-    d.s_zo = d_;
-    d.s_zi = static_cast<long long>(s) * ldc;
-    d.ldc = ldc;
-  }
-
   int H_, F_, nh_, d_;
   bool causal_;
   float eps_;

@@ -67,6 +67,9 @@ struct StageContext {
   bf16* t_h3 = nullptr;     // [R][H] scratch (head layout)
   bf16* t_qkv = nullptr;    // [R][3H]
   bf16* t_f = nullptr;      // [R][F]
+  float* att_dsum = nullptr;  // attention backward workspaces: [z][S]
+  float* att_dq = nullptr;    // [z][S][64]
+  float* ln_ws = nullptr;     // LayerNorm-backward partials [kLnBwdBlocks][2][H]
   double flops_fwd = 0.0, flops_bwd = 0.0;  // per micro-batch slice (accounting)
 };
 

@@ -74,3 +74,15 @@ def fill_uniform_bf16(dst, n, seed, tensor, idx0=0, scale=1.0):
 
 def fill_uniform_f32(dst, n, seed, tensor, idx0=0, scale=1.0):
     check(lib().dpl_k_fill_uniform_f32(_ptr(dst), n, seed, tensor, idx0, scale, _stream()))
+
+
+def attention_fwd(qkv, ctx, lse, samples, seq, heads, ldc, causal=False):
+    """Fused flash attention forward (head dim 64): qkv [3][heads][B][S][64],
+    ctx [B*S][ldc] head-merged, lse [heads*B][S]."""
+    check(lib().dpl_k_attention_fwd(_ptr(qkv), _ptr(ctx), ldc, _ptr(lse), samples, seq, heads, int(causal), _stream()))
+
+
+def attention_bwd(qkv, ctx, lse, dout, dqkv, dsum, dq_acc, samples, seq, heads, ldc, causal=False):
+    """Fused flash attention backward (head dim 64)."""
+    check(lib().dpl_k_attention_bwd(_ptr(qkv), _ptr(ctx), ldc, _ptr(lse), _ptr(dout), _ptr(dqkv), _ptr(dsum),
+                                    _ptr(dq_acc), samples, seq, heads, int(causal), _stream()))

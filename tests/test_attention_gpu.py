@@ -1,0 +1,63 @@
+"""Fused attention vs a plain torch fp32 reference on the same bf16 q, k, v."""
+import math
+
+import pytest
+import torch
+
+from paper_2007_01045_b200 import kernels as K
+
+pytestmark = pytest.mark.gpu
+
+
+def _ref(qkv, B, S, nh, causal):
+    q, k, v = (qkv[i].float() for i in range(3))  # [nh][B][S][64]
+    sc = q @ k.transpose(-1, -2) / math.sqrt(64)
+    if causal:
+        sc = sc.masked_fill(torch.triu(torch.ones(S, S, dtype=torch.bool, device=qkv.device), 1), float("-inf"))
+    lse = torch.logsumexp(sc, -1)
+    o = torch.softmax(sc, -1) @ v  # [nh][B][S][64]
+    return o.permute(1, 2, 0, 3).reshape(B * S, nh * 64), lse.reshape(nh * B, S)
+
+
+@pytest.mark.parametrize("B,S,nh,causal", [(2, 128, 2, False), (2, 512, 4, False), (3, 512, 2, True),
+                                           (1, 1024, 2, True), (4, 256, 16, False)])
+def test_attention_forward(cuda, B, S, nh, causal):
+    g = torch.Generator(device="cpu").manual_seed(B * S + nh)
+    qkv = (torch.randn(3, nh, B, S, 64, generator=g) * 1.5).to(torch.bfloat16).to(cuda)
+    ctx = torch.zeros(B * S, nh * 64, dtype=torch.bfloat16, device=cuda)
+    lse = torch.zeros(nh * B, S, device=cuda)
+    K.attention_fwd(qkv, ctx, lse, B, S, nh, nh * 64, causal)
+    torch.cuda.synchronize()
+    ro, rl = _ref(qkv, B, S, nh, causal)
+    err = (ctx.float() - ro).abs().max().item()
+    assert err < 2e-2 * ro.abs().max().item() + 1e-3, err
+    assert (lse - rl).abs().max().item() < 1e-2
+
+
+@pytest.mark.parametrize("B,S,nh,causal", [(2, 128, 2, False), (2, 512, 4, False), (3, 512, 2, True),
+                                           (1, 1024, 2, True)])
+def test_attention_backward(cuda, B, S, nh, causal):
+    g = torch.Generator(device="cpu").manual_seed(7 * B + S + nh)
+    qkv = (torch.randn(3, nh, B, S, 64, generator=g) * 1.5).to(torch.bfloat16).to(cuda)
+    dout = torch.randn(nh, B, S, 64, generator=g).to(torch.bfloat16).to(cuda)
+    H = nh * 64
+    ctx = torch.zeros(B * S, H, dtype=torch.bfloat16, device=cuda)
+    lse = torch.zeros(nh * B, S, device=cuda)
+    K.attention_fwd(qkv, ctx, lse, B, S, nh, H, causal)
+    dqkv = torch.zeros(B * S, 3 * H, dtype=torch.bfloat16, device=cuda)
+    dsum = torch.zeros(nh * B, S, device=cuda)
+    dq_acc = torch.zeros(nh * B, S, 64, device=cuda)
+    K.attention_bwd(qkv, ctx, lse, dout, dqkv, dsum, dq_acc, B, S, nh, H, causal)
+    torch.cuda.synchronize()
+    # reference gradients via autograd in fp32 on the same bf16 inputs
+    q, k, v = (qkv[i].float().clone().requires_grad_(True) for i in range(3))
+    sc = q @ k.transpose(-1, -2) / math.sqrt(64)
+    if causal:
+        sc = sc.masked_fill(torch.triu(torch.ones(S, S, dtype=torch.bool, device=cuda), 1), float("-inf"))
+    o = torch.softmax(sc, -1) @ v
+    dq, dk, dv = torch.autograd.grad(o, (q, k, v), dout.float())
+    merge = lambda t: t.permute(1, 2, 0, 3).reshape(B * S, H)  # noqa: E731
+    for name, got, ref in (("dq", dqkv[:, :H], merge(dq)), ("dk", dqkv[:, H:2 * H], merge(dk)),
+                           ("dv", dqkv[:, 2 * H:], merge(dv))):
+        rel = ((got.float() - ref).norm() / ref.norm()).item()
+        assert rel < 2e-2, (name, rel)

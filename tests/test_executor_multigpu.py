@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 MLP = dict(kind="mlp", layers=4, hidden=256)
-BERT = dict(kind="bert", layers=4, hidden=256, heads=4, ffn=1024, seq=64)
+BERT = dict(kind="bert", layers=4, hidden=256, heads=4, ffn=1024, seq=128)
 
 CASES = [
     (2, MLP, {"stages": [{"layers": [0, 2], "gpus": [0]}, {"layers": [2, 4], "gpus": [1]}]}, 4, 24),
