@@ -408,6 +408,7 @@ def main():
                      "kernel": "gemm_bf16_tcgen05 (all launches of one step, CUDA events per launch)",
                      "peak_source": f"bf16_tflops_sustained of {peaks_src}", "gemm_share_of_step": gemm_share,
                      "shapes": prof["shapes"][:16]},
+        "kernels": sorted(prof.get("kernels", []), key=lambda k: -k["seconds"]),
         "clocks": clk,
         "gpu_launches": total_launches,
         "wall_s": t_wall,

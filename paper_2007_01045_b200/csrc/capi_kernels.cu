@@ -3,6 +3,7 @@
 
 #include <atomic>
 #include <exception>
+#include <stdexcept>
 #include <string>
 
 #include "dapple.h"
@@ -15,6 +16,29 @@ thread_local std::string g_last_error;
 std::atomic<long long> g_launches{0};
 void count_launch(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+KernelTimer& kernel_timer() {
+  static KernelTimer t;
+  return t;
+}
+cudaEvent_t KernelTimer::take() {
+  if (used == pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    pool.push_back(e);
+  }
+  return pool[used++];
+}
+TimedLaunch::TimedLaunch(const char* name, cudaStream_t s, double flops) : s_(s), on_(kernel_timer().enabled) {
+  if (!on_) return;
+  KernelTimer& t = kernel_timer();
+  KernelTimer::Rec r{name, t.take(), t.take(), flops};
+  cudaEventRecord(r.start, s);
+  t.recs.push_back(r);
+}
+TimedLaunch::~TimedLaunch() {
+  if (on_) cudaEventRecord(kernel_timer().recs.back().end, s_);
+}
 
 int fail(const std::string& what) {
   g_last_error = what;
@@ -106,7 +130,13 @@ int dpl_k_layernorm_fwd(const void* x, const float* gamma, const float* beta, vo
 int dpl_k_layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd, const float* gamma,
                         const void* dresid, void* dx, float* dgamma, float* dbeta, int rows, int h, void* stream) {
   return guarded([&] {
-    dpl::layernorm_bwd(dy, x, mean, rstd, gamma, dresid, dx, dgamma, dbeta, rows, h, static_cast<cudaStream_t>(stream));
+    float* ws = nullptr;
+    const size_t bytes = static_cast<size_t>(dpl::kLnBwdBlocks) * 4 * h * sizeof(float);
+    if (cudaMallocAsync(reinterpret_cast<void**>(&ws), bytes, static_cast<cudaStream_t>(stream)) != cudaSuccess)
+      throw std::runtime_error("layernorm_bwd: workspace allocation failed");
+    dpl::layernorm_bwd(dy, x, mean, rstd, gamma, dresid, dx, dgamma, dbeta, rows, h, static_cast<cudaStream_t>(stream),
+                       ws);
+    cudaFreeAsync(ws, static_cast<cudaStream_t>(stream));
   });
 }
 

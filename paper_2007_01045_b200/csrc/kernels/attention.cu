@@ -612,6 +612,7 @@ void AttentionOp::forward(cudaStream_t s) const {
   p.ldc = desc_.ldc;
   p.lse = desc_.lse;
   count_launch();
+  TimedLaunch timed_("attention_fwd", s, 4.0 * p.z_count * desc_.seq * desc_.seq * kD / (desc_.causal ? 2 : 1));
   attn_fwd_kernel<<<dim3(desc_.seq / kT, p.z_count), kFwdThreads, kFwdSmem, s>>>(p);
 }
 
@@ -622,6 +623,7 @@ void AttentionOp::backward(cudaStream_t s) const {
   const int rows = z_count * desc_.seq;
   const float scale = 1.0f / std::sqrt(static_cast<float>(kD));
   count_launch(3);
+  TimedLaunch timed_("attention_bwd", s, 10.0 * z_count * desc_.seq * desc_.seq * kD / (desc_.causal ? 2 : 1));
   attn_bwd_prep_kernel<<<std::min((rows + 7) / 8, 148 * 16), 256, 0, s>>>(
       static_cast<const __nv_bfloat16*>(desc_.dout), static_cast<const __nv_bfloat16*>(desc_.ctx), desc_.ldc,
       desc_.dsum, desc_.dq_acc, desc_.seq, desc_.samples, rows);

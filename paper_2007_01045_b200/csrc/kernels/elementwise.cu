@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <stdexcept>
 #include <cstdint>
 #include <type_traits>
 
@@ -68,25 +69,47 @@ __device__ __forceinline__ void store8(__nv_bfloat16* p, const float (&f)[8]) {
 }
 
 // ------------------------------------------------------------ LayerNorm
+__device__ __forceinline__ void unpack8(const uint4& r, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 x = __bfloat1622float2(h[e]);
+    f[2 * e] = x.x;
+    f[2 * e + 1] = x.y;
+  }
+}
+__device__ __forceinline__ void ldg8(const float* p, float (&f)[8]) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+  f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
+
+// One warp per row; the row stays in registers as packed bf16 (4 registers
+// per 8 values) and gamma / beta are re-read through L1, so the kernel fits
+// 64 registers and keeps 32 warps per SM in flight.
 template <int kMaxVec>
-__global__ void layernorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ gamma,
-                                     const float* __restrict__ beta, __nv_bfloat16* __restrict__ y,
-                                     float* __restrict__ mean_out, float* __restrict__ rstd_out, int rows, int h,
-                                     float eps) {
+__global__ void __launch_bounds__(256, 4)
+    layernorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ gamma,
+                         const float* __restrict__ beta, __nv_bfloat16* __restrict__ y, float* __restrict__ mean_out,
+                         float* __restrict__ rstd_out, int rows, int h, float eps) {
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nvec = h / 8;
   for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < rows; row += gridDim.x * warps) {
     const __nv_bfloat16* xr = x + static_cast<long long>(row) * h;
-    float v[kMaxVec][8];
+    uint4 raw[kMaxVec];
+#pragma unroll
+    for (int i = 0; i < kMaxVec; ++i)
+      if (lane + 32 * i < nvec) raw[i] = *reinterpret_cast<const uint4*>(xr + (lane + 32 * i) * 8);
     float s = 0.f;
 #pragma unroll
     for (int i = 0; i < kMaxVec; ++i) {
-      const int vi = lane + 32 * i;
-      if (vi < nvec) {
-        load8(xr + vi * 8, v[i]);
+      if (lane + 32 * i < nvec) {
+        float v[8];
+        unpack8(raw[i], v);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) s += v[i][e];
+        for (int e = 0; e < 8; ++e) s += v[e];
       }
     }
     const float mean = warp_sum(s) / h;
@@ -94,11 +117,10 @@ __global__ void layernorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, const 
 #pragma unroll
     for (int i = 0; i < kMaxVec; ++i) {
       if (lane + 32 * i < nvec) {
+        float v[8];
+        unpack8(raw[i], v);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float d = v[i][e] - mean;
-          q += d * d;
-        }
+        for (int e = 0; e < 8; ++e) q += (v[e] - mean) * (v[e] - mean);
       }
     }
     const float rstd = rsqrtf(warp_sum(q) / h + eps);
@@ -107,11 +129,12 @@ __global__ void layernorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, const 
     for (int i = 0; i < kMaxVec; ++i) {
       const int vi = lane + 32 * i;
       if (vi < nvec) {
-        float g[8], b[8], o[8];
-        load8(gamma + vi * 8, g);
-        load8(beta + vi * 8, b);
+        float v[8], g[8], b[8], o[8];
+        unpack8(raw[i], v);
+        ldg8(gamma + vi * 8, g);
+        ldg8(beta + vi * 8, b);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = (v[i][e] - mean) * rstd * g[e] + b[e];
+        for (int e = 0; e < 8; ++e) o[e] = (v[e] - mean) * rstd * g[e] + b[e];
         store8(yr + vi * 8, o);
       }
     }
@@ -123,46 +146,44 @@ __global__ void layernorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, const 
 }
 
 // dx = rstd * (g*dy - mean(g*dy) - xhat * mean(g*dy*xhat)) [+ dresid]
-// dgamma += sum_rows dy*xhat, dbeta += sum_rows dy
+// Row kernel: one warp per row, pure streaming (no column reductions); x and
+// dy stay packed in registers, xhat and g*dy are recomputed in pass 2.
 template <int kMaxVec>
-__global__ void layernorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
-                                     const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
-                                     const float* __restrict__ gamma, const __nv_bfloat16* __restrict__ dresid,
-                                     __nv_bfloat16* __restrict__ dx, float* __restrict__ dgamma,
-                                     float* __restrict__ dbeta, float* __restrict__ ws, int rows, int h) {
-  extern __shared__ float red[];  // [warps][2][h]
+__global__ void __launch_bounds__(256, 4)
+    layernorm_bwd_rows_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+                              const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
+                              const float* __restrict__ gamma, const __nv_bfloat16* __restrict__ dresid,
+                              __nv_bfloat16* __restrict__ dx, int rows, int h) {
   const int warps = blockDim.x >> 5;
-  const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nvec = h / 8;
-  float dg[kMaxVec][8], db[kMaxVec][8];
-#pragma unroll
-  for (int i = 0; i < kMaxVec; ++i)
-#pragma unroll
-    for (int e = 0; e < 8; ++e) dg[i][e] = db[i][e] = 0.f;
-
-  for (int row = blockIdx.x * warps + warp; row < rows; row += gridDim.x * warps) {
+  for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < rows; row += gridDim.x * warps) {
     const long long base = static_cast<long long>(row) * h;
     const float mean = mean_in[row];
     const float rstd = rstd_in[row];
-    float xh[kMaxVec][8], gd[kMaxVec][8];
+    uint4 rx[kMaxVec], rd[kMaxVec];
+#pragma unroll
+    for (int i = 0; i < kMaxVec; ++i) {
+      const int vi = lane + 32 * i;
+      if (vi < nvec) {
+        rx[i] = *reinterpret_cast<const uint4*>(x + base + vi * 8);
+        rd[i] = *reinterpret_cast<const uint4*>(dy + base + vi * 8);
+      }
+    }
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int i = 0; i < kMaxVec; ++i) {
       const int vi = lane + 32 * i;
       if (vi < nvec) {
         float xv[8], dv[8], g[8];
-        load8(x + base + vi * 8, xv);
-        load8(dy + base + vi * 8, dv);
-        load8(gamma + vi * 8, g);
+        unpack8(rx[i], xv);
+        unpack8(rd[i], dv);
+        ldg8(gamma + vi * 8, g);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          xh[i][e] = (xv[e] - mean) * rstd;
-          gd[i][e] = dv[e] * g[e];
-          s1 += gd[i][e];
-          s2 += gd[i][e] * xh[i][e];
-          dg[i][e] += dv[e] * xh[i][e];
-          db[i][e] += dv[e];
+          const float gd = dv[e] * g[e];
+          s1 += gd;
+          s2 += gd * ((xv[e] - mean) * rstd);
         }
       }
     }
@@ -172,57 +193,102 @@ __global__ void layernorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const
     for (int i = 0; i < kMaxVec; ++i) {
       const int vi = lane + 32 * i;
       if (vi < nvec) {
-        float o[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = rstd * (gd[i][e] - m1 - xh[i][e] * m2);
+        float xv[8], dv[8], g[8], rr[8], o[8];
+        unpack8(rx[i], xv);
+        unpack8(rd[i], dv);
+        ldg8(gamma + vi * 8, g);
         if (dresid) {
-          float r[8];
-          load8(dresid + base + vi * 8, r);
+          load8(dresid + base + vi * 8, rr);
+        } else {
 #pragma unroll
-          for (int e = 0; e < 8; ++e) o[e] += r[e];
+          for (int e = 0; e < 8; ++e) rr[e] = 0.f;
         }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = rstd * (dv[e] * g[e] - m1 - ((xv[e] - mean) * rstd) * m2) + rr[e];
         store8(dx + base + vi * 8, o);
       }
     }
   }
-  // block reduction of the column partials, then one atomic per column
+}
+
+// Column reductions over a slab of 64 rows (block = 32 column vectors x 8
+// row phases):
+//   0: sum dy*xhat (dgamma)  1: sum dy (dbeta)  2: sum dresid  3: sum dx
+// -> ws[blockIdx.y][nred][h]; ln_param_reduce_kernel sums the slabs.
+template <int kRed>
+__global__ void __launch_bounds__(256, 4)
+    ln_bwd_cols_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+                       const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
+                       const __nv_bfloat16* __restrict__ dresid, const __nv_bfloat16* __restrict__ dx,
+                       float* __restrict__ ws, int rows, int h) {
+  __shared__ float part[8][kRed][257];
+  const int vx = threadIdx.x & 31, ry = threadIdx.x >> 5;
+  const int vi = blockIdx.x * 32 + vx;
+  const int nvec = h / 8;
+  const int r0 = blockIdx.y * 64;
+  float acc[kRed][8];
 #pragma unroll
-  for (int i = 0; i < kMaxVec; ++i) {
-    const int vi = lane + 32 * i;
-    if (vi < nvec) {
+  for (int k = 0; k < kRed; ++k)
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        red[(warp * 2) * h + vi * 8 + e] = dg[i][e];
-        red[(warp * 2 + 1) * h + vi * 8 + e] = db[i][e];
+    for (int e = 0; e < 8; ++e) acc[k][e] = 0.f;
+  if (vi < nvec) {
+#pragma unroll 4
+    for (int t = 0; t < 8; ++t) {
+      const int r = r0 + ry + 8 * t;
+      if (r < rows) {
+        const long long off = static_cast<long long>(r) * h + vi * 8;
+        float xv[8], dv[8];
+        load8(x + off, xv);
+        load8(dy + off, dv);
+        const float mean = mean_in[r], rstd = rstd_in[r];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          acc[0][e] += dv[e] * ((xv[e] - mean) * rstd);
+          acc[1][e] += dv[e];
+        }
+        if constexpr (kRed > 2) {
+          float a[8];
+          load8(dresid + off, a);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[2][e] += a[e];
+        }
+        if constexpr (kRed > 3) {
+          float b[8];
+          load8(dx + off, b);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[3][e] += b[e];
+        }
       }
     }
   }
+#pragma unroll
+  for (int k = 0; k < kRed; ++k)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) part[ry][k][vx * 8 + e] = acc[k][e];
   __syncthreads();
-  for (int c = threadIdx.x; c < h; c += blockDim.x) {
-    float a = 0.f, b = 0.f;
-    for (int w = 0; w < warps; ++w) {
-      a += red[(w * 2) * h + c];
-      b += red[(w * 2 + 1) * h + c];
-    }
-    if (ws) {  // per-block partials, summed by ln_param_reduce_kernel
-      ws[static_cast<long long>(blockIdx.x) * 2 * h + c] = a;
-      ws[static_cast<long long>(blockIdx.x) * 2 * h + h + c] = b;
-    } else {
-      atomicAdd(dgamma + c, a);
-      atomicAdd(dbeta + c, b);
+  const int c = threadIdx.x;  // 256 columns
+  const int col = blockIdx.x * 256 + c;
+  if (col < h) {
+#pragma unroll
+    for (int k = 0; k < kRed; ++k) {
+      float sum = 0.f;
+#pragma unroll
+      for (int y = 0; y < 8; ++y) sum += part[y][k][c];
+      ws[(static_cast<long long>(blockIdx.y) * kRed + k) * h + col] = sum;
     }
   }
 }
 
-// dgamma[c] += sum_b ws[b][0][c]; dbeta[c] += sum_b ws[b][1][c]
-__global__ void ln_param_reduce_kernel(const float* __restrict__ ws, float* __restrict__ dgamma,
-                                       float* __restrict__ dbeta, int blocks, int h) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= 2 * h) return;
+// dst_k[c] += sum_b ws[b][k][c] for each of the nred column reductions
+__global__ void ln_param_reduce_kernel(const float* __restrict__ ws, float* d0, float* d1, float* d2, float* d3,
+                                       int blocks, int nred, int h) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nred * h) return;
   float s = 0.f;
-  for (int b = 0; b < blocks; ++b) s += ws[static_cast<long long>(b) * 2 * h + c];
-  if (c < h) dgamma[c] += s;
-  else dbeta[c - h] += s;
+  for (int b = 0; b < blocks; ++b) s += ws[static_cast<long long>(b) * nred * h + i];
+  const int k = i / h, c = i % h;
+  float* d = k == 0 ? d0 : k == 1 ? d1 : k == 2 ? d2 : d3;
+  d[c] += s;
 }
 
 // ------------------------------------------------------------ softmax
@@ -317,7 +383,7 @@ __global__ void softmax_bwd_kernel(const __nv_bfloat16* __restrict__ p, const fl
 // db[c] += sum_r dy[r][c].  Block = 32 column-vectors (256 columns) x 8 row
 // phases; a warp reads 512 contiguous bytes of a row; the 8 row phases are
 // reduced in shared memory, then one atomic per column per block.
-__global__ void colsum_acc_kernel(const __nv_bfloat16* __restrict__ dy, float* __restrict__ db, int rows, int cols,
+__global__ void __launch_bounds__(256, 4) colsum_acc_kernel(const __nv_bfloat16* __restrict__ dy, float* __restrict__ db, int rows, int cols,
                                   int rows_per_block) {
   __shared__ float part[8][256 + 1];
   const int vx = threadIdx.x & 31, ry = threadIdx.x >> 5;
@@ -327,11 +393,19 @@ __global__ void colsum_acc_kernel(const __nv_bfloat16* __restrict__ dy, float* _
   const int r1 = min(rows, r0 + rows_per_block);
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (vi < nvec) {
-    for (int r = r0 + ry; r < r1; r += 8) {
-      float f[8];
-      load8(dy + static_cast<long long>(r) * cols + vi * 8, f);
+    for (int r = r0 + ry; r < r1; r += 32) {
+      uint4 f[4];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] += f[e];
+      for (int t = 0; t < 4; ++t)  // 4 independent loads in flight
+        if (r + 8 * t < r1) f[t] = *reinterpret_cast<const uint4*>(dy + static_cast<long long>(r + 8 * t) * cols + vi * 8);
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (r + 8 * t < r1) {
+          float v[8];
+          unpack8(f[t], v);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] += v[e];
+        }
     }
   }
 #pragma unroll
@@ -455,6 +529,7 @@ int grid_for(long long work, int threads) {
 void layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y, float* mean, float* rstd, int rows,
                    int h, float eps, cudaStream_t s) {
   count_launch();
+  TimedLaunch timed_("layernorm_fwd", s);
   const int warps = 8;
   const int grid = std::max(1, std::min((rows + warps - 1) / warps, 148 * 8));
   dispatch_vec(h, [&](auto v) {
@@ -465,23 +540,37 @@ void layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y
 
 void layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd, const float* gamma,
                    const void* dresid, void* dx, float* dgamma, float* dbeta, int rows, int h, cudaStream_t s,
-                   float* ws) {
-  count_launch(ws ? 2 : 1);
+                   float* ws, float* dresid_colsum, float* dx_colsum) {
+  count_launch(3);
+  TimedLaunch timed_("layernorm_bwd", s);
+  if (!ws) throw std::invalid_argument("layernorm_bwd: workspace required");
+  if (dx_colsum && !dresid_colsum) throw std::invalid_argument("layernorm_bwd: dx_colsum needs dresid_colsum");
+  if (dresid_colsum && !dresid) throw std::invalid_argument("layernorm_bwd: dresid_colsum needs dresid");
   const int warps = 8;
-  const int grid = std::max(1, std::min((rows + warps - 1) / warps, kLnBwdBlocks));
-  const size_t smem = static_cast<size_t>(warps) * 2 * h * sizeof(float);
+  const int grid = std::max(1, std::min((rows + warps - 1) / warps, 148 * 8));
+  const auto* pdy = static_cast<const __nv_bfloat16*>(dy);
+  const auto* px = static_cast<const __nv_bfloat16*>(x);
+  const auto* pr = static_cast<const __nv_bfloat16*>(dresid);
+  auto* pdx = static_cast<__nv_bfloat16*>(dx);
   dispatch_vec(h, [&](auto v) {
-    auto* k = layernorm_bwd_kernel<decltype(v)::value>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    k<<<grid, warps * 32, smem, s>>>(static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), mean,
-                                     rstd, gamma, static_cast<const __nv_bfloat16*>(dresid),
-                                     static_cast<__nv_bfloat16*>(dx), dgamma, dbeta, ws, rows, h);
+    layernorm_bwd_rows_kernel<decltype(v)::value><<<grid, warps * 32, 0, s>>>(pdy, px, mean, rstd, gamma, pr, pdx,
+                                                                              rows, h);
   });
-  if (ws) ln_param_reduce_kernel<<<(2 * h + 255) / 256, 256, 0, s>>>(ws, dgamma, dbeta, grid, h);
+  const int nred = dx_colsum ? 4 : (dresid_colsum ? 3 : 2);
+  const int slabs = (rows + 63) / 64;
+  if (static_cast<long long>(slabs) * nred * h > static_cast<long long>(kLnBwdBlocks) * 4 * h)
+    throw std::invalid_argument("layernorm_bwd: too many rows for the workspace");
+  const dim3 cg((h / 8 + 31) / 32, slabs);
+  if (nred == 2) ln_bwd_cols_kernel<2><<<cg, 256, 0, s>>>(pdy, px, mean, rstd, pr, pdx, ws, rows, h);
+  else if (nred == 3) ln_bwd_cols_kernel<3><<<cg, 256, 0, s>>>(pdy, px, mean, rstd, pr, pdx, ws, rows, h);
+  else ln_bwd_cols_kernel<4><<<cg, 256, 0, s>>>(pdy, px, mean, rstd, pr, pdx, ws, rows, h);
+  ln_param_reduce_kernel<<<(nred * h + 255) / 256, 256, 0, s>>>(ws, dgamma, dbeta, dresid_colsum, dx_colsum, slabs,
+                                                                nred, h);
 }
 
 void softmax_fwd(const float* s, void* p, int rows, int len, int q_len, int causal, cudaStream_t st) {
   count_launch();
+  TimedLaunch timed_("softmax_fwd", st);
   const int warps = 8;
   const int grid = std::max(1, std::min((rows + warps - 1) / warps, 148 * 16));
   dispatch_vec(len, [&](auto v) {
@@ -492,6 +581,7 @@ void softmax_fwd(const float* s, void* p, int rows, int len, int q_len, int caus
 
 void softmax_bwd(const void* p, const float* dp, void* ds, int rows, int len, cudaStream_t st) {
   count_launch();
+  TimedLaunch timed_("softmax_bwd", st);
   const int warps = 8;
   const int grid = std::max(1, std::min((rows + warps - 1) / warps, 148 * 16));
   dispatch_vec(len, [&](auto v) {
@@ -502,6 +592,7 @@ void softmax_bwd(const void* p, const float* dp, void* ds, int rows, int len, cu
 
 void colsum_acc(const void* dy, float* db, int rows, int cols, cudaStream_t s) {
   count_launch();
+  TimedLaunch timed_("colsum_acc", s);
   const int gx = (cols + 255) / 256;
   // about two blocks per SM, at least 64 rows per block
   int gy = std::max(1, std::min((rows + 63) / 64, (148 * 2 + gx - 1) / gx));
@@ -512,6 +603,7 @@ void colsum_acc(const void* dy, float* db, int rows, int cols, cudaStream_t s) {
 
 void mse_loss(const void* y, const void* t, void* dy, float* loss_acc, long long n, float grad_scale, cudaStream_t s) {
   count_launch();
+  TimedLaunch timed_("mse_loss", s);
   mse_kernel<<<grid_for(n / 8, 256), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(y),
                                                    static_cast<const __nv_bfloat16*>(t),
                                                    static_cast<__nv_bfloat16*>(dy), loss_acc, n, grad_scale);
@@ -519,12 +611,14 @@ void mse_loss(const void* y, const void* t, void* dy, float* loss_acc, long long
 
 void sgd_apply(float* w32, float* g, void* w16, long long n, float lr, cudaStream_t s) {
   count_launch();
+  TimedLaunch timed_("sgd_apply", s);
   sgd_kernel<<<grid_for(n / 4, 256), 256, 0, s>>>(w32, g, static_cast<__nv_bfloat16*>(w16), n, lr);
 }
 
 void fill_uniform_bf16(void* dst, long long n, uint64_t seed, uint64_t tensor, long long idx0, float scale,
                        cudaStream_t s) {
   count_launch();
+  TimedLaunch timed_("fill_uniform", s);
   fill_uniform_bf16_kernel<<<grid_for(n, 256), 256, 0, s>>>(static_cast<__nv_bfloat16*>(dst), n, seed, tensor, idx0,
                                                             scale);
 }
@@ -532,16 +626,19 @@ void fill_uniform_bf16(void* dst, long long n, uint64_t seed, uint64_t tensor, l
 void fill_uniform_f32(float* dst, long long n, uint64_t seed, uint64_t tensor, long long idx0, float scale,
                       cudaStream_t s) {
   count_launch();
+  TimedLaunch timed_("fill_uniform", s);
   fill_uniform_f32_kernel<<<grid_for(n, 256), 256, 0, s>>>(dst, n, seed, tensor, idx0, scale);
 }
 
 void fill_const_f32(float* dst, long long n, float v, cudaStream_t s) {
   count_launch();
+  TimedLaunch timed_("fill_const", s);
   fill_const_f32_kernel<<<grid_for(n, 256), 256, 0, s>>>(dst, n, v);
 }
 
 void cast_f32_bf16(const float* src, void* dst, long long n, cudaStream_t s) {
   count_launch();
+  TimedLaunch timed_("cast_f32_bf16", s);
   cast_f32_bf16_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, static_cast<__nv_bfloat16*>(dst), n);
 }
 

@@ -11,12 +11,13 @@ namespace dpl {
 
 void layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y, float* mean, float* rstd, int rows,
                    int h, float eps, cudaStream_t s);
-// ws (optional): kLnBwdBlocks * 2 * h floats of scratch; with it the
-// gamma/beta gradients are reduced in a second pass instead of atomics.
-constexpr int kLnBwdBlocks = 148 * 2;
+// ws: kLnBwdBlocks * 4 * h floats of scratch.  Optionally also accumulates
+// the column sums of dresid and of dx (bias gradients of the neighbouring
+// layers) so they need no separate pass.
+constexpr int kLnBwdBlocks = 148 * 4;
 void layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd, const float* gamma,
                    const void* dresid, void* dx, float* dgamma, float* dbeta, int rows, int h, cudaStream_t s,
-                   float* ws = nullptr);
+                   float* ws, float* dresid_colsum = nullptr, float* dx_colsum = nullptr);
 void softmax_fwd(const float* s, void* p, int rows, int len, int q_len, int causal, cudaStream_t st);
 void softmax_bwd(const void* p, const float* dp, void* ds, int rows, int len, cudaStream_t st);
 void colsum_acc(const void* dy, float* db, int rows, int cols, cudaStream_t s);

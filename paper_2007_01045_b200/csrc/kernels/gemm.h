@@ -102,6 +102,32 @@ class GemmOp {
 void count_launch(long long n = 1);
 long long launch_count();
 
+// Optional per-kernel timing of every libdapple launch (CUDA events on the
+// launching stream), enabled for one profiled step by bench.py.
+struct KernelTimer {
+  struct Rec {
+    const char* name;
+    cudaEvent_t start, end;
+    double flops;
+  };
+  bool enabled = false;
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  cudaEvent_t take();
+};
+KernelTimer& kernel_timer();
+// RAII helper: brackets one launch when the timer is enabled
+class TimedLaunch {
+ public:
+  TimedLaunch(const char* name, cudaStream_t s, double flops = 0.0);
+  ~TimedLaunch();
+
+ private:
+  cudaStream_t s_;
+  bool on_;
+};
+
 // Optional per-launch timing of GEMMs (CUDA events around each launch on the
 // launching stream) used by bench.py for the live roofline number.
 struct GemmProfile {

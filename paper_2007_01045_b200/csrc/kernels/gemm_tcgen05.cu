@@ -580,6 +580,7 @@ void GemmCache::run(const GemmDesc& d, cudaStream_t s) {
 
 void GemmOp::launch(cudaStream_t stream) const {
   count_launch();
+  TimedLaunch timed_("gemm_bf16_tcgen05", stream, flops());
   switch (bn_) {
     case 64: gemm_bf16_tcgen05<64><<<grid_, kThreads, smem_, stream>>>(params_); break;
     case 128: gemm_bf16_tcgen05<128><<<grid_, kThreads, smem_, stream>>>(params_); break;

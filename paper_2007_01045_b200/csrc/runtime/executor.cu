@@ -113,6 +113,9 @@ class Executor {
   void set_gemm_profile(bool on) {
     ctx_.gemms.profile.enabled = on;
     ctx_.gemms.profile.reset();
+    kernel_timer().enabled = on;
+    kernel_timer().recs.clear();
+    kernel_timer().used = 0;
   }
   std::string gemm_profile_json() const;
   std::string timeline_json() const;
@@ -293,7 +296,7 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
     const size_t z = static_cast<size_t>(spec_.heads) * ctx_.samples;
     ctx_.att_dsum = static_cast<float*>(mem_.alloc(z * spec_.seq * 4));
     ctx_.att_dq = static_cast<float*>(mem_.alloc(RH * 4));
-    ctx_.ln_ws = static_cast<float*>(mem_.alloc(static_cast<size_t>(kLnBwdBlocks) * 2 * spec_.hidden * 4));
+    ctx_.ln_ws = static_cast<float*>(mem_.alloc(static_cast<size_t>(kLnBwdBlocks) * 4 * spec_.hidden * 4));
     ctx_.t_h = static_cast<bf16*>(mem_.alloc(RH * 2));
     ctx_.t_h2 = static_cast<bf16*>(mem_.alloc(RH * 2));
     ctx_.t_h3 = static_cast<bf16*>(mem_.alloc(RH * 2));
@@ -697,6 +700,35 @@ std::string Executor::gemm_profile_json() const {
     shapes.push_back(std::move(e));
   }
   out["shapes"] = std::move(shapes);
+  // every libdapple kernel of the profiled step, grouped by kernel
+  struct K {
+    std::string name;
+    long long launches = 0;
+    double seconds = 0, flops = 0;
+  };
+  std::vector<K> ks;
+  for (const auto& r : kernel_timer().recs) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.start, r.end);
+    auto it = std::find_if(ks.begin(), ks.end(), [&](const K& k) { return k.name == r.name; });
+    if (it == ks.end()) {
+      ks.push_back({r.name});
+      it = ks.end() - 1;
+    }
+    it->launches++;
+    it->seconds += ms * 1e-3;
+    it->flops += r.flops;
+  }
+  Value kernels = Value::array();
+  for (const K& k : ks) {
+    Value e = Value::object();
+    e["kernel"] = k.name;
+    e["launches"] = k.launches;
+    e["seconds"] = k.seconds;
+    if (k.flops > 0) e["tflops"] = k.flops / k.seconds * 1e-12;
+    kernels.push_back(std::move(e));
+  }
+  out["kernels"] = std::move(kernels);
   return out.dump();
 }
 

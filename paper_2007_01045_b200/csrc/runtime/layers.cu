@@ -255,7 +255,6 @@ class TransformerLayer final : public Layer {
 
     // FFN2: dW2 += dy^T g ; db2 ; dz1 = (dy W2) * gelu'(z1)
     ctx.gemms.run(plain(H_, F_, R, dy, H_, true, st.g, F_, true, g32_ + w2_, F_, kOutF32Acc), str);
-    colsum_acc(dy, g32_ + b2_, R, H_, str);
     {
       GemmDesc d = plain(R, F_, H_, dy, H_, false, w16_ + w2_, F_, true, dz1, F_, kDGelu);
       d.aux_in = st.z1;
@@ -265,12 +264,12 @@ class TransformerLayer final : public Layer {
     ctx.gemms.run(plain(F_, H_, R, dz1, F_, true, st.ln2, H_, true, g32_ + w1_, H_, kOutF32Acc), str);
     colsum_acc(dz1, g32_ + b1_, R, F_, str);
     ctx.gemms.run(plain(R, H_, F_, dz1, F_, false, w16_ + w1_, H_, true, dln, H_, kOutBf16), str);
-    // LN2 backward (+ residual gradient dy)
+    // LN2 backward (+ residual gradient dy); also db2 = colsum(dy) and
+    // dbo = colsum(dh) from the rows it already holds
     layernorm_bwd(dln, st.h, st.mean2, st.rstd2, w32_ + ln2g_, dy, dh, g32_ + ln2g_, g32_ + ln2b_, R, H_, str,
-                  ctx.ln_ws);
+                  ctx.ln_ws, g32_ + b2_, g32_ + bo_);
     // O projection: dWo += dh^T ctx ; dbo ; dctx = dh Wo (head-split store)
     ctx.gemms.run(plain(H_, H_, R, dh, H_, true, st.ctx, H_, true, g32_ + wo_, H_, kOutF32Acc), str);
-    colsum_acc(dh, g32_ + bo_, R, H_, str);
     {
       GemmDesc d = plain(R, H_, H_, dh, H_, false, w16_ + wo_, H_, true, dctx_h, d_, kOutBf16);
       d.ndiv = d_;
