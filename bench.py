@@ -334,9 +334,11 @@ def main():
         bub.append(merged["bubble"])
         spans.append((merged["start"], merged["end"]))
     total_launches = sum(gather(launches, world))
-    # device-timed: first forward of the first timed step to the end of the
-    # last rank's last step, on the GPUs' global timer (max over ranks)
-    device_s = spans[-1][1] - spans[0][0]
+    # device-timed: on each rank's own GPU timer, start of the first timed
+    # step to the end of the last one; the job time is the max over ranks
+    own = [all_tls[r][-1]["t0_ns"] * 1e-9 + all_tls[r][-1]["step_s"] - all_tls[r][0]["t0_ns"] * 1e-9
+           for r in range(world)]
+    device_s = max(own)
     value = args.steps * gbs / device_s
 
     # ------------------------------------------------------------ GEMM roofline (one profiled step)

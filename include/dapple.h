@@ -140,6 +140,10 @@ const char* dpl_exec_timeline(dpl_exec* ex);
 /* Copies a parameter / gradient tensor (by name) to host, for parity. */
 int dpl_exec_read_tensor(dpl_exec* ex, const char* name, int grad, void* host, size_t bytes);
 int dpl_exec_info(dpl_exec* ex, char* buf, size_t cap);
+/* Cross-GPU timer calibration (collective over phases 1..world-1, a host
+ * barrier between the responder's call and rank 0's): on rank 0 returns the
+ * offset of rank `phase`'s %globaltimer relative to rank 0's. */
+int dpl_exec_clock_calibrate(dpl_exec* ex, int phase, long long* offset_ns);
 /* Per-launch GEMM timing (CUDA events around every GEMM launch of the next
  * steps) and its summary as JSON {launches, seconds, flops, shapes[]}. */
 int dpl_exec_gemm_profile(dpl_exec* ex, int enable);

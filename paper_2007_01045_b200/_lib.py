@@ -65,6 +65,7 @@ _PROTOS = {
     "dpl_exec_timeline": (ctypes.c_char_p, [_VP]),
     "dpl_exec_read_tensor": (_I, [_VP, ctypes.c_char_p, _I, _VP, ctypes.c_size_t]),
     "dpl_exec_info": (_I, [_VP, ctypes.c_char_p, ctypes.c_size_t]),
+    "dpl_exec_clock_calibrate": (_I, [_VP, _I, ctypes.POINTER(_LL)]),
     "dpl_exec_gemm_profile": (_I, [_VP, _I]),
     "dpl_exec_gemm_profile_json": (ctypes.c_char_p, [_VP]),
     "dpl_exec_disconnect": (_I, [_VP]),

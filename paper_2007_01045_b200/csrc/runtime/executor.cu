@@ -14,10 +14,15 @@
 //
 // Cross-GPU dependencies never involve the host: a sender pushes its rows
 // straight into the receiver's buffer (cudaMemcpyAsync to a CUDA-IPC
-// mapping), then a one-thread kernel stores a sequence number into the
-// receiver's flag word; the receiver's compute stream waits on that word
-// with cuStreamWaitValue32(GEQ).  The whole step is enqueued without a host
-// round trip; the host synchronises once at the end.
+// mapping), then a one-thread kernel stores i+1 into the receiver's flag word
+// for micro-batch i; the receiver's compute stream waits on that word with
+// cuStreamWaitValue32(GEQ).  Flags live in two banks used by alternate steps;
+// each rank clears its own bank at the end of the step that used it (safe:
+// the bank is next signalled two steps later, after this rank's step end).
+//
+// The step is captured once into a CUDA graph per bank parity (and per host
+// input buffer pair) and replayed with one cudaGraphLaunch per step, so the
+// ~10^4 kernels of a BERT-48 step run back to back with no host launch gaps.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
@@ -86,6 +91,43 @@ __global__ void wait_kernel(const uint32_t* flag, uint32_t value) {
   } while (static_cast<int32_t>(v - value) < 0);
 }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Clock-offset ping-pong between rank 0 (initiator) and one peer (responder)
+// over peer-mapped words; both kernels run at the same time on different
+// GPUs.  out[k] = {t_send, t_peer, t_recv} on the initiator (t_peer copied
+// back by the responder).
+__global__ void clock_ping_kernel(volatile uint32_t* ping_remote, volatile uint32_t* pong_local,
+                                  volatile unsigned long long* peer_time_local, unsigned long long* out, int rounds) {
+  for (int k = 1; k <= rounds; ++k) {
+    const unsigned long long t0 = globaltimer();
+    *ping_remote = k;
+    __threadfence_system();
+    while (*pong_local != static_cast<uint32_t>(k)) {
+    }
+    const unsigned long long t2 = globaltimer();
+    __threadfence_system();
+    out[3 * (k - 1)] = t0;
+    out[3 * (k - 1) + 1] = *peer_time_local;
+    out[3 * (k - 1) + 2] = t2;
+  }
+}
+__global__ void clock_pong_kernel(volatile uint32_t* ping_local, volatile uint32_t* pong_remote,
+                                  volatile unsigned long long* peer_time_remote, int rounds) {
+  for (int k = 1; k <= rounds; ++k) {
+    while (*ping_local != static_cast<uint32_t>(k)) {
+    }
+    *peer_time_remote = globaltimer();
+    __threadfence_system();
+    *pong_remote = k;
+    __threadfence_system();
+  }
+}
+
 __global__ void stamp_kernel(unsigned long long* out) {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -93,6 +135,9 @@ __global__ void stamp_kernel(unsigned long long* out) {
 }
 
 using Route = pipeplan::SplitConcatRoute;
+
+// after the flag banks: {ping u32, pong u32, peer_time u64} for clock calibration
+constexpr size_t kCalibBytes = 256;
 
 struct BlockEvents {
   cudaEvent_t start = nullptr, end = nullptr;
@@ -109,6 +154,8 @@ class Executor {
   void connect(const uint8_t* blobs, size_t blob_len, int world);
   void nccl_init(const void* id);
   void disconnect();
+  // ns to add to this rank's %globaltimer to express it on rank 0's timer
+  long long calibrate_clock(int phase);
   float step(const void* host_input, const void* host_target);
   void set_gemm_profile(bool on) {
     ctx_.gemms.profile.enabled = on;
@@ -156,20 +203,32 @@ class Executor {
   float* loss_acc_ = nullptr;
   unsigned long long* t0_ = nullptr;
   // receive region (one cudaMalloc, exported over CUDA IPC):
-  //   [recv_act M x R x H][recv_grad M x R x H][flags: act[world], grad[world]]
+  //   [recv_act M x R x H][recv_grad M x R x H][flags: bank[2] x {act[world], grad[world]}]
   uint8_t* recv_ = nullptr;
   size_t recv_bytes_ = 0, recv_grad_off_ = 0, flags_off_ = 0;
   std::vector<uint8_t*> peer_recv_;  // by rank (IPC-mapped), null if unused
+  long long clock_offset_ns_ = 0;
   std::vector<int> peer_rows_;       // rows per slice of each rank's stage
 
   cudaStream_t compute_ = nullptr, send_act_ = nullptr, send_grad_s_ = nullptr, reduce_ = nullptr;
   ncclComm_t comm_ = nullptr;
   cudaEvent_t ev_begin_ = nullptr, ev_end_ = nullptr, ev_reduce_done_ = nullptr;
-  cudaEvent_t ev_sa_done_ = nullptr, ev_sg_done_ = nullptr;
+  cudaEvent_t ev_sa_done_ = nullptr, ev_sg_done_ = nullptr, ev_fork_ = nullptr, ev_last_bwd_ = nullptr;
   std::vector<BlockEvents> fwd_ev_, bwd_ev_, send_fwd_ev_, send_bwd_ev_;
   std::vector<cudaEvent_t> layer_done_, fwd_done_, bwd_done_;
   long long steps_done_ = 0;
+  int bank_ = 0;
   float last_loss_ = NAN;
+  float* loss_host_ = nullptr;  // pinned
+  bool use_graph_ = true, capturing_ = false;
+  struct GraphKey {
+    int bank;
+    const void* in;
+    const void* tgt;
+    bool operator==(const GraphKey& o) const { return bank == o.bank && in == o.in && tgt == o.tgt; }
+  };
+  std::vector<std::pair<GraphKey, cudaGraphExec_t>> graphs_;
+  void enqueue_step(const void* host_input, const void* host_target);
   double flops_per_step_ = 0.0;
 
   // --- helpers
@@ -181,14 +240,18 @@ class Executor {
   bf16* recv_grad(int i) const {
     return reinterpret_cast<bf16*>(recv_ + recv_grad_off_) + static_cast<size_t>(i) * ctx_.rows * spec_.hidden;
   }
-  uint32_t* flags() const { return reinterpret_cast<uint32_t*>(recv_ + flags_off_); }
+  // flag bank of the current step (parity)
+  uint32_t* flags() const { return reinterpret_cast<uint32_t*>(recv_ + flags_off_) + bank_ * 2 * world_; }
   size_t layout_grad_off(int rows) const;
   size_t layout_flags_off(int rows) const;
   void wait_flag(cudaStream_t s, uint32_t* flag, uint32_t value);
   void signal(cudaStream_t s, uint32_t* remote_flag, uint32_t value);
   void forward(int i, uint32_t base);
   void backward(int i, uint32_t base);
-  void record(cudaEvent_t e, cudaStream_t s) { DPL_CUDA(cudaEventRecord(e, s)); }
+  // timing events become event-record nodes when the step is captured
+  void record(cudaEvent_t e, cudaStream_t s) {
+    DPL_CUDA(capturing_ ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s));
+  }
 };
 
 Executor::Executor(const Value& cfg, int device) : device_(device) {
@@ -213,6 +276,7 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
   if (cfg.contains("seed")) seed_ = static_cast<uint64_t>(cfg.at("seed").as_int());
   if (cfg.contains("timeline")) timeline_ = cfg.at("timeline").as_bool();
   if (cfg.contains("apply")) apply_ = cfg.at("apply").as_bool();
+  if (cfg.contains("graph")) use_graph_ = cfg.at("graph").as_bool();
   if (M_ < 1 || gbs_ % M_ != 0) throw std::invalid_argument("dpl exec: GBS must be a multiple of M");
   B_ = gbs_ / M_;
 
@@ -326,7 +390,7 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
   // receive region: one allocation so a single IPC handle covers it
   recv_grad_off_ = layout_grad_off(ctx_.rows);
   flags_off_ = layout_flags_off(ctx_.rows);
-  recv_bytes_ = flags_off_ + 2 * static_cast<size_t>(world_) * 4;
+  recv_bytes_ = flags_off_ + 4 * static_cast<size_t>(world_) * 4 + kCalibBytes;
   recv_ = static_cast<uint8_t*>(mem_.alloc(recv_bytes_));
   peer_recv_.assign(world_, nullptr);
   peer_rows_.assign(world_, 0);
@@ -341,6 +405,8 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
   mk_nt(&ev_reduce_done_);
   mk_nt(&ev_sa_done_);
   mk_nt(&ev_sg_done_);
+  mk_nt(&ev_fork_);
+  mk_nt(&ev_last_bwd_);
   fwd_ev_.resize(M_);
   bwd_ev_.resize(M_);
   send_fwd_ev_.resize(M_);
@@ -361,6 +427,7 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
     const bool need_dx = !(k_ == 0 && li == 0);
     flops_per_step_ += M_ * (layers_[li]->flops_fwd(ctx_) + layers_[li]->flops_bwd(ctx_, need_dx));
   }
+  DPL_CUDA(cudaMallocHost(reinterpret_cast<void**>(&loss_host_), sizeof(float)));
   // parameters initialised and every buffer (incl. the IPC-exported flags)
   // zeroed before any peer can see this rank
   DPL_CUDA(cudaDeviceSynchronize());
@@ -379,6 +446,9 @@ size_t Executor::layout_flags_off(int rows) const { return 2 * layout_grad_off(r
 void Executor::disconnect() {
   cudaSetDevice(device_);
   cudaDeviceSynchronize();
+  // captured steps reference the communicator and the peer mappings
+  for (auto& g : graphs_) cudaGraphExecDestroy(g.second);
+  graphs_.clear();
   if (comm_) {
     ncclCommDestroy(comm_);
     comm_ = nullptr;
@@ -391,6 +461,7 @@ void Executor::disconnect() {
 
 Executor::~Executor() {
   disconnect();
+  if (loss_host_) cudaFreeHost(loss_host_);
   for (cudaStream_t s : {compute_, send_act_, send_grad_s_, reduce_})
     if (s) cudaStreamDestroy(s);
 }
@@ -408,6 +479,11 @@ void Executor::connect(const uint8_t* blobs, size_t blob_len, int world) {
   std::vector<int> peers;
   for (const Route& r : out_routes_) peers.push_back(r.dst_gpu);
   for (const Route& r : in_routes_) peers.push_back(r.src_gpu);
+  if (rank_ == 0) {
+    for (int p = 1; p < world_; ++p) peers.push_back(p);
+  } else {
+    peers.push_back(0);
+  }
   for (int p : peers) {
     if (p == rank_ || peer_recv_[p]) continue;
     cudaIpcMemHandle_t h;
@@ -418,6 +494,47 @@ void Executor::connect(const uint8_t* blobs, size_t blob_len, int world) {
   }
 }
 
+// Called collectively: phase p (1..world-1) calibrates rank p against rank 0;
+// the host side barriers between phases.  Returns this rank's offset.
+long long Executor::calibrate_clock(int phase) {
+  if (world_ == 1 || (rank_ != 0 && rank_ != phase)) return clock_offset_ns_;
+  constexpr int kRounds = 64;
+  auto calib = [&](uint8_t* region, int rows) {
+    uint8_t* base = region + layout_flags_off(rows) + 4 * static_cast<size_t>(world_) * 4;
+    return base;
+  };
+  DPL_CUDA(cudaSetDevice(device_));
+  // words start at zero (zeroed allocation) and are only ever counted up
+  // 1..kRounds per responder, so no re-zeroing (and no zeroing race) is needed
+  uint8_t* mine = calib(recv_, ctx_.rows);
+  if (rank_ == 0) {
+    uint8_t* peer = calib(peer_recv_[phase], peer_rows_[phase]);
+    unsigned long long* out = nullptr;
+    DPL_CUDA(cudaMalloc(&out, 3 * kRounds * sizeof(unsigned long long)));
+    clock_ping_kernel<<<1, 1, 0, compute_>>>(reinterpret_cast<uint32_t*>(peer), reinterpret_cast<uint32_t*>(mine + 4),
+                                             reinterpret_cast<unsigned long long*>(mine + 8), out, kRounds);
+    DPL_CUDA(cudaStreamSynchronize(compute_));
+    std::vector<unsigned long long> h(3 * kRounds);
+    DPL_CUDA(cudaMemcpy(h.data(), out, h.size() * 8, cudaMemcpyDeviceToHost));
+    cudaFree(out);
+    // offset of the peer relative to rank 0 from the tightest round trip
+    long long best_rtt = -1, offset = 0;
+    for (int k = 0; k < kRounds; ++k) {
+      const long long t0 = h[3 * k], tp = h[3 * k + 1], t2 = h[3 * k + 2];
+      if (best_rtt < 0 || t2 - t0 < best_rtt) {
+        best_rtt = t2 - t0;
+        offset = tp - (t0 + t2) / 2;
+      }
+    }
+    return offset;  // rank 0 reports the peer's offset; the host forwards it
+  }
+  uint8_t* zero = calib(peer_recv_[0], peer_rows_[0]);
+  clock_pong_kernel<<<1, 1, 0, compute_>>>(reinterpret_cast<uint32_t*>(mine), reinterpret_cast<uint32_t*>(zero + 4),
+                                           reinterpret_cast<unsigned long long*>(zero + 8), kRounds);
+  DPL_CUDA(cudaStreamSynchronize(compute_));
+  return 0;
+}
+
 void Executor::nccl_init(const void* id) {
   if (r_ == 1) return;
   ncclUniqueId uid;
@@ -426,9 +543,13 @@ void Executor::nccl_init(const void* id) {
 }
 
 void Executor::wait_flag(cudaStream_t s, uint32_t* flag, uint32_t value) {
-  if (StreamValueFn fn = wait_value_fn()) {
-    const CUresult rc = fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flag), value, 0x0 /*GEQ*/);
-    if (rc == CUDA_SUCCESS) return;
+  static bool memops_ok = true;
+  if (memops_ok) {
+    if (StreamValueFn fn = wait_value_fn()) {
+      const CUresult rc = fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flag), value, 0x0 /*GEQ*/);
+      if (rc == CUDA_SUCCESS) return;
+    }
+    memops_ok = false;  // not available / not capturable: one-thread acquire spin on this stream
   }
   count_launch();
   wait_kernel<<<1, 1, 0, s>>>(flag, value);
@@ -470,7 +591,7 @@ void Executor::forward(int i, uint32_t base) {
       const int rows_dst = peer_rows_[r.dst_gpu];
       bf16* dst = reinterpret_cast<bf16*>(peer) + (static_cast<size_t>(i) * rows_dst + r.dst_row) * H;
       DPL_CUDA(cudaMemcpyAsync(dst, out_[i] + r.src_row * H, r.rows * H * 2, cudaMemcpyDeviceToDevice, send_act_));
-      uint32_t* flag = reinterpret_cast<uint32_t*>(peer + layout_flags_off(rows_dst)) + rank_;
+      uint32_t* flag = reinterpret_cast<uint32_t*>(peer + layout_flags_off(rows_dst)) + bank_ * 2 * world_ + rank_;
       signal(send_act_, flag, base + i + 1);
     }
     record(send_fwd_ev_[i].end, send_act_);
@@ -524,21 +645,25 @@ void Executor::backward(int i, uint32_t base) {
                   (static_cast<size_t>(i) * rows_src + r.src_row) * H;
       DPL_CUDA(cudaMemcpyAsync(dst, send_grad_[i] + r.dst_row * H, r.rows * H * 2, cudaMemcpyDeviceToDevice,
                                send_grad_s_));
-      uint32_t* flag = reinterpret_cast<uint32_t*>(peer + layout_flags_off(rows_src)) + world_ + rank_;
+      uint32_t* flag =
+          reinterpret_cast<uint32_t*>(peer + layout_flags_off(rows_src)) + bank_ * 2 * world_ + world_ + rank_;
       signal(send_grad_s_, flag, base + i + 1);
     }
     record(send_bwd_ev_[i].end, send_grad_s_);
   }
 }
 
-float Executor::step(const void* host_input, const void* host_target) {
-  DPL_CUDA(cudaSetDevice(device_));
-  const uint32_t base = static_cast<uint32_t>(steps_done_ * M_);
+void Executor::enqueue_step(const void* host_input, const void* host_target) {
+  const uint32_t base = 0;  // flag values are i+1 within the bank of this step
   const size_t H = spec_.hidden;
   const size_t RH = static_cast<size_t>(ctx_.rows) * H;
   count_launch();
   stamp_kernel<<<1, 1, 0, compute_>>>(t0_);
-  DPL_CUDA(cudaEventRecord(ev_begin_, compute_));
+  record(ev_begin_, compute_);
+  // fork every side stream from the compute stream (they join again at the
+  // end), so a captured step always has one origin and one sink
+  DPL_CUDA(cudaEventRecord(ev_fork_, compute_));
+  for (cudaStream_t side : {send_act_, send_grad_s_, reduce_}) DPL_CUDA(cudaStreamWaitEvent(side, ev_fork_, 0));
   DPL_CUDA(cudaMemsetAsync(loss_acc_, 0, 4, compute_));
 
   // sample rows [row0, row0 + samples) of micro-batch i owned by this replica
@@ -571,7 +696,10 @@ float Executor::step(const void* host_input, const void* host_target) {
     }
   }
   if (k_ == S_ - 1 && comm_) {
-    DPL_CUDA(cudaStreamWaitEvent(reduce_, bwd_ev_[M_ - 1].end, 0));
+    // sync (non-timing) event: timing events are external nodes in a
+    // captured step and cannot carry dependencies
+    DPL_CUDA(cudaEventRecord(ev_last_bwd_, compute_));
+    DPL_CUDA(cudaStreamWaitEvent(reduce_, ev_last_bwd_, 0));
     DPL_NCCL(ncclAllReduce(loss_acc_, loss_acc_, 1, ncclFloat, ncclSum, comm_, reduce_));
   }
   DPL_CUDA(cudaEventRecord(ev_reduce_done_, reduce_));
@@ -580,18 +708,57 @@ float Executor::step(const void* host_input, const void* host_target) {
   DPL_CUDA(cudaStreamWaitEvent(compute_, ev_reduce_done_, 0));
   DPL_CUDA(cudaStreamWaitEvent(compute_, ev_sa_done_, 0));
   DPL_CUDA(cudaStreamWaitEvent(compute_, ev_sg_done_, 0));
-  DPL_CUDA(cudaEventRecord(ev_end_, compute_));
-  float loss = NAN;
-  if (k_ == S_ - 1) {
-    DPL_CUDA(cudaMemcpyAsync(&loss, loss_acc_, 4, cudaMemcpyDeviceToHost, compute_));
+  record(ev_end_, compute_);
+  if (k_ == S_ - 1) DPL_CUDA(cudaMemcpyAsync(loss_host_, loss_acc_, 4, cudaMemcpyDeviceToHost, compute_));
+  // clear this step's flag bank (signalled again two steps from now)
+  DPL_CUDA(cudaMemsetAsync(flags(), 0, 2 * static_cast<size_t>(world_) * 4, compute_));
+}
+
+float Executor::step(const void* host_input, const void* host_target) {
+  DPL_CUDA(cudaSetDevice(device_));
+  const bool profiling = ctx_.gemms.profile.enabled || kernel_timer().enabled;
+  if (!use_graph_ || profiling) {
+    enqueue_step(host_input, host_target);
+  } else {
+    const GraphKey key{bank_, host_input, host_target};
+    cudaGraphExec_t exec = nullptr;
+    for (auto& g : graphs_)
+      if (g.first == key) exec = g.second;
+    // capture (a stream memory op that cannot be captured invalidates the
+    // capture; wait_flag then switches to its kernel form and we retry once)
+    for (int attempt = 0; !exec && attempt < 2; ++attempt) {
+      cudaGraph_t graph = nullptr;
+      DPL_CUDA(cudaStreamBeginCapture(compute_, cudaStreamCaptureModeRelaxed));
+      capturing_ = true;
+      bool ok = true;
+      try {
+        enqueue_step(host_input, host_target);
+      } catch (...) {
+        ok = false;
+      }
+      capturing_ = false;
+      const cudaError_t end = cudaStreamEndCapture(compute_, &graph);
+      if (ok && end == cudaSuccess && graph) {
+        DPL_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        graphs_.push_back({key, exec});
+      }
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();
+      if (!exec && attempt == 1) throw std::runtime_error("dpl exec: step capture failed");
+    }
+    DPL_CUDA(cudaGraphLaunch(exec, compute_));
   }
   DPL_CUDA(cudaStreamSynchronize(compute_));
   DPL_CUDA(cudaGetLastError());
   ++steps_done_;
-  if (k_ == S_ - 1) loss = loss / static_cast<float>(numel_global_);
+  bank_ ^= 1;
+  float loss = NAN;
+  if (k_ == S_ - 1) loss = *loss_host_ / static_cast<float>(numel_global_);
   last_loss_ = loss;
   return loss;
 }
+
+
 
 std::string Executor::timeline_json() const {
   auto ms = [&](cudaEvent_t e) {
@@ -855,6 +1022,10 @@ const char* dpl_exec_gemm_profile_json(dpl_exec* ex) {
     ex->reply = std::string("{\"error\":\"") + e.what() + "\"}";
   }
   return ex->reply.c_str();
+}
+
+int dpl_exec_clock_calibrate(dpl_exec* ex, int phase, long long* offset_ns) {
+  return exec_guard([&] { *offset_ns = ex->impl->calibrate_clock(phase); });
 }
 
 int dpl_exec_disconnect(dpl_exec* ex) {

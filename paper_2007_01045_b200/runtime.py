@@ -9,6 +9,7 @@ from __future__ import annotations
 import ctypes
 import json
 import math
+import os
 from typing import Optional
 
 from ._lib import check, lib
@@ -25,7 +26,8 @@ class Executor:
         self.rank, self.world = rank, world
         self.device = rank if device is None else device
         cfg = {"model": model, "plan": self.plan, "M": micro_batches, "gbs": gbs, "lr": lr, "seed": seed,
-               "rank": rank, "world": world, "apply": apply, "timeline": timeline}
+               "rank": rank, "world": world, "apply": apply, "timeline": timeline,
+               "graph": os.environ.get("DPL_GRAPH", "1") != "0"}
         h = ctypes.c_void_p()
         check(lib().dpl_exec_create(json.dumps(cfg).encode(), self.device, ctypes.byref(h)))
         self._h = h
@@ -60,6 +62,31 @@ class Executor:
         dist.all_gather_object(ids, my_id)
         if len(stage["gpus"]) > 1:
             check(lib().dpl_exec_nccl_init(self._h, ids[leader]))
+        self.clock_offsets_ns = self._calibrate_clocks()
+
+    def _calibrate_clocks(self):
+        """%globaltimer differs between GPUs; rank 0 ping-pongs every peer over
+        NVLink peer memory and the offsets are shared, so merged timelines are
+        on rank 0's clock."""
+        import threading
+        import torch.distributed as dist
+        offsets = [0] * self.world
+        for phase in range(1, self.world):
+            off = ctypes.c_longlong(0)
+            if self.rank == phase:
+                # responder first: it zeroes its words, then spins for pings
+                dist.barrier()
+                check(lib().dpl_exec_clock_calibrate(self._h, phase, ctypes.byref(off)))
+            elif self.rank == 0:
+                dist.barrier()
+                check(lib().dpl_exec_clock_calibrate(self._h, phase, ctypes.byref(off)))
+                offsets[phase] = off.value
+            else:
+                dist.barrier()
+            dist.barrier()
+        allv = [None] * self.world
+        dist.all_gather_object(allv, offsets if self.rank == 0 else None)
+        return allv[0]
 
     # ----------------------------------------------------------- step
     def step(self, host_input=None, host_target=None) -> float:
@@ -80,7 +107,10 @@ class Executor:
         return json.loads(lib().dpl_exec_gemm_profile_json(self._h).decode())
 
     def timeline(self) -> dict:
-        return json.loads(lib().dpl_exec_timeline(self._h).decode())
+        tl = json.loads(lib().dpl_exec_timeline(self._h).decode())
+        # express t0 on rank 0's GPU timer
+        tl["t0_ns"] -= getattr(self, "clock_offsets_ns", [0] * self.world)[self.rank]
+        return tl
 
     def read(self, layer: int, name: str, count: int, grad: bool = False):
         import numpy as np
