@@ -33,11 +33,15 @@ TimedLaunch::TimedLaunch(const char* name, cudaStream_t s, double flops) : s_(s)
   if (!on_) return;
   KernelTimer& t = kernel_timer();
   KernelTimer::Rec r{name, t.take(), t.take(), flops};
-  cudaEventRecord(r.start, s);
+  if (t.capturing) cudaEventRecordWithFlags(r.start, s, cudaEventRecordExternal);
+  else cudaEventRecord(r.start, s);
   t.recs.push_back(r);
 }
 TimedLaunch::~TimedLaunch() {
-  if (on_) cudaEventRecord(kernel_timer().recs.back().end, s_);
+  if (!on_) return;
+  KernelTimer& t = kernel_timer();
+  if (t.capturing) cudaEventRecordWithFlags(t.recs.back().end, s_, cudaEventRecordExternal);
+  else cudaEventRecord(t.recs.back().end, s_);
 }
 
 int fail(const std::string& what) {

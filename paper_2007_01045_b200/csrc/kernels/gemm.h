@@ -111,6 +111,7 @@ struct KernelTimer {
     double flops;
   };
   bool enabled = false;
+  bool capturing = false;  // records become external event nodes of a captured step
   std::vector<Rec> recs;
   std::vector<cudaEvent_t> pool;
   size_t used = 0;

@@ -572,9 +572,12 @@ void GemmCache::run(const GemmDesc& d, cudaStream_t s) {
   r.K = d.K;
   r.batch = d.batch;
   r.bn = op.bn();
-  cudaEventRecord(r.start, s);
+  const bool ext = kernel_timer().capturing;
+  if (ext) cudaEventRecordWithFlags(r.start, s, cudaEventRecordExternal);
+  else cudaEventRecord(r.start, s);
   op.launch(s);
-  cudaEventRecord(r.end, s);
+  if (ext) cudaEventRecordWithFlags(r.end, s, cudaEventRecordExternal);
+  else cudaEventRecord(r.end, s);
   profile.recs.push_back(r);
 }
 

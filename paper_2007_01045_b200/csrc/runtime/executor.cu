@@ -163,6 +163,15 @@ class Executor {
     kernel_timer().enabled = on;
     kernel_timer().recs.clear();
     kernel_timer().used = 0;
+    // the profiled graph is captured afresh so its event records are current
+    for (auto it = graphs_.begin(); it != graphs_.end();) {
+      if (it->first.profile) {
+        cudaGraphExecDestroy(it->second);
+        it = graphs_.erase(it);
+      } else {
+        ++it;
+      }
+    }
   }
   std::string gemm_profile_json() const;
   std::string timeline_json() const;
@@ -225,7 +234,10 @@ class Executor {
     int bank;
     const void* in;
     const void* tgt;
-    bool operator==(const GraphKey& o) const { return bank == o.bank && in == o.in && tgt == o.tgt; }
+    bool profile;
+    bool operator==(const GraphKey& o) const {
+      return bank == o.bank && in == o.in && tgt == o.tgt && profile == o.profile;
+    }
   };
   std::vector<std::pair<GraphKey, cudaGraphExec_t>> graphs_;
   void enqueue_step(const void* host_input, const void* host_target);
@@ -717,10 +729,12 @@ void Executor::enqueue_step(const void* host_input, const void* host_target) {
 float Executor::step(const void* host_input, const void* host_target) {
   DPL_CUDA(cudaSetDevice(device_));
   const bool profiling = ctx_.gemms.profile.enabled || kernel_timer().enabled;
-  if (!use_graph_ || profiling) {
+  if (!use_graph_) {
     enqueue_step(host_input, host_target);
   } else {
-    const GraphKey key{bank_, host_input, host_target};
+    // a profiled step is its own graph (per-launch timing events inside);
+    // its records are re-registered on every capture
+    const GraphKey key{bank_, host_input, host_target, profiling};
     cudaGraphExec_t exec = nullptr;
     for (auto& g : graphs_)
       if (g.first == key) exec = g.second;
@@ -730,6 +744,7 @@ float Executor::step(const void* host_input, const void* host_target) {
       cudaGraph_t graph = nullptr;
       DPL_CUDA(cudaStreamBeginCapture(compute_, cudaStreamCaptureModeRelaxed));
       capturing_ = true;
+      kernel_timer().capturing = true;
       bool ok = true;
       try {
         enqueue_step(host_input, host_target);
@@ -737,6 +752,7 @@ float Executor::step(const void* host_input, const void* host_target) {
         ok = false;
       }
       capturing_ = false;
+      kernel_timer().capturing = false;
       const cudaError_t end = cudaStreamEndCapture(compute_, &graph);
       if (ok && end == cudaSuccess && graph) {
         DPL_CUDA(cudaGraphInstantiate(&exec, graph, 0));
