@@ -65,6 +65,7 @@ struct alignas(64) GemmParams {
   int M, N, K, batch;
   int a_mn_major, b_mn_major;
   int num_m_blocks, num_n_blocks, num_k_blocks, num_tiles;
+  int k_splits, kb_per_split;  // split-K (fp32-accumulate outputs only)
   uint32_t epi;
   float alpha;
   void* C;

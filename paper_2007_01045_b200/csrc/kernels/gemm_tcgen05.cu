@@ -192,7 +192,18 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int z, int r
   } else {
     float* c = static_cast<float*>(p.C) + off;
     const bool acc = kind == kOutF32Acc;
-    if (full) {
+    if (acc && p.k_splits > 1) {
+      // split-K partial sums meet in the fp32 accumulator
+      if (full) {
+        float4* c4 = reinterpret_cast<float4*>(c);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) atomicAdd(c4 + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < ncols) atomicAdd(c + j, v[j]);
+      }
+    } else if (full) {
       float4* c4 = reinterpret_cast<float4*>(c);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -256,11 +267,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        const int z = t / tiles_per_z;
-        const int r = t % tiles_per_z;
+        const int ks = t % p.k_splits;
+        const int tt = t / p.k_splits;
+        const int z = tt / tiles_per_z;
+        const int r = tt % tiles_per_z;
         const int mb = r % p.num_m_blocks;
         const int nb = r / p.num_m_blocks;
-        for (int kb = 0; kb < p.num_k_blocks; ++kb) {
+        const int kb0 = ks * p.kb_per_split;
+        const int kb1 = min(p.num_k_blocks, kb0 + p.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
           uint8_t* sa = smem_a + stage * C::kABytes;
@@ -302,10 +317,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        const int ks = t % p.k_splits;
+        const int kb0 = ks * p.kb_per_split;
+        const int kb1 = min(p.num_k_blocks, kb0 + p.kb_per_split);
         ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
-        for (int kb = 0; kb < p.num_k_blocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
           const uint32_t sa = ptx::smem_addr(smem_a + stage * C::kABytes);
@@ -314,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
           for (int k = 0; k < kBK / 16; ++k) {
             const uint64_t ad = ptx::smem_desc_sw128(sa + k * a_step, a_lbo, 1024);
             const uint64_t bd = ptx::smem_desc_sw128(sb + k * b_step, b_lbo, 1024);
-            ptx::mma_bf16(tmem_d, ad, bd, idesc, (kb | k) != 0);
+            ptx::mma_bf16(tmem_d, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
           }
           ptx::mma_commit(&empty[stage]);
           if (++stage == S) {
@@ -337,8 +355,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-      const int z = t / tiles_per_z;
-      const int r = t % tiles_per_z;
+      const int tt = t / p.k_splits;
+      const int z = tt / tiles_per_z;
+      const int r = tt % tiles_per_z;
       const int mb = r % p.num_m_blocks;
       const int nb = r / p.num_m_blocks;
       ptx::mbar_wait(&tmem_full[acc], acc_phase);
@@ -445,6 +464,7 @@ void GemmOp::prepare(const GemmDesc& d) {
   if (d.M <= 0 || d.N <= 0 || d.K <= 0 || d.batch <= 0) throw std::invalid_argument("dpl gemm: empty problem");
   if (d.ndiv % 32 != 0) throw std::invalid_argument("dpl gemm: ndiv must be a multiple of 32");
   int bn = d.force_bn;
+  if (bn == 0 && (d.epi & kOutMask) == kOutF32Acc && d.N > 128) bn = 256;  // split-K fills the machine
   if (bn == 0) {
     if (d.N <= 64) {
       bn = 64;
@@ -479,7 +499,19 @@ void GemmOp::prepare(const GemmDesc& d) {
   p.num_m_blocks = ceil_div(d.M, kBM);
   p.num_n_blocks = ceil_div(d.N, bn);
   p.num_k_blocks = ceil_div(d.K, kBK);
-  p.num_tiles = p.num_m_blocks * p.num_n_blocks * d.batch;
+  p.k_splits = 1;
+  p.kb_per_split = p.num_k_blocks;
+  if ((d.epi & kOutMask) == kOutF32Acc) {
+    // too few tiles for the SMs: split K (>= 8 k-blocks per split) and let
+    // the fp32 accumulator absorb the partial sums atomically
+    const int sms = num_sms();
+    const int tiles = p.num_m_blocks * p.num_n_blocks * d.batch;
+    int splits = 1;
+    while (tiles * splits * 2 <= sms && p.num_k_blocks / (splits * 2) >= 8) splits *= 2;
+    p.kb_per_split = ceil_div(p.num_k_blocks, splits);
+    p.k_splits = ceil_div(p.num_k_blocks, p.kb_per_split);
+  }
+  p.num_tiles = p.num_m_blocks * p.num_n_blocks * d.batch * p.k_splits;
   p.epi = d.epi;
   p.alpha = d.alpha;
   p.C = d.C;
