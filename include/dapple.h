@@ -70,6 +70,7 @@ typedef struct dpl_gemm_desc {
   const void* resid;
   void* aux_out;
   int force_bn;
+  int force_1sm; /* 1: never use the cta_group::2 pair kernel */
 } dpl_gemm_desc;
 
 #define DPL_EPI_OUT_BF16 0u

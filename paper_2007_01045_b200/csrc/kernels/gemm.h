@@ -56,6 +56,7 @@ struct GemmDesc {
   const void* resid = nullptr;
   void* aux_out = nullptr;
   int force_bn = 0;  // 0 = heuristic; else 64/128/256
+  int force_1sm = 0; // 1 = never use the CTA-pair kernel
 };
 
 // Device-visible launch parameters (one per prepared GEMM).
@@ -66,6 +67,7 @@ struct alignas(64) GemmParams {
   int a_mn_major, b_mn_major;
   int num_m_blocks, num_n_blocks, num_k_blocks, num_tiles;
   int k_splits, kb_per_split;  // split-K (fp32-accumulate outputs only)
+  int two_sm;                  // cta_group::2 pair kernel (256 x 256 tiles)
   uint32_t epi;
   float alpha;
   void* C;
@@ -87,6 +89,7 @@ class GemmOp {
   void prepare(const GemmDesc& d);
   void launch(cudaStream_t stream) const;
   int bn() const { return bn_; }
+  bool two_sm() const { return params_.two_sm != 0; }
   int grid() const { return grid_; }
   double flops() const { return 2.0 * params_.M * params_.N * static_cast<double>(params_.K) * params_.batch; }
   const GemmParams& params() const { return params_; }

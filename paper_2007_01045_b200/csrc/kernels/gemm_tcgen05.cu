@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -399,6 +400,197 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
   }
 }
 
+
+// ---------------------------------------------------------------- CTA pair
+// cta_group::2 variant: a cluster of two CTAs on one TPC computes a 256 x 256
+// tile.  Each CTA stages its own 128 rows of A and its own 128-column half of
+// B (32 KB per stage instead of 48 KB for the same MMA work per SM); the
+// leader CTA issues M=256 MMAs that read both CTAs' smem and write each CTA's
+// 128 accumulator rows into its own TMEM.  Both CTAs' TMA bytes land on the
+// leader's full barrier; the leader's commits multicast to both CTAs' empty /
+// tmem_full barriers; both CTAs' epilogue warps release the leader's
+// tmem_empty barrier.
+namespace pair {
+constexpr int kBN = 256;
+constexpr int kABytes = kBM * kBK * 2;        // 16 KB: this CTA's 128 rows of A
+constexpr int kBBytes = (kBN / 2) * kBK * 2;  // 16 KB: this CTA's half of B
+constexpr int kStageBytes = kABytes + kBBytes;
+constexpr int kStages = (kSmemBudget - 2048) / kStageBytes > 8 ? 8 : (kSmemBudget - 2048) / kStageBytes;
+constexpr int kSmem = 1024 + kStages * kStageBytes + 1024;
+}  // namespace pair
+
+__global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __grid_constant__ GemmParams p) {
+  using namespace pair;
+  constexpr int S = kStages;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + S * kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * kStageBytes);
+  uint64_t* empty = full + S;
+  uint64_t* tmem_full = empty + S;
+  uint64_t* tmem_empty = tmem_full + 2;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+  const uint32_t warp = ptx::warp_id();
+  const uint32_t lane = ptx::lane_id();
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair_id = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&p.tma_a);
+    ptx::tma_prefetch_desc(&p.tma_b);
+    for (int s = 0; s < S; ++s) {
+      ptx::mbar_init(&full[s], 2);   // leader's expect_tx + the peer's remote arrive
+      ptx::mbar_init(&empty[s], 1);  // one multicast commit
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tmem_full[a], 1);
+      ptx::mbar_init(&tmem_empty[a], 2 * kEpiWarps);  // one arrive per epilogue warp of both CTAs
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc_2sm<512>(tmem_base_slot);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_slot;
+  const int tiles_per_z = p.num_m_blocks * p.num_n_blocks;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair_id; t < p.num_tiles; t += n_pairs) {
+        const int ks = t % p.k_splits;
+        const int tt = t / p.k_splits;
+        const int z = tt / tiles_per_z;
+        const int r = tt % tiles_per_z;
+        const int mb = r % p.num_m_blocks;
+        const int nb = r / p.num_m_blocks;
+        const int kb0 = ks * p.kb_per_split;
+        const int kb1 = min(p.num_k_blocks, kb0 + p.kb_per_split);
+        const int m0 = mb * 256 + rank * 128;
+        const int n0 = nb * kBN + rank * (kBN / 2);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
+          else ptx::mbar_arrive_cluster(&full[stage], 0);
+          uint8_t* sa = smem_a + stage * kABytes;
+          uint8_t* sb = smem_b + stage * kBBytes;
+          if (!p.a_mn_major) {
+            ptx::tma_load_3d_2sm(sa, &p.tma_a, &full[stage], kb * kBK, m0, z);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) ptx::tma_load_3d_2sm(sa + j * 64 * kBK * 2, &p.tma_a, &full[stage], m0 + j * 64, kb * kBK, z);
+          }
+          if (!p.b_mn_major) {
+            ptx::tma_load_3d_2sm(sb, &p.tma_b, &full[stage], kb * kBK, n0, z);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) ptx::tma_load_3d_2sm(sb + j * 64 * kBK * 2, &p.tma_b, &full[stage], n0 + j * 64, kb * kBK, z);
+          }
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      const uint32_t idesc = ptx::idesc_bf16_f32(256, kBN, p.a_mn_major != 0, p.b_mn_major != 0);
+      const uint32_t a_lbo = p.a_mn_major ? 64 * kBK * 2 : 16;
+      const uint32_t b_lbo = p.b_mn_major ? 64 * kBK * 2 : 16;
+      const uint32_t a_step = p.a_mn_major ? 16 * 128 : 32;
+      const uint32_t b_step = p.b_mn_major ? 16 * 128 : 32;
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = pair_id; t < p.num_tiles; t += n_pairs) {
+        const int ks = t % p.k_splits;
+        const int kb0 = ks * p.kb_per_split;
+        const int kb1 = min(p.num_k_blocks, kb0 + p.kb_per_split);
+        ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * kBN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t sa = ptx::smem_addr(smem_a + stage * kABytes);
+          const uint32_t sb = ptx::smem_addr(smem_b + stage * kBBytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            const uint64_t ad = ptx::smem_desc_sw128(sa + k * a_step, a_lbo, 1024);
+            const uint64_t bd = ptx::smem_desc_sw128(sb + k * b_step, b_lbo, 1024);
+            ptx::mma_bf16_2sm(tmem_d, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+          }
+          ptx::mma_commit_2sm(&empty[stage]);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::mma_commit_2sm(&tmem_full[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const uint32_t quad = warp & 3;
+    const int half = (warp - 4) >> 2;
+    constexpr int kChunks = kBN / 32;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = pair_id; t < p.num_tiles; t += n_pairs) {
+      const int tt = t / p.k_splits;
+      const int z = tt / tiles_per_z;
+      const int r = tt % tiles_per_z;
+      const int mb = r % p.num_m_blocks;
+      const int nb = r / p.num_m_blocks;
+      ptx::mbar_wait(&tmem_full[acc], acc_phase);
+      ptx::tc_fence_after();
+      const int row = mb * 256 + rank * 128 + quad * 32 + lane;
+      const uint32_t tbase = tmem_base + ((quad * 32) << 16) + acc * kBN;
+      uint32_t ra[32], rb[32];
+      ptx::tmem_ld_32x32b_x32(tbase + half * 32, ra);
+      ptx::tmem_wait_ld();
+#pragma unroll 1
+      for (int c = half; c < kChunks; c += 4) {
+        const bool more = c + 2 < kChunks;
+        if (more) ptx::tmem_ld_32x32b_x32(tbase + (c + 2) * 32, rb);
+        epilogue_chunk(p, z, row, nb * kBN + c * 32, ra);
+        ptx::tmem_wait_ld();
+        if (!more) break;
+        if (c + 4 < kChunks) ptx::tmem_ld_32x32b_x32(tbase + (c + 4) * 32, ra);
+        epilogue_chunk(p, z, row, nb * kBN + (c + 2) * 32, rb);
+        ptx::tmem_wait_ld();
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) ptx::mbar_arrive(&tmem_empty[acc]);
+        else ptx::mbar_arrive_cluster(&tmem_empty[acc], 0);
+      }
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_2sm<512>(tmem_base);
+  }
+}
+
 // ---------------------------------------------------------------- host side
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -484,8 +676,15 @@ void GemmOp::prepare(const GemmDesc& d) {
       }
     }
   }
+  static const bool pair_enabled = [] {
+    const char* e = std::getenv("DPL_GEMM_2SM");
+    return !(e && e[0] == '0');
+  }();
+  const bool two_sm = pair_enabled && !d.force_1sm && bn == 256 && d.M >= 256;
+  const int bm = two_sm ? 256 : kBM;
   GemmParams& p = params_;
   p = GemmParams{};
+  p.two_sm = two_sm;
   p.M = d.M;
   p.N = d.N;
   p.K = d.K;
@@ -495,8 +694,8 @@ void GemmOp::prepare(const GemmDesc& d) {
   p.tma_a = d.a_mn_major ? make_map(d.A, d.M, d.K, d.lda, d.batch, d.a_batch_stride, kBK)
                          : make_map(d.A, d.K, d.M, d.lda, d.batch, d.a_batch_stride, kBM);
   p.tma_b = d.b_mn_major ? make_map(d.B, d.N, d.K, d.ldb, d.batch, d.b_batch_stride, kBK)
-                         : make_map(d.B, d.K, d.N, d.ldb, d.batch, d.b_batch_stride, bn);
-  p.num_m_blocks = ceil_div(d.M, kBM);
+                         : make_map(d.B, d.K, d.N, d.ldb, d.batch, d.b_batch_stride, two_sm ? bn / 2 : bn);
+  p.num_m_blocks = ceil_div(d.M, bm);
   p.num_n_blocks = ceil_div(d.N, bn);
   p.num_k_blocks = ceil_div(d.K, kBK);
   p.k_splits = 1;
@@ -504,7 +703,7 @@ void GemmOp::prepare(const GemmDesc& d) {
   if ((d.epi & kOutMask) == kOutF32Acc) {
     // too few tiles for the SMs: split K (>= 8 k-blocks per split) and let
     // the fp32 accumulator absorb the partial sums atomically
-    const int sms = num_sms();
+    const int sms = two_sm ? num_sms() / 2 : num_sms();
     const int tiles = p.num_m_blocks * p.num_n_blocks * d.batch;
     int splits = 1;
     while (tiles * splits * 2 <= sms && p.num_k_blocks / (splits * 2) >= 8) splits *= 2;
@@ -538,7 +737,15 @@ void GemmOp::prepare(const GemmDesc& d) {
                                                                    (d.s_zi * 2) % 16 == 0 && (d.s_no * 2) % 16 == 0);
   p.vec_ok = aligned && aux_aligned;
   bn_ = bn;
-  grid_ = std::min(p.num_tiles, num_sms());
+  grid_ = two_sm ? 2 * std::min(p.num_tiles, num_sms() / 2) : std::min(p.num_tiles, num_sms());
+  if (two_sm) {
+    smem_ = pair::kSmem;
+    static std::once_flag once;
+    std::call_once(once, [] {
+      cudaFuncSetAttribute(gemm_bf16_tcgen05_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize, pair::kSmem);
+    });
+    return;
+  }
   switch (bn) {
     case 64: smem_ = Cfg<64>::kSmem; configure_kernel<64>(); break;
     case 128: smem_ = Cfg<128>::kSmem; configure_kernel<128>(); break;
@@ -564,7 +771,7 @@ const GemmOp& GemmCache::get(const GemmDesc& d) {
                          static_cast<long long>(reinterpret_cast<uintptr_t>(d.bias)),
                          static_cast<long long>(reinterpret_cast<uintptr_t>(d.aux_in)),
                          static_cast<long long>(reinterpret_cast<uintptr_t>(d.resid)),
-                         static_cast<long long>(reinterpret_cast<uintptr_t>(d.aux_out)), d.force_bn};
+                         static_cast<long long>(reinterpret_cast<uintptr_t>(d.aux_out)), d.force_bn, d.force_1sm};
   std::string key(reinterpret_cast<const char*>(f), sizeof f);
   uint32_t a;
   std::memcpy(&a, &d.alpha, 4);
@@ -616,6 +823,23 @@ void GemmCache::run(const GemmDesc& d, cudaStream_t s) {
 void GemmOp::launch(cudaStream_t stream) const {
   count_launch();
   TimedLaunch timed_("gemm_bf16_tcgen05", stream, flops());
+  if (params_.two_sm) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid_);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem_;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_bf16_tcgen05_2sm, params_);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("dpl gemm: pair launch failed: ") + cudaGetErrorString(e));
+    return;
+  }
   switch (bn_) {
     case 64: gemm_bf16_tcgen05<64><<<grid_, kThreads, smem_, stream>>>(params_); break;
     case 128: gemm_bf16_tcgen05<128><<<grid_, kThreads, smem_, stream>>>(params_); break;

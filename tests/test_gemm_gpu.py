@@ -19,19 +19,20 @@ def _close(out, ref, tol):
 
 
 @pytest.mark.parametrize("M,N,Kd", [(128, 256, 64), (256, 512, 1024), (300, 200, 136), (1024, 3072, 1024),
-                                    (64, 64, 16), (513, 1000, 520)])
+                                    (64, 64, 16), (513, 1000, 520), (4096, 1024, 1024)])
 @pytest.mark.parametrize("bn", [0, 64, 128, 256])
-def test_gemm_kk(cuda, M, N, Kd, bn):
+@pytest.mark.parametrize("one_sm", [False, True])
+def test_gemm_kk(cuda, M, N, Kd, bn, one_sm):
     A = _rand(M, Kd, dev=cuda, seed=1)
     B = _rand(N, Kd, dev=cuda, seed=2)
     C = torch.zeros(M, N, dtype=torch.bfloat16, device=cuda)
-    K.gemm(A, B, C, M, N, Kd, lda=Kd, ldb=Kd, ldc=N, force_bn=bn)
+    K.gemm(A, B, C, M, N, Kd, lda=Kd, ldb=Kd, ldc=N, force_bn=bn, force_1sm=one_sm)
     torch.cuda.synchronize()
     _close(C, A.float() @ B.float().T, 2e-2)
 
 
 @pytest.mark.parametrize("a_mn,b_mn", [(True, False), (False, True), (True, True)])
-@pytest.mark.parametrize("M,N,Kd", [(256, 256, 128), (384, 640, 1024), (200, 136, 72)])
+@pytest.mark.parametrize("M,N,Kd", [(256, 256, 128), (384, 640, 1024), (200, 136, 72), (1000, 520, 264)])
 @pytest.mark.parametrize("bn", [64, 128, 256])
 def test_gemm_mn_major(cuda, a_mn, b_mn, M, N, Kd, bn):
     At = _rand(Kd, M, dev=cuda, seed=3) if a_mn else _rand(M, Kd, dev=cuda, seed=3)
