@@ -32,6 +32,7 @@
 
 #include "attention.h"
 #include "gemm.h"
+#include "launch.cuh"
 #include "ptx.cuh"
 
 namespace dpl {
@@ -121,6 +122,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  ptx::pdl_wait();
   // TMEM columns: S [0,128), O buffers [128,192) [192,256)
 
   if (warp == 0) {
@@ -273,6 +275,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
     p.lse[static_cast<long long>(z) * p.S + q] = (m + log2f(l)) * 0.69314718055994531f;
   }
 
+  ptx::pdl_trigger();
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 2) {
@@ -355,6 +358,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  ptx::pdl_wait();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -506,6 +510,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
     }
   }
 
+  ptx::pdl_trigger();
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 2) {
@@ -519,6 +524,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
 __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ dout, const __nv_bfloat16* __restrict__ out,
                                      long long ldo, float* __restrict__ dsum, float* __restrict__ dq_acc, int S, int B,
                                      int rows) {
+  ptx::pdl_wait();
   const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
   for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < rows; row += gridDim.x * warps) {
     const int z = row / S, q = row % S, b = z % B, h = z / B;
@@ -544,6 +550,7 @@ __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ dout, con
 // dqkv[b*S+q][h*64+j] = bf16(scale * dq_acc[z][q][j])
 __global__ void attn_bwd_dq_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv, long long ld,
                                    float scale, int S, int B, int rows) {
+  ptx::pdl_wait();
   const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
   for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < rows; row += gridDim.x * warps) {
     const int z = row / S, q = row % S, b = z % B, h = z / B;
@@ -613,7 +620,7 @@ void AttentionOp::forward(cudaStream_t s) const {
   p.lse = desc_.lse;
   count_launch();
   TimedLaunch timed_("attention_fwd", s, 4.0 * p.z_count * desc_.seq * desc_.seq * kD / (desc_.causal ? 2 : 1));
-  attn_fwd_kernel<<<dim3(desc_.seq / kT, p.z_count), kFwdThreads, kFwdSmem, s>>>(p);
+  launch_pdl(attn_fwd_kernel, dim3(desc_.seq / kT, p.z_count), dim3(kFwdThreads), kFwdSmem, s, p);
 }
 
 void AttentionOp::backward(cudaStream_t s) const {
@@ -624,9 +631,9 @@ void AttentionOp::backward(cudaStream_t s) const {
   const float scale = 1.0f / std::sqrt(static_cast<float>(kD));
   count_launch(3);
   TimedLaunch timed_("attention_bwd", s, 10.0 * z_count * desc_.seq * desc_.seq * kD / (desc_.causal ? 2 : 1));
-  attn_bwd_prep_kernel<<<std::min((rows + 7) / 8, 148 * 16), 256, 0, s>>>(
-      static_cast<const __nv_bfloat16*>(desc_.dout), static_cast<const __nv_bfloat16*>(desc_.ctx), desc_.ldc,
-      desc_.dsum, desc_.dq_acc, desc_.seq, desc_.samples, rows);
+  launch_pdl(attn_bwd_prep_kernel, dim3(std::min((rows + 7) / 8, 148 * 16)), dim3(256), 0, s,
+             static_cast<const __nv_bfloat16*>(desc_.dout), static_cast<const __nv_bfloat16*>(desc_.ctx), desc_.ldc,
+             desc_.dsum, desc_.dq_acc, desc_.seq, desc_.samples, rows);
   AttnBwdParams p;
   p.qkv = fwd_map_;
   p.dout = dout_map_;
@@ -643,9 +650,9 @@ void AttentionOp::backward(cudaStream_t s) const {
   p.dqkv = static_cast<__nv_bfloat16*>(desc_.dqkv);
   p.ld = 3LL * desc_.heads * kD;
   p.H = desc_.heads * kD;
-  attn_bwd_kernel<<<dim3(desc_.seq / kT, z_count), kBwdThreads, kBwdSmem, s>>>(p);
-  attn_bwd_dq_kernel<<<std::min((rows + 7) / 8, 148 * 16), 256, 0, s>>>(desc_.dq_acc, p.dqkv, p.ld, scale, desc_.seq,
-                                                                        desc_.samples, rows);
+  launch_pdl(attn_bwd_kernel, dim3(desc_.seq / kT, z_count), dim3(kBwdThreads), kBwdSmem, s, p);
+  launch_pdl(attn_bwd_dq_kernel, dim3(std::min((rows + 7) / 8, 148 * 16)), dim3(256), 0, s,
+             static_cast<const float*>(desc_.dq_acc), p.dqkv, p.ld, scale, desc_.seq, desc_.samples, rows);
 }
 
 }  // namespace dpl

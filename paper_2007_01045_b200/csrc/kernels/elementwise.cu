@@ -14,6 +14,8 @@
 
 #include "elementwise.h"
 #include "gemm.h"
+#include "launch.cuh"
+#include "ptx.cuh"
 
 namespace dpl {
 
@@ -93,6 +95,7 @@ __global__ void __launch_bounds__(256, 4)
     layernorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ gamma,
                          const float* __restrict__ beta, __nv_bfloat16* __restrict__ y, float* __restrict__ mean_out,
                          float* __restrict__ rstd_out, int rows, int h, float eps) {
+  ptx::pdl_wait();
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nvec = h / 8;
@@ -154,6 +157,7 @@ __global__ void __launch_bounds__(256, 4)
                               const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
                               const float* __restrict__ gamma, const __nv_bfloat16* __restrict__ dresid,
                               __nv_bfloat16* __restrict__ dx, int rows, int h) {
+  ptx::pdl_wait();
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nvec = h / 8;
@@ -221,6 +225,7 @@ __global__ void __launch_bounds__(256, 4)
                        const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
                        const __nv_bfloat16* __restrict__ dresid, const __nv_bfloat16* __restrict__ dx,
                        float* __restrict__ ws, int rows, int h) {
+  ptx::pdl_wait();
   __shared__ float part[8][kRed][257];
   const int vx = threadIdx.x & 31, ry = threadIdx.x >> 5;
   const int vi = blockIdx.x * 32 + vx;
@@ -282,6 +287,7 @@ __global__ void __launch_bounds__(256, 4)
 // dst_k[c] += sum_b ws[b][k][c] for each of the nred column reductions
 __global__ void ln_param_reduce_kernel(const float* __restrict__ ws, float* d0, float* d1, float* d2, float* d3,
                                        int blocks, int nred, int h) {
+  ptx::pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nred * h) return;
   float s = 0.f;
@@ -297,6 +303,7 @@ __global__ void ln_param_reduce_kernel(const float* __restrict__ ws, float* d0, 
 template <int kMaxVec>
 __global__ void softmax_fwd_kernel(const float* __restrict__ s, __nv_bfloat16* __restrict__ p, int rows, int len,
                                    int q_len, int causal) {
+  ptx::pdl_wait();
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nvec = len / 8;
@@ -348,6 +355,7 @@ __global__ void softmax_fwd_kernel(const float* __restrict__ s, __nv_bfloat16* _
 template <int kMaxVec>
 __global__ void softmax_bwd_kernel(const __nv_bfloat16* __restrict__ p, const float* __restrict__ dp,
                                    __nv_bfloat16* __restrict__ ds, int rows, int len) {
+  ptx::pdl_wait();
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nvec = len / 8;
@@ -385,6 +393,7 @@ __global__ void softmax_bwd_kernel(const __nv_bfloat16* __restrict__ p, const fl
 // reduced in shared memory, then one atomic per column per block.
 __global__ void __launch_bounds__(256, 4) colsum_acc_kernel(const __nv_bfloat16* __restrict__ dy, float* __restrict__ db, int rows, int cols,
                                   int rows_per_block) {
+  ptx::pdl_wait();
   __shared__ float part[8][256 + 1];
   const int vx = threadIdx.x & 31, ry = threadIdx.x >> 5;
   const int vi = blockIdx.x * 32 + vx;
@@ -426,6 +435,7 @@ __global__ void __launch_bounds__(256, 4) colsum_acc_kernel(const __nv_bfloat16*
 __global__ void mse_kernel(const __nv_bfloat16* __restrict__ y, const __nv_bfloat16* __restrict__ t,
                            __nv_bfloat16* __restrict__ dy, float* __restrict__ loss_acc, long long n,
                            float grad_scale) {
+  ptx::pdl_wait();
   float local = 0.f;
   const long long nvec = n / 8;
   for (long long vi = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; vi < nvec;
@@ -456,6 +466,7 @@ __global__ void mse_kernel(const __nv_bfloat16* __restrict__ y, const __nv_bfloa
 // w32 -= lr * g ; w16 = bf16(w32) ; g = 0   (fp32 master weights)
 __global__ void sgd_kernel(float* __restrict__ w32, float* __restrict__ g, __nv_bfloat16* __restrict__ w16,
                            long long n, float lr) {
+  ptx::pdl_wait();
   const long long nvec = n / 4;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < nvec;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -497,22 +508,26 @@ __device__ __forceinline__ float hash_uniform(uint64_t seed, uint64_t tensor, ui
 // dst[r][c] = scale * U(-1,1) keyed by (seed, tensor, (row0 + r) * cols + c)
 __global__ void fill_uniform_bf16_kernel(__nv_bfloat16* dst, long long n, uint64_t seed, uint64_t tensor,
                                          long long idx0, float scale) {
+  ptx::pdl_wait();
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x)
     dst[i] = __float2bfloat16_rn(scale * hash_uniform(seed, tensor, static_cast<uint64_t>(idx0 + i)));
 }
 __global__ void fill_uniform_f32_kernel(float* dst, long long n, uint64_t seed, uint64_t tensor, long long idx0,
                                         float scale) {
+  ptx::pdl_wait();
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x)
     dst[i] = scale * hash_uniform(seed, tensor, static_cast<uint64_t>(idx0 + i));
 }
 __global__ void fill_const_f32_kernel(float* dst, long long n, float v) {
+  ptx::pdl_wait();
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x)
     dst[i] = v;
 }
 __global__ void cast_f32_bf16_kernel(const float* src, __nv_bfloat16* dst, long long n) {
+  ptx::pdl_wait();
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x)
     dst[i] = __float2bfloat16_rn(src[i]);
@@ -533,7 +548,7 @@ void layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y
   const int warps = 8;
   const int grid = std::max(1, std::min((rows + warps - 1) / warps, 148 * 8));
   dispatch_vec(h, [&](auto v) {
-    layernorm_fwd_kernel<decltype(v)::value><<<grid, warps * 32, 0, s>>>(
+    launch_pdl(layernorm_fwd_kernel<decltype(v)::value>, dim3(grid), dim3(warps * 32), 0, s, 
         static_cast<const __nv_bfloat16*>(x), gamma, beta, static_cast<__nv_bfloat16*>(y), mean, rstd, rows, h, eps);
   });
 }
@@ -553,7 +568,7 @@ void layernorm_bwd(const void* dy, const void* x, const float* mean, const float
   const auto* pr = static_cast<const __nv_bfloat16*>(dresid);
   auto* pdx = static_cast<__nv_bfloat16*>(dx);
   dispatch_vec(h, [&](auto v) {
-    layernorm_bwd_rows_kernel<decltype(v)::value><<<grid, warps * 32, 0, s>>>(pdy, px, mean, rstd, gamma, pr, pdx,
+    launch_pdl(layernorm_bwd_rows_kernel<decltype(v)::value>, dim3(grid), dim3(warps * 32), 0, s, pdy, px, mean, rstd, gamma, pr, pdx,
                                                                               rows, h);
   });
   const int nred = dx_colsum ? 4 : (dresid_colsum ? 3 : 2);
@@ -561,10 +576,10 @@ void layernorm_bwd(const void* dy, const void* x, const float* mean, const float
   if (static_cast<long long>(slabs) * nred * h > static_cast<long long>(kLnBwdBlocks) * 4 * h)
     throw std::invalid_argument("layernorm_bwd: too many rows for the workspace");
   const dim3 cg((h / 8 + 31) / 32, slabs);
-  if (nred == 2) ln_bwd_cols_kernel<2><<<cg, 256, 0, s>>>(pdy, px, mean, rstd, pr, pdx, ws, rows, h);
-  else if (nred == 3) ln_bwd_cols_kernel<3><<<cg, 256, 0, s>>>(pdy, px, mean, rstd, pr, pdx, ws, rows, h);
-  else ln_bwd_cols_kernel<4><<<cg, 256, 0, s>>>(pdy, px, mean, rstd, pr, pdx, ws, rows, h);
-  ln_param_reduce_kernel<<<(nred * h + 255) / 256, 256, 0, s>>>(ws, dgamma, dbeta, dresid_colsum, dx_colsum, slabs,
+  if (nred == 2) launch_pdl(ln_bwd_cols_kernel<2>, dim3(cg), dim3(256), 0, s, pdy, px, mean, rstd, pr, pdx, ws, rows, h);
+  else if (nred == 3) launch_pdl(ln_bwd_cols_kernel<3>, dim3(cg), dim3(256), 0, s, pdy, px, mean, rstd, pr, pdx, ws, rows, h);
+  else launch_pdl(ln_bwd_cols_kernel<4>, dim3(cg), dim3(256), 0, s, pdy, px, mean, rstd, pr, pdx, ws, rows, h);
+  launch_pdl(ln_param_reduce_kernel, dim3((nred * h + 255) / 256), dim3(256), 0, s, ws, dgamma, dbeta, dresid_colsum, dx_colsum, slabs,
                                                                 nred, h);
 }
 
@@ -574,7 +589,7 @@ void softmax_fwd(const float* s, void* p, int rows, int len, int q_len, int caus
   const int warps = 8;
   const int grid = std::max(1, std::min((rows + warps - 1) / warps, 148 * 16));
   dispatch_vec(len, [&](auto v) {
-    softmax_fwd_kernel<decltype(v)::value><<<grid, warps * 32, 0, st>>>(s, static_cast<__nv_bfloat16*>(p), rows, len,
+    launch_pdl(softmax_fwd_kernel<decltype(v)::value>, dim3(grid), dim3(warps * 32), 0, st, s, static_cast<__nv_bfloat16*>(p), rows, len,
                                                                         q_len, causal);
   });
 }
@@ -585,7 +600,7 @@ void softmax_bwd(const void* p, const float* dp, void* ds, int rows, int len, cu
   const int warps = 8;
   const int grid = std::max(1, std::min((rows + warps - 1) / warps, 148 * 16));
   dispatch_vec(len, [&](auto v) {
-    softmax_bwd_kernel<decltype(v)::value><<<grid, warps * 32, 0, st>>>(static_cast<const __nv_bfloat16*>(p), dp,
+    launch_pdl(softmax_bwd_kernel<decltype(v)::value>, dim3(grid), dim3(warps * 32), 0, st, static_cast<const __nv_bfloat16*>(p), dp,
                                                                         static_cast<__nv_bfloat16*>(ds), rows, len);
   });
 }
@@ -598,13 +613,13 @@ void colsum_acc(const void* dy, float* db, int rows, int cols, cudaStream_t s) {
   int gy = std::max(1, std::min((rows + 63) / 64, (148 * 2 + gx - 1) / gx));
   const int rpb = (rows + gy - 1) / gy;
   gy = (rows + rpb - 1) / rpb;
-  colsum_acc_kernel<<<dim3(gx, gy), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(dy), db, rows, cols, rpb);
+  launch_pdl(colsum_acc_kernel, dim3(gx, gy), dim3(256), 0, s, static_cast<const __nv_bfloat16*>(dy), db, rows, cols, rpb);
 }
 
 void mse_loss(const void* y, const void* t, void* dy, float* loss_acc, long long n, float grad_scale, cudaStream_t s) {
   count_launch();
   TimedLaunch timed_("mse_loss", s);
-  mse_kernel<<<grid_for(n / 8, 256), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(y),
+  launch_pdl(mse_kernel, dim3(grid_for(n / 8, 256)), dim3(256), 0, s, static_cast<const __nv_bfloat16*>(y),
                                                    static_cast<const __nv_bfloat16*>(t),
                                                    static_cast<__nv_bfloat16*>(dy), loss_acc, n, grad_scale);
 }
@@ -612,14 +627,14 @@ void mse_loss(const void* y, const void* t, void* dy, float* loss_acc, long long
 void sgd_apply(float* w32, float* g, void* w16, long long n, float lr, cudaStream_t s) {
   count_launch();
   TimedLaunch timed_("sgd_apply", s);
-  sgd_kernel<<<grid_for(n / 4, 256), 256, 0, s>>>(w32, g, static_cast<__nv_bfloat16*>(w16), n, lr);
+  launch_pdl(sgd_kernel, dim3(grid_for(n / 4, 256)), dim3(256), 0, s, w32, g, static_cast<__nv_bfloat16*>(w16), n, lr);
 }
 
 void fill_uniform_bf16(void* dst, long long n, uint64_t seed, uint64_t tensor, long long idx0, float scale,
                        cudaStream_t s) {
   count_launch();
   TimedLaunch timed_("fill_uniform", s);
-  fill_uniform_bf16_kernel<<<grid_for(n, 256), 256, 0, s>>>(static_cast<__nv_bfloat16*>(dst), n, seed, tensor, idx0,
+  launch_pdl(fill_uniform_bf16_kernel, dim3(grid_for(n, 256)), dim3(256), 0, s, static_cast<__nv_bfloat16*>(dst), n, seed, tensor, idx0,
                                                             scale);
 }
 
@@ -627,19 +642,19 @@ void fill_uniform_f32(float* dst, long long n, uint64_t seed, uint64_t tensor, l
                       cudaStream_t s) {
   count_launch();
   TimedLaunch timed_("fill_uniform", s);
-  fill_uniform_f32_kernel<<<grid_for(n, 256), 256, 0, s>>>(dst, n, seed, tensor, idx0, scale);
+  launch_pdl(fill_uniform_f32_kernel, dim3(grid_for(n, 256)), dim3(256), 0, s, dst, n, seed, tensor, idx0, scale);
 }
 
 void fill_const_f32(float* dst, long long n, float v, cudaStream_t s) {
   count_launch();
   TimedLaunch timed_("fill_const", s);
-  fill_const_f32_kernel<<<grid_for(n, 256), 256, 0, s>>>(dst, n, v);
+  launch_pdl(fill_const_f32_kernel, dim3(grid_for(n, 256)), dim3(256), 0, s, dst, n, v);
 }
 
 void cast_f32_bf16(const float* src, void* dst, long long n, cudaStream_t s) {
   count_launch();
   TimedLaunch timed_("cast_f32_bf16", s);
-  cast_f32_bf16_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, static_cast<__nv_bfloat16*>(dst), n);
+  launch_pdl(cast_f32_bf16_kernel, dim3(grid_for(n, 256)), dim3(256), 0, s, src, static_cast<__nv_bfloat16*>(dst), n);
 }
 
 }  // namespace dpl

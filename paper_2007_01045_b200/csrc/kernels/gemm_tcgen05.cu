@@ -27,6 +27,7 @@
 #include <string>
 
 #include "gemm.h"
+#include "launch.cuh"
 #include "ptx.cuh"
 
 namespace dpl {
@@ -74,8 +75,42 @@ __device__ __forceinline__ long long out_offset(const GemmParams& p, int z, int 
          static_cast<long long>(m) * p.ldc + static_cast<long long>(n / p.ndiv) * p.s_no + (n % p.ndiv);
 }
 
+// Global operands of one thread's 32-column epilogue chunk (bias, residual,
+// activation input), loaded one chunk ahead so their latency overlaps the
+// previous chunk's math.
+// One prefetched bf16 operand: the residual if kResid, else the activation
+// input of kDGelu / kDRelu (a GEMM that needs both loads aux_in directly).
+struct EpiExtras {
+  uint4 v[4];
+};
+
+__device__ __forceinline__ const __nv_bfloat16* prefetched_tensor(const GemmParams& p) {
+  if (p.epi & kResid) return p.resid;
+  if (p.epi & (kDGelu | kDRelu)) return p.aux_in;
+  return nullptr;
+}
+
+__device__ __forceinline__ void epilogue_prefetch(const GemmParams& p, int z, int row, int n0, EpiExtras& x) {
+  const __nv_bfloat16* src = prefetched_tensor(p);
+  if (!src || row >= p.M || n0 >= p.N || !p.vec_ok || p.N - n0 < 32) return;
+  const uint4* s4 = reinterpret_cast<const uint4*>(src + out_offset(p, z, row, n0));
+#pragma unroll
+  for (int q = 0; q < 4; ++q) x.v[q] = s4[q];
+}
+
+__device__ __forceinline__ void unpack_bf16x8(const uint4& r, float* f) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 v = __bfloat1622float2(h[e]);
+    f[2 * e] = v.x;
+    f[2 * e + 1] = v.y;
+  }
+}
+
 // Apply the epilogue to one thread's 32 consecutive columns of one row.
-__device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int z, int row, int n0, const uint32_t (&raw)[32]) {
+__device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int z, int row, int n0, const uint32_t (&raw)[32],
+                                               const EpiExtras& x) {
   if (row >= p.M || n0 >= p.N) return;
   const long long off = out_offset(p, z, row, n0);
   const int ncols = min(32, p.N - n0);
@@ -108,42 +143,35 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int z, int r
   }
   if (epi & kResid) {
     if (full) {
-      const uint4* r4 = reinterpret_cast<const uint4*>(p.resid + off);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const uint4 r = r4[q];
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+        float f[8];
+        unpack_bf16x8(x.v[q], f);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 f = __bfloat1622float2(h[e]);
-          v[8 * q + 2 * e] += f.x;
-          v[8 * q + 2 * e + 1] += f.y;
-        }
+        for (int e = 0; e < 8; ++e) v[8 * q + e] += f[e];
       }
     } else {
       _Pragma("unroll") for (int j = 0; j < 32; ++j) if (j < ncols) v[j] += __bfloat162float(p.resid[off + j]);
     }
   }
   if (epi & (kDGelu | kDRelu)) {
-    float z[32];
+    const bool gelu = (epi & kDGelu) != 0;
     if (full) {
       const uint4* a4 = reinterpret_cast<const uint4*>(p.aux_in + off);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const uint4 r = a4[q];
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+        float zq[8];
+        unpack_bf16x8((epi & kResid) ? a4[q] : x.v[q], zq);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 f = __bfloat1622float2(h[e]);
-          z[8 * q + 2 * e] = f.x;
-          z[8 * q + 2 * e + 1] = f.y;
-        }
+        for (int e = 0; e < 8; ++e) v[8 * q + e] *= gelu ? dgelu_f(zq[e]) : (zq[e] > 0.f ? 1.f : 0.f);
       }
     } else {
-      for (int j = 0; j < 32; ++j) z[j] = j < ncols ? __bfloat162float(p.aux_in[off + j]) : 0.f;
-    }
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] *= (epi & kDGelu) ? dgelu_f(z[j]) : (z[j] > 0.f ? 1.f : 0.f);
+      for (int j = 0; j < 32; ++j) {
+        const float zj = j < ncols ? __bfloat162float(p.aux_in[off + j]) : 0.f;
+        v[j] *= gelu ? dgelu_f(zj) : (zj > 0.f ? 1.f : 0.f);
+      }
+    }
   }
   if (epi & kAuxOut) {
     if (full) {
@@ -259,6 +287,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
+  // prologue done: wait for the producer kernel's writes, let the next kernel launch
+  ptx::pdl_wait();
+  ptx::pdl_trigger();
 
   const int tiles_per_z = p.num_m_blocks * p.num_n_blocks;
 
@@ -369,17 +400,25 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
         // two register buffers, statically indexed: load chunk c+2 while
         // chunk c is processed
         uint32_t ra[32], rb[32];
+        EpiExtras xa, xb;
+        epilogue_prefetch(p, z, row, nb * BN + half * 32, xa);
         ptx::tmem_ld_32x32b_x32(tbase + half * 32, ra);
         ptx::tmem_wait_ld();
 #pragma unroll 1
         for (int c = half; c < kChunks; c += 4) {
           const bool more = c + 2 < kChunks;
-          if (more) ptx::tmem_ld_32x32b_x32(tbase + (c + 2) * 32, rb);
-          epilogue_chunk(p, z, row, nb * BN + c * 32, ra);
+          if (more) {
+            epilogue_prefetch(p, z, row, nb * BN + (c + 2) * 32, xb);
+            ptx::tmem_ld_32x32b_x32(tbase + (c + 2) * 32, rb);
+          }
+          epilogue_chunk(p, z, row, nb * BN + c * 32, ra, xa);
           ptx::tmem_wait_ld();
           if (!more) break;
-          if (c + 4 < kChunks) ptx::tmem_ld_32x32b_x32(tbase + (c + 4) * 32, ra);
-          epilogue_chunk(p, z, row, nb * BN + (c + 2) * 32, rb);
+          if (c + 4 < kChunks) {
+            epilogue_prefetch(p, z, row, nb * BN + (c + 4) * 32, xa);
+            ptx::tmem_ld_32x32b_x32(tbase + (c + 4) * 32, ra);
+          }
+          epilogue_chunk(p, z, row, nb * BN + (c + 2) * 32, rb, xb);
           ptx::tmem_wait_ld();
         }
       }
@@ -456,6 +495,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
+  ptx::pdl_wait();
+  ptx::pdl_trigger();
   const int tiles_per_z = p.num_m_blocks * p.num_n_blocks;
 
   if (warp == 0) {
@@ -557,17 +598,25 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
       const int row = mb * 256 + rank * 128 + quad * 32 + lane;
       const uint32_t tbase = tmem_base + ((quad * 32) << 16) + acc * kBN;
       uint32_t ra[32], rb[32];
+      EpiExtras xa, xb;
+      epilogue_prefetch(p, z, row, nb * kBN + half * 32, xa);
       ptx::tmem_ld_32x32b_x32(tbase + half * 32, ra);
       ptx::tmem_wait_ld();
 #pragma unroll 1
       for (int c = half; c < kChunks; c += 4) {
         const bool more = c + 2 < kChunks;
-        if (more) ptx::tmem_ld_32x32b_x32(tbase + (c + 2) * 32, rb);
-        epilogue_chunk(p, z, row, nb * kBN + c * 32, ra);
+        if (more) {
+          epilogue_prefetch(p, z, row, nb * kBN + (c + 2) * 32, xb);
+          ptx::tmem_ld_32x32b_x32(tbase + (c + 2) * 32, rb);
+        }
+        epilogue_chunk(p, z, row, nb * kBN + c * 32, ra, xa);
         ptx::tmem_wait_ld();
         if (!more) break;
-        if (c + 4 < kChunks) ptx::tmem_ld_32x32b_x32(tbase + (c + 4) * 32, ra);
-        epilogue_chunk(p, z, row, nb * kBN + (c + 2) * 32, rb);
+        if (c + 4 < kChunks) {
+          epilogue_prefetch(p, z, row, nb * kBN + (c + 4) * 32, xa);
+          ptx::tmem_ld_32x32b_x32(tbase + (c + 4) * 32, ra);
+        }
+        epilogue_chunk(p, z, row, nb * kBN + (c + 2) * 32, rb, xb);
         ptx::tmem_wait_ld();
       }
       ptx::tc_fence_before();
@@ -829,21 +878,23 @@ void GemmOp::launch(cudaStream_t stream) const {
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem_;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_bf16_tcgen05_2sm, params_);
     if (e != cudaSuccess) throw std::runtime_error(std::string("dpl gemm: pair launch failed: ") + cudaGetErrorString(e));
     return;
   }
   switch (bn_) {
-    case 64: gemm_bf16_tcgen05<64><<<grid_, kThreads, smem_, stream>>>(params_); break;
-    case 128: gemm_bf16_tcgen05<128><<<grid_, kThreads, smem_, stream>>>(params_); break;
-    case 256: gemm_bf16_tcgen05<256><<<grid_, kThreads, smem_, stream>>>(params_); break;
+    case 64: launch_pdl(gemm_bf16_tcgen05<64>, dim3(grid_), dim3(kThreads), smem_, stream, params_); break;
+    case 128: launch_pdl(gemm_bf16_tcgen05<128>, dim3(grid_), dim3(kThreads), smem_, stream, params_); break;
+    case 256: launch_pdl(gemm_bf16_tcgen05<256>, dim3(grid_), dim3(kThreads), smem_, stream, params_); break;
     default: throw std::logic_error("dpl gemm: launch before prepare");
   }
 }
