@@ -175,7 +175,7 @@ def host_batches(model: dict, plan: dict, rank: int, m: int, slice_samples: int,
     return inp, tgt
 
 
-def predicted_latency(model, plan, timelines, m, n):
+def predicted_latency(model, plan, timelines, m, n, schedule="dapple"):
     """Builds a B200 layer profile from the measured blocks (per-layer F/B of
     the full micro-batch = block time x r / layers on the stage) and asks the
     host planner for est_latency (estimator.cpp:56-86) and sim_latency
@@ -208,7 +208,9 @@ def predicted_latency(model, plan, timelines, m, n):
                "inter_latency_us": 10.0, "per_gpu_memory_gb": 180.0}
     seq = pipeplan.build_stage_sequence(plan, profile, cluster)
     est = pipeplan.estimate_latency(seq, m)
-    sim = pipeplan.simulate_plan(plan, profile, cluster, m)
+    # the measured B blocks already contain any re-computed forward, so the
+    # calibrated profile is simulated without apply_recompute
+    sim = pipeplan.simulate_plan(plan, profile, cluster, m, schedule=schedule)
     blocks = sim["timeline"]["blocks"]
     busy = 0.0
     for x, i, kind, s, e in blocks:
@@ -279,6 +281,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-layers", type=int, default=8)
     ap.add_argument("--seed", type=int, default=1234)
+    ap.add_argument("--schedule", default="dapple", choices=["dapple", "gpipe"])
+    ap.add_argument("--recompute", action="store_true")
+    ap.add_argument("--timeline-out", default=None,
+                    help="write the last timed step's measured timeline (CSV + SVG, reference writers) here")
     args = ap.parse_args()
     rank, world = dist_setup()
     if args.impl == "reference":
@@ -300,7 +306,8 @@ def main():
     gbs = M * args.slice * r0
     lib = _lib.lib()
 
-    ex = Executor(model, plan, M, gbs, lr=1e-4, seed=args.seed, rank=rank, world=world, device=rank)
+    ex = Executor(model, plan, M, gbs, lr=1e-4, seed=args.seed, rank=rank, world=world, device=rank,
+                  schedule=args.schedule, recompute=args.recompute)
     clocks = ClockSampler() if rank == 0 else None
     if clocks:
         clocks.start()
@@ -386,7 +393,18 @@ def main():
             traffic = json.load(f).get("bytes_per_launch")
     except Exception:
         pass
-    pred = predicted_latency(model, plan, [all_tls[r][-1] for r in range(world)], M, world)
+    pred = predicted_latency(model, plan, [all_tls[r][-1] for r in range(world)], M, world, args.schedule)
+    from paper_2007_01045_b200 import pipeplan
+    phi_tl = info["phi_expanded"] if args.schedule == "dapple" else [M] * (2 * S - 1)
+    exported = pipeplan.timeline_export(merge_timelines([all_tls[r][-1] for r in range(world)], M, S), M,
+                                        2 * S - 1, phi_tl, plan, pred["profile"], pred["cluster"])
+    if args.timeline_out:
+        os.makedirs(args.timeline_out, exist_ok=True)
+        tag = f"{args.model}_n{world}_{args.schedule}{'_rc' if args.recompute else ''}"
+        with open(os.path.join(args.timeline_out, f"timeline_{tag}.csv"), "w") as f:
+            f.write(exported["csv"])
+        with open(os.path.join(args.timeline_out, f"timeline_{tag}.svg"), "w") as f:
+            f.write(exported["svg"])
     measured_ms = statistics.mean(lat) * 1e3
     fps = flops_per_sample(model)
     line = {
@@ -400,6 +418,9 @@ def main():
                    "l2": "working set (GBs of activations) far larger than the 126 MB L2"},
         "bubble": statistics.mean(bub),
         "device_s": device_s,
+        "schedule": {"kind": args.schedule, "recompute": args.recompute, "stash_slots": info["stash_slots"],
+                     "peak_activations_measured": exported["peak_activations"],
+                     "device_bytes": info.get("device_bytes")},
         "latency": {"measured_ms": measured_ms, "est_ms": pred["est_ms"], "sim_ms": pred["sim_ms"],
                     "sim_bubble": pred["sim_bubble"], "pivot": pred["pivot"],
                     "measured_over_sim": measured_ms / pred["sim_ms"],

@@ -42,6 +42,12 @@ struct ExecOptions {
   double lr = 1e-3;
   std::uint64_t seed = 1234;
   bool apply = true;
+  /// Block order: DAPPLE early-backward (default) or GPipe all-forward-first
+  /// (stage_chain, simulator.cpp:161-167).
+  ScheduleKind schedule = ScheduleKind::dapple;
+  /// Keep only stage inputs; each backward block re-runs the stage forward
+  /// (the executed counterpart of apply_recompute, simulator.cpp:216-221).
+  bool recompute = false;
   /// Plumbing for world > 1: all-gather of one byte string per rank
   /// (CUDA-IPC handles, NCCL ids, timelines), e.g. over torch.distributed
   /// or MPI.  Must be collective and return the strings in rank order.

@@ -304,6 +304,43 @@ Value dispatch(const Value& req) {
     out["routes"] = std::move(routes);
     return out;
   }
+  if (op == "timeline_export") {
+    // a measured (or any) timeline in timeline_to_json form -> the
+    // reference's CSV / SVG writers (io.cpp) and its block-level metrics
+    const Value& t = req.at("timeline");
+    Timeline tl;
+    tl.micro_batches = static_cast<int>(t.at("M").as_int());
+    tl.stage_count = static_cast<int>(t.at("S").as_int());
+    for (const Value& p : t.at("phi").items()) tl.phi.push_back(static_cast<int>(p.as_int()));
+    tl.blocks.resize(static_cast<size_t>(2) * tl.micro_batches * tl.stage_count);
+    for (const Value& b : t.at("blocks").items()) {
+      const int x = static_cast<int>(b[0].as_int()), i = static_cast<int>(b[1].as_int());
+      const bool fwd = b[2].as_int() == 0;
+      if (x < 0 || x >= tl.stage_count || i < 0 || i >= tl.micro_batches)
+        throw std::invalid_argument("timeline_export: block out of range");
+      Block& blk = fwd ? tl.forward(i, x) : tl.backward(i, x);
+      blk.stage = x;
+      blk.micro_batch = i;
+      blk.kind = fwd ? BlockKind::forward : BlockKind::backward;
+      blk.start = b[3].as_double();
+      blk.end = b[4].as_double();
+    }
+    std::ostringstream csv;
+    write_timeline_csv(csv, tl);
+    out["csv"] = csv.str();
+    Value peaks = Value::array();
+    for (int p : peak_activations(tl)) peaks.push_back(p);
+    out["peak_activations"] = std::move(peaks);
+    if (req.contains("plan")) {
+      const StageCostSequence seq = build_stage_sequence(plan_of(req.at("plan")), profile_of(req.at("profile")),
+                                                         cluster_of(req.at("cluster")));
+      std::ostringstream svg;
+      write_timeline_svg(svg, tl, seq);
+      out["svg"] = svg.str();
+      out["latency"] = batch_latency(tl, seq);
+    }
+    return out;
+  }
   if (op == "timeline_svg") {
     const ModelProfile prof = profile_of(req.at("profile"));
     const ClusterSpec cl = cluster_of(req.at("cluster"));

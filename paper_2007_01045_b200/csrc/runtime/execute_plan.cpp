@@ -40,7 +40,9 @@ PlanExecution execute_plan(const PipelinePlan& plan, const ModelProfile& profile
                            int micro_batches, const ExecOptions& opts) {
   PlanExecution out;
   out.seq = build_stage_sequence(plan, profile, cluster);  // validates the plan (model.cpp:100-131)
-  const std::vector<int> phi = resolve_phi(plan, out.seq, micro_batches);
+  const std::vector<int> phi = opts.schedule == ScheduleKind::gpipe
+                                   ? std::vector<int>(out.seq.size(), micro_batches)  // simulator.cpp:164-166
+                                   : resolve_phi(plan, out.seq, micro_batches);
 
   Value cfg = Value::object();
   cfg["model"] = Value::parse(opts.model_json);
@@ -52,6 +54,8 @@ PlanExecution execute_plan(const PipelinePlan& plan, const ModelProfile& profile
   cfg["rank"] = opts.rank;
   cfg["world"] = opts.world;
   cfg["apply"] = opts.apply;
+  cfg["schedule"] = opts.schedule == ScheduleKind::gpipe ? "gpipe" : "dapple";
+  cfg["recompute"] = opts.recompute;
   dpl_exec* ex = nullptr;
   ok(dpl_exec_create(cfg.dump().c_str(), opts.device, &ex));
   try {

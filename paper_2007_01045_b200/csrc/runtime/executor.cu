@@ -193,6 +193,9 @@ class Executor {
   long long numel_global_ = 0;
   bool timeline_ = true;
   bool apply_ = true;  // false: keep the accumulated gradients (parity reads)
+  bool gpipe_ = false;      // all-forward-first chain (simulator.cpp:161-167)
+  bool recompute_ = false;  // re-run the stage forward inside each backward (simulator.cpp:216-221)
+  int stash_slots_ = 1;     // layer-internal activation sets kept alive
 
   // --- device state
   DeviceMemory mem_;
@@ -209,6 +212,7 @@ class Executor {
   std::vector<bf16*> target_, dloss_;    // last stage, per slot
   std::vector<bf16*> send_grad_;         // first-layer dX per micro-batch (stage > 0)
   bf16* gbuf_[2] = {nullptr, nullptr};
+  bf16* rc_out_ = nullptr;  // output of the re-computed forward (discarded)
   float* loss_acc_ = nullptr;
   unsigned long long* t0_ = nullptr;
   // receive region (one cudaMalloc, exported over CUDA IPC):
@@ -289,6 +293,8 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
   if (cfg.contains("timeline")) timeline_ = cfg.at("timeline").as_bool();
   if (cfg.contains("apply")) apply_ = cfg.at("apply").as_bool();
   if (cfg.contains("graph")) use_graph_ = cfg.at("graph").as_bool();
+  if (cfg.contains("schedule")) gpipe_ = cfg.at("schedule").as_string() == "gpipe";
+  if (cfg.contains("recompute")) recompute_ = cfg.at("recompute").as_bool();
   if (M_ < 1 || gbs_ % M_ != 0) throw std::invalid_argument("dpl exec: GBS must be a multiple of M");
   B_ = gbs_ / M_;
 
@@ -330,8 +336,11 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
     phi_expanded_.resize(Se);
     for (int x = 0; x < Se; ++x) phi_expanded_[x] = std::min(Se - x, M_);
   }
-  phi_ = std::min(phi_expanded_[2 * k_], M_);
-  chain_ = pipeplan::stage_chain(M_, phi_, pipeplan::ScheduleKind::dapple);
+  phi_ = gpipe_ ? M_ : std::min(phi_expanded_[2 * k_], M_);
+  chain_ = pipeplan::stage_chain(M_, phi_, gpipe_ ? pipeplan::ScheduleKind::gpipe : pipeplan::ScheduleKind::dapple);
+  // live micro-batches per stage = phi (DAPPLE) or M (GPipe); with
+  // re-computation only the stage inputs stay alive and one stash set is reused
+  stash_slots_ = recompute_ ? 1 : phi_;
 
   if (k_ > 0) {
     for (const Route& r : pipeplan::splitconcat_routes(plan_.stages[k_ - 1], mine, B_, spec_.seq))
@@ -347,7 +356,7 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
   ctx_.spec = spec_;
   ctx_.samples = B_ / r_;
   ctx_.rows = ctx_.samples * spec_.seq;
-  ctx_.slots = phi_;
+  ctx_.slots = stash_slots_;
   ctx_.mem = &mem_;
   DPL_CUDA(cudaStreamCreateWithFlags(&compute_, cudaStreamNonBlocking));
   mem_.set_stream(compute_);
@@ -382,7 +391,8 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
   for (auto& layer : layers_) layer->alloc_stash(ctx_);
   act_.assign(L(), {});
   for (int li = 1; li < L(); ++li)
-    for (int s = 0; s < phi_; ++s) act_[li].push_back(static_cast<bf16*>(mem_.alloc(RH * 2)));
+    for (int s = 0; s < stash_slots_; ++s) act_[li].push_back(static_cast<bf16*>(mem_.alloc(RH * 2)));
+  if (recompute_) rc_out_ = static_cast<bf16*>(mem_.alloc(RH * 2));
   if (k_ == 0)
     for (int s = 0; s < phi_; ++s) in_.push_back(static_cast<bf16*>(mem_.alloc(RH * 2)));
   for (int i = 0; i < M_; ++i) out_.push_back(static_cast<bf16*>(mem_.alloc(RH * 2)));
@@ -437,7 +447,7 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
 
   for (size_t li = 0; li < layers_.size(); ++li) {
     const bool need_dx = !(k_ == 0 && li == 0);
-    flops_per_step_ += M_ * (layers_[li]->flops_fwd(ctx_) + layers_[li]->flops_bwd(ctx_, need_dx));
+    flops_per_step_ += M_ * ((recompute_ ? 2 : 1) * layers_[li]->flops_fwd(ctx_) + layers_[li]->flops_bwd(ctx_, need_dx));
   }
   DPL_CUDA(cudaMallocHost(reinterpret_cast<void**>(&loss_host_), sizeof(float)));
   // parameters initialised and every buffer (incl. the IPC-exported flags)
@@ -573,7 +583,8 @@ void Executor::signal(cudaStream_t s, uint32_t* remote_flag, uint32_t value) {
 }
 
 void Executor::forward(int i, uint32_t base) {
-  const int slot = i % phi_;
+  const int slot = i % phi_;                         // stage input / target / loss-grad buffers
+  const int ss = recompute_ ? 0 : i % stash_slots_;  // layer-internal stash
   const size_t H = spec_.hidden;
   const bf16* x;
   if (k_ == 0) {
@@ -584,8 +595,8 @@ void Executor::forward(int i, uint32_t base) {
   }
   record(fwd_ev_[i].start, compute_);
   for (int li = 0; li < L(); ++li) {
-    bf16* y = li + 1 < L() ? act_[li + 1][slot] : out_[i];
-    layers_[li]->forward(ctx_, slot, x, y);
+    bf16* y = li + 1 < L() ? act_[li + 1][ss] : out_[i];
+    layers_[li]->forward(ctx_, ss, x, y);
     x = y;
   }
   if (k_ == S_ - 1) {
@@ -612,6 +623,7 @@ void Executor::forward(int i, uint32_t base) {
 
 void Executor::backward(int i, uint32_t base) {
   const int slot = i % phi_;
+  const int ss = recompute_ ? 0 : i % stash_slots_;
   const size_t H = spec_.hidden;
   const bf16* dy;
   if (k_ == S_ - 1) {
@@ -621,10 +633,19 @@ void Executor::backward(int i, uint32_t base) {
     dy = recv_grad(i);
   }
   record(bwd_ev_[i].start, compute_);
+  if (recompute_) {
+    // the backward block first re-runs the stage forward (B' = B + F)
+    const bf16* x = k_ == 0 ? in_[slot] : recv_act(i);
+    for (int li = 0; li < L(); ++li) {
+      bf16* y = li + 1 < L() ? act_[li + 1][ss] : rc_out_;
+      layers_[li]->forward(ctx_, ss, x, y);
+      x = y;
+    }
+  }
   const bool last_mb = i == M_ - 1;
   int pp = 0;
   for (int li = L() - 1; li >= 0; --li) {
-    const bf16* x = li > 0 ? act_[li][slot] : (k_ == 0 ? in_[slot] : recv_act(i));
+    const bf16* x = li > 0 ? act_[li][ss] : (k_ == 0 ? in_[slot] : recv_act(i));
     bf16* dx = nullptr;
     if (li > 0) {
       dx = gbuf_[pp];
@@ -632,7 +653,7 @@ void Executor::backward(int i, uint32_t base) {
     } else if (k_ > 0) {
       dx = send_grad_[i];
     }
-    layers_[li]->backward(ctx_, slot, x, dy, dx);
+    layers_[li]->backward(ctx_, ss, x, dy, dx);
     dy = dx;
     if (last_mb) {
       // this layer's gradients are final: AllReduce over the replica group
@@ -924,6 +945,9 @@ std::string Executor::info() const {
   v["layers"] = std::vector<int>{lo_, hi_};
   v["phi"] = phi_;
   v["phi_expanded"] = phi_expanded_;
+  v["schedule"] = gpipe_ ? "gpipe" : "dapple";
+  v["recompute"] = recompute_;
+  v["stash_slots"] = stash_slots_;
   v["rows"] = ctx_.rows;
   v["micro_batch_samples"] = B_;
   v["params"] = static_cast<long long>(n_params_);

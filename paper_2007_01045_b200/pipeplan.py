@@ -90,3 +90,19 @@ def splitconcat_time(size, src, dst, cluster):
 def enumerate_placements(cluster, count, free=None):
     kw = {} if free is None else {"free": free}
     return call("enumerate_placements", cluster=cluster, count=count, **kw)["placements"]
+
+
+def timeline_export(timeline, micro_batches, stage_count, phi, plan_json=None, profile=None, cluster=None):
+    """A measured timeline (runtime.merge_timelines) through the reference's
+    writers: {"csv": write_timeline_csv (io.cpp), "peak_activations"
+    (simulator.cpp), and with plan/profile/cluster also "svg"
+    (write_timeline_svg) and "latency" (batch_latency)}.  Times are shifted
+    so the first forward starts at 0, as in a simulated timeline."""
+    import math
+    blocks = [b for b in timeline["blocks"] if not math.isnan(b[3])]
+    t0 = min(b[3] for b in blocks) if blocks else 0.0
+    req = {"timeline": {"M": micro_batches, "S": stage_count, "phi": list(phi),
+                        "blocks": [[x, i, k, s - t0, e - t0] for x, i, k, s, e in blocks]}}
+    if plan_json is not None:
+        req.update(plan=plan_json, profile=profile, cluster=cluster)
+    return call("timeline_export", **req)

@@ -20,13 +20,14 @@ BLOB_BYTES = 64  # cudaIpcMemHandle_t
 class Executor:
     def __init__(self, model: dict, plan, micro_batches: int, gbs: int, *, lr: float = 1e-3, seed: int = 1234,
                  rank: int = 0, world: int = 1, device: Optional[int] = None, apply: bool = True,
-                 timeline: bool = True):
+                 timeline: bool = True, schedule: str = "dapple", recompute: bool = False):
         self.plan = json.loads(plan) if isinstance(plan, str) else plan
         self.model, self.M, self.gbs = model, micro_batches, gbs
         self.rank, self.world = rank, world
         self.device = rank if device is None else device
         cfg = {"model": model, "plan": self.plan, "M": micro_batches, "gbs": gbs, "lr": lr, "seed": seed,
                "rank": rank, "world": world, "apply": apply, "timeline": timeline,
+               "schedule": schedule, "recompute": recompute,
                "graph": os.environ.get("DPL_GRAPH", "1") != "0"}
         h = ctypes.c_void_p()
         check(lib().dpl_exec_create(json.dumps(cfg).encode(), self.device, ctypes.byref(h)))

@@ -23,14 +23,21 @@ def main():
     torch.cuda.set_device(rank)
     dist.init_process_group("gloo")
     model, plan, M, gbs = spec["model"], spec["plan"], spec["M"], spec["gbs"]
+    sched = {"schedule": spec.get("schedule", "dapple"), "recompute": spec.get("recompute", False)}
     exact = full_batch_step(model, gbs)
     emu = full_batch_step(model, gbs, bf16=True)
     stage = next(s for s in plan["stages"] if rank in s["gpus"])
     layers = range(*stage["layers"])
     results = {}
     for apply in (False, True):
-        ex = Executor(model, plan, M, gbs, lr=1e-3, rank=rank, world=world, apply=apply)
+        ex = Executor(model, plan, M, gbs, lr=1e-3, rank=rank, world=world, apply=apply, **sched)
         loss = ex.step()
+        if sched["schedule"] == "gpipe":
+            # measured block order: every forward of this stage before its first backward
+            blocks = [b for b in ex.timeline()["blocks"] if b[0] % 2 == 0 and b[3] >= 0]
+            last_f = max(b[4] for b in blocks if b[2] == 0)
+            first_b = min(b[3] for b in blocks if b[2] == 1)
+            assert last_f <= first_b, (last_f, first_b)
         if stage is plan["stages"][-1]:
             check_loss(loss, emu, exact)
         if apply:
@@ -45,7 +52,7 @@ def main():
                               "latency_ms": tl["latency"] * 1e3, "bubble": tl["bubble"]}), flush=True)
         ex.close()
     # more steps must keep working (flag sequence numbers advance)
-    ex = Executor(model, plan, M, gbs, lr=1e-3, rank=rank, world=world)
+    ex = Executor(model, plan, M, gbs, lr=1e-3, rank=rank, world=world, **sched)
     ex.step()
     ex.step()
     ex.close()

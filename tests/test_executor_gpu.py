@@ -46,3 +46,20 @@ def test_two_steps_loss_decreases(cuda):
     tl = ex.timeline()
     assert len(tl["blocks"]) == 2 * 4 and tl["step_s"] > 0
     ex.close()
+
+
+@pytest.mark.parametrize("schedule,recompute", [("gpipe", False), ("dapple", True), ("gpipe", True)])
+def test_single_gpu_schedules_match_oracle(cuda, schedule, recompute):
+    """GPipe block order and re-computation leave the step's numerics unchanged."""
+    from paper_2007_01045_b200.runtime import Executor
+    model = dict(kind="bert", layers=2, hidden=256, heads=4, ffn=1024, seq=128)
+    plan = {"stages": [{"layers": [0, 2], "gpus": [0], "replication": 1}]}
+    exact = full_batch_step(model, 8)
+    emu = full_batch_step(model, 8, bf16=True)
+    ex = Executor(model, plan, 4, 8, lr=1e-3, apply=False, schedule=schedule, recompute=recompute)
+    info = ex.info
+    assert info["schedule"] == schedule and info["recompute"] == recompute
+    assert info["stash_slots"] == (1 if recompute else 4 if schedule == "gpipe" else info["phi"])
+    check_loss(ex.step(), emu, exact)
+    check_grads(ex, emu, exact, range(2), "bert", 2)
+    ex.close()

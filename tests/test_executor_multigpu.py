@@ -24,6 +24,15 @@ CASES = [
     (4, BERT, {"stages": [{"layers": [0, 1], "gpus": [0]}, {"layers": [1, 2], "gpus": [1]},
                           {"layers": [2, 3], "gpus": [2]}, {"layers": [3, 4], "gpus": [3]}]}, 8, 8),
 ]
+TWO = {"stages": [{"layers": [0, 2], "gpus": [0]}, {"layers": [2, 4], "gpus": [1]}]}
+# GPipe / re-computation on the device (the schedules of the paper's Table VI)
+SCHED_CASES = [
+    (2, BERT, TWO, 4, 8, "gpipe", False),
+    (2, MLP, TWO, 4, 24, "dapple", True),
+    (2, BERT, TWO, 4, 8, "gpipe", True),
+    (4, BERT, {"stages": [{"layers": [0, 2], "gpus": [0, 1]}, {"layers": [2, 4], "gpus": [2, 3]}]}, 4, 16,
+     "dapple", True),
+]
 
 
 def _gpus():
@@ -41,6 +50,19 @@ def test_multi_gpu_step_matches_oracle(n, model, plan, M, gbs):
     spec = json.dumps({"model": model, "plan": plan, "M": M, "gbs": gbs})
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", "--master-port=29517", os.path.join(HERE, "mgpu_worker.py"), spec]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    print(r.stdout[-4000:])
+    assert r.returncode == 0, r.stderr[-4000:]
+
+
+@pytest.mark.parametrize("n,model,plan,M,gbs,schedule,recompute", SCHED_CASES)
+def test_multi_gpu_schedules_match_oracle(n, model, plan, M, gbs, schedule, recompute):
+    if _gpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    spec = json.dumps({"model": model, "plan": plan, "M": M, "gbs": gbs, "schedule": schedule,
+                       "recompute": recompute})
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", "--master-port=29518", os.path.join(HERE, "mgpu_worker.py"), spec]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     print(r.stdout[-4000:])
     assert r.returncode == 0, r.stderr[-4000:]

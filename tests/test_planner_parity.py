@@ -143,3 +143,22 @@ def test_splitconcat_routes_partition_the_rows(b_mb, ra, rb):
         assert start == pos
         pos += rows
     assert pos == b_mb * 512
+
+
+def test_timeline_export_reproduces_reference_writers():
+    """The exporter used for MEASURED timelines (bench --timeline-out) goes
+    through the same write_timeline_csv / peak_activations / batch_latency as
+    the reference: fed each golden simulate_plan timeline it must return the
+    reference's own CSV, peaks and latency byte for byte."""
+    cases = [g for g in GOLDEN if g["request"]["op"] == "simulate_plan"]
+    assert cases
+    for g in cases:
+        req, want = g["request"], g["response"]
+        tl = want["timeline"]
+        got = pipeplan.call("timeline_export", timeline=tl, plan=req["plan"], profile=req["profile"],
+                            cluster=req["cluster"])
+        assert got["csv"] == want["csv"]
+        assert got["peak_activations"] == want["peaks"]
+        if not req.get("recompute"):
+            assert got["latency"] == want["latency"]
+        assert got["svg"].startswith("<svg")
