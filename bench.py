@@ -143,44 +143,87 @@ def gather(obj, world):
     return out
 
 
+def broadcast(obj, world):
+    if world == 1:
+        return obj
+    import torch.distributed as dist
+    box = [obj]
+    dist.broadcast_object_list(box, src=0)
+    return box[0]
+
+
 def barrier(world):
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
 
 
-def host_batches(model: dict, plan: dict, rank: int, m: int, slice_samples: int, seed: int):
+def host_batches(model: dict, plan: dict, rank: int, m: int, B: int, seed: int):
     """Pinned host copies of this rank's input / target slices of every
-    micro-batch (the e2e leg's H2D sources), same values the device
-    generator would produce."""
-    import numpy as np
+    micro-batch (the e2e leg's H2D sources): generated once by the library's
+    own device generator (dpl_k_fill_uniform_bf16, the same keyed hash the
+    executor uses), then copied to pinned host memory before timing."""
     import torch
-    from oracle.executor_ref import Model, batch_data  # data generator shared with the device
-    mm = Model.from_dict(model)
+    from paper_2007_01045_b200 import kernels
     stages = plan["stages"]
     k = next(i for i, s in enumerate(stages) if rank in s["gpus"])
     rep = stages[k]["gpus"].index(rank)
     r = len(stages[k]["gpus"])
-    B = slice_samples * r
-    ins, tgts = [], []
-    for i in range(m):
-        x, t = batch_data(mm, seed, i * B + rep * slice_samples, slice_samples)
-        ins.append(x)
-        tgts.append(t)
-    def pinned(arrs):
-        a = torch.from_numpy(np.stack(arrs)).to(torch.bfloat16)
-        return a.pin_memory()
-    inp = pinned(ins) if k == 0 else None
-    tgt = pinned(tgts) if k == len(stages) - 1 else None
+    s0, s1 = B * rep // r, B * (rep + 1) // r  # this replica's samples of each micro-batch
+    seq, h = model.get("seq", 1), model["hidden"]
+    rows = (s1 - s0) * seq
+
+    def gen(tensor_id):
+        out = torch.empty((m, rows, h), dtype=torch.bfloat16, device="cuda")
+        for i in range(m):
+            kernels.fill_uniform_bf16(out[i], rows * h, seed, tensor_id, (i * B + s0) * seq * h)
+        torch.cuda.synchronize()
+        return out.cpu().pin_memory()
+
+    inp = gen(1) if k == 0 else None            # tensor ids of layers.h kTensorInput / kTensorTarget
+    tgt = gen(2) if k == len(stages) - 1 else None
     return inp, tgt
 
 
-def predicted_latency(model, plan, timelines, m, n, schedule="dapple"):
-    """Builds a B200 layer profile from the measured blocks (per-layer F/B of
-    the full micro-batch = block time x r / layers on the stage) and asks the
-    host planner for est_latency (estimator.cpp:56-86) and sim_latency
-    (simulate_plan, planner.cpp:491-514) of the executed plan."""
-    from paper_2007_01045_b200 import pipeplan
+def b200_cluster(n: int, mem_gb: float = 180.0) -> dict:
+    # NVLink 5 through NVSwitch: measured 770 GB/s peer copy (B200_PROFILING.md)
+    return {"seps": [n], "intra_bw_gbps": 770.0, "inter_bw_gbps": 50.0, "intra_latency_us": 5.0,
+            "inter_latency_us": 10.0, "per_gpu_memory_gb": mem_gb}
+
+
+def profile_model(model: dict, mb: int, reps: int = 5) -> dict:
+    """The B200 layer profile (reference profile JSON, model.cpp:162-173):
+    every layer's F/B timed on this GPU at the micro-batch size, in step order
+    (Executor.layer_profile)."""
+    from paper_2007_01045_b200.runtime import Executor
+    L = model["layers"]
+    ex = Executor(model, {"stages": [{"layers": [0, L], "gpus": [0], "replication": 1}]}, 1, mb,
+                  rank=0, world=1, timeline=False, apply=False)
+    try:
+        return ex.layer_profile(reps)
+    finally:
+        ex.close()
+
+
+def slice_profile(profiles: dict, plan: dict, mb: int) -> dict:
+    """The executed plan's profile at the sizes its replicas actually run:
+    stage k's layers take the layer times profiled at the largest replica
+    slice ceil(mb / r_k), scaled by r_k so aggregate_stage's division by r
+    (model.cpp:228-229) returns the slice time."""
+    base = profiles[mb]
+    layers = [dict(l) for l in base["layers"]]
+    for st in plan["stages"]:
+        r = len(st["gpus"])
+        sl = profiles[-(-mb // r)]
+        for l in range(*st["layers"]):
+            layers[l]["fwd_time_us"] = sl["layers"][l]["fwd_time_us"] * r
+            layers[l]["bwd_time_us"] = sl["layers"][l]["bwd_time_us"] * r
+    return {**base, "layers": layers}
+
+
+def calibrated_profile(model, plan, timelines) -> dict:
+    """Per-layer F/B of the full micro-batch from a run's measured blocks
+    (block time x r / layers on the stage)."""
     stages = plan["stages"]
     per_layer = {}
     for k, st in enumerate(stages):
@@ -198,27 +241,29 @@ def predicted_latency(model, plan, timelines, m, n, schedule="dapple"):
         for l in range(lo, hi):
             per_layer[l] = (f, b)
     h = model["hidden"]
-    act = 8 * len(stages[0]["gpus"]) * model.get("seq", 1) * h * 2  # one micro-batch's boundary activation
     params = (12 * h * h + 13 * h) * 4 if model["kind"] != "mlp" else (h * h + h) * 4
-    profile = {"profile_batch_size": 8, "layers": [
-        {"fwd_time_us": per_layer[l][0] * 1e6, "bwd_time_us": per_layer[l][1] * 1e6, "activation_bytes": act,
-         "param_bytes": params} for l in range(model["layers"])]}
-    # NVLink 5 through NVSwitch: measured 770 GB/s peer copy, AR bus bw 725 GB/s (B200_PROFILING.md)
-    cluster = {"seps": [n], "intra_bw_gbps": 770.0, "inter_bw_gbps": 50.0, "intra_latency_us": 5.0,
-               "inter_latency_us": 10.0, "per_gpu_memory_gb": 180.0}
+    return {"profile_batch_size": 8, "layers": [
+        {"fwd_time_us": per_layer[l][0] * 1e6, "bwd_time_us": per_layer[l][1] * 1e6,
+         "activation_bytes": 8 * model.get("seq", 1) * h * 2, "param_bytes": params} for l in range(model["layers"])]}
+
+
+def predicted_latency(plan, profile, cluster, m, n, schedule="dapple"):
+    """est_latency (estimator.cpp:56-86) and sim_latency (simulate_plan,
+    planner.cpp:491-514) of the executed plan under `profile`, plus the
+    simulated bubble."""
+    from paper_2007_01045_b200 import pipeplan
+    stages = plan["stages"]
     seq = pipeplan.build_stage_sequence(plan, profile, cluster)
     est = pipeplan.estimate_latency(seq, m)
-    # the measured B blocks already contain any re-computed forward, so the
+    # the measured B blocks already contain any re-computed forward, so a
     # calibrated profile is simulated without apply_recompute
     sim = pipeplan.simulate_plan(plan, profile, cluster, m, schedule=schedule)
-    blocks = sim["timeline"]["blocks"]
     busy = 0.0
-    for x, i, kind, s, e in blocks:
+    for x, i, kind, s, e in sim["timeline"]["blocks"]:
         if x % 2 == 0:
             busy += (e - s) * len(stages[x // 2]["gpus"])
-    sim_bubble = 1.0 - busy / (n * sim["latency"])
-    return {"est_ms": est["total"] * 1e3, "sim_ms": sim["latency"] * 1e3, "sim_bubble": sim_bubble,
-            "pivot": est["pivot"], "profile": profile, "cluster": cluster}
+    return {"est_ms": est["total"] * 1e3, "sim_ms": sim["latency"] * 1e3,
+            "sim_bubble": 1.0 - busy / (n * sim["latency"]), "pivot": est["pivot"]}
 
 
 def cpu_baseline(model: dict, budget_layers: int | None = None) -> dict:
@@ -281,6 +326,11 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-layers", type=int, default=8)
     ap.add_argument("--seed", type=int, default=1234)
+    ap.add_argument("--plan", default="forced", choices=["forced", "planner"],
+                    help="forced: [0,L)x1 / 2 stages x N/2; planner: the host planner's plan for the B200 profile")
+    ap.add_argument("--mem-gb", type=float, default=180.0, help="per_gpu_memory_gb given to the planner")
+    ap.add_argument("--global-batch", type=int, default=0, help="default: M x slice x (N/2 or 1)")
+    ap.add_argument("--no-profile", action="store_true", help="skip the pre-run B200 layer profile")
     ap.add_argument("--schedule", default="dapple", choices=["dapple", "gpipe"])
     ap.add_argument("--recompute", action="store_true")
     ap.add_argument("--timeline-out", default=None,
@@ -298,12 +348,31 @@ def main():
     from paper_2007_01045_b200 import _lib
     from paper_2007_01045_b200.runtime import Executor, merge_timelines
 
+    from paper_2007_01045_b200 import pipeplan
     model = MODELS[args.model]
-    plan = make_plan(world, model["layers"])
+    M = args.micro_batches
+    gbs = args.global_batch or M * args.slice * max(1, world // 2)
+    cluster = b200_cluster(world, args.mem_gb)
+    # pre-run B200 layer profile at the micro-batch size: the planner's input
+    # and the source of the predicted L (a real prediction, made before the run)
+    mb = gbs // M
+    profiles = {}  # samples -> B200 layer profile at that size
+    if not args.no_profile or args.plan == "planner":
+        profiles[mb] = profile_model(model, mb) if rank == 0 else None
+    if args.plan == "planner":
+        plan = pipeplan.plan(profiles[mb], cluster, M)["plan"] if rank == 0 else None
+        plan = broadcast(plan, world)
+    else:
+        plan = make_plan(world, model["layers"])
+    if profiles and rank == 0:
+        for st in plan["stages"]:
+            size = -(-mb // len(st["gpus"]))
+            if size not in profiles:
+                profiles[size] = profile_model(model, size)
+    profiles = broadcast(profiles, world)
+    profile = slice_profile(profiles, plan, mb) if profiles else None
     S = len(plan["stages"])
     r0 = len(plan["stages"][0]["gpus"])
-    M = args.micro_batches
-    gbs = M * args.slice * r0
     lib = _lib.lib()
 
     ex = Executor(model, plan, M, gbs, lr=1e-4, seed=args.seed, rank=rank, world=world, device=rank,
@@ -359,7 +428,7 @@ def main():
     # ------------------------------------------------------------ e2e (public API, host buffers)
     e2e = None
     if not args.no_e2e:
-        inp, tgt = host_batches(model, plan, rank, M, args.slice, args.seed)
+        inp, tgt = host_batches(model, plan, rank, M, gbs // M, args.seed)
         ex.step(inp, tgt)  # warm the H2D path
         barrier(world)
         t0 = time.perf_counter()
@@ -393,13 +462,23 @@ def main():
             traffic = json.load(f).get("bytes_per_launch")
     except Exception:
         pass
-    pred = predicted_latency(model, plan, [all_tls[r][-1] for r in range(world)], M, world, args.schedule)
-    from paper_2007_01045_b200 import pipeplan
+    calib = calibrated_profile(model, plan, [all_tls[r][-1] for r in range(world)])
+    pred_cal = predicted_latency(plan, calib, cluster, M, world, args.schedule)
+    pred = None
+    if profile is not None:
+        prof_run = profile
+        if args.recompute:
+            prof_run = {**profile, "layers": [{**l, "bwd_time_us": l["bwd_time_us"] + l["fwd_time_us"]}
+                                              for l in profile["layers"]]}  # apply_recompute, simulator.cpp:216-221
+        pred = predicted_latency(plan, prof_run, cluster, M, world, args.schedule)
     phi_tl = info["phi_expanded"] if args.schedule == "dapple" else [M] * (2 * S - 1)
     exported = pipeplan.timeline_export(merge_timelines([all_tls[r][-1] for r in range(world)], M, S), M,
-                                        2 * S - 1, phi_tl, plan, pred["profile"], pred["cluster"])
+                                        2 * S - 1, phi_tl, plan, calib, cluster)
     if args.timeline_out:
         os.makedirs(args.timeline_out, exist_ok=True)
+        for size, pr in profiles.items():  # the B200 profiles, in the reference's profile format
+            with open(os.path.join(args.timeline_out, f"profile_{args.model}_mb{size}.json"), "w") as f:
+                f.write(pipeplan.call("load_profile", profile=json.dumps(pr))["json"])
         tag = f"{args.model}_n{world}_{args.schedule}{'_rc' if args.recompute else ''}"
         with open(os.path.join(args.timeline_out, f"timeline_{tag}.csv"), "w") as f:
             f.write(exported["csv"])
@@ -413,7 +492,9 @@ def main():
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded splitmix64 inputs/targets, random-init "
                                                       "weights)",
         "config": {"workload": args.model, **model, "global_batch": gbs, "micro_batches": M,
-                   "slice_samples": args.slice, "plan": [[s["layers"], s["gpus"]] for s in plan["stages"]],
+                   "plan_source": "host planner (pipeplan.plan on the B200 profile, per_gpu_memory_gb="
+                                  f"{args.mem_gb:g})" if args.plan == "planner" else "forced",
+                   "plan": [[s["layers"], s["gpus"]] for s in plan["stages"]],
                    "phi": info["phi_expanded"], "parallelism": f"{S} stages x {r0} replicas",
                    "l2": "working set (GBs of activations) far larger than the 126 MB L2"},
         "bubble": statistics.mean(bub),
@@ -421,10 +502,13 @@ def main():
         "schedule": {"kind": args.schedule, "recompute": args.recompute, "stash_slots": info["stash_slots"],
                      "peak_activations_measured": exported["peak_activations"],
                      "device_bytes": info.get("device_bytes")},
-        "latency": {"measured_ms": measured_ms, "est_ms": pred["est_ms"], "sim_ms": pred["sim_ms"],
-                    "sim_bubble": pred["sim_bubble"], "pivot": pred["pivot"],
-                    "measured_over_sim": measured_ms / pred["sim_ms"],
-                    "profile": "per-layer F/B calibrated from this run's measured blocks"},
+        "latency": {"measured_ms": measured_ms,
+                    "predicted": None if pred is None else {
+                        **pred, "measured_over_sim": measured_ms / pred["sim_ms"],
+                        "profile": "B200 layer profiles taken before the run (Executor.layer_profile) at "
+                                   f"the replica slice sizes {sorted(profiles)}, planner cost model"},
+                    "calibrated": {**pred_cal, "measured_over_sim": measured_ms / pred_cal["sim_ms"],
+                                   "profile": "per-layer F/B from this run's measured blocks"}},
         "tflops_per_gpu": fps * value / world / 1e12,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,

@@ -149,6 +149,12 @@ int dpl_exec_clock_calibrate(dpl_exec* ex, int phase, long long* offset_ns);
  * steps) and its summary as JSON {launches, seconds, flops, shapes[]}. */
 int dpl_exec_gemm_profile(dpl_exec* ex, int enable);
 const char* dpl_exec_gemm_profile_json(dpl_exec* ex);
+/* B200 layer profiler: times this rank's layers (F in order, then B in
+ * reverse, one event between layers, median of `reps` chains) at this
+ * replica's micro-batch slice and returns the reference's profile JSON
+ * (profile_to_json, reference model.cpp:162-173; ingested by load_profile,
+ * model.cpp:128-153).  NULL on error (dpl_last_error). */
+const char* dpl_exec_layer_profile(dpl_exec* ex, int reps);
 /* Multi-rank teardown: disconnect on every rank (unmaps peers' IPC regions,
  * destroys the NCCL communicator), barrier, then destroy. */
 int dpl_exec_disconnect(dpl_exec* ex);

@@ -280,8 +280,9 @@ def full_batch_step(model, gbs: int, seed: int = 1234, lr: float = 1e-3, dtype=n
 
 def scheduled_step(model, plan: dict, micro_batches: int, gbs: int, seed: int = 1234, lr: float = 1e-3,
                    dtype=np.float64) -> StepResult:
-    """The DAPPLE step as the plan executes it: every stage replica owns an
-    even row slice of each micro-batch, activations and gradients cross stage
+    """The DAPPLE step as the plan executes it: replica j of a stage with r
+    replicas owns samples [B*j/r, B*(j+1)/r) of each micro-batch (an even
+    split when r divides B), activations and gradients cross stage
     boundaries by interval overlap (Split-Concat), each replica accumulates
     its gradients over the micro-batches in chain order B_0..B_{M-1}, and the
     replica group sums them (AllReduce) before the update."""
@@ -298,19 +299,19 @@ def scheduled_step(model, plan: dict, micro_batches: int, gbs: int, seed: int = 
         for k, st in enumerate(stages):
             r = len(st["gpus"])
             lo, hi = st["layers"]
-            b = B // r
+            cut = [B * j // r for j in range(r + 1)]  # sample boundaries of the replica slices
             if k == 0:
-                xs = [batch_data(model, seed, i * B + j * b, b)[0].astype(dtype) for j in range(r)]
+                xs = [batch_data(model, seed, i * B + cut[j], cut[j + 1] - cut[j])[0].astype(dtype)
+                      for j in range(r)]
             else:
                 whole = np.concatenate(xs, axis=0)  # split-concat: rows are batch-major
-                rows = b * model.seq
-                xs = [whole[j * rows:(j + 1) * rows] for j in range(r)]
+                xs = [whole[cut[j] * model.seq:cut[j + 1] * model.seq] for j in range(r)]
             stage_caches = []
             for j in range(r):
                 x = xs[j]
                 cs = []
                 for l in range(lo, hi):
-                    x, c = layer_forward(model, l, params[l], x, b)
+                    x, c = layer_forward(model, l, params[l], x, cut[j + 1] - cut[j])
                     cs.append(c)
                 xs[j] = x
                 stage_caches.append(cs)
@@ -318,10 +319,10 @@ def scheduled_step(model, plan: dict, micro_batches: int, gbs: int, seed: int = 
         # loss on the last stage
         last = stages[-1]
         r = len(last["gpus"])
-        b = B // r
+        cut = [B * j // r for j in range(r + 1)]
         dys = []
         for j in range(r):
-            t = batch_data(model, seed, i * B + j * b, b)[1].astype(dtype)
+            t = batch_data(model, seed, i * B + cut[j], cut[j + 1] - cut[j])[1].astype(dtype)
             diff = xs[j] - t
             loss += float((diff * diff).sum())
             dys.append(2.0 * diff / numel)
@@ -329,15 +330,15 @@ def scheduled_step(model, plan: dict, micro_batches: int, gbs: int, seed: int = 
             st = stages[k]
             r = len(st["gpus"])
             lo, hi = st["layers"]
-            b = B // r
+            cut = [B * j // r for j in range(r + 1)]
             if k != len(stages) - 1:
                 whole = np.concatenate(dys, axis=0)
-                rows = b * model.seq
-                dys = [whole[j * rows:(j + 1) * rows] for j in range(r)]
+                dys = [whole[cut[j] * model.seq:cut[j + 1] * model.seq] for j in range(r)]
             for j in range(r):
                 dy = dys[j]
                 for li, l in reversed(list(enumerate(range(lo, hi)))):
-                    dy, g = layer_backward(model, l, params[l], caches[k][j][li], dy, b, need_dx=(l > 0))
+                    dy, g = layer_backward(model, l, params[l], caches[k][j][li], dy, cut[j + 1] - cut[j],
+                                           need_dx=(l > 0))
                     for name, v in g.items():
                         key = (k, j, l, name)
                         acc[key] = acc[key] + v if key in acc else v

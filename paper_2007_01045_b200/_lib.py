@@ -68,9 +68,23 @@ _PROTOS = {
     "dpl_exec_clock_calibrate": (_I, [_VP, _I, ctypes.POINTER(_LL)]),
     "dpl_exec_gemm_profile": (_I, [_VP, _I]),
     "dpl_exec_gemm_profile_json": (ctypes.c_char_p, [_VP]),
+    "dpl_exec_layer_profile": (ctypes.c_char_p, [_VP, ctypes.c_int]),
     "dpl_exec_disconnect": (_I, [_VP]),
     "dpl_exec_destroy": (None, [_VP]),
 }
+
+
+def _preload_torch_nccl():
+    """libdapple needs libnccl.so.2; make it resolve to the copy torch bundles
+    (nvidia/nccl), so loading libdapple before `import torch` cannot pin the
+    older system NCCL that libtorch_cuda then fails to link against."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for root in (spec.submodule_search_locations or []) if spec else []:
+        path = os.path.join(root, "nccl", "lib", "libnccl.so.2")
+        if os.path.exists(path):
+            ctypes.CDLL(path, mode=ctypes.RTLD_GLOBAL)
+            return
 
 
 def lib():
@@ -80,6 +94,7 @@ def lib():
         return _lib
     if not os.path.exists(LIB_PATH):
         raise DappleError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    _preload_torch_nccl()
     handle = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
     for name, (res, args) in _PROTOS.items():
         fn = getattr(handle, name, None)

@@ -11,8 +11,8 @@ std::vector<SplitConcatRoute> splitconcat_routes(const Stage& from, const Stage&
                                                  int rows_per_sample) {
   const int ra = from.replication(), rb = to.replication();
   if (ra < 1 || rb < 1) throw std::invalid_argument("splitconcat_routes: empty device set");
-  if (micro_batch_samples % ra != 0 || micro_batch_samples % rb != 0)
-    throw std::invalid_argument("splitconcat_routes: micro-batch does not split evenly over the replicas");
+  if (micro_batch_samples < ra || micro_batch_samples < rb)
+    throw std::invalid_argument("splitconcat_routes: micro-batch has fewer samples than replicas");
   const std::int64_t B = micro_batch_samples;
   std::vector<SplitConcatRoute> out;
   for (int i = 0; i < ra; ++i) {

@@ -174,6 +174,7 @@ class Executor {
     }
   }
   std::string gemm_profile_json() const;
+  std::string layer_profile_json(int reps);
   std::string timeline_json() const;
   void read_tensor(const std::string& name, bool grad, void* host, size_t bytes);
   std::string info() const;
@@ -248,7 +249,8 @@ class Executor {
   double flops_per_step_ = 0.0;
 
   // --- helpers
-  int rows_of_stage(int k) const { return B_ / plan_.stages[k].replication() * spec_.seq; }
+  // first sample of replica j's slice in this rank's stage (or stage k)
+  int slice_lo(int j, int r = 0) const { return static_cast<int>(1LL * B_ * j / (r ? r : r_)); }
   int L() const { return hi_ - lo_; }
   bf16* recv_act(int i) const {
     return reinterpret_cast<bf16*>(recv_) + static_cast<size_t>(i) * ctx_.rows * spec_.hidden;
@@ -308,9 +310,12 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
     if (st.layer_lo != expect || st.layer_hi <= st.layer_lo)
       throw std::invalid_argument("dpl exec: plan stages must partition the layers");
     expect = st.layer_hi;
-    if (B_ % st.replication() != 0)
-      throw std::invalid_argument("dpl exec: micro-batch of " + std::to_string(B_) + " samples does not split evenly over " +
-                                  std::to_string(st.replication()) + " replicas (PAPER.md:1222-1231)");
+    // replica j owns samples [B*j/r, B*(j+1)/r) of every micro-batch
+    // (uneven when r does not divide B, as the planner's
+    // cost model allows, costmodel/model.cpp:228-229)
+    if (B_ < st.replication())
+      throw std::invalid_argument("dpl exec: micro-batch of " + std::to_string(B_) + " samples is smaller than " +
+                                  std::to_string(st.replication()) + " replicas");
     for (size_t j = 0; j < st.devices.size(); ++j) {
       if (st.devices[j] >= world_) throw std::invalid_argument("dpl exec: plan uses GPU ids beyond the world size");
       if (st.devices[j] == rank_) {
@@ -354,7 +359,7 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
 
   // --- context, layers, parameters
   ctx_.spec = spec_;
-  ctx_.samples = B_ / r_;
+  ctx_.samples = slice_lo(rep_ + 1) - slice_lo(rep_);
   ctx_.rows = ctx_.samples * spec_.seq;
   ctx_.slots = stash_slots_;
   ctx_.mem = &mem_;
@@ -417,7 +422,10 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
   peer_recv_.assign(world_, nullptr);
   peer_rows_.assign(world_, 0);
   for (int k = 0; k < S_; ++k)
-    for (int d : plan_.stages[k].devices) peer_rows_[d] = rows_of_stage(k);
+    for (int j = 0; j < plan_.stages[k].replication(); ++j) {
+      const int rk = plan_.stages[k].replication();
+      peer_rows_[plan_.stages[k].devices[j]] = (slice_lo(j + 1, rk) - slice_lo(j, rk)) * spec_.seq;
+    }
 
   // events
   auto mk = [](cudaEvent_t* e) { DPL_CUDA(cudaEventCreate(e)); };
@@ -700,7 +708,7 @@ void Executor::enqueue_step(const void* host_input, const void* host_target) {
   DPL_CUDA(cudaMemsetAsync(loss_acc_, 0, 4, compute_));
 
   // sample rows [row0, row0 + samples) of micro-batch i owned by this replica
-  const long long slice_first = 1LL * rep_ * (B_ / r_);
+  const long long slice_first = slice_lo(rep_);
   for (const pipeplan::ChainOp& op : chain_) {
     const int i = op.micro_batch;
     const int slot = i % phi_;
@@ -857,6 +865,82 @@ void Executor::read_tensor(const std::string& name, bool grad, void* host, size_
     return;
   }
   throw std::invalid_argument("dpl exec: unknown tensor " + name);
+}
+
+// B200 layer profiler (the reference only ingests
+// profiles, model.cpp:128-153).  Runs this stage's layers on the compute
+// stream in step order -- F of layer lo..hi-1 then B of hi-1..lo, loss
+// included in the last layer's F -- with a timing event between layers, so
+// each layer sees the L2 state it sees inside a step.  Median over `reps`
+// chains.  Output: profile_to_json (model.cpp:162-173) at
+// profile_batch_size = this replica's samples per micro-batch.
+std::string Executor::layer_profile_json(int reps) {
+  if (reps < 1) throw std::invalid_argument("layer_profile: reps must be >= 1");
+  if (recompute_) throw std::invalid_argument("layer_profile: executor built with recompute");
+  const size_t H = spec_.hidden;
+  const int n = L();
+  std::vector<cudaEvent_t> fe(n + 1), be(n + 1);
+  for (auto* v : {&fe, &be})
+    for (cudaEvent_t& e : *v) DPL_CUDA(cudaEventCreate(&e));
+  std::vector<std::vector<float>> ft(n), bt(n);
+  if (k_ == 0) fill_uniform_bf16(in_[0], static_cast<long long>(ctx_.rows) * H, seed_, kTensorInput, 0, 1.0f, compute_);
+  if (k_ == S_ - 1)
+    fill_uniform_bf16(target_[0], static_cast<long long>(ctx_.rows) * H, seed_, kTensorTarget, 0, 1.0f, compute_);
+  const bf16* x0 = k_ == 0 ? in_[0] : recv_act(0);
+  for (int rep = 0; rep < reps + 1; ++rep) {  // first chain is a warm-up
+    const bf16* x = x0;
+    DPL_CUDA(cudaEventRecord(fe[0], compute_));
+    for (int li = 0; li < n; ++li) {
+      bf16* y = li + 1 < n ? act_[li + 1][0] : out_[0];
+      layers_[li]->forward(ctx_, 0, x, y);
+      if (li == n - 1 && k_ == S_ - 1)
+        mse_loss(out_[0], target_[0], dloss_[0], loss_acc_, static_cast<long long>(ctx_.rows) * H,
+                 2.0f / static_cast<float>(numel_global_), compute_);
+      DPL_CUDA(cudaEventRecord(fe[li + 1], compute_));
+      x = y;
+    }
+    const bf16* dy = k_ == S_ - 1 ? dloss_[0] : recv_grad(0);
+    int pp = 0;
+    DPL_CUDA(cudaEventRecord(be[n], compute_));
+    for (int li = n - 1; li >= 0; --li) {
+      const bf16* xin = li > 0 ? act_[li][0] : x0;
+      bf16* dx = li > 0 ? gbuf_[pp] : (k_ > 0 ? send_grad_[0] : nullptr);
+      pp ^= 1;
+      layers_[li]->backward(ctx_, 0, xin, dy, dx);
+      DPL_CUDA(cudaEventRecord(be[li], compute_));
+      dy = dx;
+    }
+    DPL_CUDA(cudaStreamSynchronize(compute_));
+    if (rep == 0) continue;
+    for (int li = 0; li < n; ++li) {
+      float a = 0, b = 0;
+      DPL_CUDA(cudaEventElapsedTime(&a, fe[li], fe[li + 1]));
+      DPL_CUDA(cudaEventElapsedTime(&b, be[li + 1], be[li]));
+      ft[li].push_back(a);
+      bt[li].push_back(b);
+    }
+  }
+  for (auto* v : {&fe, &be})
+    for (cudaEvent_t e : *v) cudaEventDestroy(e);
+  // the profiled chains accumulated into the gradient buffers: clear them
+  DPL_CUDA(cudaMemsetAsync(g32_, 0, n_params_ * sizeof(float), compute_));
+  DPL_CUDA(cudaStreamSynchronize(compute_));
+  auto median = [](std::vector<float> v) {
+    std::sort(v.begin(), v.end());
+    return v[v.size() / 2];
+  };
+  pipeplan::ModelProfile prof;
+  prof.profile_batch_size = ctx_.samples;
+  for (int li = 0; li < n; ++li) {
+    pipeplan::LayerProfile l;
+    l.index = lo_ + li;
+    l.fwd_time = median(ft[li]) * 1e-3;
+    l.bwd_time = median(bt[li]) * 1e-3;
+    l.activation_bytes = static_cast<std::int64_t>(ctx_.rows) * static_cast<std::int64_t>(H) * 2;  // bf16 output
+    l.param_bytes = static_cast<std::int64_t>(layers_[li]->param_count()) * 4;                       // fp32 master
+    prof.layers.push_back(l);
+  }
+  return pipeplan::profile_to_json(prof);
 }
 
 std::string Executor::gemm_profile_json() const {
@@ -1060,6 +1144,16 @@ const char* dpl_exec_gemm_profile_json(dpl_exec* ex) {
     ex->reply = ex->impl->gemm_profile_json();
   } catch (const std::exception& e) {
     ex->reply = std::string("{\"error\":\"") + e.what() + "\"}";
+  }
+  return ex->reply.c_str();
+}
+
+const char* dpl_exec_layer_profile(dpl_exec* ex, int reps) {
+  try {
+    ex->reply = ex->impl->layer_profile_json(reps);
+  } catch (const std::exception& e) {
+    dpl::fail(e.what());
+    return nullptr;
   }
   return ex->reply.c_str();
 }

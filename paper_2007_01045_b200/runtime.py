@@ -104,6 +104,14 @@ class Executor:
     def gemm_profile(self, enable: bool):
         check(lib().dpl_exec_gemm_profile(self._h, int(enable)))
 
+    def layer_profile(self, reps: int = 5) -> dict:
+        """This stage's layers timed on the GPU at this replica's micro-batch
+        slice, as the reference's profile JSON (model.cpp:162-173)."""
+        out = lib().dpl_exec_layer_profile(self._h, reps)
+        if out is None:
+            raise RuntimeError(lib().dpl_last_error().decode())
+        return json.loads(out.decode())
+
     def gemm_profile_report(self) -> dict:
         return json.loads(lib().dpl_exec_gemm_profile_json(self._h).decode())
 

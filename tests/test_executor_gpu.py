@@ -1,5 +1,7 @@
 """Single-GPU executor parity: the full DAPPLE step (S=1 plan, M micro-batches
 accumulated on the device) vs the fp64 CPU oracle on the same seed."""
+import json
+
 import numpy as np
 import pytest
 
@@ -62,4 +64,30 @@ def test_single_gpu_schedules_match_oracle(cuda, schedule, recompute):
     assert info["stash_slots"] == (1 if recompute else 4 if schedule == "gpipe" else info["phi"])
     check_loss(ex.step(), emu, exact)
     check_grads(ex, emu, exact, range(2), "bert", 2)
+    ex.close()
+
+
+def test_layer_profiler_emits_reference_profile(cuda):
+    """Executor.layer_profile: per-layer F/B measured on the GPU, in the
+    reference's profile format (round-trips through load_profile)."""
+    from paper_2007_01045_b200 import pipeplan
+    from paper_2007_01045_b200.runtime import Executor
+    model = dict(kind="bert", layers=3, hidden=256, heads=4, ffn=1024, seq=128)
+    plan = {"stages": [{"layers": [0, 3], "gpus": [0], "replication": 1}]}
+    ex = Executor(model, plan, 2, 8, apply=False)
+    prof = ex.layer_profile(3)
+    assert prof["profile_batch_size"] == 4
+    assert len(prof["layers"]) == 3
+    h = 256
+    for l in prof["layers"]:
+        assert l["fwd_time_us"] > 0 and l["bwd_time_us"] > l["fwd_time_us"] * 0.5
+        assert l["activation_bytes"] == 4 * 128 * h * 2
+        assert l["param_bytes"] == (12 * h * h + 13 * h) * 4
+    loaded = pipeplan.call("load_profile", profile=json.dumps(prof))
+    assert len(loaded["layers"]) == 3 and loaded["profile_batch_size"] == 4
+    # the profiler leaves the gradient buffers clean: a step afterwards still matches the oracle
+    exact = full_batch_step(model, 8)
+    emu = full_batch_step(model, 8, bf16=True)
+    check_loss(ex.step(), emu, exact)
+    check_grads(ex, emu, exact, range(3), "bert", 3)
     ex.close()

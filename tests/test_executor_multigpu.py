@@ -24,6 +24,12 @@ CASES = [
     (4, BERT, {"stages": [{"layers": [0, 1], "gpus": [0]}, {"layers": [1, 2], "gpus": [1]},
                           {"layers": [2, 3], "gpus": [2]}, {"layers": [3, 4], "gpus": [3]}]}, 8, 8),
 ]
+# replicas that do not divide the micro-batch (planner plans such as [0,6)x1 [6,48)x7 at mb=8)
+CASES += [
+    (2, MLP, {"stages": [{"layers": [0, 4], "gpus": [0, 1]}]}, 4, 28),
+    (4, MLP, {"stages": [{"layers": [0, 3], "gpus": [0, 1, 2]}, {"layers": [3, 4], "gpus": [3]}]}, 4, 28),
+    (4, BERT, {"stages": [{"layers": [0, 1], "gpus": [0]}, {"layers": [1, 4], "gpus": [1, 2, 3]}]}, 2, 8),
+]
 TWO = {"stages": [{"layers": [0, 2], "gpus": [0]}, {"layers": [2, 4], "gpus": [1]}]}
 # GPipe / re-computation on the device (the schedules of the paper's Table VI)
 SCHED_CASES = [

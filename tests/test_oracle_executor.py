@@ -13,6 +13,9 @@ PLANS = [
     {"stages": [{"layers": [0, 1], "gpus": [0, 1]}, {"layers": [1, 4], "gpus": [2, 3]}]},
     {"stages": [{"layers": [0, 3], "gpus": [0, 1, 2]}, {"layers": [3, 4], "gpus": [3]}]},
     {"stages": [{"layers": [0, 1], "gpus": [0]}, {"layers": [1, 2], "gpus": [1, 2, 3]}, {"layers": [2, 4], "gpus": [4, 5]}]},
+    # replica counts that do not divide the 12-sample micro-batch (uneven slices)
+    {"stages": [{"layers": [0, 1], "gpus": [0]}, {"layers": [1, 4], "gpus": [1, 2, 3, 4, 5, 6, 7]}]},
+    {"stages": [{"layers": [0, 2], "gpus": [0, 1, 2, 3, 4]}, {"layers": [2, 4], "gpus": [5, 6]}]},
 ]
 
 

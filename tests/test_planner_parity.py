@@ -125,24 +125,32 @@ def test_stage_chain_matches_survey_order():
     assert [k for k, _ in pipeplan.stage_chain(4, 1, "gpipe")] == ["F"] * 4 + ["B"] * 4
 
 
-@pytest.mark.parametrize("b_mb,ra,rb", [(6, 3, 1), (6, 1, 3), (12, 4, 3), (8, 2, 4), (8, 4, 4)])
+@pytest.mark.parametrize("b_mb,ra,rb", [(6, 3, 1), (6, 1, 3), (12, 4, 3), (8, 2, 4), (8, 4, 4),
+                                        (8, 1, 7), (8, 7, 1), (7, 2, 3), (5, 5, 4), (9, 4, 6)])
 def test_splitconcat_routes_partition_the_rows(b_mb, ra, rb):
     plan = {"stages": [{"layers": [0, 1], "gpus": list(range(ra))},
                        {"layers": [1, 2], "gpus": list(range(ra, ra + rb))}]}
     routes = pipeplan.call("splitconcat_routes", plan=plan, boundary=0, micro_batch=b_mb, rows_per_sample=512)["routes"]
     assert len(routes) <= ra + rb - 1
-    covered = sorted((s * (b_mb // ra) * 512 + so, r) for s, d, so, do, r in routes)
+    # replica j owns samples [b*j/r, b*(j+1)/r) (uneven when r does not divide b)
+    covered = sorted((b_mb * s // ra * 512 + so, r) for s, d, so, do, r in routes)
     pos = 0
     for start, rows in covered:  # source rows are covered exactly once, in order
         assert start == pos
         pos += rows
     assert pos == b_mb * 512
-    dst = sorted(((d - ra) * (b_mb // rb) * 512 + do, r) for s, d, so, do, r in routes)
+    dst = sorted((b_mb * (d - ra) // rb * 512 + do, r) for s, d, so, do, r in routes)
     pos = 0
     for start, rows in dst:
         assert start == pos
         pos += rows
     assert pos == b_mb * 512
+
+
+def test_splitconcat_routes_reject_more_replicas_than_samples():
+    plan = {"stages": [{"layers": [0, 1], "gpus": [0, 1, 2]}, {"layers": [1, 2], "gpus": [3]}]}
+    with pytest.raises(ValueError):
+        pipeplan.call("splitconcat_routes", plan=plan, boundary=0, micro_batch=2, rows_per_sample=1)
 
 
 def test_timeline_export_reproduces_reference_writers():
