@@ -8,6 +8,9 @@ every micro-batch.  Plans:
   N = 1   [0,48) x1                         (the step: 8 micro-batches accumulated)
   N >= 2  [0,24) x N/2 | [24,48) x N/2      (BASELINE's 2-stage shape; 2 x 4 at N = 8)
 so the global batch is 64 samples per replica group (GBS = 64 * N / S).
+--model gpt2-1.5b (configs[3], C4): GPT-2 1.5B with token embedding and
+causal-LM cross-entropy head (vocab 50304), a straight N-stage pipeline,
+M = 32 micro-batches of 1 sample (GBS 32 at every N: strong scaling).
 
 Metric: training samples/s of the whole job (value: device-timed, inputs
 generated in HBM; e2e: through the public API with pinned host inputs /
@@ -34,7 +37,8 @@ sys.path.insert(0, ROOT)
 
 MODELS = {
     "bert48": dict(kind="bert", layers=48, hidden=1024, heads=16, ffn=4096, seq=512),
-    "gpt2-1.5b": dict(kind="gpt", layers=48, hidden=1600, heads=25, ffn=6400, seq=1024),
+    # C4: GPT-2 1.5B, causal-LM cross-entropy over the padded 50304-token vocabulary
+    "gpt2-1.5b": dict(kind="gpt", layers=48, hidden=1600, heads=25, ffn=6400, seq=1024, vocab=50304),
     "mlp16": dict(kind="mlp", layers=16, hidden=1024),
 }
 METRIC = "training samples/sec at 1/2/4/8 B200; pipeline bubble %; predicted-vs-measured L"
@@ -48,12 +52,23 @@ def flops_per_sample(m: dict) -> float:
         return 6.0 * m["hidden"] ** 2 * m["layers"]
     h, s, f = m["hidden"], m["seq"], m["ffn"]
     per_token = 2 * (4 * h * h + 2 * h * f) + 4 * s * h
-    return 3.0 * per_token * s * m["layers"]
+    head = 2.0 * h * m.get("vocab", 0)  # LM head projection (SURVEY: 160,822,400 FLOP/token at V=50257)
+    return 3.0 * (per_token * m["layers"] + head) * s
 
 
-def make_plan(n: int, layers: int) -> dict:
+# per-workload defaults (BASELINE.json configs): C2 BERT-48 2 stages x N/2,
+# M=8; C4 GPT-2 a straight N-stage pipeline, M=32 micro-batches of 1 sample
+DEFAULTS = {"bert48": dict(micro_batches=8, slice=8, straight=False),
+            "gpt2-1.5b": dict(micro_batches=32, slice=1, straight=True),
+            "mlp16": dict(micro_batches=8, slice=8, straight=False)}
+
+
+def make_plan(n: int, layers: int, straight: bool = False) -> dict:
     if n == 1:
         return {"stages": [{"layers": [0, layers], "gpus": [0], "replication": 1}]}
+    if straight:
+        cuts = [layers * k // n for k in range(n + 1)]
+        return {"stages": [{"layers": [cuts[k], cuts[k + 1]], "gpus": [k], "replication": 1} for k in range(n)]}
     half = n // 2
     cut = layers // 2
     return {"stages": [{"layers": [0, cut], "gpus": list(range(half)), "replication": half},
@@ -173,10 +188,17 @@ def host_batches(model: dict, plan: dict, rank: int, m: int, B: int, seed: int):
     seq, h = model.get("seq", 1), model["hidden"]
     rows = (s1 - s0) * seq
 
+    vocab = model.get("vocab", 0)
+
     def gen(tensor_id):
-        out = torch.empty((m, rows, h), dtype=torch.bfloat16, device="cuda")
-        for i in range(m):
-            kernels.fill_uniform_bf16(out[i], rows * h, seed, tensor_id, (i * B + s0) * seq * h)
+        if vocab:  # token ids [M][rows] int32
+            out = torch.empty((m, rows), dtype=torch.int32, device="cuda")
+            for i in range(m):
+                kernels.fill_tokens(out[i], rows, seed, tensor_id, (i * B + s0) * seq, vocab)
+        else:
+            out = torch.empty((m, rows, h), dtype=torch.bfloat16, device="cuda")
+            for i in range(m):
+                kernels.fill_uniform_bf16(out[i], rows * h, seed, tensor_id, (i * B + s0) * seq * h)
         torch.cuda.synchronize()
         return out.cpu().pin_memory()
 
@@ -320,8 +342,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="dapple", choices=["dapple", "reference"])
     ap.add_argument("--model", default="bert48", choices=sorted(MODELS))
-    ap.add_argument("--micro-batches", type=int, default=8)
-    ap.add_argument("--slice", type=int, default=8, help="samples per replica slice of a micro-batch")
+    ap.add_argument("--micro-batches", type=int, default=None, help="default per workload (DEFAULTS)")
+    ap.add_argument("--slice", type=int, default=None, help="samples per replica slice of a micro-batch")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-layers", type=int, default=8)
@@ -336,6 +358,9 @@ def main():
     ap.add_argument("--timeline-out", default=None,
                     help="write the last timed step's measured timeline (CSV + SVG, reference writers) here")
     args = ap.parse_args()
+    dflt = DEFAULTS[args.model]
+    args.micro_batches = args.micro_batches or dflt["micro_batches"]
+    args.slice = args.slice or dflt["slice"]
     rank, world = dist_setup()
     if args.impl == "reference":
         run_reference(args, rank, world)
@@ -351,7 +376,8 @@ def main():
     from paper_2007_01045_b200 import pipeplan
     model = MODELS[args.model]
     M = args.micro_batches
-    gbs = args.global_batch or M * args.slice * max(1, world // 2)
+    straight = dflt["straight"]
+    gbs = args.global_batch or M * args.slice * (1 if straight else max(1, world // 2))
     cluster = b200_cluster(world, args.mem_gb)
     # pre-run B200 layer profile at the micro-batch size: the planner's input
     # and the source of the predicted L (a real prediction, made before the run)
@@ -363,7 +389,7 @@ def main():
         plan = pipeplan.plan(profiles[mb], cluster, M)["plan"] if rank == 0 else None
         plan = broadcast(plan, world)
     else:
-        plan = make_plan(world, model["layers"])
+        plan = make_plan(world, model["layers"], straight)
     if profiles and rank == 0:
         for st in plan["stages"]:
             size = -(-mb // len(st["gpus"]))
@@ -437,7 +463,8 @@ def main():
         torch.cuda.synchronize()
         barrier(world)
         t_e2e = time.perf_counter() - t0
-        h2d = (inp.numel() * 2 if inp is not None else 0) + (tgt.numel() * 2 if tgt is not None else 0)
+        h2d = (inp.numel() * inp.element_size() if inp is not None else 0) + \
+            (tgt.numel() * tgt.element_size() if tgt is not None else 0)
         d2h = 4 if rank in plan["stages"][-1]["gpus"] else 0
         sums = gather((h2d, d2h, t_e2e), world)
         e2e = {"value": args.steps * gbs / max(s[2] for s in sums), "unit": "samples/s",
@@ -488,8 +515,8 @@ def main():
     fps = flops_per_sample(model)
     line = {
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": measured_ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded splitmix64 inputs/targets, random-init "
+        "warmup": args.warmup, "ms_per_step": measured_ms, "higher_is_better": True,
+        "scaling": "strong" if straight else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded splitmix64 inputs/targets, random-init "
                                                       "weights)",
         "config": {"workload": args.model, **model, "global_batch": gbs, "micro_batches": M,
                    "plan_source": "host planner (pipeplan.plan on the B200 profile, per_gpu_memory_gb="

@@ -105,6 +105,16 @@ int dpl_k_colsum_acc(const void* dy, float* db, int rows, int cols, void* stream
 int dpl_k_mse_loss(const void* y, const void* t, void* dy, float* loss_acc, long long n, float grad_scale,
                    void* stream);
 int dpl_k_sgd_apply(float* w32, float* g, void* w16, long long n, float lr, void* stream);
+/* GPT language-model ends (config C4; no reference counterpart -- the
+ * reference has no numerical executor).
+ * tokens: dst[i] = (splitmix64(seed, tensor, idx0+i) >> 32) % vocab
+ * embed:  x[r] = wte[tok[r]] + wpe[r % seq]; backward red.adds into fp32 grads
+ * cross_entropy: per row loss_acc += lse(row) - row[tgt]; row <- (softmax - onehot) * grad_scale */
+int dpl_k_fill_tokens(int* dst, long long n, uint64_t seed, uint64_t tensor, long long idx0, int vocab, void* stream);
+int dpl_k_embed_fwd(const int* tok, const void* wte, const void* wpe, void* x, int rows, int seq, int h, void* stream);
+int dpl_k_embed_bwd(const int* tok, const void* dx, float* gwte, float* gwpe, int rows, int seq, int h, void* stream);
+int dpl_k_cross_entropy(void* logits, const int* tgt, float* loss_acc, int rows, int vocab, float grad_scale,
+                        void* stream);
 int dpl_k_fill_uniform_bf16(void* dst, long long n, uint64_t seed, uint64_t tensor, long long idx0, float scale,
                             void* stream);
 int dpl_k_fill_uniform_f32(float* dst, long long n, uint64_t seed, uint64_t tensor, long long idx0, float scale,

@@ -36,14 +36,19 @@ _M1 = np.uint64(0xBF58476D1CE4E5B9)
 _M2 = np.uint64(0x94D649BB133111EB)
 
 
-def hash_uniform(seed: int, tensor: int, idx) -> np.ndarray:
-    """U(-1, 1) float32 keyed by (seed, tensor id, element index)."""
+def mix64(seed: int, tensor: int, idx) -> np.ndarray:
+    """splitmix64 finaliser of seed + tensor*K_T + idx*K_I (uint64)."""
     idx = np.asarray(idx, dtype=np.uint64)
     with np.errstate(over="ignore"):
         z = np.uint64(seed) + np.uint64(tensor) * _K_TENSOR + idx * _K_INDEX
         z = (z ^ (z >> np.uint64(30))) * _M1
         z = (z ^ (z >> np.uint64(27))) * _M2
-        z = z ^ (z >> np.uint64(31))
+        return z ^ (z >> np.uint64(31))
+
+
+def hash_uniform(seed: int, tensor: int, idx) -> np.ndarray:
+    """U(-1, 1) float32 keyed by (seed, tensor id, element index)."""
+    z = mix64(seed, tensor, idx)
     u = (z >> np.uint64(40)).astype(np.float32) * np.float32(1.0 / 16777216.0)
     return u * np.float32(2.0) - np.float32(1.0)
 
@@ -87,11 +92,13 @@ class Model:
     seq: int = 1
     causal: bool = False
     eps: float = 1e-5
+    vocab: int = 0  # > 0: GPT language model (token ids in, causal-LM cross-entropy out)
 
     @staticmethod
     def from_dict(d: dict) -> "Model":
         m = Model(kind=d["kind"], layers=d["layers"], hidden=d["hidden"], heads=d.get("heads", 16),
-                  ffn=d.get("ffn", 4 * d["hidden"]), seq=d.get("seq", 1), causal=d.get("causal", False))
+                  ffn=d.get("ffn", 4 * d["hidden"]), seq=d.get("seq", 1), causal=d.get("causal", False),
+                  vocab=d.get("vocab", 0))
         if m.kind == "mlp":
             m.seq = 1
         if m.kind == "gpt":
@@ -124,6 +131,64 @@ def batch_data(model: Model, seed: int, sample0: int, samples: int):
     idx = np.arange(n, dtype=np.uint64) + np.uint64(sample0 * model.seq * model.hidden)
     shape = (samples * model.seq, model.hidden)
     return hash_uniform(seed, 1, idx).reshape(shape), hash_uniform(seed, 2, idx).reshape(shape)
+
+
+# ---------------------------------------------------------------- GPT LM ends
+# Token ids and the LM parameters exactly as the device makes them
+# (csrc/kernels/lm.cu fill_tokens, csrc/runtime/layers.cu TokenEmbedding /
+# LmHead bind): inputs use tensor id 1, targets id 2, element index = global
+# token index; wte / wpe ~ U(+-0.1) (ids 100, 101), Wout ~ U(+-1/sqrt(H))
+# (id 112), LN_f gamma = 1, beta = 0.
+def lm_tokens(model: Model, seed: int, sample0: int, samples: int):
+    idx = np.arange(samples * model.seq, dtype=np.uint64) + np.uint64(sample0 * model.seq)
+    tok = (mix64(seed, 1, idx) >> np.uint64(32)) % np.uint64(model.vocab)
+    tgt = (mix64(seed, 2, idx) >> np.uint64(32)) % np.uint64(model.vocab)
+    return tok.astype(np.int64), tgt.astype(np.int64)
+
+
+def init_lm(model: Model, seed: int) -> dict:
+    H, V, S = model.hidden, model.vocab, model.seq
+    return {"wte": _u(seed, 100, V * H, 0.1).reshape(V, H), "wpe": _u(seed, 101, S * H, 0.1).reshape(S, H),
+            "lnf_g": np.ones(H, np.float32), "lnf_b": np.zeros(H, np.float32),
+            "Wout": _u(seed, 112, V * H, np.float32(1.0) / np.sqrt(np.float32(H))).reshape(V, H)}
+
+
+def embed_forward(model: Model, p: dict, tok: np.ndarray, q=None):
+    q = q or _ident
+    pos = np.arange(tok.size) % model.seq
+    return q(q(p["wte"])[tok] + q(p["wpe"])[pos])
+
+
+def embed_backward(model: Model, tok: np.ndarray, dx: np.ndarray) -> dict:
+    gwte = np.zeros((model.vocab, model.hidden), dx.dtype)
+    np.add.at(gwte, tok, dx)
+    gwpe = dx.reshape(-1, model.seq, model.hidden).sum(0)
+    return {"wte": gwte, "wpe": gwpe}
+
+
+def head_forward(model: Model, p: dict, y: np.ndarray, tgt: np.ndarray, ntok_global: int, q=None):
+    """Returns (sum of token CE, cache).  The logits are stored in bf16 and the
+    gradient (softmax - onehot) / ntok_global replaces them (lm.cu)."""
+    q = q or _ident
+    xn, c = _ln_fwd(y, p["lnf_g"], p["lnf_b"], model.eps)
+    xn = q(xn)
+    logits = q(xn @ q(p["Wout"]).T)
+    m = logits.max(-1, keepdims=True)
+    e = np.exp(logits - m)
+    ssum = e.sum(-1, keepdims=True)
+    rows = np.arange(logits.shape[0])
+    loss = float((np.log(ssum[:, 0]) + m[:, 0] - logits[rows, tgt]).sum())
+    d = e / ssum
+    d[rows, tgt] -= 1.0
+    return loss, (xn, c, q(d / ntok_global))
+
+
+def head_backward(model: Model, p: dict, cache, q=None):
+    q = q or _ident
+    xn, c, dlog = cache
+    g = {"Wout": dlog.T @ xn}
+    dy, g["lnf_g"], g["lnf_b"] = _ln_bwd(q(dlog @ q(p["Wout"])), p["lnf_g"], c)
+    return q(dy), g
 
 
 def bf16_round(a) -> np.ndarray:
@@ -258,23 +323,42 @@ def full_batch_step(model, gbs: int, seed: int = 1234, lr: float = 1e-3, dtype=n
     layers = range(model.layers) if layers is None else layers
     q = bf16_round if bf16 else _ident
     params = {l: {k: v.astype(dtype) for k, v in init_layer(model, l, seed).items()} for l in layers}
-    x, t = batch_data(model, seed, 0, gbs)
-    x, t = q(x.astype(dtype)), q(t.astype(dtype))
+    lm = model.vocab > 0
+    if lm:
+        lmp = {k: v.astype(dtype) for k, v in init_lm(model, seed).items()}
+        tok, tgt = lm_tokens(model, seed, 0, gbs)
+        x = embed_forward(model, lmp, tok, q)
+    else:
+        x, t = batch_data(model, seed, 0, gbs)
+        x, t = q(x.astype(dtype)), q(t.astype(dtype))
     caches = []
     for l in layers:
         x, c = layer_forward(model, l, params[l], x, gbs, q=q)
         caches.append(c)
-    numel = gbs * model.seq * model.hidden
-    diff = x - t
-    loss = float((diff * diff).sum() / numel)
-    dy = q(2.0 * diff / numel)
-    res = StepResult(loss)
+    res = StepResult(0.0)
+
+    def record(owner, g, p):
+        for k, v in g.items():
+            res.grads[(owner, k)] = v
+            res.params[(owner, k)] = p[k].astype(np.float32) - np.float32(lr) * v.astype(np.float32)
+
+    if lm:
+        ntok = gbs * model.seq
+        lsum, hc = head_forward(model, lmp, x, tgt, ntok, q)
+        res.loss = lsum / ntok
+        dy, g = head_backward(model, lmp, hc, q)
+        record("head", g, lmp)
+    else:
+        numel = gbs * model.seq * model.hidden
+        diff = x - t
+        res.loss = float((diff * diff).sum() / numel)
+        dy = q(2.0 * diff / numel)
     for li in reversed(range(len(caches))):
         l = list(layers)[li]
-        dy, g = layer_backward(model, l, params[l], caches[li], dy, gbs, need_dx=li > 0, q=q)
-        for k, v in g.items():
-            res.grads[(l, k)] = v
-            res.params[(l, k)] = (params[l][k].astype(np.float32) - np.float32(lr) * v.astype(np.float32))
+        dy, g = layer_backward(model, l, params[l], caches[li], dy, gbs, need_dx=li > 0 or lm, q=q)
+        record(l, g, params[l])
+    if lm:
+        record("emb", embed_backward(model, tok, dy), lmp)
     return res
 
 
@@ -290,8 +374,17 @@ def scheduled_step(model, plan: dict, micro_batches: int, gbs: int, seed: int = 
     stages = plan["stages"]
     B = gbs // micro_batches
     params = {l: {k: v.astype(dtype) for k, v in init_layer(model, l, seed).items()} for l in range(model.layers)}
-    numel = gbs * model.seq * model.hidden
-    acc = {}  # (stage, replica, layer, name) -> grad
+    lm = model.vocab > 0
+    if lm:
+        params["emb"] = params["head"] = {k: v.astype(dtype) for k, v in init_lm(model, seed).items()}
+        numel = gbs * model.seq  # CE is a mean over the global batch's tokens
+    else:
+        numel = gbs * model.seq * model.hidden
+    acc = {}  # (stage, replica, layer | "emb" | "head", name) -> grad
+
+    def add(key, v):
+        acc[key] = acc[key] + v if key in acc else v
+
     loss = 0.0
     for i in range(micro_batches):
         xs = None  # per-replica input slices of the current stage
@@ -300,7 +393,10 @@ def scheduled_step(model, plan: dict, micro_batches: int, gbs: int, seed: int = 
             r = len(st["gpus"])
             lo, hi = st["layers"]
             cut = [B * j // r for j in range(r + 1)]  # sample boundaries of the replica slices
-            if k == 0:
+            if k == 0 and lm:
+                toks = [lm_tokens(model, seed, i * B + cut[j], cut[j + 1] - cut[j])[0] for j in range(r)]
+                xs = [embed_forward(model, params["emb"], t) for t in toks]
+            elif k == 0:
                 xs = [batch_data(model, seed, i * B + cut[j], cut[j + 1] - cut[j])[0].astype(dtype)
                       for j in range(r)]
             else:
@@ -322,6 +418,15 @@ def scheduled_step(model, plan: dict, micro_batches: int, gbs: int, seed: int = 
         cut = [B * j // r for j in range(r + 1)]
         dys = []
         for j in range(r):
+            if lm:
+                tgt = lm_tokens(model, seed, i * B + cut[j], cut[j + 1] - cut[j])[1]
+                lsum, hc = head_forward(model, params["head"], xs[j], tgt, numel)
+                loss += lsum
+                dy, g = head_backward(model, params["head"], hc)
+                for name in ("Wout", "lnf_g", "lnf_b"):
+                    add((len(stages) - 1, j, "head", name), g[name])
+                dys.append(dy)
+                continue
             t = batch_data(model, seed, i * B + cut[j], cut[j + 1] - cut[j])[1].astype(dtype)
             diff = xs[j] - t
             loss += float((diff * diff).sum())
@@ -338,10 +443,12 @@ def scheduled_step(model, plan: dict, micro_batches: int, gbs: int, seed: int = 
                 dy = dys[j]
                 for li, l in reversed(list(enumerate(range(lo, hi)))):
                     dy, g = layer_backward(model, l, params[l], caches[k][j][li], dy, cut[j + 1] - cut[j],
-                                           need_dx=(l > 0))
+                                           need_dx=(l > 0 or lm))
                     for name, v in g.items():
-                        key = (k, j, l, name)
-                        acc[key] = acc[key] + v if key in acc else v
+                        add((k, j, l, name), v)
+                if k == 0 and lm:
+                    for name, v in embed_backward(model, toks[j], dy).items():
+                        add((0, j, "emb", name), v)
                 dys[j] = dy
     res = StepResult(loss / numel)
     for k, st in enumerate(stages):
@@ -351,6 +458,13 @@ def scheduled_step(model, plan: dict, micro_batches: int, gbs: int, seed: int = 
                 g = sum(acc[(k, j, l, name)] for j in range(len(st["gpus"])))  # AllReduce
                 res.grads[(l, name)] = g
                 res.params[(l, name)] = params[l][name].astype(np.float32) - np.float32(lr) * g.astype(np.float32)
+    if lm:
+        for k, owner, names in ((0, "emb", ("wte", "wpe")), (len(stages) - 1, "head", ("Wout", "lnf_g", "lnf_b"))):
+            for name in names:
+                g = sum(acc[(k, j, owner, name)] for j in range(len(stages[k]["gpus"])))
+                res.grads[(owner, name)] = g
+                res.params[(owner, name)] = (params[owner][name].astype(np.float32) -
+                                             np.float32(lr) * g.astype(np.float32))
     return res
 
 
@@ -365,21 +479,37 @@ class CpuTrainer:
         self.seed, self.dtype = seed, dtype
         self.params = {l: {k: v.astype(dtype) for k, v in init_layer(self.model, l, seed).items()}
                        for l in range(self.model.layers)}
+        if self.model.vocab > 0:
+            self.lm = {k: v.astype(dtype) for k, v in init_lm(self.model, seed).items()}
 
     def step(self, sample0: int, samples: int, lr: float = 1e-3) -> float:
         m = self.model
-        x, t = batch_data(m, self.seed, sample0, samples)
-        x, t = x.astype(self.dtype), t.astype(self.dtype)
+        lm = m.vocab > 0
+        if lm:
+            tok, tgt = lm_tokens(m, self.seed, sample0, samples)
+            x = embed_forward(m, self.lm, tok)
+        else:
+            x, t = batch_data(m, self.seed, sample0, samples)
+            x, t = x.astype(self.dtype), t.astype(self.dtype)
         caches = []
         for l in range(m.layers):
             x, c = layer_forward(m, l, self.params[l], x, samples)
             caches.append(c)
-        numel = samples * m.seq * m.hidden
-        diff = x - t
-        loss = float((diff * diff).sum() / numel)
-        dy = (2.0 / numel) * diff
+        if lm:
+            ntok = samples * m.seq
+            lsum, hc = head_forward(m, self.lm, x, tgt, ntok)
+            loss = lsum / ntok
+            dy, g_head = head_backward(m, self.lm, hc)
+        else:
+            numel = samples * m.seq * m.hidden
+            diff = x - t
+            loss = float((diff * diff).sum() / numel)
+            dy = (2.0 / numel) * diff
         for l in reversed(range(m.layers)):
-            dy, g = layer_backward(m, l, self.params[l], caches[l], dy, samples, need_dx=l > 0)
+            dy, g = layer_backward(m, l, self.params[l], caches[l], dy, samples, need_dx=l > 0 or lm)
             for k, v in g.items():
                 self.params[l][k] -= self.dtype(lr) * v.astype(self.dtype)
+        if lm:
+            for k, v in list(g_head.items()) + list(embed_backward(m, tok, dy).items()):
+                self.lm[k] -= self.dtype(lr) * v.astype(self.dtype)
         return loss

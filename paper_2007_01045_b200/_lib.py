@@ -53,6 +53,10 @@ _PROTOS = {
     "dpl_k_colsum_acc": (_I, [_VP, _VP, _I, _I, _VP]),
     "dpl_k_mse_loss": (_I, [_VP, _VP, _VP, _VP, _LL, _F, _VP]),
     "dpl_k_sgd_apply": (_I, [_VP, _VP, _VP, _LL, _F, _VP]),
+    "dpl_k_fill_tokens": (_I, [_VP, _LL, _U64, _U64, _LL, _I, _VP]),
+    "dpl_k_embed_fwd": (_I, [_VP, _VP, _VP, _VP, _I, _I, _I, _VP]),
+    "dpl_k_embed_bwd": (_I, [_VP, _VP, _VP, _VP, _I, _I, _I, _VP]),
+    "dpl_k_cross_entropy": (_I, [_VP, _VP, _VP, _I, _I, _F, _VP]),
     "dpl_k_fill_uniform_bf16": (_I, [_VP, _LL, _U64, _U64, _LL, _F, _VP]),
     "dpl_k_fill_uniform_f32": (_I, [_VP, _LL, _U64, _U64, _LL, _F, _VP]),
     "dpl_k_launch_count": (_LL, []),

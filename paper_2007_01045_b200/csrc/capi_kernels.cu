@@ -9,6 +9,7 @@
 #include "dapple.h"
 #include "kernels/attention.h"
 #include "kernels/elementwise.h"
+#include "kernels/lm.h"
 #include "kernels/gemm.h"
 
 namespace dpl {
@@ -159,6 +160,24 @@ int dpl_k_colsum_acc(const void* dy, float* db, int rows, int cols, void* stream
 int dpl_k_mse_loss(const void* y, const void* t, void* dy, float* loss_acc, long long n, float grad_scale,
                    void* stream) {
   return guarded([&] { dpl::mse_loss(y, t, dy, loss_acc, n, grad_scale, static_cast<cudaStream_t>(stream)); });
+}
+
+int dpl_k_fill_tokens(int* dst, long long n, uint64_t seed, uint64_t tensor, long long idx0, int vocab, void* stream) {
+  return guarded([&] { dpl::fill_tokens(dst, n, seed, tensor, idx0, vocab, static_cast<cudaStream_t>(stream)); });
+}
+
+int dpl_k_embed_fwd(const int* tok, const void* wte, const void* wpe, void* x, int rows, int seq, int h, void* stream) {
+  return guarded([&] { dpl::embed_fwd(tok, wte, wpe, x, rows, seq, h, static_cast<cudaStream_t>(stream)); });
+}
+
+int dpl_k_embed_bwd(const int* tok, const void* dx, float* gwte, float* gwpe, int rows, int seq, int h, void* stream) {
+  return guarded([&] { dpl::embed_bwd(tok, dx, gwte, gwpe, rows, seq, h, static_cast<cudaStream_t>(stream)); });
+}
+
+int dpl_k_cross_entropy(void* logits, const int* tgt, float* loss_acc, int rows, int vocab, float grad_scale,
+                        void* stream) {
+  return guarded(
+      [&] { dpl::cross_entropy_fwd_bwd(logits, tgt, loss_acc, rows, vocab, grad_scale, static_cast<cudaStream_t>(stream)); });
 }
 
 int dpl_k_sgd_apply(float* w32, float* g, void* w16, long long n, float lr, void* stream) {

@@ -40,6 +40,7 @@
 #include "dapple.h"
 #include "host/json.hpp"
 #include "kernels/elementwise.h"
+#include "kernels/lm.h"
 #include "layers.h"
 #include "pipeplan/executor.hpp"
 #include "pipeplan/io.hpp"
@@ -212,6 +213,14 @@ class Executor {
   std::vector<bf16*> out_;               // stage output per micro-batch
   std::vector<bf16*> target_, dloss_;    // last stage, per slot
   std::vector<bf16*> send_grad_;         // first-layer dX per micro-batch (stage > 0)
+  // GPT language model (spec_.vocab > 0): embedding on the first stage,
+  // LN_f + vocabulary projection + cross-entropy on the last
+  std::unique_ptr<TokenEmbedding> emb_;
+  std::unique_ptr<LmHead> head_;
+  size_t emb_off_ = 0, head_off_ = 0;
+  std::vector<int*> tok_, tgt_tok_;  // token ids / targets per slot
+  cudaEvent_t emb_done_ = nullptr, head_done_ = nullptr;
+  float loss_norm_ = 1.0f;  // loss = sum / loss_norm_ (MSE: GBS*seq*H elements, CE: GBS*seq tokens)
   bf16* gbuf_[2] = {nullptr, nullptr};
   bf16* rc_out_ = nullptr;  // output of the re-computed forward (discarded)
   float* loss_acc_ = nullptr;
@@ -246,6 +255,9 @@ class Executor {
   };
   std::vector<std::pair<GraphKey, cudaGraphExec_t>> graphs_;
   void enqueue_step(const void* host_input, const void* host_target);
+  // this rank's gradients of one parameter block are final: AllReduce over
+  // the replica group and apply on the reduce stream
+  void reduce_apply(cudaEvent_t ready, size_t off, size_t n);
   double flops_per_step_ = 0.0;
 
   // --- helpers
@@ -284,6 +296,9 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
   spec_.causal = m.contains("causal") && m.at("causal").as_bool();
   if (spec_.kind == "mlp") spec_.seq = 1;
   if (spec_.kind == "gpt") spec_.causal = true;
+  if (m.contains("vocab")) spec_.vocab = static_cast<int>(m.at("vocab").as_int());
+  if (spec_.vocab > 0 && (spec_.kind != "gpt" || spec_.vocab % 8 != 0))
+    throw std::invalid_argument("dpl exec: vocab needs kind gpt and a multiple of 8");
 
   plan_ = pipeplan::plan_from_json(cfg.at("plan").is_string() ? cfg.at("plan").as_string() : cfg.at("plan").dump());
   M_ = static_cast<int>(cfg.at("M").as_int());
@@ -356,6 +371,7 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
       if (r.src_gpu == rank_) out_routes_.push_back(r);
   }
   numel_global_ = 1LL * gbs_ * spec_.seq * spec_.hidden;
+  loss_norm_ = spec_.vocab > 0 ? static_cast<float>(1LL * gbs_ * spec_.seq) : static_cast<float>(numel_global_);
 
   // --- context, layers, parameters
   ctx_.spec = spec_;
@@ -375,11 +391,23 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
     param_off_.push_back(n_params_);
     n_params_ += (layer->param_count() + 63) / 64 * 64;  // keep every layer 256B aligned
   }
+  if (spec_.vocab > 0 && k_ == 0) {
+    emb_ = std::make_unique<TokenEmbedding>(spec_);
+    emb_off_ = n_params_;
+    n_params_ += (emb_->param_count() + 63) / 64 * 64;
+  }
+  if (spec_.vocab > 0 && k_ == S_ - 1) {
+    head_ = std::make_unique<LmHead>(spec_);
+    head_off_ = n_params_;
+    n_params_ += (head_->param_count() + 63) / 64 * 64;
+  }
   w32_ = static_cast<float*>(mem_.alloc(n_params_ * 4));
   g32_ = static_cast<float*>(mem_.alloc(n_params_ * 4));
   w16_ = static_cast<bf16*>(mem_.alloc(n_params_ * 2));
   for (size_t li = 0; li < layers_.size(); ++li)
     layers_[li]->bind(w32_ + param_off_[li], g32_ + param_off_[li], w16_ + param_off_[li], seed_, compute_);
+  if (emb_) emb_->bind(w32_ + emb_off_, g32_ + emb_off_, w16_ + emb_off_, seed_, compute_);
+  if (head_) head_->bind(w32_ + head_off_, g32_ + head_off_, w16_ + head_off_, seed_, compute_);
 
   const size_t RH = static_cast<size_t>(ctx_.rows) * spec_.hidden;
   if (spec_.kind != "mlp") {
@@ -403,10 +431,15 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
   for (int i = 0; i < M_; ++i) out_.push_back(static_cast<bf16*>(mem_.alloc(RH * 2)));
   if (k_ == S_ - 1) {
     for (int s = 0; s < phi_; ++s) {
-      target_.push_back(static_cast<bf16*>(mem_.alloc(RH * 2)));
+      if (!head_) target_.push_back(static_cast<bf16*>(mem_.alloc(RH * 2)));
       dloss_.push_back(static_cast<bf16*>(mem_.alloc(RH * 2)));
     }
   }
+  // the head's logits-gradient stash lives from F_i to B_i like the loss
+  // gradient (phi slots, also under re-computation)
+  if (head_) head_->alloc_stash(ctx_, phi_);
+  for (int s = 0; s < phi_ && emb_; ++s) tok_.push_back(static_cast<int*>(mem_.alloc(ctx_.rows * 4)));
+  for (int s = 0; s < phi_ && head_; ++s) tgt_tok_.push_back(static_cast<int*>(mem_.alloc(ctx_.rows * 4)));
   if (k_ > 0)
     for (int i = 0; i < M_; ++i) send_grad_.push_back(static_cast<bf16*>(mem_.alloc(RH * 2)));
   gbuf_[0] = static_cast<bf16*>(mem_.alloc(RH * 2));
@@ -448,15 +481,18 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
     }
   layer_done_.resize(L());
   for (auto& e : layer_done_) mk_nt(&e);
+  mk_nt(&emb_done_);
+  mk_nt(&head_done_);
   fwd_done_.resize(M_);
   bwd_done_.resize(M_);
   for (auto& e : fwd_done_) mk_nt(&e);
   for (auto& e : bwd_done_) mk_nt(&e);
 
   for (size_t li = 0; li < layers_.size(); ++li) {
-    const bool need_dx = !(k_ == 0 && li == 0);
+    const bool need_dx = !(k_ == 0 && li == 0) || emb_;
     flops_per_step_ += M_ * ((recompute_ ? 2 : 1) * layers_[li]->flops_fwd(ctx_) + layers_[li]->flops_bwd(ctx_, need_dx));
   }
+  if (head_) flops_per_step_ += M_ * (head_->flops_fwd(ctx_) + head_->flops_bwd(ctx_));
   DPL_CUDA(cudaMallocHost(reinterpret_cast<void**>(&loss_host_), sizeof(float)));
   // parameters initialised and every buffer (incl. the IPC-exported flags)
   // zeroed before any peer can see this rank
@@ -602,12 +638,16 @@ void Executor::forward(int i, uint32_t base) {
     x = recv_act(i);
   }
   record(fwd_ev_[i].start, compute_);
+  if (emb_) emb_->forward(ctx_, tok_[slot], in_[slot]);
   for (int li = 0; li < L(); ++li) {
     bf16* y = li + 1 < L() ? act_[li + 1][ss] : out_[i];
     layers_[li]->forward(ctx_, ss, x, y);
     x = y;
   }
-  if (k_ == S_ - 1) {
+  if (head_) {
+    // causal-LM cross-entropy, mean over the global batch's tokens
+    head_->forward(ctx_, slot, out_[i], tgt_tok_[slot], loss_acc_, 1.0f / loss_norm_);
+  } else if (k_ == S_ - 1) {
     // MSE over the whole global batch: loss = sum (y-t)^2 / numel, dY = 2 (y-t) / numel
     mse_loss(out_[i], target_[slot], dloss_[slot], loss_acc_, static_cast<long long>(ctx_.rows) * H,
              2.0f / static_cast<float>(numel_global_), compute_);
@@ -641,6 +681,11 @@ void Executor::backward(int i, uint32_t base) {
     dy = recv_grad(i);
   }
   record(bwd_ev_[i].start, compute_);
+  const bool last_mb = i == M_ - 1;
+  if (head_) {
+    head_->backward(ctx_, slot, out_[i], dloss_[slot]);
+    if (last_mb) reduce_apply(head_done_, head_off_, head_->param_count());
+  }
   if (recompute_) {
     // the backward block first re-runs the stage forward (B' = B + F)
     const bf16* x = k_ == 0 ? in_[slot] : recv_act(i);
@@ -650,7 +695,6 @@ void Executor::backward(int i, uint32_t base) {
       x = y;
     }
   }
-  const bool last_mb = i == M_ - 1;
   int pp = 0;
   for (int li = L() - 1; li >= 0; --li) {
     const bf16* x = li > 0 ? act_[li][ss] : (k_ == 0 ? in_[slot] : recv_act(i));
@@ -660,19 +704,18 @@ void Executor::backward(int i, uint32_t base) {
       pp ^= 1;
     } else if (k_ > 0) {
       dx = send_grad_[i];
+    } else if (emb_) {
+      dx = gbuf_[pp];
     }
     layers_[li]->backward(ctx_, ss, x, dy, dx);
     dy = dx;
-    if (last_mb) {
-      // this layer's gradients are final: AllReduce over the replica group
-      // and apply while the remaining layers' backward runs
-      DPL_CUDA(cudaEventRecord(layer_done_[li], compute_));
-      DPL_CUDA(cudaStreamWaitEvent(reduce_, layer_done_[li], 0));
-      const size_t off = param_off_[li];
-      const size_t n = layers_[li]->param_count();
-      if (comm_) DPL_NCCL(ncclAllReduce(g32_ + off, g32_ + off, n, ncclFloat, ncclSum, comm_, reduce_));
-      if (apply_) sgd_apply(w32_ + off, g32_ + off, w16_ + off, static_cast<long long>(n), lr_, reduce_);
-    }
+    // this layer's gradients are final: AllReduce + apply while the
+    // remaining layers' backward runs
+    if (last_mb) reduce_apply(layer_done_[li], param_off_[li], layers_[li]->param_count());
+  }
+  if (emb_) {
+    emb_->backward(ctx_, tok_[slot], dy);
+    if (last_mb) reduce_apply(emb_done_, emb_off_, emb_->param_count());
   }
   record(bwd_ev_[i].end, compute_);
   if (k_ > 0) {
@@ -692,6 +735,13 @@ void Executor::backward(int i, uint32_t base) {
     }
     record(send_bwd_ev_[i].end, send_grad_s_);
   }
+}
+
+void Executor::reduce_apply(cudaEvent_t ready, size_t off, size_t n) {
+  DPL_CUDA(cudaEventRecord(ready, compute_));
+  DPL_CUDA(cudaStreamWaitEvent(reduce_, ready, 0));
+  if (comm_) DPL_NCCL(ncclAllReduce(g32_ + off, g32_ + off, n, ncclFloat, ncclSum, comm_, reduce_));
+  if (apply_) sgd_apply(w32_ + off, g32_ + off, w16_ + off, static_cast<long long>(n), lr_, reduce_);
 }
 
 void Executor::enqueue_step(const void* host_input, const void* host_target) {
@@ -715,7 +765,16 @@ void Executor::enqueue_step(const void* host_input, const void* host_target) {
     if (op.kind == pipeplan::BlockKind::forward) {
       const long long sample0 = 1LL * i * B_ + slice_first;
       const long long idx0 = sample0 * spec_.seq * static_cast<long long>(H);
-      if (k_ == 0) {
+      const long long tok0 = sample0 * spec_.seq;
+      const size_t rows = static_cast<size_t>(ctx_.rows);
+      if (emb_) {  // token ids: [M][rows] int32 on the host
+        if (host_input) {
+          DPL_CUDA(cudaMemcpyAsync(tok_[slot], static_cast<const int*>(host_input) + i * rows, rows * 4,
+                                   cudaMemcpyHostToDevice, compute_));
+        } else {
+          fill_tokens(tok_[slot], static_cast<long long>(rows), seed_, kTensorInput, tok0, spec_.vocab, compute_);
+        }
+      } else if (k_ == 0) {
         if (host_input) {
           DPL_CUDA(cudaMemcpyAsync(in_[slot], static_cast<const bf16*>(host_input) + static_cast<size_t>(i) * RH,
                                    RH * 2, cudaMemcpyHostToDevice, compute_));
@@ -723,7 +782,14 @@ void Executor::enqueue_step(const void* host_input, const void* host_target) {
           fill_uniform_bf16(in_[slot], static_cast<long long>(RH), seed_, kTensorInput, idx0, 1.0f, compute_);
         }
       }
-      if (k_ == S_ - 1) {
+      if (head_) {
+        if (host_target) {
+          DPL_CUDA(cudaMemcpyAsync(tgt_tok_[slot], static_cast<const int*>(host_target) + i * rows, rows * 4,
+                                   cudaMemcpyHostToDevice, compute_));
+        } else {
+          fill_tokens(tgt_tok_[slot], static_cast<long long>(rows), seed_, kTensorTarget, tok0, spec_.vocab, compute_);
+        }
+      } else if (k_ == S_ - 1) {
         if (host_target) {
           DPL_CUDA(cudaMemcpyAsync(target_[slot], static_cast<const bf16*>(host_target) + static_cast<size_t>(i) * RH,
                                    RH * 2, cudaMemcpyHostToDevice, compute_));
@@ -798,7 +864,7 @@ float Executor::step(const void* host_input, const void* host_target) {
   ++steps_done_;
   bank_ ^= 1;
   float loss = NAN;
-  if (k_ == S_ - 1) loss = *loss_host_ / static_cast<float>(numel_global_);
+  if (k_ == S_ - 1) loss = *loss_host_ / loss_norm_;
   last_loss_ = loss;
   return loss;
 }
@@ -851,8 +917,23 @@ void Executor::read_tensor(const std::string& name, bool grad, void* host, size_
   // name = "<global layer>.<tensor>" ; only layers of this stage are readable
   const size_t dot = name.find('.');
   if (dot == std::string::npos) throw std::invalid_argument("dpl exec: tensor name must be <layer>.<name>");
-  const int layer = std::stoi(name.substr(0, dot));
   const std::string t = name.substr(dot + 1);
+  const std::string owner = name.substr(0, dot);
+  if (owner == "emb" || owner == "head") {
+    const bool e = owner == "emb";
+    if (e ? !emb_ : !head_) throw std::out_of_range("dpl exec: " + owner + " not on this stage");
+    for (const Layer::Named& n : e ? emb_->tensors() : head_->tensors()) {
+      if (n.name != t) continue;
+      if (bytes != n.count * 4) throw std::invalid_argument("dpl exec: size mismatch for " + name);
+      const float* src = (grad ? g32_ : w32_) + (e ? emb_off_ : head_off_) + n.offset;
+      DPL_CUDA(cudaSetDevice(device_));
+      DPL_CUDA(cudaDeviceSynchronize());
+      DPL_CUDA(cudaMemcpy(host, src, bytes, cudaMemcpyDeviceToHost));
+      return;
+    }
+    throw std::invalid_argument("dpl exec: unknown tensor " + name);
+  }
+  const int layer = std::stoi(owner);
   if (layer < lo_ || layer >= hi_) throw std::out_of_range("dpl exec: layer not on this stage");
   const int li = layer - lo_;
   for (const Layer::Named& n : layers_[li]->tensors()) {
@@ -883,17 +964,22 @@ std::string Executor::layer_profile_json(int reps) {
   for (auto* v : {&fe, &be})
     for (cudaEvent_t& e : *v) DPL_CUDA(cudaEventCreate(&e));
   std::vector<std::vector<float>> ft(n), bt(n);
-  if (k_ == 0) fill_uniform_bf16(in_[0], static_cast<long long>(ctx_.rows) * H, seed_, kTensorInput, 0, 1.0f, compute_);
-  if (k_ == S_ - 1)
+  if (emb_) fill_tokens(tok_[0], ctx_.rows, seed_, kTensorInput, 0, spec_.vocab, compute_);
+  else if (k_ == 0) fill_uniform_bf16(in_[0], static_cast<long long>(ctx_.rows) * H, seed_, kTensorInput, 0, 1.0f, compute_);
+  if (head_) fill_tokens(tgt_tok_[0], ctx_.rows, seed_, kTensorTarget, 0, spec_.vocab, compute_);
+  else if (k_ == S_ - 1)
     fill_uniform_bf16(target_[0], static_cast<long long>(ctx_.rows) * H, seed_, kTensorTarget, 0, 1.0f, compute_);
   const bf16* x0 = k_ == 0 ? in_[0] : recv_act(0);
   for (int rep = 0; rep < reps + 1; ++rep) {  // first chain is a warm-up
     const bf16* x = x0;
     DPL_CUDA(cudaEventRecord(fe[0], compute_));
+    if (emb_) emb_->forward(ctx_, tok_[0], in_[0]);  // counted in layer 0 (profile layers are the blocks)
     for (int li = 0; li < n; ++li) {
       bf16* y = li + 1 < n ? act_[li + 1][0] : out_[0];
       layers_[li]->forward(ctx_, 0, x, y);
-      if (li == n - 1 && k_ == S_ - 1)
+      if (li == n - 1 && head_)
+        head_->forward(ctx_, 0, out_[0], tgt_tok_[0], loss_acc_, 1.0f / loss_norm_);  // counted in the last layer
+      else if (li == n - 1 && k_ == S_ - 1)
         mse_loss(out_[0], target_[0], dloss_[0], loss_acc_, static_cast<long long>(ctx_.rows) * H,
                  2.0f / static_cast<float>(numel_global_), compute_);
       DPL_CUDA(cudaEventRecord(fe[li + 1], compute_));
@@ -902,11 +988,13 @@ std::string Executor::layer_profile_json(int reps) {
     const bf16* dy = k_ == S_ - 1 ? dloss_[0] : recv_grad(0);
     int pp = 0;
     DPL_CUDA(cudaEventRecord(be[n], compute_));
+    if (head_) head_->backward(ctx_, 0, out_[0], dloss_[0]);
     for (int li = n - 1; li >= 0; --li) {
       const bf16* xin = li > 0 ? act_[li][0] : x0;
-      bf16* dx = li > 0 ? gbuf_[pp] : (k_ > 0 ? send_grad_[0] : nullptr);
+      bf16* dx = li > 0 || emb_ ? gbuf_[pp] : (k_ > 0 ? send_grad_[0] : nullptr);
       pp ^= 1;
       layers_[li]->backward(ctx_, 0, xin, dy, dx);
+      if (li == 0 && emb_) emb_->backward(ctx_, tok_[0], dx);
       DPL_CUDA(cudaEventRecord(be[li], compute_));
       dy = dx;
     }
@@ -937,7 +1025,10 @@ std::string Executor::layer_profile_json(int reps) {
     l.fwd_time = median(ft[li]) * 1e-3;
     l.bwd_time = median(bt[li]) * 1e-3;
     l.activation_bytes = static_cast<std::int64_t>(ctx_.rows) * static_cast<std::int64_t>(H) * 2;  // bf16 output
-    l.param_bytes = static_cast<std::int64_t>(layers_[li]->param_count()) * 4;                       // fp32 master
+    size_t np = layers_[li]->param_count();
+    if (li == 0 && emb_) np += emb_->param_count();
+    if (li == n - 1 && head_) np += head_->param_count();
+    l.param_bytes = static_cast<std::int64_t>(np) * 4;  // fp32 master
     prof.layers.push_back(l);
   }
   return pipeplan::profile_to_json(prof);
@@ -1032,6 +1123,7 @@ std::string Executor::info() const {
   v["schedule"] = gpipe_ ? "gpipe" : "dapple";
   v["recompute"] = recompute_;
   v["stash_slots"] = stash_slots_;
+  v["vocab"] = spec_.vocab;
   v["rows"] = ctx_.rows;
   v["micro_batch_samples"] = B_;
   v["params"] = static_cast<long long>(n_params_);

@@ -8,6 +8,7 @@
 
 #include "kernels/attention.h"
 #include "kernels/elementwise.h"
+#include "kernels/lm.h"
 #include "layers.h"
 
 namespace dpl {
@@ -347,6 +348,77 @@ std::unique_ptr<Layer> make_layer(const ModelSpec& spec, int global_index) {
   if (spec.kind == "mlp") return std::make_unique<MlpLayer>(spec, global_index);
   if (spec.kind == "bert" || spec.kind == "gpt") return std::make_unique<TransformerLayer>(spec, global_index);
   throw std::invalid_argument("dpl: unknown model kind '" + spec.kind + "'");
+}
+
+// ------------------------------------------------------------------ LM ends
+void TokenEmbedding::bind(float* w32, float* g32, bf16* w16, uint64_t seed, cudaStream_t s) {
+  g32_ = g32;
+  w16_ = w16;
+  const size_t nte = static_cast<size_t>(v_) * h_;
+  fill_uniform_f32(w32, static_cast<long long>(nte), seed, kTensorWte, 0, 0.1f, s);
+  fill_uniform_f32(w32 + nte, static_cast<long long>(seq_) * h_, seed, kTensorWpe, 0, 0.1f, s);
+  cast_f32_bf16(w32, w16, static_cast<long long>(param_count()), s);
+}
+
+void TokenEmbedding::forward(StageContext& ctx, const int* tok, bf16* x) {
+  embed_fwd(tok, w16_, w16_ + static_cast<size_t>(v_) * h_, x, ctx.rows, seq_, h_, ctx.stream);
+}
+
+void TokenEmbedding::backward(StageContext& ctx, const int* tok, const bf16* dx) {
+  embed_bwd(tok, dx, g32_, g32_ + static_cast<size_t>(v_) * h_, ctx.rows, seq_, h_, ctx.stream);
+}
+
+std::vector<Layer::Named> TokenEmbedding::tensors() const {
+  return {{"wte", 0, static_cast<size_t>(v_) * h_}, {"wpe", static_cast<size_t>(v_) * h_, static_cast<size_t>(seq_) * h_}};
+}
+
+// params: [lnf_g H][lnf_b H][Wout V*H]
+void LmHead::bind(float* w32, float* g32, bf16* w16, uint64_t seed, cudaStream_t s) {
+  w32_ = w32;
+  g32_ = g32;
+  w16_ = w16;
+  fill_const_f32(w32, h_, 1.0f, s);
+  fill_const_f32(w32 + h_, h_, 0.0f, s);
+  fill_uniform_f32(w32 + 2 * h_, static_cast<long long>(v_) * h_, seed, kTensorWout, 0,
+                   1.0f / std::sqrt(static_cast<float>(h_)), s);
+  cast_f32_bf16(w32, w16, static_cast<long long>(param_count()), s);
+}
+
+void LmHead::alloc_stash(StageContext& ctx, int slots) {
+  const size_t R = ctx.rows;
+  for (int k = 0; k < slots; ++k) {
+    Slot st;
+    st.xn = alloc_n<bf16>(ctx, R * h_);
+    st.mean = alloc_n<float>(ctx, R);
+    st.rstd = alloc_n<float>(ctx, R);
+    st.dlogits = alloc_n<bf16>(ctx, R * static_cast<size_t>(v_));
+    slots_.push_back(st);
+  }
+  dxn_ = alloc_n<bf16>(ctx, R * h_);
+}
+
+void LmHead::forward(StageContext& ctx, int slot, const bf16* y, const int* tgt, float* loss_acc, float grad_scale) {
+  const Slot& st = slots_[slot];
+  const int R = ctx.rows;
+  layernorm_fwd(y, w32_, w32_ + h_, st.xn, st.mean, st.rstd, R, h_, eps_, ctx.stream);
+  // logits [R][V] = xn Wout^T  (tcgen05, bf16 out)
+  ctx.gemms.run(plain(R, v_, h_, st.xn, h_, false, w16_ + 2 * h_, h_, false, st.dlogits, v_, kOutBf16), ctx.stream);
+  cross_entropy_fwd_bwd(st.dlogits, tgt, loss_acc, R, v_, grad_scale, ctx.stream);
+}
+
+void LmHead::backward(StageContext& ctx, int slot, const bf16* y, bf16* dy) {
+  const Slot& st = slots_[slot];
+  const int R = ctx.rows;
+  // dWout += dlogits^T xn ; dxn = dlogits Wout
+  ctx.gemms.run(plain(v_, h_, R, st.dlogits, v_, true, st.xn, h_, true, g32_ + 2 * h_, h_, kOutF32Acc), ctx.stream);
+  ctx.gemms.run(plain(R, h_, v_, st.dlogits, v_, false, w16_ + 2 * h_, h_, true, dxn_, h_, kOutBf16), ctx.stream);
+  layernorm_bwd(dxn_, y, st.mean, st.rstd, w32_, nullptr, dy, g32_, g32_ + h_, R, h_, ctx.stream, ctx.ln_ws);
+}
+
+std::vector<Layer::Named> LmHead::tensors() const {
+  return {{"lnf_g", 0, static_cast<size_t>(h_)},
+          {"lnf_b", static_cast<size_t>(h_), static_cast<size_t>(h_)},
+          {"Wout", 2 * static_cast<size_t>(h_), static_cast<size_t>(v_) * h_}};
 }
 
 }  // namespace dpl

@@ -34,6 +34,7 @@ struct ModelSpec {
   int seq = 1;  // tokens per sample (1 for the MLP)
   bool causal = false;
   float ln_eps = 1e-5f;
+  int vocab = 0;  // > 0: GPT language model (token ids in, cross-entropy out)
 };
 
 // Device memory owned by one stage replica (freed by the executor).
@@ -96,6 +97,63 @@ class Layer {
 };
 
 std::unique_ptr<Layer> make_layer(const ModelSpec& spec, int global_index);
+
+// GPT language-model ends (config C4).  Not profile layers of their own:
+// the embedding runs inside the first stage's F/B blocks before layer 0 /
+// after its backward, the head inside the last stage's blocks after the
+// last layer ("head on stage 7").
+//   x = wte[tok] + wpe[pos]                       (TokenEmbedding)
+//   loss = CE(LN_f(y) Wout^T, tgt)               (LmHead; Wout [V][H], untied)
+class TokenEmbedding {
+ public:
+  explicit TokenEmbedding(const ModelSpec& spec) : v_(spec.vocab), h_(spec.hidden), seq_(spec.seq) {}
+  size_t param_count() const { return static_cast<size_t>(v_) * h_ + static_cast<size_t>(seq_) * h_; }
+  void bind(float* w32, float* g32, bf16* w16, uint64_t seed, cudaStream_t s);
+  void forward(StageContext& ctx, const int* tok, bf16* x);
+  void backward(StageContext& ctx, const int* tok, const bf16* dx);
+  std::vector<Layer::Named> tensors() const;
+
+ private:
+  int v_, h_, seq_;
+  float* g32_ = nullptr;
+  bf16* w16_ = nullptr;
+};
+
+class LmHead {
+ public:
+  explicit LmHead(const ModelSpec& spec) : v_(spec.vocab), h_(spec.hidden), eps_(spec.ln_eps) {}
+  size_t param_count() const { return 2 * static_cast<size_t>(h_) + static_cast<size_t>(v_) * h_; }
+  void bind(float* w32, float* g32, bf16* w16, uint64_t seed, cudaStream_t s);
+  void alloc_stash(StageContext& ctx, int slots);
+  // y: the last block's output; accumulates sum_rows CE into loss_acc and
+  // leaves (softmax - onehot) * grad_scale of this slot for backward
+  void forward(StageContext& ctx, int slot, const bf16* y, const int* tgt, float* loss_acc, float grad_scale);
+  // dy <- gradient w.r.t. y; Wout / LN_f gradients accumulated
+  void backward(StageContext& ctx, int slot, const bf16* y, bf16* dy);
+  double flops_fwd(const StageContext& ctx) const { return 2.0 * ctx.rows * static_cast<double>(v_) * h_; }
+  double flops_bwd(const StageContext& ctx) const { return 4.0 * ctx.rows * static_cast<double>(v_) * h_; }
+  std::vector<Layer::Named> tensors() const;
+
+ private:
+  int v_, h_;
+  float eps_;
+  float* w32_ = nullptr;
+  float* g32_ = nullptr;
+  bf16* w16_ = nullptr;
+  struct Slot {
+    bf16* xn;
+    float* mean;
+    float* rstd;
+    bf16* dlogits;  // [R][V]: logits, then in place their gradient
+  };
+  std::vector<Slot> slots_;
+  bf16* dxn_ = nullptr;
+};
+
+// LM tensor ids (shared with oracle/executor_ref.py init_lm / lm_tokens)
+constexpr uint64_t kTensorWte = 100;
+constexpr uint64_t kTensorWpe = 101;
+constexpr uint64_t kTensorWout = 112;
 
 // Synthetic data tensor ids (shared with oracle/executor_ref.py).
 constexpr uint64_t kTensorInput = 1;

@@ -65,6 +65,23 @@ def mse_loss(y, t, dy, loss_acc, n, grad_scale):
     check(lib().dpl_k_mse_loss(_ptr(y), _ptr(t), _ptr(dy), _ptr(loss_acc), n, grad_scale, _stream()))
 
 
+def fill_tokens(dst, n, seed, tensor, idx0, vocab):
+    check(lib().dpl_k_fill_tokens(_ptr(dst), n, seed, tensor, idx0, vocab, _stream()))
+
+
+def embed_fwd(tok, wte, wpe, x, rows, seq, h):
+    check(lib().dpl_k_embed_fwd(_ptr(tok), _ptr(wte), _ptr(wpe), _ptr(x), rows, seq, h, _stream()))
+
+
+def embed_bwd(tok, dx, gwte, gwpe, rows, seq, h):
+    check(lib().dpl_k_embed_bwd(_ptr(tok), _ptr(dx), _ptr(gwte), _ptr(gwpe), rows, seq, h, _stream()))
+
+
+def cross_entropy(logits, tgt, loss_acc, rows, vocab, grad_scale):
+    """In place: logits rows -> (softmax - onehot(tgt)) * grad_scale; loss_acc += sum CE."""
+    check(lib().dpl_k_cross_entropy(_ptr(logits), _ptr(tgt), _ptr(loss_acc), rows, vocab, grad_scale, _stream()))
+
+
 def sgd_apply(w32, g, w16, n, lr):
     check(lib().dpl_k_sgd_apply(_ptr(w32), _ptr(g), _ptr(w16), n, lr, _stream()))
 

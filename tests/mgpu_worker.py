@@ -44,6 +44,9 @@ def main():
             results[apply] = check_update(ex, emu, layers, model["kind"], model, 1e-3)
         else:
             results[apply] = check_grads(ex, emu, exact, layers, model["kind"], model["layers"])
+            if model.get("vocab"):
+                from test_lm_gpu import _check_lm_tensors
+                _check_lm_tensors(ex, emu, exact, stage is plan["stages"][0], stage is plan["stages"][-1])
         parts = [None] * world
         dist.all_gather_object(parts, ex.timeline())
         if rank == 0:

@@ -30,6 +30,12 @@ CASES += [
     (4, MLP, {"stages": [{"layers": [0, 3], "gpus": [0, 1, 2]}, {"layers": [3, 4], "gpus": [3]}]}, 4, 28),
     (4, BERT, {"stages": [{"layers": [0, 1], "gpus": [0]}, {"layers": [1, 4], "gpus": [1, 2, 3]}]}, 2, 8),
 ]
+# GPT language model (embedding on stage 0, LN_f + vocab projection + CE on the last stage)
+LMGPT = dict(kind="gpt", layers=4, hidden=256, heads=4, ffn=1024, seq=128, vocab=1000)
+CASES += [
+    (2, LMGPT, {"stages": [{"layers": [0, 2], "gpus": [0]}, {"layers": [2, 4], "gpus": [1]}]}, 4, 8),
+    (4, LMGPT, {"stages": [{"layers": [0, 2], "gpus": [0, 1]}, {"layers": [2, 4], "gpus": [2, 3]}]}, 4, 16),
+]
 TWO = {"stages": [{"layers": [0, 2], "gpus": [0]}, {"layers": [2, 4], "gpus": [1]}]}
 # GPipe / re-computation on the device (the schedules of the paper's Table VI)
 SCHED_CASES = [

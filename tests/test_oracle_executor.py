@@ -75,3 +75,40 @@ def test_manual_backward_matches_autograd(kind):
     for l in range(m.layers):
         for k, v in params[l].items():
             assert np.allclose(v.grad.numpy(), res.grads[(l, k)], rtol=1e-9, atol=1e-13), (l, k)
+
+
+@pytest.mark.parametrize("plan", [PLANS[0], PLANS[3], PLANS[6]])
+def test_scheduled_equals_full_batch_lm(plan):
+    """GPT language model (token embedding + LN_f/vocab projection/CE head)."""
+    m = dict(kind="gpt", layers=4, hidden=32, heads=2, ffn=64, seq=8, vocab=40)
+    gbs, M = 24, 2
+    a = full_batch_step(m, gbs)
+    b = scheduled_step(m, plan, M, gbs)
+    assert abs(a.loss - b.loss) <= 1e-12 * abs(a.loss)
+    assert ("emb", "wte") in a.grads and ("head", "Wout") in a.grads
+    for key, g in a.grads.items():
+        assert np.allclose(b.grads[key], g, rtol=1e-10, atol=1e-14), key
+
+
+def test_lm_head_and_embedding_match_autograd():
+    """The oracle's manual LM-end gradients equal torch autograd in fp64."""
+    import torch
+    from oracle.executor_ref import embed_backward, embed_forward, head_backward, head_forward, init_lm, lm_tokens
+    m = Model.from_dict(dict(kind="gpt", layers=1, hidden=16, heads=2, ffn=32, seq=4, vocab=24))
+    p = {k: v.astype(np.float64) for k, v in init_lm(m, 7).items()}
+    tok, tgt = lm_tokens(m, 7, 0, 3)
+    assert tok.min() >= 0 and tok.max() < 24 and len(set(tok.tolist())) > 4
+    x = embed_forward(m, p, tok)
+    lsum, cache = head_forward(m, p, x, tgt, tok.size)
+    dx, g = head_backward(m, p, cache)
+    ge = embed_backward(m, tok, dx)
+    tp = {k: torch.tensor(v, requires_grad=True) for k, v in p.items()}
+    pos = torch.arange(tok.size) % m.seq
+    tx = tp["wte"][torch.tensor(tok)] + tp["wpe"][pos]
+    xn = torch.nn.functional.layer_norm(tx, (m.hidden,), tp["lnf_g"], tp["lnf_b"], eps=m.eps)
+    loss = torch.nn.functional.cross_entropy(xn @ tp["Wout"].T, torch.tensor(tgt), reduction="mean")
+    loss.backward()
+    assert abs(loss.item() - lsum / tok.size) < 1e-12
+    for k, v in [("Wout", g["Wout"]), ("lnf_g", g["lnf_g"]), ("lnf_b", g["lnf_b"]), ("wte", ge["wte"]),
+                 ("wpe", ge["wpe"])]:
+        assert np.allclose(tp[k].grad.numpy(), v, rtol=1e-9, atol=1e-12), k
