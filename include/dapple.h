@@ -71,6 +71,11 @@ typedef struct dpl_gemm_desc {
   void* aux_out;
   int force_bn;
   int force_1sm; /* 1: never use the cta_group::2 pair kernel */
+  /* optional: per-CTA phase timestamps (SM clock64 cycles), 16 u64 per CTA:
+   * entry, prologue done, first TMA issued, first MMA, last MMA committed,
+   * epilogue start, epilogue end, exit, then (TMA epilogue, first epilogue
+   * warp) input ready / store issued for its first 4 chunks.  NULL = off. */
+  unsigned long long* trace;
 } dpl_gemm_desc;
 
 #define DPL_EPI_OUT_BF16 0u

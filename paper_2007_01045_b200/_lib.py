@@ -30,6 +30,7 @@ class GemmDesc(ctypes.Structure):
         ("s_no", ctypes.c_longlong), ("epi", ctypes.c_uint32), ("alpha", ctypes.c_float),
         ("bias", ctypes.c_void_p), ("aux_in", ctypes.c_void_p), ("resid", ctypes.c_void_p),
         ("aux_out", ctypes.c_void_p), ("force_bn", ctypes.c_int), ("force_1sm", ctypes.c_int),
+        ("trace", ctypes.c_void_p),
     ]
 
 

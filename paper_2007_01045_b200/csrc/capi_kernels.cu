@@ -80,6 +80,7 @@ int dpl_k_gemm(const dpl_gemm_desc* d, void* stream) {
     g.C = d->C; g.ldc = d->ldc; g.zdiv = d->zdiv; g.s_zo = d->s_zo; g.s_zi = d->s_zi;
     g.ndiv = d->ndiv; g.s_no = d->s_no; g.epi = d->epi; g.alpha = d->alpha; g.bias = d->bias;
     g.aux_in = d->aux_in; g.resid = d->resid; g.aux_out = d->aux_out; g.force_bn = d->force_bn; g.force_1sm = d->force_1sm;
+    g.trace = d->trace;
     dpl::GemmOp op;
     op.prepare(g);
     op.launch(static_cast<cudaStream_t>(stream));

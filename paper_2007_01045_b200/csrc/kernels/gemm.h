@@ -57,12 +57,24 @@ struct GemmDesc {
   void* aux_out = nullptr;
   int force_bn = 0;  // 0 = heuristic; else 64/128/256
   int force_1sm = 0; // 1 = never use the CTA-pair kernel
+  unsigned long long* trace = nullptr;  // per-CTA phase timestamps (16 per CTA), diagnostics
 };
 
 // Device-visible launch parameters (one per prepared GEMM).
 struct alignas(64) GemmParams {
   CUtensorMap tma_a;
   CUtensorMap tma_b;
+  // TMA epilogue (tma_epi): 5-D maps over C's addressing
+  //   [n % inner][m][n / inner][z % zdiv][z / zdiv], box 32 x 32
+  CUtensorMap tma_c;  // output: bulk store (bf16 / fp32) or fp32 bulk reduce-add
+  CUtensorMap tma_x;  // residual / activation input (bulk load) or aux_out (bulk store)
+  int tma_epi;
+  int c_inner;
+  int stages;          // smem ring depth (runtime: what the epilogue carve-out leaves)
+  int epi_warp_bytes;  // TMA epilogue smem per epilogue warp
+  int epi_out_bytes;   // one output chunk buffer (2 KB bf16 / 4 KB fp32)
+  int epi_nx;          // extra-tensor chunk buffers per warp
+  int epi_tile_cols;   // columns of one CTA tile (bias slice staged per warp)
   int M, N, K, batch;
   int a_mn_major, b_mn_major;
   int num_m_blocks, num_n_blocks, num_k_blocks, num_tiles;
@@ -79,6 +91,7 @@ struct alignas(64) GemmParams {
   const __nv_bfloat16* resid;
   __nv_bfloat16* aux_out;
   int vec_ok;
+  unsigned long long* trace;
 };
 
 // A prepared GEMM: tensor maps encoded once, launched many times (the

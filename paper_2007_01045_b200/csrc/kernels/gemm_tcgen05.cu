@@ -38,16 +38,20 @@ constexpr int kBM = 128;
 constexpr int kBK = 64;  // one 128-byte swizzle atom of bf16
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 128 + 32 * kEpiWarps;
-constexpr int kSmemBudget = 227 * 1024;
+constexpr int kSmemBudget = 227 * 1024;  // dynamic smem of every GEMM CTA
+constexpr int kMaxStages = 8;
+constexpr int kMaxNx = 4;  // TMA epilogue extra-tensor buffers per warp
+constexpr int kEpiBars = kMaxNx + 1;  // per epilogue warp: x buffers + bias slice
 
+// smem: [1 KB align slack][stages x stage][epilogue carve-out][1 KB barriers];
+// the split between ring depth and epilogue staging is per GEMM (host)
 template <int BN>
 struct Cfg {
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = std::min(8, (kSmemBudget - 2048) / kStageBytes);
   static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
-  static constexpr int kSmem = 1024 /*align slack*/ + kStages * kStageBytes + 1024 /*barriers*/;
+  static constexpr int kSmem = kSmemBudget;
 };
 
 // GELU, tanh form (as GPT-2 / BERT implementations use):
@@ -68,6 +72,13 @@ __device__ __forceinline__ float dgelu_f(float x) {
   const float x2 = x * x;
   const float t = tanh_fast(kGeluK0 * fmaf(kGeluK1 * x, x2, x));
   return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * kGeluK0 * fmaf(3.0f * kGeluK1, x2, 1.0f);
+}
+
+// diagnostics: phase timestamps per CTA (GemmDesc::trace)
+__device__ __forceinline__ void trace_mark(const GemmParams& p, int slot) {
+  if (p.trace) {
+    p.trace[blockIdx.x * 16 + slot] = clock64();  // SM cycles (compare within one CTA)
+  }
 }
 
 __device__ __forceinline__ long long out_offset(const GemmParams& p, int z, int m, int n) {
@@ -252,19 +263,226 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int z, int r
   }
 }
 
+// ---------------------------------------------------------------- TMA epilogue
+// Per epilogue warp a smem region (p.epi_warp_bytes) holding two 32-row x
+// 32-column output chunk buffers (chunk g is staged while chunk g-1's bulk
+// store drains) and p.epi_nx chunk buffers of the extra tensor: the
+// residual / activation input (bulk-loaded as soon as the warp starts the
+// tile, so its DRAM latency hides under the mainloop) or the aux output
+// (bulk-stored with the output).
+//   bf16 chunk: 32 rows x 64 B, 64B-swizzled:  unit q of row r at r*64  + ((q ^ (r>>1 & 3)) << 4)
+//   fp32 chunk: 32 rows x 128 B, 128B-swizzled: unit q of row r at r*128 + ((q ^ (r & 7)) << 4)
+// so a warp's row-per-lane 16-byte accesses are bank-conflict free.  TMEM
+// loads are double buffered: chunk j+1 streams out of TMEM while chunk j is
+// processed.
+constexpr int kXBytes = 32 * 32 * 2;
+
+struct EpiTma {
+  uint8_t* region;  // this warp's region
+  uint64_t* xbar;   // this warp's input barriers (one per x buffer, then the bias slice's)
+  uint32_t seq;     // chunks processed by this warp
+  uint32_t xph;     // input barrier phase bits (bit kMaxNx: bias)
+};
+
+__device__ __forceinline__ bool epi_has_x_in(const GemmParams& p) { return (p.epi & (kResid | kDGelu | kDRelu)) != 0; }
+
+__device__ __forceinline__ void epi_coords(const GemmParams& p, int z, int m, int n, int (&c)[5]) {
+  c[0] = n % p.c_inner;
+  c[1] = m;
+  c[2] = n / p.c_inner;
+  c[3] = z % p.zdiv;
+  c[4] = z / p.zdiv;
+}
+
+__device__ __forceinline__ uint8_t* epi_xbuf(const GemmParams& p, const EpiTma& e, int b) {
+  return e.region + 2 * p.epi_out_bytes + b * kXBytes;
+}
+// bias slice of the current tile: after the output and x buffers
+__device__ __forceinline__ float* epi_bias(const GemmParams& p, const EpiTma& e) {
+  return reinterpret_cast<float*>(e.region + p.epi_warp_bytes - p.epi_tile_cols * 4);
+}
+
+// lane 0: bulk-load the extra input of the chunk at (row0, n0) into x buffer b
+__device__ __forceinline__ void epi_issue_x(const GemmParams& p, EpiTma& e, int b, int z, int row0, int n0) {
+  int c[5];
+  epi_coords(p, z, row0, n0, c);
+  ptx::mbar_arrive_expect_tx(&e.xbar[b], kXBytes);
+  ptx::tma_load_5d(epi_xbuf(p, e, b), &p.tma_x, &e.xbar[b], c[0], c[1], c[2], c[3], c[4]);
+}
+
+// Before the tile's accumulator is ready: prefetch up to epi_nx input chunks
+// of this warp (chunk j covers columns col0 + (half + 2 j) * 32).
+template <int kPerWarp>
+__device__ __forceinline__ void epi_tile_prefetch(const GemmParams& p, EpiTma& e, int z, int row0, int col0, int half) {
+  const uint32_t lane = ptx::lane_id();
+  const bool bias = (p.epi & kBias) != 0;
+  if (!epi_has_x_in(p) && !bias) return;
+  // the previous tile's generic reads of these buffers precede the new bulk loads
+  ptx::fence_proxy_async_smem();
+  __syncwarp();
+  if (lane != 0) return;
+  if (bias) {
+    const int cols = min(p.epi_tile_cols, p.N - col0);
+    const uint32_t bytes = static_cast<uint32_t>((cols * 4 + 15) & ~15);
+    ptx::mbar_arrive_expect_tx(&e.xbar[kMaxNx], bytes);
+    ptx::bulk_load(epi_bias(p, e), p.bias + col0, bytes, &e.xbar[kMaxNx]);
+  }
+  if (!epi_has_x_in(p)) return;
+#pragma unroll
+  for (int j = 0; j < kPerWarp; ++j) {
+    const int n0 = col0 + (half + 2 * j) * 32;
+    if (j < p.epi_nx && n0 < p.N) epi_issue_x(p, e, (e.seq + j) % p.epi_nx, z, row0, n0);
+  }
+}
+
+#define EPI_MARK(J, K) \
+  if (threadIdx.x == 128 && e.seq < 2 && (J) < 2) trace_mark(p, 8 + (J) * 4 + (K))
+
+template <int kPerWarp>
+__device__ __forceinline__ void epi_tile_tma(const GemmParams& p, EpiTma& e, uint32_t tbase, int z, int row0, int col0,
+                                             int half) {
+  const uint32_t lane = ptx::lane_id();
+  const uint32_t epi = p.epi;
+  const bool x_in = epi_has_x_in(p);
+  const uint32_t kind = epi & kOutMask;
+  const bool f32 = kind != kOutBf16;
+  if (epi & kBias) {
+    ptx::mbar_wait(&e.xbar[kMaxNx], (e.xph >> kMaxNx) & 1);
+    e.xph ^= 1u << kMaxNx;
+  }
+  const float* bias_s = epi_bias(p, e) - col0;  // indexed by global column
+#pragma unroll 1
+  for (int j = 0; j < kPerWarp; ++j) {
+    const int c = half + 2 * j;
+    const int n0 = col0 + c * 32;
+    uint32_t raw[32];
+    ptx::tmem_ld_32x32b_x32(tbase + c * 32, raw);
+    ptx::tmem_wait_ld();
+    EPI_MARK(j, 0);
+    if (n0 >= p.N) {  // chunk entirely right of the matrix (no load was issued for it)
+      ++e.seq;
+      continue;
+    }
+    const int ob = e.seq & 1;
+    const int xb = e.seq % p.epi_nx;
+    float v[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(raw[k]) * p.alpha;
+    if (epi & kBias) {  // smem broadcast reads (columns past N hold junk; they are clipped on store)
+      const float4* b4 = reinterpret_cast<const float4*>(bias_s + n0);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 bb = b4[q];
+        v[4 * q] += bb.x;
+        v[4 * q + 1] += bb.y;
+        v[4 * q + 2] += bb.z;
+        v[4 * q + 3] += bb.w;
+      }
+    }
+    uint8_t* xbuf = epi_xbuf(p, e, xb);
+    if (x_in) {
+      EPI_MARK(j, 2);
+      ptx::mbar_wait(&e.xbar[xb], (e.xph >> xb) & 1);
+      e.xph ^= 1u << xb;
+      EPI_MARK(j, 3);
+      float xv[32];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 r = *reinterpret_cast<const uint4*>(xbuf + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4));
+        unpack_bf16x8(r, xv + 8 * q);
+      }
+      // buffers are refilled only when a warp has more chunks than buffers
+      if (j + p.epi_nx < kPerWarp) {
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        const int n2 = col0 + (c + 2 * p.epi_nx) * 32;
+        if (lane == 0 && n2 < p.N) epi_issue_x(p, e, xb, z, row0, n2);
+      }
+      if (epi & kResid) {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) v[k] += xv[k];
+      } else if (epi & kDGelu) {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) v[k] *= dgelu_f(xv[k]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) v[k] *= xv[k] > 0.f ? 1.f : 0.f;
+      }
+    }
+    EPI_MARK(j, 1);
+    // output buffer ob (and the aux buffer) were last read by the bulk store two chunks ago
+    if (lane == 0) ptx::bulk_wait_read<1>();
+    __syncwarp();
+    if (epi & kAuxOut) {
+      uint8_t* abuf = epi_xbuf(p, e, ob);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 w;
+        uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          __nv_bfloat162 h = __floats2bfloat162_rn(v[8 * q + 2 * k], v[8 * q + 2 * k + 1]);
+          wp[k] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        *reinterpret_cast<uint4*>(abuf + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) = w;
+      }
+    }
+    if (epi & kGelu) {
+#pragma unroll
+      for (int k = 0; k < 32; ++k) v[k] = gelu_f(v[k]);
+    } else if (epi & kRelu) {
+#pragma unroll
+      for (int k = 0; k < 32; ++k) v[k] = fmaxf(v[k], 0.f);
+    }
+    uint8_t* obuf = e.region + ob * p.epi_out_bytes;
+    if (f32) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<float4*>(obuf + lane * 128 + ((q ^ (lane & 7)) << 4)) =
+            make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 w;
+        uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          __nv_bfloat162 h = __floats2bfloat162_rn(v[8 * q + 2 * k], v[8 * q + 2 * k + 1]);
+          wp[k] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        *reinterpret_cast<uint4*>(obuf + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) = w;
+      }
+    }
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      int cc[5];
+      epi_coords(p, z, row0, n0, cc);
+      if (kind == kOutF32Acc) ptx::tma_reduce_add_5d(&p.tma_c, obuf, cc[0], cc[1], cc[2], cc[3], cc[4]);
+      else ptx::tma_store_5d(&p.tma_c, obuf, cc[0], cc[1], cc[2], cc[3], cc[4]);
+      if (epi & kAuxOut) ptx::tma_store_5d(&p.tma_x, epi_xbuf(p, e, ob), cc[0], cc[1], cc[2], cc[3], cc[4]);
+      ptx::bulk_commit();
+    }
+    ++e.seq;
+  }
+}
+
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_constant__ GemmParams p) {
+  if (threadIdx.x == 0) trace_mark(p, 0);
   using C = Cfg<BN>;
-  constexpr int S = C::kStages;
+  const int S = p.stages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + S * C::kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes);
+  uint8_t* smem_epi = smem + S * C::kStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_epi + kEpiWarps * p.epi_warp_bytes);
   uint64_t* empty = full + S;
   uint64_t* tmem_full = empty + S;
   uint64_t* tmem_empty = tmem_full + 2;
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  uint64_t* xbar = tmem_empty + 2;  // kMaxNx per epilogue warp (TMA epilogue inputs)
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(xbar + kEpiBars * kEpiWarps);
 
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
@@ -280,6 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
       ptx::mbar_init(&tmem_full[a], 1);
       ptx::mbar_init(&tmem_empty[a], 32 * kEpiWarps);
     }
+    for (int i = 0; i < kEpiBars * kEpiWarps; ++i) ptx::mbar_init(&xbar[i], 1);
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc<C::kTmemCols>(tmem_base_slot);
@@ -290,6 +509,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
   // prologue done: wait for the producer kernel's writes, let the next kernel launch
   ptx::pdl_wait();
   ptx::pdl_trigger();
+  if (threadIdx.x == 0) trace_mark(p, 1);
 
   const int tiles_per_z = p.num_m_blocks * p.num_n_blocks;
 
@@ -298,6 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      const int first_tile = blockIdx.x;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
         const int ks = t % p.k_splits;
         const int tt = t / p.k_splits;
@@ -326,6 +547,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
             for (int j = 0; j < BN / 64; ++j)
               ptx::tma_load_3d(sb + j * 64 * kBK * 2, &p.tma_b, &full[stage], nb * BN + j * 64, kb * kBK, z);
           }
+          if (t == first_tile && kb == kb0) trace_mark(p, 2);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -358,6 +580,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
         for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
+          if (t == static_cast<int>(blockIdx.x) && kb == kb0) trace_mark(p, 3);
           const uint32_t sa = ptx::smem_addr(smem_a + stage * C::kABytes);
           const uint32_t sb = ptx::smem_addr(smem_b + stage * C::kBBytes);
 #pragma unroll
@@ -373,12 +596,41 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
           }
         }
         ptx::mma_commit(&tmem_full[acc]);
+        trace_mark(p, 4);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
         }
       }
     }
+  } else if (warp >= 4 && p.tma_epi) {
+    // ------------------------------------------------------------ TMA epilogue
+    const uint32_t quad = warp & 3;
+    const int half = (warp - 4) >> 2;
+    EpiTma e{smem_epi + (warp - 4) * p.epi_warp_bytes, xbar + kEpiBars * (warp - 4), 0, 0};
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      const int tt = t / p.k_splits;
+      const int z = tt / tiles_per_z;
+      const int r = tt % tiles_per_z;
+      const int mb = r % p.num_m_blocks;
+      const int nb = r / p.num_m_blocks;
+      const int row0 = mb * kBM + quad * 32;
+      epi_tile_prefetch<BN / 64>(p, e, z, row0, nb * BN, half);
+      ptx::mbar_wait(&tmem_full[acc], acc_phase);
+      ptx::tc_fence_after();
+      if (warp == 4 && ptx::lane_id() == 0 && t == static_cast<int>(blockIdx.x)) trace_mark(p, 5);
+      epi_tile_tma<BN / 64>(p, e, tmem_base + ((quad * 32) << 16) + acc * BN, z, row0, nb * BN, half);
+      ptx::tc_fence_before();
+      if (warp == 4 && ptx::lane_id() == 0) trace_mark(p, 6);
+      ptx::mbar_arrive(&tmem_empty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+    if (ptx::lane_id() == 0) ptx::bulk_wait<0>();
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const uint32_t quad = warp & 3;          // TMEM lane quadrant this warp may access
@@ -394,6 +646,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
       const int nb = r / p.num_m_blocks;
       ptx::mbar_wait(&tmem_full[acc], acc_phase);
       ptx::tc_fence_after();
+      if (warp == 4 && lane == 0 && t == static_cast<int>(blockIdx.x)) trace_mark(p, 5);
       const int row = mb * kBM + quad * 32 + lane;
       const uint32_t tbase = tmem_base + ((quad * 32) << 16) + acc * BN;
       if (half < kChunks) {
@@ -423,6 +676,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
         }
       }
       ptx::tc_fence_before();
+      if (warp == 4 && lane == 0) trace_mark(p, 6);
       ptx::mbar_arrive(&tmem_empty[acc]);
       if (++acc == 2) {
         acc = 0;
@@ -437,6 +691,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
     ptx::tc_fence_after();
     ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
   }
+  if (threadIdx.x == 0) trace_mark(p, 7);
 }
 
 
@@ -454,22 +709,24 @@ constexpr int kBN = 256;
 constexpr int kABytes = kBM * kBK * 2;        // 16 KB: this CTA's 128 rows of A
 constexpr int kBBytes = (kBN / 2) * kBK * 2;  // 16 KB: this CTA's half of B
 constexpr int kStageBytes = kABytes + kBBytes;
-constexpr int kStages = (kSmemBudget - 2048) / kStageBytes > 8 ? 8 : (kSmemBudget - 2048) / kStageBytes;
-constexpr int kSmem = 1024 + kStages * kStageBytes + 1024;
+constexpr int kSmem = kSmemBudget;
 }  // namespace pair
 
 __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __grid_constant__ GemmParams p) {
+  if (threadIdx.x == 0) trace_mark(p, 0);
   using namespace pair;
-  constexpr int S = kStages;
+  const int S = p.stages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + S * kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * kStageBytes);
+  uint8_t* smem_epi = smem + S * kStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_epi + kEpiWarps * p.epi_warp_bytes);
   uint64_t* empty = full + S;
   uint64_t* tmem_full = empty + S;
   uint64_t* tmem_empty = tmem_full + 2;
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  uint64_t* xbar = tmem_empty + 2;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(xbar + kEpiBars * kEpiWarps);
 
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
@@ -488,6 +745,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
       ptx::mbar_init(&tmem_full[a], 1);
       ptx::mbar_init(&tmem_empty[a], 2 * kEpiWarps);  // one arrive per epilogue warp of both CTAs
     }
+    for (int i = 0; i < kEpiBars * kEpiWarps; ++i) ptx::mbar_init(&xbar[i], 1);
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc_2sm<512>(tmem_base_slot);
@@ -497,12 +755,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
   const uint32_t tmem_base = *tmem_base_slot;
   ptx::pdl_wait();
   ptx::pdl_trigger();
+  if (threadIdx.x == 0) trace_mark(p, 1);
   const int tiles_per_z = p.num_m_blocks * p.num_n_blocks;
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      const int first_tile = pair_id;
       for (int t = pair_id; t < p.num_tiles; t += n_pairs) {
         const int ks = t % p.k_splits;
         const int tt = t / p.k_splits;
@@ -532,6 +792,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
 #pragma unroll
             for (int j = 0; j < 2; ++j) ptx::tma_load_3d_2sm(sb + j * 64 * kBK * 2, &p.tma_b, &full[stage], n0 + j * 64, kb * kBK, z);
           }
+          if (t == first_tile && kb == kb0) trace_mark(p, 2);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -560,6 +821,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
         for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
+          if (t == pair_id && kb == kb0) trace_mark(p, 3);
           const uint32_t sa = ptx::smem_addr(smem_a + stage * kABytes);
           const uint32_t sb = ptx::smem_addr(smem_b + stage * kBBytes);
 #pragma unroll
@@ -575,12 +837,44 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
           }
         }
         ptx::mma_commit_2sm(&tmem_full[acc]);
+        trace_mark(p, 4);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
         }
       }
     }
+  } else if (warp >= 4 && p.tma_epi) {
+    const uint32_t quad = warp & 3;
+    const int half = (warp - 4) >> 2;
+    EpiTma e{smem_epi + (warp - 4) * p.epi_warp_bytes, xbar + kEpiBars * (warp - 4), 0, 0};
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = pair_id; t < p.num_tiles; t += n_pairs) {
+      const int tt = t / p.k_splits;
+      const int z = tt / tiles_per_z;
+      const int r = tt % tiles_per_z;
+      const int mb = r % p.num_m_blocks;
+      const int nb = r / p.num_m_blocks;
+      const int row0 = mb * 256 + rank * 128 + quad * 32;
+      epi_tile_prefetch<kBN / 64>(p, e, z, row0, nb * kBN, half);
+      ptx::mbar_wait(&tmem_full[acc], acc_phase);
+      ptx::tc_fence_after();
+      if (warp == 4 && lane == 0 && t == pair_id) trace_mark(p, 5);
+      epi_tile_tma<kBN / 64>(p, e, tmem_base + ((quad * 32) << 16) + acc * kBN, z, row0, nb * kBN, half);
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (warp == 4 && lane == 0) trace_mark(p, 6);
+      if (lane == 0) {
+        if (leader) ptx::mbar_arrive(&tmem_empty[acc]);
+        else ptx::mbar_arrive_cluster(&tmem_empty[acc], 0);
+      }
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+    if (lane == 0) ptx::bulk_wait<0>();
   } else if (warp >= 4) {
     const uint32_t quad = warp & 3;
     const int half = (warp - 4) >> 2;
@@ -595,6 +889,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
       const int nb = r / p.num_m_blocks;
       ptx::mbar_wait(&tmem_full[acc], acc_phase);
       ptx::tc_fence_after();
+      if (warp == 4 && lane == 0 && t == pair_id) trace_mark(p, 5);
       const int row = mb * 256 + rank * 128 + quad * 32 + lane;
       const uint32_t tbase = tmem_base + ((quad * 32) << 16) + acc * kBN;
       uint32_t ra[32], rb[32];
@@ -621,6 +916,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
       }
       ptx::tc_fence_before();
       __syncwarp();
+      if (warp == 4 && lane == 0) trace_mark(p, 6);
       if (lane == 0) {
         if (leader) ptx::mbar_arrive(&tmem_empty[acc]);
         else ptx::mbar_arrive_cluster(&tmem_empty[acc], 0);
@@ -633,11 +929,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
   }
 
   ptx::tc_fence_before();
-  ptx::cluster_sync();
+  ptx::cluster_sync_relaxed();
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc_2sm<512>(tmem_base);
   }
+  if (threadIdx.x == 0) trace_mark(p, 7);
 }
 
 // ---------------------------------------------------------------- host side
@@ -675,6 +972,31 @@ CUtensorMap make_map(const void* base, long long inner, long long outer, long lo
                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (rc != CUDA_SUCCESS) throw std::runtime_error("dpl gemm: cuTensorMapEncodeTiled failed (" + std::to_string(rc) + ")");
+  return map;
+}
+
+// 5-D map over the epilogue addressing of C (gemm.h):
+//   [n % inner][m][n / inner][z % zdiv][z / zdiv], box 32 columns x 32 rows.
+// Size-1 dimensions get a consistent non-zero stride.
+CUtensorMap make_epi_map(const void* base, bool f32, const GemmDesc& d, int inner, int nhi) {
+  const long long esz = f32 ? 4 : 2;
+  const long long zhi = d.batch / d.zdiv;
+  const long long s1 = d.ldc;
+  const long long s2 = nhi > 1 ? d.s_no : s1 * d.M;
+  const long long s3 = d.zdiv > 1 ? d.s_zi : s2 * nhi;
+  const long long s4 = zhi > 1 ? d.s_zo : s3 * d.zdiv;
+  CUtensorMap map;
+  cuuint64_t dims[5] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(d.M), static_cast<cuuint64_t>(nhi),
+                        static_cast<cuuint64_t>(d.zdiv), static_cast<cuuint64_t>(zhi)};
+  cuuint64_t strides[4] = {static_cast<cuuint64_t>(s1 * esz), static_cast<cuuint64_t>(s2 * esz),
+                           static_cast<cuuint64_t>(s3 * esz), static_cast<cuuint64_t>(s4 * esz)};
+  cuuint32_t box[5] = {32, 32, 1, 1, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  const CUresult rc = encode_fn()(&map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5,
+                                  const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                  f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (rc != CUDA_SUCCESS) throw std::runtime_error("dpl gemm: epilogue tensor map failed (" + std::to_string(rc) + ")");
   return map;
 }
 
@@ -785,6 +1107,55 @@ void GemmOp::prepare(const GemmDesc& d) {
   const bool aux_aligned = !(d.aux_in || d.resid || d.aux_out) || ((d.ldc * 2) % 16 == 0 && (d.s_zo * 2) % 16 == 0 &&
                                                                    (d.s_zi * 2) % 16 == 0 && (d.s_no * 2) % 16 == 0);
   p.vec_ok = aligned && aux_aligned;
+  p.trace = d.trace;
+  // TMA epilogue: bulk tensor stores / fp32 reduce-adds from swizzled smem
+  // chunks, extra input bulk-loaded ahead of use (see EpiTma)
+  {
+    static const bool tma_enabled = [] {
+      const char* e = std::getenv("DPL_GEMM_TMA_EPI");
+      return !(e && e[0] == '0');
+    }();
+    const uint32_t kind = d.epi & kOutMask;
+    const bool x_in = (d.epi & (kResid | kDGelu | kDRelu)) != 0;
+    const bool two_in = (d.epi & kResid) && (d.epi & (kDGelu | kDRelu));
+    const bool aux = (d.epi & kAuxOut) != 0;
+    bool ok = tma_enabled && p.vec_ok && d.N >= 32 && d.batch % d.zdiv == 0 && (d.ndiv >= d.N || d.N % d.ndiv == 0) &&
+              !two_in && !(x_in && aux);
+    if (kind != kOutBf16 && (x_in || aux)) ok = false;
+    if ((d.epi & kBias) && (d.N % 4 != 0 || reinterpret_cast<uintptr_t>(d.bias) % 16 != 0)) ok = false;
+    const int stage_bytes = two_sm ? pair::kStageBytes : (kBM + bn) * kBK * 2;
+    const int ring = kSmemBudget - 2048;
+    p.stages = std::min(kMaxStages, ring / stage_bytes);
+    if (ok) {
+      // carve the staging out of the ring, keeping >= 4 stages
+      const int per_warp = (two_sm ? pair::kBN : bn) / 64;  // chunks per epilogue warp per tile
+      p.epi_out_bytes = kind == kOutBf16 ? 2048 : 4096;
+      p.epi_nx = x_in ? std::min(kMaxNx, per_warp) : (aux ? 2 : 1);
+      p.epi_tile_cols = two_sm ? pair::kBN : bn;
+      const int bias_bytes = (d.epi & kBias) ? p.epi_tile_cols * 4 : 0;
+      for (;;) {
+        // 1 KB multiple: every warp's chunk buffers stay swizzle-atom aligned
+        p.epi_warp_bytes = (2 * p.epi_out_bytes + (x_in || aux ? p.epi_nx * kXBytes : 0) + bias_bytes + 1023) & ~1023;
+        p.stages = std::min(kMaxStages, (ring - kEpiWarps * p.epi_warp_bytes) / stage_bytes);
+        if (p.stages >= 4 || !x_in || p.epi_nx <= 2) break;
+        p.epi_nx /= 2;
+      }
+      ok = p.stages >= 4;
+    }
+    if (!ok) {
+      p.epi_warp_bytes = 0;
+      p.stages = std::min(kMaxStages, ring / stage_bytes);
+    }
+    if (ok) {
+      const int inner = d.ndiv >= d.N ? d.N : d.ndiv;
+      const int nhi = d.N / inner;
+      p.c_inner = inner;
+      p.tma_c = make_epi_map(d.C, kind != kOutBf16, d, inner, nhi);
+      const void* x = x_in ? ((d.epi & kResid) ? d.resid : d.aux_in) : (aux ? d.aux_out : nullptr);
+      if (x) p.tma_x = make_epi_map(x, false, d, inner, nhi);
+      p.tma_epi = 1;
+    }
+  }
   bn_ = bn;
   grid_ = two_sm ? 2 * std::min(p.num_tiles, num_sms() / 2) : std::min(p.num_tiles, num_sms());
   if (two_sm) {
@@ -820,7 +1191,8 @@ const GemmOp& GemmCache::get(const GemmDesc& d) {
                          static_cast<long long>(reinterpret_cast<uintptr_t>(d.bias)),
                          static_cast<long long>(reinterpret_cast<uintptr_t>(d.aux_in)),
                          static_cast<long long>(reinterpret_cast<uintptr_t>(d.resid)),
-                         static_cast<long long>(reinterpret_cast<uintptr_t>(d.aux_out)), d.force_bn, d.force_1sm};
+                         static_cast<long long>(reinterpret_cast<uintptr_t>(d.aux_out)), d.force_bn, d.force_1sm,
+                         static_cast<long long>(reinterpret_cast<uintptr_t>(d.trace))};
   std::string key(reinterpret_cast<const char*>(f), sizeof f);
   uint32_t a;
   std::memcpy(&a, &d.alpha, 4);
