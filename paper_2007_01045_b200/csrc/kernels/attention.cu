@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -286,10 +287,14 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
 
 // ---------------------------------------------------------------- backward
 // One CTA per (z, 128-key tile j), looping over query tiles i:
-//   S  = Q_i K_j^T,  dP = dO_i V_j^T                      (TMEM, 128 x 128 each)
-//   P  = exp(scale*S - lse),  dS = P * (dP - D)           (softmax warps -> smem bf16)
-//   dV += P^T dO_i,  dK += dS^T Q_i                         (TMEM, accumulate over i)
-//   dQ_i = dS K_j  -> fp32 atomics into dq_acc[z][S][64]   (summed over the key tiles)
+//   MMA1(i):  S = Q_i K_j^T,  dP = dO_i V_j^T                (TMEM, 128 x 128 each)
+//   softmax:  P = exp(scale*S - lse),  dS = P * (dP - D)     (warps 4-11 -> smem bf16)
+//   MMA2(i):  dV += P^T dO_i,  dK += dS^T Q_i                 (TMEM, accumulate over i)
+//             dQ_i = dS K_j  -> fp32 atomics into dq_acc[z][S][64] (summed over the key tiles)
+// Software pipeline: P/dS are double buffered in smem and the MMA warp
+// issues MMA1(i+1) before MMA2(i), so the softmax of tile i+1 runs on the
+// CUDA cores while the tensor core does tile i's gradient MMAs; the dQ_i
+// drain follows softmax(i+1).
 // D = rowsum(dO * O) comes from attn_bwd_prep_kernel; dq_acc is turned into
 // bf16 by attn_bwd_dq_kernel.  dK, dV are written head-merged into dqkv.
 constexpr int kBwdThreads = 384;  // warps 4-11: two per TMEM lane quadrant
@@ -314,19 +319,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
   uint8_t* sV = sK + kTileBytes;              // 16 KB
   uint8_t* sQ = sV + kTileBytes;              // 2 x 16 KB
   uint8_t* sO = sQ + 2 * kTileBytes;          // 2 x 16 KB (dO)
-  uint8_t* sP = sO + 2 * kTileBytes;          // 32 KB (two 64-key halves)
-  uint8_t* sS = sP + 2 * kTileBytes;          // 32 KB (dS)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sS + 2 * kTileBytes);
+  uint8_t* sP = sO + 2 * kTileBytes;          // 2 buffers x 32 KB (two 64-key halves each)
+  uint8_t* sS = sP + 4 * kTileBytes;          // 2 buffers x 32 KB (dS)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sS + 4 * kTileBytes);
   uint64_t* kv_full = bars;
   uint64_t* qdo_full = bars + 1;   // [2]
   uint64_t* qdo_empty = bars + 3;  // [2]
   uint64_t* sp_full = bars + 5;
   uint64_t* sp_empty = bars + 6;
-  uint64_t* pds_full = bars + 7;
-  uint64_t* pds_empty = bars + 8;
-  uint64_t* dq_full = bars + 9;
-  uint64_t* dq_empty = bars + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* pds_full = bars + 7;   // [2]
+  uint64_t* pds_empty = bars + 9;  // [2]
+  uint64_t* dq_full = bars + 11;
+  uint64_t* dq_empty = bars + 12;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
 
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
   const int j = blockIdx.x, z = blockIdx.y;
@@ -344,11 +349,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&qdo_full[i], 1);
       ptx::mbar_init(&qdo_empty[i], 1);
+      ptx::mbar_init(&pds_full[i], 256);
+      ptx::mbar_init(&pds_empty[i], 1);
     }
     ptx::mbar_init(sp_full, 1);
     ptx::mbar_init(sp_empty, 256);
-    ptx::mbar_init(pds_full, 256);
-    ptx::mbar_init(pds_empty, 1);
     ptx::mbar_init(dq_full, 1);
     ptx::mbar_init(dq_empty, 256);
     ptx::fence_barrier_init();
@@ -379,9 +384,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
       const uint32_t id_tt = ptx::idesc_bf16_f32(kT, kD, true, true);    // dV, dK: A^T, B MN-major
       const uint32_t id_dq = ptx::idesc_bf16_f32(kT, kD, false, true);   // dQ: dS K-major, K MN-major
       const uint32_t ak = ptx::smem_addr(sK), av = ptx::smem_addr(sV);
-      const uint32_t ap = ptx::smem_addr(sP), as = ptx::smem_addr(sS);
-      ptx::mbar_wait(kv_full, 0);
-      for (int it = 0; it < n_iter; ++it) {
+      // MMA1(it): S / dP of query tile it into TMEM (single buffer, freed by the softmax warps)
+      auto mma1 = [&](int it) {
         const int st = it & 1;
         const uint32_t aq = ptx::smem_addr(sQ + st * kTileBytes), ao = ptx::smem_addr(sO + st * kTileBytes);
         ptx::mbar_wait(&qdo_full[st], (it >> 1) & 1);
@@ -395,8 +399,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
                         ptx::smem_desc_sw128(av + k * 32, 16, 1024), id_sq, k > 0);
         }
         ptx::mma_commit(sp_full);
-        ptx::mbar_wait(pds_full, it & 1);
-        ptx::mbar_wait(dq_empty, (it & 1) ^ 1);
+      };
+      ptx::mbar_wait(kv_full, 0);
+      if (n_iter > 0) mma1(0);
+      for (int it = 0; it < n_iter; ++it) {
+        const int st = it & 1, b = it & 1;
+        const uint32_t aq = ptx::smem_addr(sQ + st * kTileBytes), ao = ptx::smem_addr(sO + st * kTileBytes);
+        const uint32_t ap = ptx::smem_addr(sP + b * 2 * kTileBytes), as = ptx::smem_addr(sS + b * 2 * kTileBytes);
+        ptx::mbar_wait(&pds_full[b], (it >> 1) & 1);  // softmax(it) wrote P / dS (and read S / dP)
+        if (it + 1 < n_iter) mma1(it + 1);            // next tile's scores overlap this tile's gradients
+        ptx::mbar_wait(dq_empty, (it & 1) ^ 1);       // dQ(it-1) drained
         ptx::tc_fence_after();
 #pragma unroll
         for (int k = 0; k < kT / 16; ++k) {
@@ -411,7 +423,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
                         ptx::smem_desc_sw128(ak + row_step, 16, 1024), id_dq, k > 0);
         }
         ptx::mma_commit(&qdo_empty[st]);
-        ptx::mma_commit(pds_empty);
+        ptx::mma_commit(&pds_empty[b]);
         ptx::mma_commit(dq_full);
       }
     }
@@ -421,30 +433,56 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
     const int r = quad * 32 + lane;
     const uint32_t trow = (quad * 32) << 16;
     const int b = z % p.B, h = z / p.B;
+    // dQ partial of query tile `it` (this key tile's share) -> fp32 atomics
+    auto drain_dq = [&](int it) {
+      const int q = (i_first + it) * kT + r;
+      ptx::mbar_wait(dq_full, it & 1);
+      ptx::tc_fence_after();
+      float4* dst = reinterpret_cast<float4*>(p.dq_acc + (static_cast<long long>(z) * p.S + q) * kD);
+      const int c = half;  // 32 of the 64 dQ columns
+      uint32_t v[32];
+      ptx::tmem_ld_32x32b_x32(tmem + trow + 384 + c * 32, v);
+      ptx::tmem_wait_ld();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(dq_empty);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        atomicAdd(dst + c * 8 + u, make_float4(__uint_as_float(v[4 * u]), __uint_as_float(v[4 * u + 1]),
+                                               __uint_as_float(v[4 * u + 2]), __uint_as_float(v[4 * u + 3])));
+    };
     for (int it = 0; it < n_iter; ++it) {
       const int i = i_first + it, q = i * kT + r;
+      const int pb = it & 1;
       const float lse2 = p.lse[static_cast<long long>(z) * p.S + q] * 1.4426950408889634f;
       const float dsum = p.dsum[static_cast<long long>(z) * p.S + q];
       const bool diag = p.causal && i == j;
       ptx::mbar_wait(sp_full, it & 1);
       ptx::tc_fence_after();
-      ptx::mbar_wait(pds_empty, (it & 1) ^ 1);  // previous P / dS consumed by the MMAs
-#pragma unroll 1
-      for (int c = 2 * half; c < 2 * half + 2; ++c) {
-        uint32_t vs[32], vp[32];
-        ptx::tmem_ld_32x32b_x32(tmem + trow + c * 32, vs);
-        ptx::tmem_ld_32x32b_x32(tmem + trow + 128 + c * 32, vp);
-        ptx::tmem_wait_ld();
+      uint32_t vs[2][32], vp[2][32];
+      ptx::tmem_ld_32x32b_x32(tmem + trow + (2 * half) * 32, vs[0]);
+      ptx::tmem_ld_32x32b_x32(tmem + trow + 128 + (2 * half) * 32, vp[0]);
+      ptx::tmem_ld_32x32b_x32(tmem + trow + (2 * half + 1) * 32, vs[1]);
+      ptx::tmem_ld_32x32b_x32(tmem + trow + 128 + (2 * half + 1) * 32, vp[1]);
+      ptx::tmem_wait_ld();
+      // S / dP are in registers: MMA1(it+1) may overwrite them
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(sp_empty);
+      ptx::mbar_wait(&pds_empty[pb], ((it >> 1) & 1) ^ 1);  // MMA2(it-2) done with this P / dS buffer
+      uint8_t* hp0 = sP + pb * 2 * kTileBytes;
+      uint8_t* hs0 = sS + pb * 2 * kTileBytes;
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        const int c = 2 * half + cc;
         float pv[32], dv[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
           const bool masked = diag && (k0 + c * 32 + e > q);
-          const float pe = masked ? 0.f : exp2_fast(__uint_as_float(vs[e]) * p.scale_log2 - lse2);
+          const float pe = masked ? 0.f : exp2_fast(__uint_as_float(vs[cc][e]) * p.scale_log2 - lse2);
           pv[e] = pe;
-          dv[e] = pe * (__uint_as_float(vp[e]) - dsum);
+          dv[e] = pe * (__uint_as_float(vp[cc][e]) - dsum);
         }
-        uint8_t* hp = sP + (c >> 1) * kTileBytes;
-        uint8_t* hs = sS + (c >> 1) * kTileBytes;
+        uint8_t* hp = hp0 + (c >> 1) * kTileBytes;
+        uint8_t* hs = hs0 + (c >> 1) * kTileBytes;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int chunk = (c & 1) * 4 + u;
@@ -461,31 +499,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
           *reinterpret_cast<uint4*>(hs + sw128(r, chunk)) = w;
         }
       }
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(sp_empty);
       fence_async_smem();
-      ptx::mbar_arrive(pds_full);
-      // dQ_i partial of this key tile -> fp32 atomics
-      ptx::mbar_wait(dq_full, it & 1);
-      ptx::tc_fence_after();
-      float4* dst = reinterpret_cast<float4*>(p.dq_acc + (static_cast<long long>(z) * p.S + q) * kD);
-      {
-        const int c = half;  // 32 of the 64 dQ columns
-        uint32_t v[32];
-        ptx::tmem_ld_32x32b_x32(tmem + trow + 384 + c * 32, v);
-        ptx::tmem_wait_ld();
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          atomicAdd(dst + c * 8 + u, make_float4(__uint_as_float(v[4 * u]), __uint_as_float(v[4 * u + 1]),
-                                                 __uint_as_float(v[4 * u + 2]), __uint_as_float(v[4 * u + 3])));
-      }
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(dq_empty);
+      ptx::mbar_arrive(&pds_full[pb]);
+      if (it > 0) drain_dq(it - 1);
     }
+    if (n_iter > 0) drain_dq(n_iter - 1);
     // dV, dK of this key tile (all MMAs done once the last dQ arrived)
-    if (n_iter == 0) {
-      // causal tile with no queries: cannot happen (i_first = j < n_q)
-    }
     const int key = k0 + r;
     __nv_bfloat16* row = p.dqkv + static_cast<long long>(b * p.S + key) * p.ld + h * kD;
     {
@@ -560,7 +579,7 @@ __global__ void attn_bwd_dq_kernel(const float* __restrict__ dq_acc, __nv_bfloat
   }
 }
 
-constexpr int kBwdSmem = 1024 + 10 * kTileBytes + 256;
+constexpr int kBwdSmem = 1024 + 14 * kTileBytes + 256;
 
 PFN_cuTensorMapEncodeTiled_v12000 encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
