@@ -538,44 +538,51 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
   }
 }
 
-// D[z][q] = sum_j dO[z][q][j] * O[b*S+q][h*64+j]; zeroes dq_acc.  One warp
-// per row, 8 lanes x 8 elements.
+// D[z][q] = sum_j dO[z][q][j] * O[b*S+q][h*64+j]; zeroes dq_acc.  Four rows
+// per warp: 8 lanes x 8 elements (16-byte loads) per row, 16-byte zero stores.
 __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ dout, const __nv_bfloat16* __restrict__ out,
                                      long long ldo, float* __restrict__ dsum, float* __restrict__ dq_acc, int S, int B,
                                      int rows) {
   ptx::pdl_wait();
-  const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
-  for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < rows; row += gridDim.x * warps) {
+  const int lane = threadIdx.x & 31, sub = lane >> 3, l8 = lane & 7;
+  const int groups = (blockDim.x >> 5) * 4;
+  for (int row = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 4 + sub; row < rows;
+       row += gridDim.x * groups) {
     const int z = row / S, q = row % S, b = z % B, h = z / B;
+    const uint4 a = reinterpret_cast<const uint4*>(dout + static_cast<long long>(row) * kD)[l8];
+    const uint4 c = reinterpret_cast<const uint4*>(out + static_cast<long long>(b * S + q) * ldo + h * kD)[l8];
+    const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
+    const __nv_bfloat162* pc = reinterpret_cast<const __nv_bfloat162*>(&c);
     float acc = 0.f;
-    if (lane < 8) {
-      const uint4 a = reinterpret_cast<const uint4*>(dout + static_cast<long long>(row) * kD)[lane];
-      const uint4 c = reinterpret_cast<const uint4*>(out + static_cast<long long>(b * S + q) * ldo + h * kD)[lane];
-      const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
-      const __nv_bfloat162* pc = reinterpret_cast<const __nv_bfloat162*>(&c);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 x = __bfloat1622float2(pa[e]), y = __bfloat1622float2(pc[e]);
-        acc += x.x * y.x + x.y * y.y;
-      }
+    for (int e = 0; e < 4; ++e) {
+      const float2 x = __bfloat1622float2(pa[e]), y = __bfloat1622float2(pc[e]);
+      acc += x.x * y.x + x.y * y.y;
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) dsum[row] = acc;
-    reinterpret_cast<float2*>(dq_acc + static_cast<long long>(row) * kD)[lane] = make_float2(0.f, 0.f);
+    for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (l8 == 0) dsum[row] = acc;
+    float4* zq = reinterpret_cast<float4*>(dq_acc + static_cast<long long>(row) * kD);
+    zq[2 * l8] = make_float4(0.f, 0.f, 0.f, 0.f);
+    zq[2 * l8 + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
 }
 
-// dqkv[b*S+q][h*64+j] = bf16(scale * dq_acc[z][q][j])
+// dqkv[b*S+q][h*64+j] = bf16(scale * dq_acc[z][q][j]); two rows per warp,
+// 16 lanes x 4 floats per row
 __global__ void attn_bwd_dq_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv, long long ld,
                                    float scale, int S, int B, int rows) {
   ptx::pdl_wait();
-  const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
-  for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < rows; row += gridDim.x * warps) {
+  const int lane = threadIdx.x & 31, sub = lane >> 4, l16 = lane & 15;
+  const int groups = (blockDim.x >> 5) * 2;
+  for (int row = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 2 + sub; row < rows;
+       row += gridDim.x * groups) {
     const int z = row / S, q = row % S, b = z % B, h = z / B;
-    const float2 v = reinterpret_cast<const float2*>(dq_acc + static_cast<long long>(row) * kD)[lane];
-    reinterpret_cast<uint32_t*>(dqkv + static_cast<long long>(b * S + q) * ld + h * kD)[lane] =
-        pack_bf16(scale * v.x, scale * v.y);
+    const float4 v = reinterpret_cast<const float4*>(dq_acc + static_cast<long long>(row) * kD)[l16];
+    uint2 w;
+    w.x = pack_bf16(scale * v.x, scale * v.y);
+    w.y = pack_bf16(scale * v.z, scale * v.w);
+    reinterpret_cast<uint2*>(dqkv + static_cast<long long>(b * S + q) * ld + h * kD)[l16] = w;
   }
 }
 
@@ -650,7 +657,8 @@ void AttentionOp::backward(cudaStream_t s) const {
   const float scale = 1.0f / std::sqrt(static_cast<float>(kD));
   count_launch(3);
   TimedLaunch timed_("attention_bwd", s, 10.0 * z_count * desc_.seq * desc_.seq * kD / (desc_.causal ? 2 : 1));
-  launch_pdl(attn_bwd_prep_kernel, dim3(std::min((rows + 7) / 8, 148 * 16)), dim3(256), 0, s,
+  // rows = z * S is a multiple of 4 (S % 128 == 0): a warp's four rows are all valid or all past the end
+  launch_pdl(attn_bwd_prep_kernel, dim3(std::min((rows + 31) / 32, 148 * 16)), dim3(256), 0, s,
              static_cast<const __nv_bfloat16*>(desc_.dout), static_cast<const __nv_bfloat16*>(desc_.ctx), desc_.ldc,
              desc_.dsum, desc_.dq_acc, desc_.seq, desc_.samples, rows);
   AttnBwdParams p;
@@ -670,7 +678,7 @@ void AttentionOp::backward(cudaStream_t s) const {
   p.ld = 3LL * desc_.heads * kD;
   p.H = desc_.heads * kD;
   launch_pdl(attn_bwd_kernel, dim3(desc_.seq / kT, z_count), dim3(kBwdThreads), kBwdSmem, s, p);
-  launch_pdl(attn_bwd_dq_kernel, dim3(std::min((rows + 7) / 8, 148 * 16)), dim3(256), 0, s,
+  launch_pdl(attn_bwd_dq_kernel, dim3(std::min((rows + 15) / 16, 148 * 16)), dim3(256), 0, s,
              static_cast<const float*>(desc_.dq_acc), p.dqkv, p.ld, scale, desc_.seq, desc_.samples, rows);
 }
 

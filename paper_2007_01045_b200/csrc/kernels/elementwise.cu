@@ -284,17 +284,29 @@ __global__ void __launch_bounds__(256, 4)
   }
 }
 
-// dst_k[c] += sum_b ws[b][k][c] for each of the nred column reductions
-__global__ void ln_param_reduce_kernel(const float* __restrict__ ws, float* d0, float* d1, float* d2, float* d3,
-                                       int blocks, int nred, int h) {
+// dst_k[c] += sum_b ws[b][k][c] for each of the nred column reductions.
+// Block: 32 columns x 8 slab groups; each thread sums every 8th slab (loads
+// independent, so they overlap), then the 8 groups meet in smem.
+__global__ void __launch_bounds__(256) ln_param_reduce_kernel(const float* __restrict__ ws, float* d0, float* d1,
+                                                              float* d2, float* d3, int blocks, int nred, int h) {
   ptx::pdl_wait();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nred * h) return;
+  __shared__ float part[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + tx;  // (k, c) flattened
   float s = 0.f;
-  for (int b = 0; b < blocks; ++b) s += ws[static_cast<long long>(b) * nred * h + i];
-  const int k = i / h, c = i % h;
-  float* d = k == 0 ? d0 : k == 1 ? d1 : k == 2 ? d2 : d3;
-  d[c] += s;
+  if (i < nred * h) {
+#pragma unroll 4
+    for (int b = ty; b < blocks; b += 8) s += ws[static_cast<long long>(b) * nred * h + i];
+  }
+  part[ty][tx] = s;
+  __syncthreads();
+  if (ty == 0 && i < nred * h) {
+#pragma unroll
+    for (int y = 1; y < 8; ++y) s += part[y][tx];
+    const int k = i / h, c = i % h;
+    float* d = k == 0 ? d0 : k == 1 ? d1 : k == 2 ? d2 : d3;
+    d[c] += s;
+  }
 }
 
 // ------------------------------------------------------------ softmax
@@ -579,8 +591,8 @@ void layernorm_bwd(const void* dy, const void* x, const float* mean, const float
   if (nred == 2) launch_pdl(ln_bwd_cols_kernel<2>, dim3(cg), dim3(256), 0, s, pdy, px, mean, rstd, pr, pdx, ws, rows, h);
   else if (nred == 3) launch_pdl(ln_bwd_cols_kernel<3>, dim3(cg), dim3(256), 0, s, pdy, px, mean, rstd, pr, pdx, ws, rows, h);
   else launch_pdl(ln_bwd_cols_kernel<4>, dim3(cg), dim3(256), 0, s, pdy, px, mean, rstd, pr, pdx, ws, rows, h);
-  launch_pdl(ln_param_reduce_kernel, dim3((nred * h + 255) / 256), dim3(256), 0, s, ws, dgamma, dbeta, dresid_colsum, dx_colsum, slabs,
-                                                                nred, h);
+  launch_pdl(ln_param_reduce_kernel, dim3((nred * h + 31) / 32), dim3(256), 0, s, ws, dgamma, dbeta, dresid_colsum,
+             dx_colsum, slabs, nred, h);
 }
 
 void softmax_fwd(const float* s, void* p, int rows, int len, int q_len, int causal, cudaStream_t st) {

@@ -1,4 +1,4 @@
-"""Runs one GEMM shape a few times (for ncu): python tools/gemm_one.py o|wgrad_gpt|ffn1 [--cublas]"""
+"""Runs one GEMM shape a few times (for ncu): python tools/gemm_one.py o|ffn1|ffn2|wgrad_gpt [--cublas]"""
 import sys
 
 import torch
@@ -12,6 +12,13 @@ which = sys.argv[1]
 cub = "--cublas" in sys.argv
 if which == "o":
     M, N, Kd = 4096, 1024, 1024
+    A = torch.randn(M, Kd, device=dev).to(bf); B = torch.randn(N, Kd, device=dev).to(bf)
+    C = torch.empty(M, N, device=dev, dtype=bf); R = torch.randn(M, N, device=dev).to(bf)
+    bias = torch.zeros(N, device=dev)
+    f = (lambda: torch.matmul(A, B.T, out=C)) if cub else \
+        (lambda: K.gemm(A, B, C, M, N, Kd, lda=Kd, ldb=Kd, ldc=N, epi=K.EPI_BIAS | K.EPI_RESID, bias=bias, resid=R))
+elif which == "ffn2":
+    M, N, Kd = 4096, 1024, 4096
     A = torch.randn(M, Kd, device=dev).to(bf); B = torch.randn(N, Kd, device=dev).to(bf)
     C = torch.empty(M, N, device=dev, dtype=bf); R = torch.randn(M, N, device=dev).to(bf)
     bias = torch.zeros(N, device=dev)
