@@ -120,6 +120,15 @@ int dpl_k_embed_fwd(const int* tok, const void* wte, const void* wpe, void* x, i
 int dpl_k_embed_bwd(const int* tok, const void* dx, float* gwte, float* gwpe, int rows, int seq, int h, void* stream);
 int dpl_k_cross_entropy(void* logits, const int* tgt, float* loss_acc, int rows, int vocab, float grad_scale,
                         void* stream);
+/* VGG convolution support (config C3; NHWC bf16, 3x3 stride-1 pad-1 convs as
+ * GEMMs over columns col[(n*H+h)*W+w][(kh*3+kw)*C+c], row length kp >= 9C):
+ * im2col / col2im (gather), 2x2 max pool and its backward fused with ReLU',
+ * ReLU' alone. */
+int dpl_k_im2col3x3(const void* x, void* col, int n, int h, int w, int c, int kp, void* stream);
+int dpl_k_col2im3x3(const void* dcol, void* dx, int n, int h, int w, int c, int kp, void* stream);
+int dpl_k_maxpool2_fwd(const void* x, void* y, int n, int h, int w, int c, void* stream);
+int dpl_k_maxpool2_relu_bwd(const void* x, const void* dy, void* dz, int n, int h, int w, int c, void* stream);
+int dpl_k_relu_bwd(const void* y, const void* dy, void* dz, long long n, void* stream);
 int dpl_k_fill_uniform_bf16(void* dst, long long n, uint64_t seed, uint64_t tensor, long long idx0, float scale,
                             void* stream);
 int dpl_k_fill_uniform_f32(float* dst, long long n, uint64_t seed, uint64_t tensor, long long idx0, float scale,

@@ -93,22 +93,62 @@ class Model:
     causal: bool = False
     eps: float = 1e-5
     vocab: int = 0  # > 0: GPT language model (token ids in, causal-LM cross-entropy out)
+    # VGG-19 (kind "vgg"): image x image x 3 NHWC, conv widths width x {1,2,4,8,8}, FC fc, fc, classes
+    image: int = 224
+    width: int = 64
+    fc: int = 4096
+    classes: int = 1000
 
     @staticmethod
     def from_dict(d: dict) -> "Model":
-        m = Model(kind=d["kind"], layers=d["layers"], hidden=d["hidden"], heads=d.get("heads", 16),
-                  ffn=d.get("ffn", 4 * d["hidden"]), seq=d.get("seq", 1), causal=d.get("causal", False),
-                  vocab=d.get("vocab", 0))
+        m = Model(kind=d["kind"], layers=d["layers"], hidden=d.get("hidden", 8), heads=d.get("heads", 16),
+                  ffn=d.get("ffn", 4 * d.get("hidden", 8)), seq=d.get("seq", 1), causal=d.get("causal", False),
+                  vocab=d.get("vocab", 0), image=d.get("image", 224), width=d.get("width", 64),
+                  fc=d.get("fc", 4096), classes=d.get("classes", 1000))
         if m.kind == "mlp":
             m.seq = 1
         if m.kind == "gpt":
             m.causal = True
+        if m.kind == "vgg":
+            m.seq, m.hidden = 1, m.classes
         return m
+
+
+def vgg_layer(model: Model, l: int) -> dict:
+    """Shape of VGG profile layer l (csrc/runtime/layers.cu vgg_layer)."""
+    hw, cin, idx = model.image, 3, 0
+    for g, (convs, mult) in enumerate(zip((2, 2, 4, 4, 4), (1, 2, 4, 8, 8))):
+        for c in range(convs):
+            cout = model.width * mult
+            if idx == l:
+                return dict(conv=True, h=hw, w=hw, cin=cin, cout=cout, kp=(9 * cin + 7) // 8 * 8, pool=c == convs - 1)
+            cin, idx = cout, idx + 1
+        hw //= 2
+    fins, fouts = (hw * hw * cin, model.fc, model.fc), (model.fc, model.fc, model.classes)
+    return dict(conv=False, fin=fins[l - 16], fout=fouts[l - 16], relu=l != 18)
+
+
+def elems_per_sample(model: Model, l: int) -> int:
+    if model.kind != "vgg":
+        return model.seq * model.hidden
+    if l >= model.layers:
+        return model.classes
+    v = vgg_layer(model, l)
+    return v["h"] * v["w"] * v["cin"] if v["conv"] else v["fin"]
 
 
 def init_layer(model: Model, layer: int, seed: int) -> dict:
     """Parameters of one layer exactly as the device initialises them
     (csrc/runtime/layers.cu bind())."""
+    if model.kind == "vgg":
+        v = vgg_layer(model, layer)
+        if v["conv"]:
+            n = v["cout"] * v["kp"]
+            return {"W": _u(seed, _tid(layer, 0), n, np.sqrt(np.float32(6.0) / np.float32(9 * v["cin"]))).reshape(
+                        v["cout"], v["kp"]), "b": _u(seed, _tid(layer, 1), v["cout"], 0.05)}
+        n = v["fout"] * v["fin"]
+        return {"W": _u(seed, _tid(layer, 0), n, np.sqrt(np.float32(6.0) / np.float32(v["fin"]))).reshape(
+                    v["fout"], v["fin"]), "b": _u(seed, _tid(layer, 1), v["fout"], 0.05)}
     H, F = model.hidden, model.ffn
     if model.kind == "mlp":
         return {"W": _u(seed, _tid(layer, 0), H * H, np.sqrt(np.float32(6.0) / np.float32(H))).reshape(H, H),
@@ -122,6 +162,91 @@ def init_layer(model: Model, layer: int, seed: int) -> dict:
             "ln2_g": np.ones(H, np.float32), "ln2_b": np.zeros(H, np.float32),
             "W1": _u(seed, _tid(layer, 8), F * H, sh).reshape(F, H), "b1": _u(seed, _tid(layer, 9), F, 0.02),
             "W2": _u(seed, _tid(layer, 10), H * F, sf).reshape(H, F), "b2": _u(seed, _tid(layer, 11), H, 0.02)}
+
+
+def vgg_batch(model: Model, seed: int, sample0: int, samples: int):
+    """Images (NHWC, flattened per sample, U(-1,1) keyed by the element index)
+    and class labels (splitmix64 of the sample index mod classes)."""
+    e = elems_per_sample(model, 0)
+    idx = np.arange(samples * e, dtype=np.uint64) + np.uint64(sample0 * e)
+    x = hash_uniform(seed, 1, idx).reshape(samples, e)
+    lab = (mix64(seed, 2, np.arange(samples, dtype=np.uint64) + np.uint64(sample0)) >> np.uint64(32)) % np.uint64(
+        model.classes)
+    return x, lab.astype(np.int64)
+
+
+def _im2col(x, n, h, w, c, kp):
+    xp = np.zeros((n, h + 2, w + 2, c), x.dtype)
+    xp[:, 1:-1, 1:-1, :] = x.reshape(n, h, w, c)
+    col = np.zeros((n, h, w, kp), x.dtype)
+    for kh in range(3):
+        for kw in range(3):
+            col[..., (kh * 3 + kw) * c:(kh * 3 + kw + 1) * c] = xp[:, kh:kh + h, kw:kw + w, :]
+    return col.reshape(n * h * w, kp)
+
+
+def _col2im(dcol, n, h, w, c):
+    d = dcol.reshape(n, h, w, -1)
+    dxp = np.zeros((n, h + 2, w + 2, c), dcol.dtype)
+    for kh in range(3):
+        for kw in range(3):
+            dxp[:, kh:kh + h, kw:kw + w, :] += d[..., (kh * 3 + kw) * c:(kh * 3 + kw + 1) * c]
+    return dxp[:, 1:-1, 1:-1, :].reshape(n, h * w * c)
+
+
+def _pool_argmax(yr, n, h, w, c):
+    """First maximum of each 2x2 window in row-major window order."""
+    win = yr.reshape(n, h // 2, 2, w // 2, 2, c).transpose(0, 1, 3, 5, 2, 4).reshape(n, h // 2, w // 2, c, 4)
+    return win.max(-1), win.argmax(-1)
+
+
+def vgg_forward(model: Model, l: int, p: dict, x, n: int, q):
+    v = vgg_layer(model, l)
+    if v["conv"]:
+        col = _im2col(x, n, v["h"], v["w"], v["cin"], v["kp"])
+        yr = q(np.maximum(col @ q(p["W"]).T + p["b"], 0))
+        if not v["pool"]:
+            return yr.reshape(n, -1), (x, yr)
+        y, _ = _pool_argmax(yr, n, v["h"], v["w"], v["cout"])
+        return y.reshape(n, -1), (x, yr)
+    z = x @ q(p["W"]).T + p["b"]
+    y = q(np.maximum(z, 0) if v["relu"] else z)
+    return y, (x, y)
+
+
+def vgg_backward(model: Model, l: int, p: dict, cache, dy, n: int, need_dx: bool, q):
+    v = vgg_layer(model, l)
+    x, y = cache
+    if v["conv"]:
+        h, w, c, co = v["h"], v["w"], v["cin"], v["cout"]
+        if v["pool"]:
+            _, arg = _pool_argmax(y, n, h, w, co)
+            g = dy.reshape(n, h // 2, w // 2, co)
+            win = y.reshape(n, h // 2, 2, w // 2, 2, co).transpose(0, 1, 3, 5, 2, 4).reshape(n, h // 2, w // 2, co, 4)
+            mask = (np.arange(4) == arg[..., None]) & (win > 0)
+            dzw = mask * g[..., None]
+            dz = dzw.reshape(n, h // 2, w // 2, co, 2, 2).transpose(0, 1, 4, 2, 5, 3).reshape(n * h * w, co)
+        else:
+            dz = dy.reshape(n * h * w, co) * (y > 0)
+        col = _im2col(x, n, h, w, c, v["kp"])
+        g = {"W": dz.T @ col, "b": dz.sum(0)}
+        dx = q(_col2im(q(dz @ q(p["W"])), n, h, w, c)) if need_dx else None
+        return dx, g
+    dz = dy * (y > 0) if v["relu"] else dy
+    g = {"W": dz.T @ x, "b": dz.sum(0)}
+    return (q(dz @ q(p["W"])) if need_dx else None), g
+
+
+def class_ce(logits, labels, scale, q):
+    """sum over rows of CE and q((softmax - onehot) * scale), as lm.cu computes it."""
+    m = logits.max(-1, keepdims=True)
+    e = np.exp(logits - m)
+    ssum = e.sum(-1, keepdims=True)
+    rows = np.arange(logits.shape[0])
+    loss = float((np.log(ssum[:, 0]) + m[:, 0] - logits[rows, labels]).sum())
+    d = e / ssum
+    d[rows, labels] -= 1.0
+    return loss, q(d * scale)
 
 
 def batch_data(model: Model, seed: int, sample0: int, samples: int):
@@ -231,6 +356,8 @@ def _ln_bwd(dy, g, cache):
 def layer_forward(model: Model, layer: int, p: dict, x: np.ndarray, samples: int, q=_ident):
     """Returns (y, cache).  x: [samples * seq, H] rows.  q rounds the tensors
     the device stores in bf16 (identity in the exact mode)."""
+    if model.kind == "vgg":
+        return vgg_forward(model, layer, p, x, samples, q)
     p = _gemm_weights(p, q)
     if model.kind == "mlp":
         z = x @ p["W"].T + p["b"]
@@ -266,6 +393,8 @@ def layer_backward(model: Model, layer: int, p: dict, cache, dy: np.ndarray, sam
     """MLP layers take / return the gradient w.r.t. the pre-activation
     (layers.h gradient contract); transformer blocks w.r.t. the block
     output / input."""
+    if model.kind == "vgg":
+        return vgg_backward(model, layer, p, cache, dy, samples, need_dx, q)
     p = _gemm_weights(p, q)
     if model.kind == "mlp":
         (x,) = cache
@@ -328,6 +457,9 @@ def full_batch_step(model, gbs: int, seed: int = 1234, lr: float = 1e-3, dtype=n
         lmp = {k: v.astype(dtype) for k, v in init_lm(model, seed).items()}
         tok, tgt = lm_tokens(model, seed, 0, gbs)
         x = embed_forward(model, lmp, tok, q)
+    elif model.kind == "vgg":
+        x, labels = vgg_batch(model, seed, 0, gbs)
+        x = q(x.astype(dtype))
     else:
         x, t = batch_data(model, seed, 0, gbs)
         x, t = q(x.astype(dtype)), q(t.astype(dtype))
@@ -348,6 +480,9 @@ def full_batch_step(model, gbs: int, seed: int = 1234, lr: float = 1e-3, dtype=n
         res.loss = lsum / ntok
         dy, g = head_backward(model, lmp, hc, q)
         record("head", g, lmp)
+    elif model.kind == "vgg":
+        lsum, dy = class_ce(x, labels, 1.0 / gbs, q)
+        res.loss = lsum / gbs
     else:
         numel = gbs * model.seq * model.hidden
         diff = x - t
@@ -375,9 +510,12 @@ def scheduled_step(model, plan: dict, micro_batches: int, gbs: int, seed: int = 
     B = gbs // micro_batches
     params = {l: {k: v.astype(dtype) for k, v in init_layer(model, l, seed).items()} for l in range(model.layers)}
     lm = model.vocab > 0
+    vgg = model.kind == "vgg"
     if lm:
         params["emb"] = params["head"] = {k: v.astype(dtype) for k, v in init_lm(model, seed).items()}
         numel = gbs * model.seq  # CE is a mean over the global batch's tokens
+    elif vgg:
+        numel = gbs  # CE is a mean over the samples
     else:
         numel = gbs * model.seq * model.hidden
     acc = {}  # (stage, replica, layer | "emb" | "head", name) -> grad
@@ -396,6 +534,8 @@ def scheduled_step(model, plan: dict, micro_batches: int, gbs: int, seed: int = 
             if k == 0 and lm:
                 toks = [lm_tokens(model, seed, i * B + cut[j], cut[j + 1] - cut[j])[0] for j in range(r)]
                 xs = [embed_forward(model, params["emb"], t) for t in toks]
+            elif k == 0 and vgg:
+                xs = [vgg_batch(model, seed, i * B + cut[j], cut[j + 1] - cut[j])[0].astype(dtype) for j in range(r)]
             elif k == 0:
                 xs = [batch_data(model, seed, i * B + cut[j], cut[j + 1] - cut[j])[0].astype(dtype)
                       for j in range(r)]
@@ -425,6 +565,12 @@ def scheduled_step(model, plan: dict, micro_batches: int, gbs: int, seed: int = 
                 dy, g = head_backward(model, params["head"], hc)
                 for name in ("Wout", "lnf_g", "lnf_b"):
                     add((len(stages) - 1, j, "head", name), g[name])
+                dys.append(dy)
+                continue
+            if vgg:
+                lab = vgg_batch(model, seed, i * B + cut[j], cut[j + 1] - cut[j])[1]
+                lsum, dy = class_ce(xs[j], lab, 1.0 / numel, _ident)
+                loss += lsum
                 dys.append(dy)
                 continue
             t = batch_data(model, seed, i * B + cut[j], cut[j + 1] - cut[j])[1].astype(dtype)

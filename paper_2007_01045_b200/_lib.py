@@ -58,6 +58,11 @@ _PROTOS = {
     "dpl_k_embed_fwd": (_I, [_VP, _VP, _VP, _VP, _I, _I, _I, _VP]),
     "dpl_k_embed_bwd": (_I, [_VP, _VP, _VP, _VP, _I, _I, _I, _VP]),
     "dpl_k_cross_entropy": (_I, [_VP, _VP, _VP, _I, _I, _F, _VP]),
+    "dpl_k_im2col3x3": (_I, [_VP, _VP, _I, _I, _I, _I, _I, _VP]),
+    "dpl_k_col2im3x3": (_I, [_VP, _VP, _I, _I, _I, _I, _I, _VP]),
+    "dpl_k_maxpool2_fwd": (_I, [_VP, _VP, _I, _I, _I, _I, _VP]),
+    "dpl_k_maxpool2_relu_bwd": (_I, [_VP, _VP, _VP, _I, _I, _I, _I, _VP]),
+    "dpl_k_relu_bwd": (_I, [_VP, _VP, _VP, _LL, _VP]),
     "dpl_k_fill_uniform_bf16": (_I, [_VP, _LL, _U64, _U64, _LL, _F, _VP]),
     "dpl_k_fill_uniform_f32": (_I, [_VP, _LL, _U64, _U64, _LL, _F, _VP]),
     "dpl_k_launch_count": (_LL, []),

@@ -10,6 +10,7 @@
 #include "kernels/attention.h"
 #include "kernels/elementwise.h"
 #include "kernels/lm.h"
+#include "kernels/conv.h"
 #include "kernels/gemm.h"
 
 namespace dpl {
@@ -179,6 +180,26 @@ int dpl_k_cross_entropy(void* logits, const int* tgt, float* loss_acc, int rows,
                         void* stream) {
   return guarded(
       [&] { dpl::cross_entropy_fwd_bwd(logits, tgt, loss_acc, rows, vocab, grad_scale, static_cast<cudaStream_t>(stream)); });
+}
+
+int dpl_k_im2col3x3(const void* x, void* col, int n, int h, int w, int c, int kp, void* stream) {
+  return guarded([&] { dpl::im2col3x3(x, col, n, h, w, c, kp, static_cast<cudaStream_t>(stream)); });
+}
+
+int dpl_k_col2im3x3(const void* dcol, void* dx, int n, int h, int w, int c, int kp, void* stream) {
+  return guarded([&] { dpl::col2im3x3(dcol, dx, n, h, w, c, kp, static_cast<cudaStream_t>(stream)); });
+}
+
+int dpl_k_maxpool2_fwd(const void* x, void* y, int n, int h, int w, int c, void* stream) {
+  return guarded([&] { dpl::maxpool2_fwd(x, y, n, h, w, c, static_cast<cudaStream_t>(stream)); });
+}
+
+int dpl_k_maxpool2_relu_bwd(const void* x, const void* dy, void* dz, int n, int h, int w, int c, void* stream) {
+  return guarded([&] { dpl::maxpool2_relu_bwd(x, dy, dz, n, h, w, c, static_cast<cudaStream_t>(stream)); });
+}
+
+int dpl_k_relu_bwd(const void* y, const void* dy, void* dz, long long n, void* stream) {
+  return guarded([&] { dpl::relu_bwd(y, dy, dz, n, static_cast<cudaStream_t>(stream)); });
 }
 
 int dpl_k_sgd_apply(float* w32, float* g, void* w16, long long n, float lr, void* stream) {

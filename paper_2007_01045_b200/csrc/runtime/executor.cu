@@ -231,7 +231,8 @@ class Executor {
   size_t recv_bytes_ = 0, recv_grad_off_ = 0, flags_off_ = 0;
   std::vector<uint8_t*> peer_recv_;  // by rank (IPC-mapped), null if unused
   long long clock_offset_ns_ = 0;
-  std::vector<int> peer_rows_;       // rows per slice of each rank's stage
+  std::vector<int> peer_samples_;    // samples per micro-batch slice of each rank
+  std::vector<int> peer_stage_;      // stage of each rank
 
   cudaStream_t compute_ = nullptr, send_act_ = nullptr, send_grad_s_ = nullptr, reduce_ = nullptr;
   ncclComm_t comm_ = nullptr;
@@ -264,16 +265,21 @@ class Executor {
   // first sample of replica j's slice in this rank's stage (or stage k)
   int slice_lo(int j, int r = 0) const { return static_cast<int>(1LL * B_ * j / (r ? r : r_)); }
   int L() const { return hi_ - lo_; }
-  bf16* recv_act(int i) const {
-    return reinterpret_cast<bf16*>(recv_) + static_cast<size_t>(i) * ctx_.rows * spec_.hidden;
-  }
+  // activation elements per sample entering global layer l (model output at l == layers)
+  long long elems(int l) const { return elems_per_sample(spec_, l); }
+  bool classify() const { return spec_.kind == "vgg"; }  // labels + cross-entropy over classes
+  // one micro-batch slice of this stage's input / output activation
+  size_t in_elems() const { return static_cast<size_t>(ctx_.samples) * elems(lo_); }
+  size_t out_elems() const { return static_cast<size_t>(ctx_.samples) * elems(hi_); }
+  bf16* recv_act(int i) const { return reinterpret_cast<bf16*>(recv_) + static_cast<size_t>(i) * in_elems(); }
   bf16* recv_grad(int i) const {
-    return reinterpret_cast<bf16*>(recv_ + recv_grad_off_) + static_cast<size_t>(i) * ctx_.rows * spec_.hidden;
+    return reinterpret_cast<bf16*>(recv_ + recv_grad_off_) + static_cast<size_t>(i) * out_elems();
   }
   // flag bank of the current step (parity)
   uint32_t* flags() const { return reinterpret_cast<uint32_t*>(recv_ + flags_off_) + bank_ * 2 * world_; }
-  size_t layout_grad_off(int rows) const;
-  size_t layout_flags_off(int rows) const;
+  // receive-region layout of any rank (from the plan): [recv_act M x s x E_in][recv_grad M x s x E_out][flags]
+  size_t layout_grad_off(int rank) const;
+  size_t layout_flags_off(int rank) const;
   void wait_flag(cudaStream_t s, uint32_t* flag, uint32_t value);
   void signal(cudaStream_t s, uint32_t* remote_flag, uint32_t value);
   void forward(int i, uint32_t base);
@@ -289,7 +295,7 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
   const Value& m = cfg.at("model");
   spec_.kind = m.at("kind").as_string();
   spec_.layers = static_cast<int>(m.at("layers").as_int());
-  spec_.hidden = static_cast<int>(m.at("hidden").as_int());
+  spec_.hidden = m.contains("hidden") ? static_cast<int>(m.at("hidden").as_int()) : 8;
   if (m.contains("heads")) spec_.heads = static_cast<int>(m.at("heads").as_int());
   if (m.contains("ffn")) spec_.ffn = static_cast<int>(m.at("ffn").as_int());
   spec_.seq = m.contains("seq") ? static_cast<int>(m.at("seq").as_int()) : 1;
@@ -297,6 +303,16 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
   if (spec_.kind == "mlp") spec_.seq = 1;
   if (spec_.kind == "gpt") spec_.causal = true;
   if (m.contains("vocab")) spec_.vocab = static_cast<int>(m.at("vocab").as_int());
+  if (m.contains("image")) spec_.image = static_cast<int>(m.at("image").as_int());
+  if (m.contains("width")) spec_.width = static_cast<int>(m.at("width").as_int());
+  if (m.contains("fc")) spec_.fc = static_cast<int>(m.at("fc").as_int());
+  if (m.contains("classes")) spec_.classes = static_cast<int>(m.at("classes").as_int());
+  if (spec_.kind == "vgg") {
+    if (spec_.layers != 19 || spec_.image % 32 || spec_.width % 8 || spec_.classes % 8 || spec_.fc % 8)
+      throw std::invalid_argument("dpl exec: vgg needs 19 layers, image % 32 == 0, width / fc / classes % 8 == 0");
+    spec_.seq = 1;
+    spec_.hidden = spec_.classes;
+  }
   if (spec_.vocab > 0 && (spec_.kind != "gpt" || spec_.vocab % 8 != 0))
     throw std::invalid_argument("dpl exec: vocab needs kind gpt and a multiple of 8");
 
@@ -363,15 +379,17 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
   stash_slots_ = recompute_ ? 1 : phi_;
 
   if (k_ > 0) {
-    for (const Route& r : pipeplan::splitconcat_routes(plan_.stages[k_ - 1], mine, B_, spec_.seq))
+    for (const Route& r : pipeplan::splitconcat_routes(plan_.stages[k_ - 1], mine, B_, static_cast<int>(elems(lo_))))
       if (r.dst_gpu == rank_) in_routes_.push_back(r);
   }
   if (k_ + 1 < S_) {
-    for (const Route& r : pipeplan::splitconcat_routes(mine, plan_.stages[k_ + 1], B_, spec_.seq))
+    for (const Route& r : pipeplan::splitconcat_routes(mine, plan_.stages[k_ + 1], B_, static_cast<int>(elems(hi_))))
       if (r.src_gpu == rank_) out_routes_.push_back(r);
   }
-  numel_global_ = 1LL * gbs_ * spec_.seq * spec_.hidden;
-  loss_norm_ = spec_.vocab > 0 ? static_cast<float>(1LL * gbs_ * spec_.seq) : static_cast<float>(numel_global_);
+  numel_global_ = 1LL * gbs_ * elems(spec_.layers);
+  loss_norm_ = spec_.vocab > 0    ? static_cast<float>(1LL * gbs_ * spec_.seq)
+               : classify()       ? static_cast<float>(gbs_)  // mean CE over the samples
+                                  : static_cast<float>(numel_global_);
 
   // --- context, layers, parameters
   ctx_.spec = spec_;
@@ -410,7 +428,18 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
   if (head_) head_->bind(w32_ + head_off_, g32_ + head_off_, w16_ + head_off_, seed_, compute_);
 
   const size_t RH = static_cast<size_t>(ctx_.rows) * spec_.hidden;
-  if (spec_.kind != "mlp") {
+  if (spec_.kind == "vgg") {
+    size_t col = 0, dz = 0;
+    for (auto& layer : layers_) {
+      col = std::max(col, layer->col_elems(ctx_));
+      dz = std::max(dz, layer->dz_elems(ctx_));
+    }
+    if (col) {
+      ctx_.conv_col = static_cast<bf16*>(mem_.alloc(col * 2));
+      ctx_.conv_dcol = static_cast<bf16*>(mem_.alloc(col * 2));
+    }
+    ctx_.conv_dz = static_cast<bf16*>(mem_.alloc(std::max<size_t>(dz, 8) * 2));
+  } else if (spec_.kind != "mlp") {
     const size_t z = static_cast<size_t>(spec_.heads) * ctx_.samples;
     ctx_.att_dsum = static_cast<float*>(mem_.alloc(z * spec_.seq * 4));
     ctx_.att_dq = static_cast<float*>(mem_.alloc(RH * 4));
@@ -423,16 +452,22 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
   }
   for (auto& layer : layers_) layer->alloc_stash(ctx_);
   act_.assign(L(), {});
-  for (int li = 1; li < L(); ++li)
-    for (int s = 0; s < stash_slots_; ++s) act_[li].push_back(static_cast<bf16*>(mem_.alloc(RH * 2)));
-  if (recompute_) rc_out_ = static_cast<bf16*>(mem_.alloc(RH * 2));
+  // activation buffers sized per boundary: layer l's input is samples x elems(l)
+  const size_t smp = static_cast<size_t>(ctx_.samples);
+  size_t gmax = 8;
+  for (int li = 1; li < L(); ++li) {
+    const size_t e = smp * elems(lo_ + li);
+    gmax = std::max(gmax, e);
+    for (int s = 0; s < stash_slots_; ++s) act_[li].push_back(static_cast<bf16*>(mem_.alloc(e * 2)));
+  }
+  if (recompute_) rc_out_ = static_cast<bf16*>(mem_.alloc(out_elems() * 2));
   if (k_ == 0)
-    for (int s = 0; s < phi_; ++s) in_.push_back(static_cast<bf16*>(mem_.alloc(RH * 2)));
-  for (int i = 0; i < M_; ++i) out_.push_back(static_cast<bf16*>(mem_.alloc(RH * 2)));
+    for (int s = 0; s < phi_; ++s) in_.push_back(static_cast<bf16*>(mem_.alloc(in_elems() * 2)));
+  for (int i = 0; i < M_; ++i) out_.push_back(static_cast<bf16*>(mem_.alloc(out_elems() * 2)));
   if (k_ == S_ - 1) {
     for (int s = 0; s < phi_; ++s) {
-      if (!head_) target_.push_back(static_cast<bf16*>(mem_.alloc(RH * 2)));
-      dloss_.push_back(static_cast<bf16*>(mem_.alloc(RH * 2)));
+      if (!head_ && !classify()) target_.push_back(static_cast<bf16*>(mem_.alloc(out_elems() * 2)));
+      dloss_.push_back(static_cast<bf16*>(mem_.alloc(out_elems() * 2)));
     }
   }
   // the head's logits-gradient stash lives from F_i to B_i like the loss
@@ -440,25 +475,31 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
   if (head_) head_->alloc_stash(ctx_, phi_);
   for (int s = 0; s < phi_ && emb_; ++s) tok_.push_back(static_cast<int*>(mem_.alloc(ctx_.rows * 4)));
   for (int s = 0; s < phi_ && head_; ++s) tgt_tok_.push_back(static_cast<int*>(mem_.alloc(ctx_.rows * 4)));
+  // classification labels: one class id per sample
+  for (int s = 0; s < phi_ && classify() && k_ == S_ - 1; ++s)
+    tgt_tok_.push_back(static_cast<int*>(mem_.alloc(smp * 4)));
   if (k_ > 0)
-    for (int i = 0; i < M_; ++i) send_grad_.push_back(static_cast<bf16*>(mem_.alloc(RH * 2)));
-  gbuf_[0] = static_cast<bf16*>(mem_.alloc(RH * 2));
-  gbuf_[1] = static_cast<bf16*>(mem_.alloc(RH * 2));
+    for (int i = 0; i < M_; ++i) send_grad_.push_back(static_cast<bf16*>(mem_.alloc(in_elems() * 2)));
+  if (emb_) gmax = std::max(gmax, in_elems());
+  gbuf_[0] = static_cast<bf16*>(mem_.alloc(gmax * 2));
+  gbuf_[1] = static_cast<bf16*>(mem_.alloc(gmax * 2));
   loss_acc_ = static_cast<float*>(mem_.alloc(4));
   t0_ = static_cast<unsigned long long*>(mem_.alloc(8));
 
   // receive region: one allocation so a single IPC handle covers it
-  recv_grad_off_ = layout_grad_off(ctx_.rows);
-  flags_off_ = layout_flags_off(ctx_.rows);
-  recv_bytes_ = flags_off_ + 4 * static_cast<size_t>(world_) * 4 + kCalibBytes;
-  recv_ = static_cast<uint8_t*>(mem_.alloc(recv_bytes_));
-  peer_recv_.assign(world_, nullptr);
-  peer_rows_.assign(world_, 0);
+  peer_samples_.assign(world_, 0);
+  peer_stage_.assign(world_, 0);
   for (int k = 0; k < S_; ++k)
     for (int j = 0; j < plan_.stages[k].replication(); ++j) {
       const int rk = plan_.stages[k].replication();
-      peer_rows_[plan_.stages[k].devices[j]] = (slice_lo(j + 1, rk) - slice_lo(j, rk)) * spec_.seq;
+      peer_samples_[plan_.stages[k].devices[j]] = slice_lo(j + 1, rk) - slice_lo(j, rk);
+      peer_stage_[plan_.stages[k].devices[j]] = k;
     }
+  recv_grad_off_ = layout_grad_off(rank_);
+  flags_off_ = layout_flags_off(rank_);
+  recv_bytes_ = flags_off_ + 4 * static_cast<size_t>(world_) * 4 + kCalibBytes;
+  recv_ = static_cast<uint8_t*>(mem_.alloc(recv_bytes_));
+  peer_recv_.assign(world_, nullptr);
 
   // events
   auto mk = [](cudaEvent_t* e) { DPL_CUDA(cudaEventCreate(e)); };
@@ -499,11 +540,16 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
   DPL_CUDA(cudaDeviceSynchronize());
 }
 
-size_t Executor::layout_grad_off(int rows) const {
-  const size_t bytes = static_cast<size_t>(M_) * rows * spec_.hidden * 2;
+size_t Executor::layout_grad_off(int rank) const {
+  const pipeplan::Stage& st = plan_.stages[peer_stage_[rank]];
+  const size_t bytes = static_cast<size_t>(M_) * peer_samples_[rank] * elems(st.layer_lo) * 2;
   return (bytes + 255) & ~size_t(255);
 }
-size_t Executor::layout_flags_off(int rows) const { return 2 * layout_grad_off(rows); }
+size_t Executor::layout_flags_off(int rank) const {
+  const pipeplan::Stage& st = plan_.stages[peer_stage_[rank]];
+  const size_t bytes = static_cast<size_t>(M_) * peer_samples_[rank] * elems(st.layer_hi) * 2;
+  return layout_grad_off(rank) + ((bytes + 255) & ~size_t(255));
+}
 
 // Teardown is two-phase across ranks: every rank first unmaps its peers'
 // regions and destroys its communicator (disconnect), the ranks barrier, and
@@ -565,16 +611,16 @@ void Executor::connect(const uint8_t* blobs, size_t blob_len, int world) {
 long long Executor::calibrate_clock(int phase) {
   if (world_ == 1 || (rank_ != 0 && rank_ != phase)) return clock_offset_ns_;
   constexpr int kRounds = 64;
-  auto calib = [&](uint8_t* region, int rows) {
-    uint8_t* base = region + layout_flags_off(rows) + 4 * static_cast<size_t>(world_) * 4;
+  auto calib = [&](uint8_t* region, int rank) {
+    uint8_t* base = region + layout_flags_off(rank) + 4 * static_cast<size_t>(world_) * 4;
     return base;
   };
   DPL_CUDA(cudaSetDevice(device_));
   // words start at zero (zeroed allocation) and are only ever counted up
   // 1..kRounds per responder, so no re-zeroing (and no zeroing race) is needed
-  uint8_t* mine = calib(recv_, ctx_.rows);
+  uint8_t* mine = calib(recv_, rank_);
   if (rank_ == 0) {
-    uint8_t* peer = calib(peer_recv_[phase], peer_rows_[phase]);
+    uint8_t* peer = calib(peer_recv_[phase], phase);
     unsigned long long* out = nullptr;
     DPL_CUDA(cudaMalloc(&out, 3 * kRounds * sizeof(unsigned long long)));
     clock_ping_kernel<<<1, 1, 0, compute_>>>(reinterpret_cast<uint32_t*>(peer), reinterpret_cast<uint32_t*>(mine + 4),
@@ -594,7 +640,7 @@ long long Executor::calibrate_clock(int phase) {
     }
     return offset;  // rank 0 reports the peer's offset; the host forwards it
   }
-  uint8_t* zero = calib(peer_recv_[0], peer_rows_[0]);
+  uint8_t* zero = calib(peer_recv_[0], 0);
   clock_pong_kernel<<<1, 1, 0, compute_>>>(reinterpret_cast<uint32_t*>(mine), reinterpret_cast<uint32_t*>(zero + 4),
                                            reinterpret_cast<unsigned long long*>(zero + 8), kRounds);
   DPL_CUDA(cudaStreamSynchronize(compute_));
@@ -629,7 +675,6 @@ void Executor::signal(cudaStream_t s, uint32_t* remote_flag, uint32_t value) {
 void Executor::forward(int i, uint32_t base) {
   const int slot = i % phi_;                         // stage input / target / loss-grad buffers
   const int ss = recompute_ ? 0 : i % stash_slots_;  // layer-internal stash
-  const size_t H = spec_.hidden;
   const bf16* x;
   if (k_ == 0) {
     x = in_[slot];
@@ -647,9 +692,14 @@ void Executor::forward(int i, uint32_t base) {
   if (head_) {
     // causal-LM cross-entropy, mean over the global batch's tokens
     head_->forward(ctx_, slot, out_[i], tgt_tok_[slot], loss_acc_, 1.0f / loss_norm_);
+  } else if (k_ == S_ - 1 && classify()) {
+    // softmax cross-entropy over the classes, mean over the global batch
+    DPL_CUDA(cudaMemcpyAsync(dloss_[slot], out_[i], out_elems() * 2, cudaMemcpyDeviceToDevice, compute_));
+    cross_entropy_fwd_bwd(dloss_[slot], tgt_tok_[slot], loss_acc_, ctx_.samples, spec_.classes, 1.0f / loss_norm_,
+                          compute_);
   } else if (k_ == S_ - 1) {
     // MSE over the whole global batch: loss = sum (y-t)^2 / numel, dY = 2 (y-t) / numel
-    mse_loss(out_[i], target_[slot], dloss_[slot], loss_acc_, static_cast<long long>(ctx_.rows) * H,
+    mse_loss(out_[i], target_[slot], dloss_[slot], loss_acc_, static_cast<long long>(out_elems()),
              2.0f / static_cast<float>(numel_global_), compute_);
   }
   record(fwd_ev_[i].end, compute_);
@@ -657,12 +707,13 @@ void Executor::forward(int i, uint32_t base) {
     DPL_CUDA(cudaEventRecord(fwd_done_[i], compute_));
     DPL_CUDA(cudaStreamWaitEvent(send_act_, fwd_done_[i], 0));
     record(send_fwd_ev_[i].start, send_act_);
+    // routes are in activation elements (samples x elems(boundary))
+    const size_t eb = static_cast<size_t>(elems(hi_));
     for (const Route& r : out_routes_) {
       uint8_t* peer = peer_recv_[r.dst_gpu];
-      const int rows_dst = peer_rows_[r.dst_gpu];
-      bf16* dst = reinterpret_cast<bf16*>(peer) + (static_cast<size_t>(i) * rows_dst + r.dst_row) * H;
-      DPL_CUDA(cudaMemcpyAsync(dst, out_[i] + r.src_row * H, r.rows * H * 2, cudaMemcpyDeviceToDevice, send_act_));
-      uint32_t* flag = reinterpret_cast<uint32_t*>(peer + layout_flags_off(rows_dst)) + bank_ * 2 * world_ + rank_;
+      bf16* dst = reinterpret_cast<bf16*>(peer) + static_cast<size_t>(i) * peer_samples_[r.dst_gpu] * eb + r.dst_row;
+      DPL_CUDA(cudaMemcpyAsync(dst, out_[i] + r.src_row, r.rows * 2, cudaMemcpyDeviceToDevice, send_act_));
+      uint32_t* flag = reinterpret_cast<uint32_t*>(peer + layout_flags_off(r.dst_gpu)) + bank_ * 2 * world_ + rank_;
       signal(send_act_, flag, base + i + 1);
     }
     record(send_fwd_ev_[i].end, send_act_);
@@ -672,7 +723,6 @@ void Executor::forward(int i, uint32_t base) {
 void Executor::backward(int i, uint32_t base) {
   const int slot = i % phi_;
   const int ss = recompute_ ? 0 : i % stash_slots_;
-  const size_t H = spec_.hidden;
   const bf16* dy;
   if (k_ == S_ - 1) {
     dy = dloss_[slot];
@@ -707,6 +757,7 @@ void Executor::backward(int i, uint32_t base) {
     } else if (emb_) {
       dx = gbuf_[pp];
     }
+    ctx_.cur_y = li + 1 < L() ? act_[li + 1][ss] : (recompute_ ? rc_out_ : out_[i]);
     layers_[li]->backward(ctx_, ss, x, dy, dx);
     dy = dx;
     // this layer's gradients are final: AllReduce + apply while the
@@ -722,15 +773,14 @@ void Executor::backward(int i, uint32_t base) {
     DPL_CUDA(cudaEventRecord(bwd_done_[i], compute_));
     DPL_CUDA(cudaStreamWaitEvent(send_grad_s_, bwd_done_[i], 0));
     record(send_bwd_ev_[i].start, send_grad_s_);
+    const size_t eb = static_cast<size_t>(elems(lo_));
     for (const Route& r : in_routes_) {
       uint8_t* peer = peer_recv_[r.src_gpu];
-      const int rows_src = peer_rows_[r.src_gpu];
-      bf16* dst = reinterpret_cast<bf16*>(peer + layout_grad_off(rows_src)) +
-                  (static_cast<size_t>(i) * rows_src + r.src_row) * H;
-      DPL_CUDA(cudaMemcpyAsync(dst, send_grad_[i] + r.dst_row * H, r.rows * H * 2, cudaMemcpyDeviceToDevice,
-                               send_grad_s_));
+      bf16* dst = reinterpret_cast<bf16*>(peer + layout_grad_off(r.src_gpu)) +
+                  static_cast<size_t>(i) * peer_samples_[r.src_gpu] * eb + r.src_row;
+      DPL_CUDA(cudaMemcpyAsync(dst, send_grad_[i] + r.dst_row, r.rows * 2, cudaMemcpyDeviceToDevice, send_grad_s_));
       uint32_t* flag =
-          reinterpret_cast<uint32_t*>(peer + layout_flags_off(rows_src)) + bank_ * 2 * world_ + world_ + rank_;
+          reinterpret_cast<uint32_t*>(peer + layout_flags_off(r.src_gpu)) + bank_ * 2 * world_ + world_ + rank_;
       signal(send_grad_s_, flag, base + i + 1);
     }
     record(send_bwd_ev_[i].end, send_grad_s_);
@@ -746,8 +796,6 @@ void Executor::reduce_apply(cudaEvent_t ready, size_t off, size_t n) {
 
 void Executor::enqueue_step(const void* host_input, const void* host_target) {
   const uint32_t base = 0;  // flag values are i+1 within the bank of this step
-  const size_t H = spec_.hidden;
-  const size_t RH = static_cast<size_t>(ctx_.rows) * H;
   count_launch();
   stamp_kernel<<<1, 1, 0, compute_>>>(t0_);
   record(ev_begin_, compute_);
@@ -764,9 +812,11 @@ void Executor::enqueue_step(const void* host_input, const void* host_target) {
     const int slot = i % phi_;
     if (op.kind == pipeplan::BlockKind::forward) {
       const long long sample0 = 1LL * i * B_ + slice_first;
-      const long long idx0 = sample0 * spec_.seq * static_cast<long long>(H);
+      const long long idx0 = sample0 * elems(0);
+      const long long tidx0 = sample0 * elems(spec_.layers);
       const long long tok0 = sample0 * spec_.seq;
       const size_t rows = static_cast<size_t>(ctx_.rows);
+      const size_t ein = in_elems(), eout = out_elems();
       if (emb_) {  // token ids: [M][rows] int32 on the host
         if (host_input) {
           DPL_CUDA(cudaMemcpyAsync(tok_[slot], static_cast<const int*>(host_input) + i * rows, rows * 4,
@@ -776,10 +826,10 @@ void Executor::enqueue_step(const void* host_input, const void* host_target) {
         }
       } else if (k_ == 0) {
         if (host_input) {
-          DPL_CUDA(cudaMemcpyAsync(in_[slot], static_cast<const bf16*>(host_input) + static_cast<size_t>(i) * RH,
-                                   RH * 2, cudaMemcpyHostToDevice, compute_));
+          DPL_CUDA(cudaMemcpyAsync(in_[slot], static_cast<const bf16*>(host_input) + static_cast<size_t>(i) * ein,
+                                   ein * 2, cudaMemcpyHostToDevice, compute_));
         } else {
-          fill_uniform_bf16(in_[slot], static_cast<long long>(RH), seed_, kTensorInput, idx0, 1.0f, compute_);
+          fill_uniform_bf16(in_[slot], static_cast<long long>(ein), seed_, kTensorInput, idx0, 1.0f, compute_);
         }
       }
       if (head_) {
@@ -789,12 +839,21 @@ void Executor::enqueue_step(const void* host_input, const void* host_target) {
         } else {
           fill_tokens(tgt_tok_[slot], static_cast<long long>(rows), seed_, kTensorTarget, tok0, spec_.vocab, compute_);
         }
+      } else if (k_ == S_ - 1 && classify()) {  // class labels: [M][samples] int32 on the host
+        const size_t smp = static_cast<size_t>(ctx_.samples);
+        if (host_target) {
+          DPL_CUDA(cudaMemcpyAsync(tgt_tok_[slot], static_cast<const int*>(host_target) + i * smp, smp * 4,
+                                   cudaMemcpyHostToDevice, compute_));
+        } else {
+          fill_tokens(tgt_tok_[slot], static_cast<long long>(smp), seed_, kTensorTarget, sample0, spec_.classes,
+                      compute_);
+        }
       } else if (k_ == S_ - 1) {
         if (host_target) {
-          DPL_CUDA(cudaMemcpyAsync(target_[slot], static_cast<const bf16*>(host_target) + static_cast<size_t>(i) * RH,
-                                   RH * 2, cudaMemcpyHostToDevice, compute_));
+          DPL_CUDA(cudaMemcpyAsync(target_[slot], static_cast<const bf16*>(host_target) + static_cast<size_t>(i) * eout,
+                                   eout * 2, cudaMemcpyHostToDevice, compute_));
         } else {
-          fill_uniform_bf16(target_[slot], static_cast<long long>(RH), seed_, kTensorTarget, idx0, 1.0f, compute_);
+          fill_uniform_bf16(target_[slot], static_cast<long long>(eout), seed_, kTensorTarget, tidx0, 1.0f, compute_);
         }
       }
       forward(i, base);
@@ -958,17 +1017,17 @@ void Executor::read_tensor(const std::string& name, bool grad, void* host, size_
 std::string Executor::layer_profile_json(int reps) {
   if (reps < 1) throw std::invalid_argument("layer_profile: reps must be >= 1");
   if (recompute_) throw std::invalid_argument("layer_profile: executor built with recompute");
-  const size_t H = spec_.hidden;
   const int n = L();
   std::vector<cudaEvent_t> fe(n + 1), be(n + 1);
   for (auto* v : {&fe, &be})
     for (cudaEvent_t& e : *v) DPL_CUDA(cudaEventCreate(&e));
   std::vector<std::vector<float>> ft(n), bt(n);
   if (emb_) fill_tokens(tok_[0], ctx_.rows, seed_, kTensorInput, 0, spec_.vocab, compute_);
-  else if (k_ == 0) fill_uniform_bf16(in_[0], static_cast<long long>(ctx_.rows) * H, seed_, kTensorInput, 0, 1.0f, compute_);
+  else if (k_ == 0) fill_uniform_bf16(in_[0], static_cast<long long>(in_elems()), seed_, kTensorInput, 0, 1.0f, compute_);
   if (head_) fill_tokens(tgt_tok_[0], ctx_.rows, seed_, kTensorTarget, 0, spec_.vocab, compute_);
+  else if (k_ == S_ - 1 && classify()) fill_tokens(tgt_tok_[0], ctx_.samples, seed_, kTensorTarget, 0, spec_.classes, compute_);
   else if (k_ == S_ - 1)
-    fill_uniform_bf16(target_[0], static_cast<long long>(ctx_.rows) * H, seed_, kTensorTarget, 0, 1.0f, compute_);
+    fill_uniform_bf16(target_[0], static_cast<long long>(out_elems()), seed_, kTensorTarget, 0, 1.0f, compute_);
   const bf16* x0 = k_ == 0 ? in_[0] : recv_act(0);
   for (int rep = 0; rep < reps + 1; ++rep) {  // first chain is a warm-up
     const bf16* x = x0;
@@ -979,8 +1038,12 @@ std::string Executor::layer_profile_json(int reps) {
       layers_[li]->forward(ctx_, 0, x, y);
       if (li == n - 1 && head_)
         head_->forward(ctx_, 0, out_[0], tgt_tok_[0], loss_acc_, 1.0f / loss_norm_);  // counted in the last layer
-      else if (li == n - 1 && k_ == S_ - 1)
-        mse_loss(out_[0], target_[0], dloss_[0], loss_acc_, static_cast<long long>(ctx_.rows) * H,
+      else if (li == n - 1 && k_ == S_ - 1 && classify()) {
+        DPL_CUDA(cudaMemcpyAsync(dloss_[0], out_[0], out_elems() * 2, cudaMemcpyDeviceToDevice, compute_));
+        cross_entropy_fwd_bwd(dloss_[0], tgt_tok_[0], loss_acc_, ctx_.samples, spec_.classes, 1.0f / loss_norm_,
+                              compute_);
+      } else if (li == n - 1 && k_ == S_ - 1)
+        mse_loss(out_[0], target_[0], dloss_[0], loss_acc_, static_cast<long long>(out_elems()),
                  2.0f / static_cast<float>(numel_global_), compute_);
       DPL_CUDA(cudaEventRecord(fe[li + 1], compute_));
       x = y;
@@ -993,6 +1056,7 @@ std::string Executor::layer_profile_json(int reps) {
       const bf16* xin = li > 0 ? act_[li][0] : x0;
       bf16* dx = li > 0 || emb_ ? gbuf_[pp] : (k_ > 0 ? send_grad_[0] : nullptr);
       pp ^= 1;
+      ctx_.cur_y = li + 1 < n ? act_[li + 1][0] : out_[0];
       layers_[li]->backward(ctx_, 0, xin, dy, dx);
       if (li == 0 && emb_) emb_->backward(ctx_, tok_[0], dx);
       DPL_CUDA(cudaEventRecord(be[li], compute_));
@@ -1024,7 +1088,7 @@ std::string Executor::layer_profile_json(int reps) {
     l.index = lo_ + li;
     l.fwd_time = median(ft[li]) * 1e-3;
     l.bwd_time = median(bt[li]) * 1e-3;
-    l.activation_bytes = static_cast<std::int64_t>(ctx_.rows) * static_cast<std::int64_t>(H) * 2;  // bf16 output
+    l.activation_bytes = static_cast<std::int64_t>(ctx_.samples) * elems(lo_ + li + 1) * 2;  // bf16 output
     size_t np = layers_[li]->param_count();
     if (li == 0 && emb_) np += emb_->param_count();
     if (li == n - 1 && head_) np += head_->param_count();

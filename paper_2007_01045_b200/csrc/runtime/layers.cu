@@ -8,6 +8,7 @@
 
 #include "kernels/attention.h"
 #include "kernels/elementwise.h"
+#include "kernels/conv.h"
 #include "kernels/lm.h"
 #include "layers.h"
 
@@ -344,9 +345,177 @@ class TransformerLayer final : public Layer {
 
 }  // namespace
 
+// ------------------------------------------------------------------ VGG-19
+// Profile layers 0..15: 3x3 convs (+ReLU; the last conv of each group also
+// does the 2x2 max pool), 16..18: FC (ReLU, ReLU, logits).  Activations are
+// NHWC; a conv is  y = relu(im2col(x) W^T + b)  on the tcgen05 GEMM with
+// W [cout][kp], K ordered (kh, kw, c) and zero-padded to kp = ceil8(9 cin).
+// Gradient contract: every VGG layer takes dL/d(its output) and returns
+// dL/d(its input) (ReLU' and the pool backward are applied inside).
+VggLayerShape vgg_layer(const ModelSpec& spec, int l) {
+  static const int kConvs[5] = {2, 2, 4, 4, 4};
+  static const int kMult[5] = {1, 2, 4, 8, 8};
+  VggLayerShape v;
+  int idx = 0, hw = spec.image, cin = 3;
+  for (int g = 0; g < 5; ++g) {
+    for (int c = 0; c < kConvs[g]; ++c, ++idx) {
+      const int cout = spec.width * kMult[g];
+      if (idx == l) {
+        v.conv = true;
+        v.h = v.w = hw;
+        v.cin = cin;
+        v.cout = cout;
+        v.kp = (9 * cin + 7) / 8 * 8;
+        v.pool = c == kConvs[g] - 1;
+        return v;
+      }
+      cin = cout;
+    }
+    hw /= 2;
+  }
+  const int flat = hw * hw * cin;
+  const int fins[3] = {flat, spec.fc, spec.fc}, fouts[3] = {spec.fc, spec.fc, spec.classes};
+  if (l < 16 || l > 18) throw std::out_of_range("vgg_layer: layer index");
+  v.fin = fins[l - 16];
+  v.fout = fouts[l - 16];
+  v.relu = l != 18;
+  return v;
+}
+
+long long elems_per_sample(const ModelSpec& spec, int l) {
+  if (spec.kind != "vgg") return static_cast<long long>(spec.seq) * spec.hidden;
+  if (l >= spec.layers) return spec.classes;
+  const VggLayerShape v = vgg_layer(spec, l);
+  return v.conv ? static_cast<long long>(v.h) * v.w * v.cin : v.fin;
+}
+
+class ConvLayer final : public Layer {
+ public:
+  ConvLayer(const ModelSpec& spec, int index) : v_(vgg_layer(spec, index)), index_(index) {}
+
+  size_t param_count() const override { return static_cast<size_t>(v_.cout) * v_.kp + v_.cout; }
+  void bind(float* w32, float* g32, bf16* w16, uint64_t seed, cudaStream_t s) override {
+    w32_ = w32;
+    g32_ = g32;
+    w16_ = w16;
+    const size_t nw = static_cast<size_t>(v_.cout) * v_.kp;
+    // the padding columns kp > 9 cin meet zero columns: they never act or learn
+    init_params({{0, nw, 0, std::sqrt(6.0f / (9.0f * v_.cin))}, {nw, static_cast<size_t>(v_.cout), 1, 0.05f}},
+                index_, w32, w16, param_count(), seed, s);
+  }
+  size_t col_elems(const StageContext& c) const override { return px(c) * v_.kp; }
+  size_t dz_elems(const StageContext& c) const override { return px(c) * v_.cout; }
+  void alloc_stash(StageContext& ctx) override {
+    if (v_.pool)  // post-ReLU, pre-pool output for the pool backward
+      for (int k = 0; k < ctx.slots; ++k) yr_.push_back(alloc_n<bf16>(ctx, px(ctx) * v_.cout));
+  }
+  void forward(StageContext& ctx, int slot, const bf16* x, bf16* y) override {
+    const int n = ctx.samples;
+    const int rows = static_cast<int>(px(ctx));
+    im2col3x3(x, ctx.conv_col, n, v_.h, v_.w, v_.cin, v_.kp, ctx.stream);
+    bf16* out = v_.pool ? yr_[slot] : y;
+    GemmDesc d = plain(rows, v_.cout, v_.kp, ctx.conv_col, v_.kp, false, w16_, v_.kp, false, out, v_.cout,
+                       kBias | kRelu);
+    d.bias = w32_ + static_cast<size_t>(v_.cout) * v_.kp;
+    ctx.gemms.run(d, ctx.stream);
+    if (v_.pool) maxpool2_fwd(out, y, n, v_.h, v_.w, v_.cout, ctx.stream);
+  }
+  void backward(StageContext& ctx, int slot, const bf16* x, const bf16* dy, bf16* dx) override {
+    const int n = ctx.samples;
+    const int rows = static_cast<int>(px(ctx));
+    if (v_.pool) maxpool2_relu_bwd(yr_[slot], dy, ctx.conv_dz, n, v_.h, v_.w, v_.cout, ctx.stream);
+    else relu_bwd(ctx.cur_y, dy, ctx.conv_dz, static_cast<long long>(rows) * v_.cout, ctx.stream);
+    float* gw = g32_;
+    colsum_acc(ctx.conv_dz, gw + static_cast<size_t>(v_.cout) * v_.kp, rows, v_.cout, ctx.stream);
+    // dW += dz^T col (columns recomputed from the stashed input)
+    im2col3x3(x, ctx.conv_col, n, v_.h, v_.w, v_.cin, v_.kp, ctx.stream);
+    ctx.gemms.run(plain(v_.cout, v_.kp, rows, ctx.conv_dz, v_.cout, true, ctx.conv_col, v_.kp, true, gw, v_.kp,
+                        kOutF32Acc),
+                  ctx.stream);
+    if (dx) {
+      ctx.gemms.run(plain(rows, v_.kp, v_.cout, ctx.conv_dz, v_.cout, false, w16_, v_.kp, true, ctx.conv_dcol, v_.kp,
+                          kOutBf16),
+                    ctx.stream);
+      col2im3x3(ctx.conv_dcol, dx, n, v_.h, v_.w, v_.cin, v_.kp, ctx.stream);
+    }
+  }
+  double flops_fwd(const StageContext& ctx) const override { return 2.0 * px(ctx) * v_.cout * 9.0 * v_.cin; }
+  double flops_bwd(const StageContext& ctx, bool need_dx) const override {
+    return (need_dx ? 2.0 : 1.0) * flops_fwd(ctx);
+  }
+  std::vector<Named> tensors() const override {
+    const size_t nw = static_cast<size_t>(v_.cout) * v_.kp;
+    return {{"W", 0, nw}, {"b", nw, static_cast<size_t>(v_.cout)}};
+  }
+
+ private:
+  size_t px(const StageContext& c) const { return static_cast<size_t>(c.samples) * v_.h * v_.w; }
+  VggLayerShape v_;
+  int index_;
+  float* w32_ = nullptr;
+  float* g32_ = nullptr;
+  bf16* w16_ = nullptr;
+  std::vector<bf16*> yr_;
+};
+
+// y = x W^T + b (+ReLU), W [fout][fin]; takes / returns output / input gradients
+class FcLayer final : public Layer {
+ public:
+  FcLayer(const ModelSpec& spec, int index) : v_(vgg_layer(spec, index)), index_(index) {}
+
+  size_t param_count() const override { return static_cast<size_t>(v_.fout) * v_.fin + v_.fout; }
+  void bind(float* w32, float* g32, bf16* w16, uint64_t seed, cudaStream_t s) override {
+    w32_ = w32;
+    g32_ = g32;
+    w16_ = w16;
+    const size_t nw = static_cast<size_t>(v_.fout) * v_.fin;
+    init_params({{0, nw, 0, std::sqrt(6.0f / v_.fin)}, {nw, static_cast<size_t>(v_.fout), 1, 0.05f}}, index_, w32,
+                w16, param_count(), seed, s);
+  }
+  size_t dz_elems(const StageContext& c) const override { return static_cast<size_t>(c.samples) * v_.fout; }
+  void alloc_stash(StageContext&) override {}
+  void forward(StageContext& ctx, int, const bf16* x, bf16* y) override {
+    GemmDesc d = plain(ctx.samples, v_.fout, v_.fin, x, v_.fin, false, w16_, v_.fin, false, y, v_.fout,
+                       kBias | (v_.relu ? kRelu : 0u));
+    d.bias = w32_ + static_cast<size_t>(v_.fout) * v_.fin;
+    ctx.gemms.run(d, ctx.stream);
+  }
+  void backward(StageContext& ctx, int, const bf16* x, const bf16* dy, bf16* dx) override {
+    const int n = ctx.samples;
+    const bf16* dz = dy;
+    if (v_.relu) {
+      relu_bwd(ctx.cur_y, dy, ctx.conv_dz, static_cast<long long>(n) * v_.fout, ctx.stream);
+      dz = ctx.conv_dz;
+    }
+    ctx.gemms.run(plain(v_.fout, v_.fin, n, dz, v_.fout, true, x, v_.fin, true, g32_, v_.fin, kOutF32Acc), ctx.stream);
+    colsum_acc(dz, g32_ + static_cast<size_t>(v_.fout) * v_.fin, n, v_.fout, ctx.stream);
+    if (dx)
+      ctx.gemms.run(plain(n, v_.fin, v_.fout, dz, v_.fout, false, w16_, v_.fin, true, dx, v_.fin, kOutBf16), ctx.stream);
+  }
+  double flops_fwd(const StageContext& ctx) const override { return 2.0 * ctx.samples * v_.fin * v_.fout; }
+  double flops_bwd(const StageContext& ctx, bool need_dx) const override {
+    return (need_dx ? 2.0 : 1.0) * flops_fwd(ctx);
+  }
+  std::vector<Named> tensors() const override {
+    const size_t nw = static_cast<size_t>(v_.fout) * v_.fin;
+    return {{"W", 0, nw}, {"b", nw, static_cast<size_t>(v_.fout)}};
+  }
+
+ private:
+  VggLayerShape v_;
+  int index_;
+  float* w32_ = nullptr;
+  float* g32_ = nullptr;
+  bf16* w16_ = nullptr;
+};
+
 std::unique_ptr<Layer> make_layer(const ModelSpec& spec, int global_index) {
   if (spec.kind == "mlp") return std::make_unique<MlpLayer>(spec, global_index);
   if (spec.kind == "bert" || spec.kind == "gpt") return std::make_unique<TransformerLayer>(spec, global_index);
+  if (spec.kind == "vgg") {
+    if (global_index < 16) return std::make_unique<ConvLayer>(spec, global_index);
+    return std::make_unique<FcLayer>(spec, global_index);
+  }
   throw std::invalid_argument("dpl: unknown model kind '" + spec.kind + "'");
 }
 

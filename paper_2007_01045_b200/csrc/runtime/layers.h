@@ -35,7 +35,23 @@ struct ModelSpec {
   bool causal = false;
   float ln_eps = 1e-5f;
   int vocab = 0;  // > 0: GPT language model (token ids in, cross-entropy out)
+  // VGG-19 (kind "vgg", config C3): NHWC images image x image x 3, conv
+  // widths width x {1, 2, 4, 8, 8} (2, 2, 4, 4, 4 convs, 2x2 max pool after
+  // each group), FC fc -> fc -> classes; cross-entropy over classes
+  int image = 224, width = 64, fc = 4096, classes = 1000;
 };
+
+// One VGG profile layer: a 3x3 conv (+ReLU, + optional 2x2 pool) or an FC.
+struct VggLayerShape {
+  bool conv = false;
+  int h = 0, w = 0, cin = 0, cout = 0, kp = 0;  // conv: input spatial size, channels, padded K = 9 cin
+  bool pool = false;
+  int fin = 0, fout = 0;  // fc
+  bool relu = true;
+};
+VggLayerShape vgg_layer(const ModelSpec& spec, int l);
+// activation elements per sample entering global layer l (l == layers: the model output)
+long long elems_per_sample(const ModelSpec& spec, int l);
 
 // Device memory owned by one stage replica (freed by the executor).
 class DeviceMemory {
@@ -71,6 +87,10 @@ struct StageContext {
   float* att_dsum = nullptr;  // attention backward workspaces: [z][S]
   float* att_dq = nullptr;    // [z][S][64]
   float* ln_ws = nullptr;     // LayerNorm-backward partials [kLnBwdBlocks][2][H]
+  bf16* conv_col = nullptr;   // VGG: im2col columns (max over the stage's convs)
+  bf16* conv_dcol = nullptr;  // VGG: column gradients
+  bf16* conv_dz = nullptr;    // VGG: gradient w.r.t. the conv / FC pre-activation
+  const bf16* cur_y = nullptr;  // output of the layer whose backward runs (set by the executor)
   double flops_fwd = 0.0, flops_bwd = 0.0;  // per micro-batch slice (accounting)
 };
 
@@ -94,6 +114,9 @@ class Layer {
     size_t count;
   };
   virtual std::vector<Named> tensors() const = 0;
+  // scratch the layer needs in StageContext (VGG): columns, dz (elements)
+  virtual size_t col_elems(const StageContext&) const { return 0; }
+  virtual size_t dz_elems(const StageContext&) const { return 0; }
 };
 
 std::unique_ptr<Layer> make_layer(const ModelSpec& spec, int global_index);

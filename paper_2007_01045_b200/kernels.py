@@ -83,6 +83,26 @@ def cross_entropy(logits, tgt, loss_acc, rows, vocab, grad_scale):
     check(lib().dpl_k_cross_entropy(_ptr(logits), _ptr(tgt), _ptr(loss_acc), rows, vocab, grad_scale, _stream()))
 
 
+def im2col3x3(x, col, n, h, w, c, kp):
+    check(lib().dpl_k_im2col3x3(_ptr(x), _ptr(col), n, h, w, c, kp, _stream()))
+
+
+def col2im3x3(dcol, dx, n, h, w, c, kp):
+    check(lib().dpl_k_col2im3x3(_ptr(dcol), _ptr(dx), n, h, w, c, kp, _stream()))
+
+
+def maxpool2_fwd(x, y, n, h, w, c):
+    check(lib().dpl_k_maxpool2_fwd(_ptr(x), _ptr(y), n, h, w, c, _stream()))
+
+
+def maxpool2_relu_bwd(x, dy, dz, n, h, w, c):
+    check(lib().dpl_k_maxpool2_relu_bwd(_ptr(x), _ptr(dy), _ptr(dz), n, h, w, c, _stream()))
+
+
+def relu_bwd(y, dy, dz, n):
+    check(lib().dpl_k_relu_bwd(_ptr(y), _ptr(dy), _ptr(dz), n, _stream()))
+
+
 def sgd_apply(w32, g, w16, n, lr):
     check(lib().dpl_k_sgd_apply(_ptr(w32), _ptr(g), _ptr(w16), n, lr, _stream()))
 

@@ -25,6 +25,9 @@ EMU_DEPTH_RTOL = 0.004
 EMU_LOSS_RTOL = 2e-3
 LOSS_RTOL = 1e-2
 FP64_GRAD_RTOL = 0.25
+# VGG at test size (8-channel convs, 19 ReLU layers): bf16 storage error of
+# the exact-emulation oracle itself reaches ~30% on the first conv
+FP64_GRAD_RTOL_DEEP = 0.5
 
 
 def rel_fro(a, b):
@@ -34,7 +37,7 @@ def rel_fro(a, b):
 
 
 def tensor_names(kind):
-    if kind == "mlp":
+    if kind in ("mlp", "vgg"):
         return ["W", "b"]
     return ["ln1_g", "ln1_b", "Wqkv", "bqkv", "Wo", "bo", "ln2_g", "ln2_b", "W1", "b1", "W2", "b2"]
 
@@ -44,17 +47,18 @@ def check_loss(loss, emu, exact):
     assert abs(loss - exact.loss) <= LOSS_RTOL * abs(exact.loss), (loss, exact.loss)
 
 
-def check_grads(ex, emu, exact, layers, kind, n_layers=None):
+def check_grads(ex, emu, exact, layers, kind, n_layers=None, depth_rtol=EMU_DEPTH_RTOL, base_rtol=EMU_GRAD_RTOL):
     worst = 0.0
     n_layers = max(layers) + 1 if n_layers is None else n_layers
     for l in layers:
-        tol = EMU_GRAD_RTOL + (EMU_DEPTH_RTOL * (n_layers - 1 - l) if kind == "mlp" else 0.0)
+        tol = base_rtol + (depth_rtol * (n_layers - 1 - l) if kind in ("mlp", "vgg") else 0.0)
         for name in tensor_names(kind):
             got = ex.read(l, name, emu.grads[(l, name)].size, grad=True)
             e = rel_fro(got, emu.grads[(l, name)])
             assert e < tol, f"layer {l} {name}: grad rel err vs bf16 oracle {e:.4g} (tol {tol:.3g})"
             e64 = rel_fro(got, exact.grads[(l, name)])
-            assert e64 < FP64_GRAD_RTOL, f"layer {l} {name}: grad rel err vs fp64 oracle {e64:.4g}"
+            b64 = FP64_GRAD_RTOL_DEEP if kind == "vgg" else FP64_GRAD_RTOL
+            assert e64 < b64, f"layer {l} {name}: grad rel err vs fp64 oracle {e64:.4g}"
             worst = max(worst, e)
     return worst
 
@@ -67,7 +71,7 @@ def check_update(ex, emu, layers, kind, model, lr, seed=1234, n_layers=None):
     worst = 0.0
     n_layers = m.layers if n_layers is None else n_layers
     for l in layers:
-        ltol = EMU_GRAD_RTOL + (EMU_DEPTH_RTOL * (n_layers - 1 - l) if kind == "mlp" else 0.0)
+        ltol = EMU_GRAD_RTOL + (EMU_DEPTH_RTOL * (n_layers - 1 - l) if kind in ("mlp", "vgg") else 0.0)
         init = init_layer(m, l, seed)
         for name in tensor_names(kind):
             g = emu.grads[(l, name)].ravel()

@@ -36,6 +36,12 @@ CASES += [
     (2, LMGPT, {"stages": [{"layers": [0, 2], "gpus": [0]}, {"layers": [2, 4], "gpus": [1]}]}, 4, 8),
     (4, LMGPT, {"stages": [{"layers": [0, 2], "gpus": [0, 1]}, {"layers": [2, 4], "gpus": [2, 3]}]}, 4, 16),
 ]
+# VGG-19 (C3 shape): uneven conv / FC replication, Split-Concat of the pooled features
+VGGS = dict(kind="vgg", layers=19, image=32, width=8, fc=32, classes=16)
+CASES += [
+    (2, VGGS, {"stages": [{"layers": [0, 10], "gpus": [0]}, {"layers": [10, 19], "gpus": [1]}]}, 2, 8),
+    (4, VGGS, {"stages": [{"layers": [0, 16], "gpus": [0, 1, 2]}, {"layers": [16, 19], "gpus": [3]}]}, 2, 12),
+]
 TWO = {"stages": [{"layers": [0, 2], "gpus": [0]}, {"layers": [2, 4], "gpus": [1]}]}
 # GPipe / re-computation on the device (the schedules of the paper's Table VI)
 SCHED_CASES = [

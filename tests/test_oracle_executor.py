@@ -112,3 +112,70 @@ def test_lm_head_and_embedding_match_autograd():
     for k, v in [("Wout", g["Wout"]), ("lnf_g", g["lnf_g"]), ("lnf_b", g["lnf_b"]), ("wte", ge["wte"]),
                  ("wpe", ge["wpe"])]:
         assert np.allclose(tp[k].grad.numpy(), v, rtol=1e-9, atol=1e-12), k
+
+
+VGG = dict(kind="vgg", layers=19, image=32, width=8, fc=32, classes=16)
+
+
+@pytest.mark.parametrize("plan", [{"stages": [{"layers": [0, 19], "gpus": [0]}]},
+                                  {"stages": [{"layers": [0, 16], "gpus": [0, 1, 2]},
+                                                       {"layers": [16, 19], "gpus": [3]}]},
+                                  {"stages": [{"layers": [0, 10], "gpus": [0]}, {"layers": [10, 19], "gpus": [1, 2]}]}])
+def test_scheduled_equals_full_batch_vgg(plan):
+    """VGG-19 (convs, pools, FCs, class CE) with uneven conv/FC replication."""
+    gbs, M = 12, 2
+    a = full_batch_step(VGG, gbs)
+    b = scheduled_step(VGG, plan, M, gbs)
+    assert abs(a.loss - b.loss) <= 1e-12 * abs(a.loss)
+    for key, g in a.grads.items():
+        assert np.allclose(b.grads[key], g, rtol=1e-9, atol=1e-13), key
+
+
+def test_vgg_manual_backward_matches_autograd():
+    """The oracle's conv (im2col, (kh, kw, c) order, zero-padded K), pool
+    (first max), ReLU and FC backward equal torch autograd in fp64."""
+    import torch
+    import torch.nn.functional as F
+    from oracle.executor_ref import class_ce, layer_backward, vgg_batch, vgg_layer
+    m = Model.from_dict(VGG)
+    n = 2
+    x0, lab = vgg_batch(m, 5, 0, n)
+    params = {l: {k: v.astype(np.float64) for k, v in init_layer(m, l, 5).items()} for l in range(19)}
+    x = x0.astype(np.float64)
+    caches = []
+    for l in range(19):
+        x, c = layer_forward(m, l, params[l], x, n)
+        caches.append(c)
+    lsum, dy = class_ce(x, lab, 1.0 / n, lambda a: a)
+    grads = {}
+    for l in reversed(range(19)):
+        dy, g = layer_backward(m, l, params[l], caches[l], dy, n, need_dx=l > 0)
+        grads[l] = g
+    # torch reference in NCHW
+    tp = {l: {k: torch.tensor(v, requires_grad=True) for k, v in params[l].items()} for l in range(19)}
+    t = torch.tensor(x0, dtype=torch.float64).view(n, 32, 32, 3).permute(0, 3, 1, 2)
+    for l in range(19):
+        v = vgg_layer(m, l)
+        if v["conv"]:
+            w = tp[l]["W"][:, :9 * v["cin"]].view(v["cout"], 3, 3, v["cin"]).permute(0, 3, 1, 2)
+            t = torch.relu(F.conv2d(t, w, tp[l]["b"], padding=1))
+            if v["pool"]:
+                t = F.max_pool2d(t, 2)
+        else:
+            if t.dim() == 4:
+                t = t.permute(0, 2, 3, 1).reshape(n, -1)
+            t = t @ tp[l]["W"].T + tp[l]["b"]
+            if v["relu"]:
+                t = torch.relu(t)
+    loss = F.cross_entropy(t, torch.tensor(lab), reduction="mean")
+    loss.backward()
+    assert abs(loss.item() - lsum / n) < 1e-10
+    for l in range(19):
+        for k in ("W", "b"):
+            got = grads[l][k]
+            want = tp[l][k].grad.numpy()
+            if k == "W" and vgg_layer(m, l)["conv"]:
+                v = vgg_layer(m, l)
+                want = want[:, :9 * v["cin"]]
+                got = got[:, :9 * v["cin"]]
+            assert np.allclose(got, want, rtol=1e-8, atol=1e-12), (l, k)
