@@ -40,9 +40,25 @@ MODELS = {
     # C4: GPT-2 1.5B, causal-LM cross-entropy over the padded 50304-token vocabulary
     "gpt2-1.5b": dict(kind="gpt", layers=48, hidden=1600, heads=25, ffn=6400, seq=1024, vocab=50304),
     "mlp16": dict(kind="mlp", layers=16, hidden=1024),
+    # C3: VGG-19 on 224x224 images, 1000-class cross-entropy (convs as im2col + tcgen05 GEMM)
+    "vgg19": dict(kind="vgg", layers=19, image=224, width=64, fc=4096, classes=1000),
 }
 METRIC = "training samples/sec at 1/2/4/8 B200; pipeline bubble %; predicted-vs-measured L"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def vgg_shapes(m: dict) -> list:
+    """The 19 VGG profile layers (csrc/runtime/layers.cu vgg_layer)."""
+    out, hw, cin = [], m["image"], 3
+    for convs, mult in zip((2, 2, 4, 4, 4), (1, 2, 4, 8, 8)):
+        for c in range(convs):
+            cout = m["width"] * mult
+            out.append(dict(conv=True, h=hw, w=hw, cin=cin, cout=cout, pool=c == convs - 1))
+            cin = cout
+        hw //= 2
+    for fin, fout in ((hw * hw * cin, m["fc"]), (m["fc"], m["fc"]), (m["fc"], m["classes"])):
+        out.append(dict(conv=False, fin=fin, fout=fout))
+    return out
 
 
 def flops_per_sample(m: dict) -> float:
@@ -50,6 +66,11 @@ def flops_per_sample(m: dict) -> float:
     (24h^2 + 4sh per token per layer, x3)."""
     if m["kind"] == "mlp":
         return 6.0 * m["hidden"] ** 2 * m["layers"]
+    if m["kind"] == "vgg":  # SURVEY §8(d): 19.634 GMAC fwd at 224 x 224, x2 x3
+        f = 0.0
+        for v in vgg_shapes(m):
+            f += 2.0 * v["h"] * v["w"] * 9 * v["cin"] * v["cout"] if v["conv"] else 2.0 * v["fin"] * v["fout"]
+        return 3.0 * f
     h, s, f = m["hidden"], m["seq"], m["ffn"]
     per_token = 2 * (4 * h * h + 2 * h * f) + 4 * s * h
     head = 2.0 * h * m.get("vocab", 0)  # LM head projection (SURVEY: 160,822,400 FLOP/token at V=50257)
@@ -60,12 +81,17 @@ def flops_per_sample(m: dict) -> float:
 # M=8; C4 GPT-2 a straight N-stage pipeline, M=32 micro-batches of 1 sample
 DEFAULTS = {"bert48": dict(micro_batches=8, slice=8, straight=False),
             "gpt2-1.5b": dict(micro_batches=32, slice=1, straight=True),
-            "mlp16": dict(micro_batches=8, slice=8, straight=False)}
+            "mlp16": dict(micro_batches=8, slice=8, straight=False),
+            "vgg19": dict(micro_batches=8, slice=24, straight=False)}
 
 
-def make_plan(n: int, layers: int, straight: bool = False) -> dict:
+def make_plan(n: int, layers: int, straight: bool = False, kind: str = "") -> dict:
     if n == 1:
         return {"stages": [{"layers": [0, layers], "gpus": [0], "replication": 1}]}
+    if kind == "vgg":  # C3: conv stage on N - N/4 GPUs, FC stage on N/4 (6 + 2 at N = 8)
+        fc = max(1, n // 4)
+        return {"stages": [{"layers": [0, 16], "gpus": list(range(n - fc)), "replication": n - fc},
+                           {"layers": [16, layers], "gpus": list(range(n - fc, n)), "replication": fc}]}
     if straight:
         cuts = [layers * k // n for k in range(n + 1)]
         return {"stages": [{"layers": [cuts[k], cuts[k + 1]], "gpus": [k], "replication": 1} for k in range(n)]}
@@ -185,10 +211,27 @@ def host_batches(model: dict, plan: dict, rank: int, m: int, B: int, seed: int):
     rep = stages[k]["gpus"].index(rank)
     r = len(stages[k]["gpus"])
     s0, s1 = B * rep // r, B * (rep + 1) // r  # this replica's samples of each micro-batch
-    seq, h = model.get("seq", 1), model["hidden"]
+    seq, h = model.get("seq", 1), model.get("hidden", 0)
     rows = (s1 - s0) * seq
 
     vocab = model.get("vocab", 0)
+    if model["kind"] == "vgg":  # images [M][samples * H*W*3] bf16, labels [M][samples] int32
+        e0 = model["image"] ** 2 * 3
+        n = s1 - s0
+        inp = tgt = None
+        if k == 0:
+            x = torch.empty((m, n * e0), dtype=torch.bfloat16, device="cuda")
+            for i in range(m):
+                kernels.fill_uniform_bf16(x[i], n * e0, seed, 1, (i * B + s0) * e0)
+            torch.cuda.synchronize()
+            inp = x.cpu().pin_memory()
+        if k == len(stages) - 1:
+            lab = torch.empty((m, n), dtype=torch.int32, device="cuda")
+            for i in range(m):
+                kernels.fill_tokens(lab[i], n, seed, 2, i * B + s0, model["classes"])
+            torch.cuda.synchronize()
+            tgt = lab.cpu().pin_memory()
+        return inp, tgt
 
     def gen(tensor_id):
         if vocab:  # token ids [M][rows] int32
@@ -243,7 +286,7 @@ def slice_profile(profiles: dict, plan: dict, mb: int) -> dict:
     return {**base, "layers": layers}
 
 
-def calibrated_profile(model, plan, timelines) -> dict:
+def calibrated_profile(model, plan, timelines, base=None) -> dict:
     """Per-layer F/B of the full micro-batch from a run's measured blocks
     (block time x r / layers on the stage)."""
     stages = plan["stages"]
@@ -262,6 +305,9 @@ def calibrated_profile(model, plan, timelines) -> dict:
         b = statistics.median(b_times) * r / (hi - lo)
         for l in range(lo, hi):
             per_layer[l] = (f, b)
+    if base is not None:  # byte counts from the B200 profiler's profile
+        return {**base, "layers": [{**base["layers"][l], "fwd_time_us": per_layer[l][0] * 1e6,
+                                    "bwd_time_us": per_layer[l][1] * 1e6} for l in range(model["layers"])]}
     h = model["hidden"]
     params = (12 * h * h + 13 * h) * 4 if model["kind"] != "mlp" else (h * h + h) * 4
     return {"profile_batch_size": 8, "layers": [
@@ -377,7 +423,8 @@ def main():
     model = MODELS[args.model]
     M = args.micro_batches
     straight = dflt["straight"]
-    gbs = args.global_batch or M * args.slice * (1 if straight else max(1, world // 2))
+    strong = straight or model["kind"] == "vgg"  # fixed global batch at every N
+    gbs = args.global_batch or M * args.slice * (1 if straight or model["kind"] == "vgg" else max(1, world // 2))
     cluster = b200_cluster(world, args.mem_gb)
     # pre-run B200 layer profile at the micro-batch size: the planner's input
     # and the source of the predicted L (a real prediction, made before the run)
@@ -389,7 +436,7 @@ def main():
         plan = pipeplan.plan(profiles[mb], cluster, M)["plan"] if rank == 0 else None
         plan = broadcast(plan, world)
     else:
-        plan = make_plan(world, model["layers"], straight)
+        plan = make_plan(world, model["layers"], straight, model["kind"])
     if profiles and rank == 0:
         for st in plan["stages"]:
             size = -(-mb // len(st["gpus"]))
@@ -499,7 +546,7 @@ def main():
             traffic = json.load(f).get("bytes_per_launch")
     except Exception:
         pass
-    calib = calibrated_profile(model, plan, [all_tls[r][-1] for r in range(world)])
+    calib = calibrated_profile(model, plan, [all_tls[r][-1] for r in range(world)], profile)
     pred_cal = predicted_latency(plan, calib, cluster, M, world, args.schedule)
     pred = None
     if profile is not None:
@@ -526,7 +573,7 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": measured_ms, "higher_is_better": True,
-        "scaling": "strong" if straight else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded splitmix64 inputs/targets, random-init "
+        "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded splitmix64 inputs/targets, random-init "
                                                       "weights)",
         "config": {"workload": args.model, **model, "global_batch": gbs, "micro_batches": M,
                    "plan_source": "host planner (pipeplan.plan on the B200 profile, per_gpu_memory_gb="

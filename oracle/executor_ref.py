@@ -631,9 +631,13 @@ class CpuTrainer:
     def step(self, sample0: int, samples: int, lr: float = 1e-3) -> float:
         m = self.model
         lm = m.vocab > 0
+        vgg = m.kind == "vgg"
         if lm:
             tok, tgt = lm_tokens(m, self.seed, sample0, samples)
             x = embed_forward(m, self.lm, tok)
+        elif vgg:
+            x, labels = vgg_batch(m, self.seed, sample0, samples)
+            x = x.astype(self.dtype)
         else:
             x, t = batch_data(m, self.seed, sample0, samples)
             x, t = x.astype(self.dtype), t.astype(self.dtype)
@@ -646,6 +650,9 @@ class CpuTrainer:
             lsum, hc = head_forward(m, self.lm, x, tgt, ntok)
             loss = lsum / ntok
             dy, g_head = head_backward(m, self.lm, hc)
+        elif vgg:
+            lsum, dy = class_ce(x, labels, 1.0 / samples, _ident)
+            loss = lsum / samples
         else:
             numel = samples * m.seq * m.hidden
             diff = x - t
