@@ -434,10 +434,7 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
       col = std::max(col, layer->col_elems(ctx_));
       dz = std::max(dz, layer->dz_elems(ctx_));
     }
-    if (col) {
-      ctx_.conv_col = static_cast<bf16*>(mem_.alloc(col * 2));
-      ctx_.conv_dcol = static_cast<bf16*>(mem_.alloc(col * 2));
-    }
+    if (col) ctx_.conv_dcol = static_cast<bf16*>(mem_.alloc(col * 2));
     ctx_.conv_dz = static_cast<bf16*>(mem_.alloc(std::max<size_t>(dz, 8) * 2));
   } else if (spec_.kind != "mlp") {
     const size_t z = static_cast<size_t>(spec_.heads) * ctx_.samples;

@@ -403,18 +403,21 @@ class ConvLayer final : public Layer {
     init_params({{0, nw, 0, std::sqrt(6.0f / (9.0f * v_.cin))}, {nw, static_cast<size_t>(v_.cout), 1, 0.05f}},
                 index_, w32, w16, param_count(), seed, s);
   }
-  size_t col_elems(const StageContext& c) const override { return px(c) * v_.kp; }
+  size_t col_elems(const StageContext& c) const override { return px(c) * v_.kp; }  // dcol scratch
   size_t dz_elems(const StageContext& c) const override { return px(c) * v_.cout; }
   void alloc_stash(StageContext& ctx) override {
-    if (v_.pool)  // post-ReLU, pre-pool output for the pool backward
-      for (int k = 0; k < ctx.slots; ++k) yr_.push_back(alloc_n<bf16>(ctx, px(ctx) * v_.cout));
+    for (int k = 0; k < ctx.slots; ++k) {
+      // the forward's columns are kept for the weight gradient (no second im2col)
+      col_.push_back(alloc_n<bf16>(ctx, px(ctx) * v_.kp));
+      if (v_.pool) yr_.push_back(alloc_n<bf16>(ctx, px(ctx) * v_.cout));  // post-ReLU, pre-pool output
+    }
   }
   void forward(StageContext& ctx, int slot, const bf16* x, bf16* y) override {
     const int n = ctx.samples;
     const int rows = static_cast<int>(px(ctx));
-    im2col3x3(x, ctx.conv_col, n, v_.h, v_.w, v_.cin, v_.kp, ctx.stream);
+    im2col3x3(x, col_[slot], n, v_.h, v_.w, v_.cin, v_.kp, ctx.stream);
     bf16* out = v_.pool ? yr_[slot] : y;
-    GemmDesc d = plain(rows, v_.cout, v_.kp, ctx.conv_col, v_.kp, false, w16_, v_.kp, false, out, v_.cout,
+    GemmDesc d = plain(rows, v_.cout, v_.kp, col_[slot], v_.kp, false, w16_, v_.kp, false, out, v_.cout,
                        kBias | kRelu);
     d.bias = w32_ + static_cast<size_t>(v_.cout) * v_.kp;
     ctx.gemms.run(d, ctx.stream);
@@ -427,9 +430,9 @@ class ConvLayer final : public Layer {
     else relu_bwd(ctx.cur_y, dy, ctx.conv_dz, static_cast<long long>(rows) * v_.cout, ctx.stream);
     float* gw = g32_;
     colsum_acc(ctx.conv_dz, gw + static_cast<size_t>(v_.cout) * v_.kp, rows, v_.cout, ctx.stream);
-    // dW += dz^T col (columns recomputed from the stashed input)
-    im2col3x3(x, ctx.conv_col, n, v_.h, v_.w, v_.cin, v_.kp, ctx.stream);
-    ctx.gemms.run(plain(v_.cout, v_.kp, rows, ctx.conv_dz, v_.cout, true, ctx.conv_col, v_.kp, true, gw, v_.kp,
+    // dW += dz^T col (the forward's stashed columns)
+    (void)x;
+    ctx.gemms.run(plain(v_.cout, v_.kp, rows, ctx.conv_dz, v_.cout, true, col_[slot], v_.kp, true, gw, v_.kp,
                         kOutF32Acc),
                   ctx.stream);
     if (dx) {
@@ -456,6 +459,7 @@ class ConvLayer final : public Layer {
   float* g32_ = nullptr;
   bf16* w16_ = nullptr;
   std::vector<bf16*> yr_;
+  std::vector<bf16*> col_;  // per slot: im2col columns of the forward
 };
 
 // y = x W^T + b (+ReLU), W [fout][fin]; takes / returns output / input gradients
