@@ -170,3 +170,29 @@ def test_timeline_export_reproduces_reference_writers():
         if not req.get("recompute"):
             assert got["latency"] == want["latency"]
         assert got["svg"].startswith("<svg")
+
+
+def test_parallel_search_is_bit_identical_to_sequential():
+    """plan() expands BFS batches on worker threads (DPL_PLANNER_THREADS) and
+    replays leaderboard offers / memo decisions in FIFO order: the plan and
+    the whole top-k report must equal the single-threaded search's."""
+    import subprocess
+    import sys
+    code = """
+import json, random, sys
+sys.path.insert(0, %r)
+from paper_2007_01045_b200 import pipeplan
+r = random.Random(7)
+prof = {"profile_batch_size": 8, "layers": [{"fwd_time_us": r.uniform(100, 1000), "bwd_time_us": r.uniform(200, 2000),
+        "activation_bytes": r.randint(1 << 20, 1 << 26), "param_bytes": r.randint(1 << 20, 1 << 27)} for _ in range(20)]}
+cl = {"seps": [4, 4], "intra_bw_gbps": 300.0, "inter_bw_gbps": 25.0, "intra_latency_us": 5.0,
+      "inter_latency_us": 10.0, "per_gpu_memory_gb": 40.0}
+print(json.dumps(pipeplan.plan(prof, cl, 8, report=True), sort_keys=True))
+""" % os.path.dirname(HERE)
+    outs = []
+    for threads in ("1", "4"):
+        env = dict(os.environ, DPL_PLANNER_THREADS=threads)
+        outs.append(subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                                   check=True).stdout)
+    assert outs[0] == outs[1]
+    assert json.loads(outs[0])["report"]["states_evaluated"] > 10000
