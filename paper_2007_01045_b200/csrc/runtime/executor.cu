@@ -168,6 +168,7 @@ class Executor {
     for (auto it = graphs_.begin(); it != graphs_.end();) {
       if (it->first.profile) {
         cudaGraphExecDestroy(it->second);
+        graph_kernels_.erase(graph_kernels_.begin() + (it - graphs_.begin()));
         it = graphs_.erase(it);
       } else {
         ++it;
@@ -255,6 +256,7 @@ class Executor {
     }
   };
   std::vector<std::pair<GraphKey, cudaGraphExec_t>> graphs_;
+  std::vector<long long> graph_kernels_;  // kernel nodes of graphs_[i] (launch accounting per replay)
   void enqueue_step(const void* host_input, const void* host_target);
   // this rank's gradients of one parameter block are final: AllReduce over
   // the replica group and apply on the reduce stream
@@ -558,6 +560,7 @@ void Executor::disconnect() {
   // captured steps reference the communicator and the peer mappings
   for (auto& g : graphs_) cudaGraphExecDestroy(g.second);
   graphs_.clear();
+  graph_kernels_.clear();
   if (comm_) {
     ncclCommDestroy(comm_);
     comm_ = nullptr;
@@ -887,12 +890,17 @@ float Executor::step(const void* host_input, const void* host_target) {
     // its records are re-registered on every capture
     const GraphKey key{bank_, host_input, host_target, profiling};
     cudaGraphExec_t exec = nullptr;
-    for (auto& g : graphs_)
-      if (g.first == key) exec = g.second;
+    long long kernels = 0;
+    for (size_t gi = 0; gi < graphs_.size(); ++gi)
+      if (graphs_[gi].first == key) {
+        exec = graphs_[gi].second;
+        kernels = graph_kernels_[gi];
+      }
     // capture (a stream memory op that cannot be captured invalidates the
     // capture; wait_flag then switches to its kernel form and we retry once)
     for (int attempt = 0; !exec && attempt < 2; ++attempt) {
       cudaGraph_t graph = nullptr;
+      const long long counted0 = launch_count();
       DPL_CUDA(cudaStreamBeginCapture(compute_, cudaStreamCaptureModeRelaxed));
       capturing_ = true;
       kernel_timer().capturing = true;
@@ -905,15 +913,30 @@ float Executor::step(const void* host_input, const void* host_target) {
       capturing_ = false;
       kernel_timer().capturing = false;
       const cudaError_t end = cudaStreamEndCapture(compute_, &graph);
+      // captured launches are not executions: the kernel nodes are counted
+      // on every replay instead
+      count_launch(counted0 - launch_count());
       if (ok && end == cudaSuccess && graph) {
         DPL_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        size_t n_nodes = 0;
+        DPL_CUDA(cudaGraphGetNodes(graph, nullptr, &n_nodes));
+        std::vector<cudaGraphNode_t> nodes(n_nodes);
+        DPL_CUDA(cudaGraphGetNodes(graph, nodes.data(), &n_nodes));
+        kernels = 0;
+        for (cudaGraphNode_t nd : nodes) {
+          cudaGraphNodeType t;
+          DPL_CUDA(cudaGraphNodeGetType(nd, &t));
+          if (t == cudaGraphNodeTypeKernel) ++kernels;
+        }
         graphs_.push_back({key, exec});
+        graph_kernels_.push_back(kernels);
       }
       if (graph) cudaGraphDestroy(graph);
       cudaGetLastError();
       if (!exec && attempt == 1) throw std::runtime_error("dpl exec: step capture failed");
     }
     DPL_CUDA(cudaGraphLaunch(exec, compute_));
+    count_launch(kernels);
   }
   DPL_CUDA(cudaStreamSynchronize(compute_));
   DPL_CUDA(cudaGetLastError());

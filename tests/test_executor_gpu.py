@@ -91,3 +91,23 @@ def test_layer_profiler_emits_reference_profile(cuda):
     check_loss(ex.step(), emu, exact)
     check_grads(ex, emu, exact, range(3), "bert", 3)
     ex.close()
+
+
+def test_launch_count_covers_graph_replays(cuda):
+    """Steps replay a captured CUDA graph; every replay adds the graph's kernel
+    nodes to dpl_k_launch_count (captured launches themselves are not counted)."""
+    from paper_2007_01045_b200 import _lib
+    from paper_2007_01045_b200.runtime import Executor
+    lib = _lib.lib()
+    model = dict(kind="bert", layers=2, hidden=256, heads=4, ffn=1024, seq=128)
+    plan = {"stages": [{"layers": [0, 2], "gpus": [0], "replication": 1}]}
+    ex = Executor(model, plan, 2, 4)
+    ex.step()  # capture + first replay
+    c0 = lib.dpl_k_launch_count()
+    ex.step()
+    c1 = lib.dpl_k_launch_count()
+    ex.step()
+    c2 = lib.dpl_k_launch_count()
+    ex.close()
+    per_step = c1 - c0
+    assert per_step > 50 and c2 - c1 == per_step
