@@ -76,6 +76,7 @@ typedef struct dpl_gemm_desc {
    * epilogue start, epilogue end, exit, then (TMA epilogue, first epilogue
    * warp) input ready / store issued for its first 4 chunks.  NULL = off. */
   unsigned long long* trace;
+  float* colsum; /* DPL_EPI_COLSUM target: colsum[n] += sum_m C[m][n] (bf16 C as stored) */
 } dpl_gemm_desc;
 
 #define DPL_EPI_OUT_BF16 0u
@@ -88,6 +89,7 @@ typedef struct dpl_gemm_desc {
 #define DPL_EPI_DGELU (1u << 6)
 #define DPL_EPI_DRELU (1u << 7)
 #define DPL_EPI_RESID (1u << 8)
+#define DPL_EPI_COLSUM (1u << 9) /* + column sums of the bf16 output into desc.colsum */
 
 int dpl_k_gemm(const dpl_gemm_desc* desc, void* stream);
 /* Fused attention forward, head dim 64: qkv head-split [3][heads][B][S][64],

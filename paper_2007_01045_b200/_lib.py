@@ -30,13 +30,14 @@ class GemmDesc(ctypes.Structure):
         ("s_no", ctypes.c_longlong), ("epi", ctypes.c_uint32), ("alpha", ctypes.c_float),
         ("bias", ctypes.c_void_p), ("aux_in", ctypes.c_void_p), ("resid", ctypes.c_void_p),
         ("aux_out", ctypes.c_void_p), ("force_bn", ctypes.c_int), ("force_1sm", ctypes.c_int),
-        ("trace", ctypes.c_void_p),
+        ("trace", ctypes.c_void_p), ("colsum", ctypes.c_void_p),
     ]
 
 
 EPI_OUT_BF16, EPI_OUT_F32, EPI_OUT_F32_ACC = 0, 1, 2
 EPI_BIAS, EPI_GELU, EPI_RELU, EPI_AUX_OUT = 1 << 2, 1 << 3, 1 << 4, 1 << 5
 EPI_DGELU, EPI_DRELU, EPI_RESID = 1 << 6, 1 << 7, 1 << 8
+EPI_COLSUM = 1 << 9
 
 _VP, _I, _LL, _F, _U64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong, ctypes.c_float, ctypes.c_uint64
 

@@ -82,6 +82,7 @@ int dpl_k_gemm(const dpl_gemm_desc* d, void* stream) {
     g.ndiv = d->ndiv; g.s_no = d->s_no; g.epi = d->epi; g.alpha = d->alpha; g.bias = d->bias;
     g.aux_in = d->aux_in; g.resid = d->resid; g.aux_out = d->aux_out; g.force_bn = d->force_bn; g.force_1sm = d->force_1sm;
     g.trace = d->trace;
+    g.colsum = d->colsum;
     dpl::GemmOp op;
     op.prepare(g);
     op.launch(static_cast<cudaStream_t>(stream));

@@ -33,6 +33,7 @@ enum GemmEpilogue : uint32_t {
   kDGelu = 1u << 6,  // * gelu'(aux_in)
   kDRelu = 1u << 7,  // * relu'(aux_in)
   kResid = 1u << 8,  // + resid (bf16), added after bias, before activation
+  kColSum = 1u << 9, // also colsum[n] += sum_m C[m][n] of the stored bf16 output (bias gradient)
 };
 
 struct GemmDesc {
@@ -58,6 +59,7 @@ struct GemmDesc {
   int force_bn = 0;  // 0 = heuristic; else 64/128/256
   int force_1sm = 0; // 1 = never use the CTA-pair kernel
   unsigned long long* trace = nullptr;  // per-CTA phase timestamps (16 per CTA), diagnostics
+  float* colsum = nullptr;              // kColSum target (fp32, N)
 };
 
 // Device-visible launch parameters (one per prepared GEMM).
@@ -75,6 +77,7 @@ struct alignas(64) GemmParams {
   int epi_out_bytes;   // one output chunk buffer (2 KB bf16 / 4 KB fp32)
   int epi_nx;          // extra-tensor chunk buffers per warp
   int epi_tile_cols;   // columns of one CTA tile (bias slice staged per warp)
+  float* colsum;       // kColSum target (TMA epilogue; otherwise a colsum pass after the GEMM)
   int M, N, K, batch;
   int a_mn_major, b_mn_major;
   int num_m_blocks, num_n_blocks, num_k_blocks, num_tiles;
@@ -101,6 +104,7 @@ class GemmOp {
   GemmOp() = default;
   void prepare(const GemmDesc& d);
   void launch(cudaStream_t stream) const;
+  void launch_kernel(cudaStream_t stream) const;
   int bn() const { return bn_; }
   bool two_sm() const { return params_.two_sm != 0; }
   int grid() const { return grid_; }
@@ -110,6 +114,7 @@ class GemmOp {
 
  private:
   GemmParams params_{};
+  bool colsum_fallback_ = false;
   int bn_ = 0;
   int grid_ = 0;
   size_t smem_ = 0;

@@ -26,6 +26,7 @@
 #include <stdexcept>
 #include <string>
 
+#include "elementwise.h"
 #include "gemm.h"
 #include "launch.cuh"
 #include "ptx.cuh"
@@ -451,6 +452,19 @@ __device__ __forceinline__ void epi_tile_tma(const GemmParams& p, EpiTma& e, uin
           wp[k] = *reinterpret_cast<uint32_t*>(&h);
         }
         *reinterpret_cast<uint4*>(obuf + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) = w;
+      }
+    }
+    if (epi & kColSum) {
+      // column sums of the staged (bf16) chunk: lane j sums column j over the valid rows
+      __syncwarp();
+      if (!f32) {
+        float cs = 0.f;
+        const int q = lane >> 3, e = lane & 7;
+        const int rows = min(32, p.M - row0);
+        for (int r = 0; r < rows; ++r)
+          cs += __bfloat162float(
+              *reinterpret_cast<const __nv_bfloat16*>(obuf + r * 64 + ((q ^ ((r >> 1) & 3)) << 4) + e * 2));
+        if (n0 + static_cast<int>(lane) < p.N) atomicAdd(p.colsum + n0 + lane, cs);
       }
     }
     ptx::fence_proxy_async_smem();
@@ -1107,7 +1121,11 @@ void GemmOp::prepare(const GemmDesc& d) {
   const bool aux_aligned = !(d.aux_in || d.resid || d.aux_out) || ((d.ldc * 2) % 16 == 0 && (d.s_zo * 2) % 16 == 0 &&
                                                                    (d.s_zi * 2) % 16 == 0 && (d.s_no * 2) % 16 == 0);
   p.vec_ok = aligned && aux_aligned;
+  colsum_fallback_ = false;
   p.trace = d.trace;
+  p.colsum = d.colsum;
+  if ((d.epi & kColSum) && (!d.colsum || (d.epi & kOutMask) != kOutBf16 || d.batch != 1))
+    throw std::invalid_argument("dpl gemm: kColSum needs a colsum target, a bf16 output and batch 1");
   // TMA epilogue: bulk tensor stores / fp32 reduce-adds from swizzled smem
   // chunks, extra input bulk-loaded ahead of use (see EpiTma)
   {
@@ -1155,6 +1173,13 @@ void GemmOp::prepare(const GemmDesc& d) {
       if (x) p.tma_x = make_epi_map(x, false, d, inner, nhi);
       p.tma_epi = 1;
     }
+    // without the TMA epilogue the column sums run as a separate pass
+    colsum_fallback_ = (d.epi & kColSum) && !p.tma_epi;
+    if (colsum_fallback_) {
+      if (d.ldc != d.N || d.zdiv != 1 || d.ndiv < d.N)
+        throw std::invalid_argument("dpl gemm: kColSum fallback needs a plain [M][N] output");
+      p.epi &= ~static_cast<uint32_t>(kColSum);
+    }
   }
   bn_ = bn;
   grid_ = two_sm ? 2 * std::min(p.num_tiles, num_sms() / 2) : std::min(p.num_tiles, num_sms());
@@ -1192,7 +1217,8 @@ const GemmOp& GemmCache::get(const GemmDesc& d) {
                          static_cast<long long>(reinterpret_cast<uintptr_t>(d.aux_in)),
                          static_cast<long long>(reinterpret_cast<uintptr_t>(d.resid)),
                          static_cast<long long>(reinterpret_cast<uintptr_t>(d.aux_out)), d.force_bn, d.force_1sm,
-                         static_cast<long long>(reinterpret_cast<uintptr_t>(d.trace))};
+                         static_cast<long long>(reinterpret_cast<uintptr_t>(d.trace)),
+                         static_cast<long long>(reinterpret_cast<uintptr_t>(d.colsum))};
   std::string key(reinterpret_cast<const char*>(f), sizeof f);
   uint32_t a;
   std::memcpy(&a, &d.alpha, 4);
@@ -1242,6 +1268,12 @@ void GemmCache::run(const GemmDesc& d, cudaStream_t s) {
 }
 
 void GemmOp::launch(cudaStream_t stream) const {
+  launch_kernel(stream);
+  if (colsum_fallback_)  // kColSum without the TMA epilogue: a column-sum pass over C
+    colsum_acc(params_.C, params_.colsum, params_.M, params_.N, stream);
+}
+
+void GemmOp::launch_kernel(cudaStream_t stream) const {
   count_launch();
   TimedLaunch timed_("gemm_bf16_tcgen05", stream, flops());
   if (params_.two_sm) {

@@ -258,13 +258,14 @@ class TransformerLayer final : public Layer {
     // FFN2: dW2 += dy^T g ; db2 ; dz1 = (dy W2) * gelu'(z1)
     ctx.gemms.run(plain(H_, F_, R, dy, H_, true, st.g, F_, true, g32_ + w2_, F_, kOutF32Acc), str);
     {
-      GemmDesc d = plain(R, F_, H_, dy, H_, false, w16_ + w2_, F_, true, dz1, F_, kDGelu);
+      // db1 = colsum(dz1) accumulated by the epilogue from the staged chunks
+      GemmDesc d = plain(R, F_, H_, dy, H_, false, w16_ + w2_, F_, true, dz1, F_, kDGelu | kColSum);
       d.aux_in = st.z1;
+      d.colsum = g32_ + b1_;
       ctx.gemms.run(d, str);
     }
-    // FFN1: dW1 += dz1^T ln2 ; db1 ; dln2 = dz1 W1
+    // FFN1: dW1 += dz1^T ln2 ; dln2 = dz1 W1
     ctx.gemms.run(plain(F_, H_, R, dz1, F_, true, st.ln2, H_, true, g32_ + w1_, H_, kOutF32Acc), str);
-    colsum_acc(dz1, g32_ + b1_, R, F_, str);
     ctx.gemms.run(plain(R, H_, F_, dz1, F_, false, w16_ + w1_, H_, true, dln, H_, kOutBf16), str);
     // LN2 backward (+ residual gradient dy); also db2 = colsum(dy) and
     // dbo = colsum(dh) from the rows it already holds

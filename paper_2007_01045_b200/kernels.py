@@ -6,7 +6,7 @@ from __future__ import annotations
 import ctypes
 
 from ._lib import (EPI_AUX_OUT, EPI_BIAS, EPI_DGELU, EPI_DRELU, EPI_GELU, EPI_OUT_BF16, EPI_OUT_F32,  # noqa: F401
-                   EPI_OUT_F32_ACC, EPI_RELU, EPI_RESID, GemmDesc, check, lib)
+                   EPI_OUT_F32_ACC, EPI_RELU, EPI_RESID, EPI_COLSUM, GemmDesc, check, lib)
 
 
 def _ptr(t):
@@ -20,7 +20,7 @@ def _stream():
 
 def gemm(A, B, C, M, N, K, *, lda, ldb, ldc, a_mn_major=False, b_mn_major=False, batch=1, a_batch_stride=0,
          b_batch_stride=0, epi=EPI_OUT_BF16, alpha=1.0, bias=None, aux_in=None, resid=None, aux_out=None, zdiv=1,
-         s_zo=None, s_zi=0, ndiv=1 << 30, s_no=0, force_bn=0, force_1sm=False, trace=None):
+         s_zo=None, s_zi=0, ndiv=1 << 30, s_no=0, force_bn=0, force_1sm=False, trace=None, colsum=None):
     """C[z,m,n] = epi(alpha * sum_k A[z,m,k] * B[z,n,k]) (see csrc/kernels/gemm.h)."""
     d = GemmDesc()
     d.M, d.N, d.K, d.batch = M, N, K, batch
@@ -37,6 +37,7 @@ def gemm(A, B, C, M, N, K, *, lda, ldb, ldc, a_mn_major=False, b_mn_major=False,
     d.force_bn = force_bn
     d.force_1sm = int(force_1sm)
     d.trace = None if trace is None else trace.data_ptr()
+    d.colsum = None if colsum is None else colsum.data_ptr()
     check(lib().dpl_k_gemm(ctypes.byref(d), _stream()))
 
 

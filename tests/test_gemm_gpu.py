@@ -121,3 +121,21 @@ def test_gemm_attention_head_split_merge(cuda):
     torch.cuda.synchronize()
     ref_ctx = (P.float() @ v.float()).view(nh, B_, S, d).permute(1, 2, 0, 3).reshape(T, H)
     _close(ctx, ref_ctx, 2e-2)
+
+
+@pytest.mark.parametrize("m,n,k,one_sm", [(4096, 4096, 1024, False), (300, 200, 128, True), (1024, 1600, 6400, False)])
+def test_gemm_colsum_epilogue(cuda, m, n, k, one_sm):
+    """DPL_EPI_COLSUM: colsum[n] += sum over rows of the stored bf16 output
+    (the FFN bias gradient fused into the dgrad GEMM)."""
+    import torch
+    from paper_2007_01045_b200 import kernels as K
+    g = torch.Generator(device="cpu").manual_seed(11)
+    a = (torch.rand(m, k, generator=g) - 0.5).to(torch.bfloat16).to(cuda)
+    b = (torch.rand(n, k, generator=g) - 0.5).to(torch.bfloat16).to(cuda)
+    c = torch.empty(m, n, dtype=torch.bfloat16, device=cuda)
+    cs = torch.full((n,), 0.5, device=cuda)
+    K.gemm(a, b, c, m, n, k, lda=k, ldb=k, ldc=n, epi=K.EPI_OUT_BF16 | K.EPI_COLSUM, colsum=cs, force_1sm=one_sm)
+    torch.cuda.synchronize()
+    ref = c.float().sum(0) + 0.5
+    assert torch.allclose(c.float(), a.float() @ b.float().T, rtol=2e-2, atol=2e-2)
+    assert torch.allclose(cs, ref, rtol=1e-4, atol=1e-2 * m ** 0.5 * 0.01)
