@@ -924,9 +924,14 @@ float Executor::step(const void* host_input, const void* host_target) {
         DPL_CUDA(cudaGraphGetNodes(graph, nodes.data(), &n_nodes));
         kernels = 0;
         for (cudaGraphNode_t nd : nodes) {
+          // stream memory-op nodes (the flag waits) have no runtime-API type:
+          // the query fails for them, which is fine -- only kernels count
           cudaGraphNodeType t;
-          DPL_CUDA(cudaGraphNodeGetType(nd, &t));
-          if (t == cudaGraphNodeTypeKernel) ++kernels;
+          if (cudaGraphNodeGetType(nd, &t) == cudaSuccess) {
+            if (t == cudaGraphNodeTypeKernel) ++kernels;
+          } else {
+            cudaGetLastError();
+          }
         }
         graphs_.push_back({key, exec});
         graph_kernels_.push_back(kernels);

@@ -45,6 +45,10 @@ CASES += [
 TWO = {"stages": [{"layers": [0, 2], "gpus": [0]}, {"layers": [2, 4], "gpus": [1]}]}
 # GPipe / re-computation on the device (the schedules of the paper's Table VI)
 SCHED_CASES = [
+    (2, VGGS, {"stages": [{"layers": [0, 12], "gpus": [0]}, {"layers": [12, 19], "gpus": [1]}]}, 4, 8, "gpipe", True),
+    (2, LMGPT, TWO, 4, 8, "dapple", True),
+    (4, LMGPT, {"stages": [{"layers": [0, 1], "gpus": [0]}, {"layers": [1, 4], "gpus": [1, 2, 3]}]}, 2, 8,
+     "dapple", False),
     (2, BERT, TWO, 4, 8, "gpipe", False),
     (2, MLP, TWO, 4, 24, "dapple", True),
     (2, BERT, TWO, 4, 8, "gpipe", True),
