@@ -357,7 +357,8 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     model = MODELS[args.model]
-    layers = min(model["layers"], args.ref_layers)
+    # VGG's loss needs the classifier: always the whole 19-layer net on one sample
+    layers = model["layers"] if model["kind"] == "vgg" else min(model["layers"], args.ref_layers)
     from oracle.executor_ref import CpuTrainer
     sub = dict(model, layers=layers)
     tr = CpuTrainer(sub)
@@ -372,7 +373,8 @@ def run_reference(args, rank, world):
     unit = "samples/s"
     line = {"metric": METRIC, "value": value, "unit": unit, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+            "scaling": "strong" if DEFAULTS[args.model]["straight"] or model["kind"] == "vgg" else "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
             "config": {"workload": args.model, **model},
             "cpu_baseline": {"value": value, "unit": unit, "cores": os.cpu_count(), "kind": "port",
                              "sample": f"each step: 1 sample x {layers}/{model['layers']} layers fwd+bwd+SGD, "
