@@ -77,6 +77,11 @@ typedef struct dpl_gemm_desc {
    * warp) input ready / store issued for its first 4 chunks.  NULL = off. */
   unsigned long long* trace;
   float* colsum; /* DPL_EPI_COLSUM target: colsum[n] += sum_m C[m][n] (bf16 C as stored) */
+  /* implicit-GEMM 3x3 pad-1 convolution over NHWC conv_x [n][h][w][c], c % 64 == 0:
+   * conv_operand 1 = A is im2col(conv_x) (M = n*h*w, K = 9c); 2 = B is im2col(conv_x)
+   * MN-major (K = n*h*w, N = 9c); loaded by TMA in im2col mode, no column matrix */
+  const void* conv_x;
+  int conv_operand, conv_n, conv_h, conv_w, conv_c;
 } dpl_gemm_desc;
 
 #define DPL_EPI_OUT_BF16 0u

@@ -31,6 +31,8 @@ class GemmDesc(ctypes.Structure):
         ("bias", ctypes.c_void_p), ("aux_in", ctypes.c_void_p), ("resid", ctypes.c_void_p),
         ("aux_out", ctypes.c_void_p), ("force_bn", ctypes.c_int), ("force_1sm", ctypes.c_int),
         ("trace", ctypes.c_void_p), ("colsum", ctypes.c_void_p),
+        ("conv_x", ctypes.c_void_p), ("conv_operand", ctypes.c_int), ("conv_n", ctypes.c_int),
+        ("conv_h", ctypes.c_int), ("conv_w", ctypes.c_int), ("conv_c", ctypes.c_int),
     ]
 
 

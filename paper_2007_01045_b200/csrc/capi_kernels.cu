@@ -83,6 +83,12 @@ int dpl_k_gemm(const dpl_gemm_desc* d, void* stream) {
     g.aux_in = d->aux_in; g.resid = d->resid; g.aux_out = d->aux_out; g.force_bn = d->force_bn; g.force_1sm = d->force_1sm;
     g.trace = d->trace;
     g.colsum = d->colsum;
+    g.conv_x = d->conv_x;
+    g.conv_operand = d->conv_operand;
+    g.conv_n = d->conv_n;
+    g.conv_h = d->conv_h;
+    g.conv_w = d->conv_w;
+    g.conv_c = d->conv_c;
     dpl::GemmOp op;
     op.prepare(g);
     op.launch(static_cast<cudaStream_t>(stream));

@@ -60,6 +60,11 @@ struct GemmDesc {
   int force_1sm = 0; // 1 = never use the CTA-pair kernel
   unsigned long long* trace = nullptr;  // per-CTA phase timestamps (16 per CTA), diagnostics
   float* colsum = nullptr;              // kColSum target (fp32, N)
+  // implicit-GEMM 3x3 / pad-1 convolution over NHWC conv_x [n][h][w][c] (c % 64 == 0):
+  //   conv_operand 1: A[M = n*h*w][K = 9c] are its im2col columns (K-major, A unused)
+  //   conv_operand 2: B[K = n*h*w][N = 9c] are its im2col columns (MN-major, B unused)
+  const void* conv_x = nullptr;
+  int conv_operand = 0, conv_n = 0, conv_h = 0, conv_w = 0, conv_c = 0;
 };
 
 // Device-visible launch parameters (one per prepared GEMM).
@@ -78,6 +83,7 @@ struct alignas(64) GemmParams {
   int epi_nx;          // extra-tensor chunk buffers per warp
   int epi_tile_cols;   // columns of one CTA tile (bias slice staged per warp)
   float* colsum;       // kColSum target (TMA epilogue; otherwise a colsum pass after the GEMM)
+  int conv_operand, conv_h, conv_w, conv_c;  // implicit-GEMM convolution operand (GemmDesc)
   int M, N, K, batch;
   int a_mn_major, b_mn_major;
   int num_m_blocks, num_n_blocks, num_k_blocks, num_tiles;

@@ -75,6 +75,21 @@ __device__ __forceinline__ float dgelu_f(float x) {
   return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * kGeluK0 * fmaf(3.0f * kGeluK1, x2, 1.0f);
 }
 
+// Implicit-GEMM convolution: load the im2col tile whose first pixel (output
+// position, row-major n, h, w) is `pixel` and whose 64 channels start at
+// K / N index `kidx` (= tap * C + c0, C % 64 == 0) into dst.
+template <bool kPair>
+__device__ __forceinline__ void conv_tile_load(const GemmParams& p, const CUtensorMap* map, void* dst, uint64_t* bar,
+                                               int pixel, int kidx) {
+  const int tap = kidx / p.conv_c, c0 = kidx % p.conv_c;
+  const int hw = p.conv_h * p.conv_w;
+  const int n = pixel / hw, rem = pixel % hw;
+  const int ho = rem / p.conv_w, wo = rem % p.conv_w;
+  const uint16_t kh = static_cast<uint16_t>(tap / 3), kw = static_cast<uint16_t>(tap % 3);
+  if (kPair) ptx::tma_load_im2col_4d_2sm(dst, map, bar, c0, wo - 1, ho - 1, n, kw, kh);
+  else ptx::tma_load_im2col_4d(dst, map, bar, c0, wo - 1, ho - 1, n, kw, kh);
+}
+
 // diagnostics: phase timestamps per CTA (GemmDesc::trace)
 __device__ __forceinline__ void trace_mark(const GemmParams& p, int slot) {
   if (p.trace) {
@@ -547,14 +562,20 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
           ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
           uint8_t* sa = smem_a + stage * C::kABytes;
           uint8_t* sb = smem_b + stage * C::kBBytes;
-          if (!p.a_mn_major) {
+          if (p.conv_operand == 1) {
+            conv_tile_load<false>(p, &p.tma_a, sa, &full[stage], mb * kBM, kb * kBK);
+          } else if (!p.a_mn_major) {
             ptx::tma_load_3d(sa, &p.tma_a, &full[stage], kb * kBK, mb * kBM, z);
           } else {
 #pragma unroll
             for (int j = 0; j < kBM / 64; ++j)
               ptx::tma_load_3d(sa + j * 64 * kBK * 2, &p.tma_a, &full[stage], mb * kBM + j * 64, kb * kBK, z);
           }
-          if (!p.b_mn_major) {
+          if (p.conv_operand == 2) {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              conv_tile_load<false>(p, &p.tma_b, sb + j * 64 * kBK * 2, &full[stage], kb * kBK, nb * BN + j * 64);
+          } else if (!p.b_mn_major) {
             ptx::tma_load_3d(sb, &p.tma_b, &full[stage], kb * kBK, nb * BN, z);
           } else {
 #pragma unroll
@@ -794,13 +815,19 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
           else ptx::mbar_arrive_cluster(&full[stage], 0);
           uint8_t* sa = smem_a + stage * kABytes;
           uint8_t* sb = smem_b + stage * kBBytes;
-          if (!p.a_mn_major) {
+          if (p.conv_operand == 1) {
+            conv_tile_load<true>(p, &p.tma_a, sa, &full[stage], m0, kb * kBK);
+          } else if (!p.a_mn_major) {
             ptx::tma_load_3d_2sm(sa, &p.tma_a, &full[stage], kb * kBK, m0, z);
           } else {
 #pragma unroll
             for (int j = 0; j < 2; ++j) ptx::tma_load_3d_2sm(sa + j * 64 * kBK * 2, &p.tma_a, &full[stage], m0 + j * 64, kb * kBK, z);
           }
-          if (!p.b_mn_major) {
+          if (p.conv_operand == 2) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+              conv_tile_load<true>(p, &p.tma_b, sb + j * 64 * kBK * 2, &full[stage], kb * kBK, n0 + j * 64);
+          } else if (!p.b_mn_major) {
             ptx::tma_load_3d_2sm(sb, &p.tma_b, &full[stage], kb * kBK, n0, z);
           } else {
 #pragma unroll
@@ -1014,6 +1041,34 @@ CUtensorMap make_epi_map(const void* base, bool f32, const GemmDesc& d, int inne
   return map;
 }
 
+// im2col map over NHWC x [n][h][w][c]: a 3x3 pad-1 filter origin per output
+// pixel (pixel box corners {-1, -1}), 64 channels x `pixels` pixels per load,
+// SWIZZLE_128B (the same smem image as a [pixels x 64] K-major / MN-major tile)
+CUtensorMap make_im2col_map(const void* x, int n, int h, int w, int c, int pixels) {
+  static PFN_cuTensorMapEncodeIm2col_v12000 fn = [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !ptr)
+      throw std::runtime_error("dpl: cuTensorMapEncodeIm2col unavailable");
+    return reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(ptr);
+  }();
+  if (reinterpret_cast<uintptr_t>(x) % 16) throw std::invalid_argument("dpl gemm: conv input not 16B aligned");
+  CUtensorMap map;
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(c), static_cast<cuuint64_t>(w), static_cast<cuuint64_t>(h),
+                        static_cast<cuuint64_t>(n)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(c) * 2, static_cast<cuuint64_t>(w) * c * 2,
+                           static_cast<cuuint64_t>(h) * w * c * 2};
+  int lower[2] = {-1, -1}, upper[2] = {-1, -1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult rc = fn(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, lower, upper,
+                         64, static_cast<cuuint32_t>(pixels), estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (rc != CUDA_SUCCESS) throw std::runtime_error("dpl gemm: im2col tensor map failed (" + std::to_string(rc) + ")");
+  return map;
+}
+
 template <int BN>
 void configure_kernel() {
   static std::once_flag once;
@@ -1076,10 +1131,24 @@ void GemmOp::prepare(const GemmDesc& d) {
   p.batch = d.batch;
   p.a_mn_major = d.a_mn_major;
   p.b_mn_major = d.b_mn_major;
-  p.tma_a = d.a_mn_major ? make_map(d.A, d.M, d.K, d.lda, d.batch, d.a_batch_stride, kBK)
-                         : make_map(d.A, d.K, d.M, d.lda, d.batch, d.a_batch_stride, kBM);
-  p.tma_b = d.b_mn_major ? make_map(d.B, d.N, d.K, d.ldb, d.batch, d.b_batch_stride, kBK)
-                         : make_map(d.B, d.K, d.N, d.ldb, d.batch, d.b_batch_stride, two_sm ? bn / 2 : bn);
+  p.conv_operand = d.conv_operand;
+  if (d.conv_operand) {
+    if (d.conv_c % 64 || d.batch != 1 || !d.conv_x)
+      throw std::invalid_argument("dpl gemm: implicit conv needs C % 64 == 0, batch 1 and an input");
+    if (d.conv_operand == 1 && (d.a_mn_major || d.K != 9 * d.conv_c || d.M != d.conv_n * d.conv_h * d.conv_w))
+      throw std::invalid_argument("dpl gemm: implicit conv A operand shape");
+    if (d.conv_operand == 2 && (!d.b_mn_major || d.N != 9 * d.conv_c || d.K != d.conv_n * d.conv_h * d.conv_w))
+      throw std::invalid_argument("dpl gemm: implicit conv B operand shape");
+    p.conv_h = d.conv_h;
+    p.conv_w = d.conv_w;
+    p.conv_c = d.conv_c;
+  }
+  p.tma_a = d.conv_operand == 1 ? make_im2col_map(d.conv_x, d.conv_n, d.conv_h, d.conv_w, d.conv_c, kBM)
+            : d.a_mn_major      ? make_map(d.A, d.M, d.K, d.lda, d.batch, d.a_batch_stride, kBK)
+                                : make_map(d.A, d.K, d.M, d.lda, d.batch, d.a_batch_stride, kBM);
+  p.tma_b = d.conv_operand == 2 ? make_im2col_map(d.conv_x, d.conv_n, d.conv_h, d.conv_w, d.conv_c, kBK)
+            : d.b_mn_major      ? make_map(d.B, d.N, d.K, d.ldb, d.batch, d.b_batch_stride, kBK)
+                                : make_map(d.B, d.K, d.N, d.ldb, d.batch, d.b_batch_stride, two_sm ? bn / 2 : bn);
   p.num_m_blocks = ceil_div(d.M, bm);
   p.num_n_blocks = ceil_div(d.N, bn);
   p.num_k_blocks = ceil_div(d.K, kBK);
@@ -1218,7 +1287,9 @@ const GemmOp& GemmCache::get(const GemmDesc& d) {
                          static_cast<long long>(reinterpret_cast<uintptr_t>(d.resid)),
                          static_cast<long long>(reinterpret_cast<uintptr_t>(d.aux_out)), d.force_bn, d.force_1sm,
                          static_cast<long long>(reinterpret_cast<uintptr_t>(d.trace)),
-                         static_cast<long long>(reinterpret_cast<uintptr_t>(d.colsum))};
+                         static_cast<long long>(reinterpret_cast<uintptr_t>(d.colsum)),
+                         static_cast<long long>(reinterpret_cast<uintptr_t>(d.conv_x)), d.conv_operand, d.conv_n,
+                         d.conv_h, d.conv_w, d.conv_c};
   std::string key(reinterpret_cast<const char*>(f), sizeof f);
   uint32_t a;
   std::memcpy(&a, &d.alpha, 4);

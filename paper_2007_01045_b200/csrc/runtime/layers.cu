@@ -408,18 +408,25 @@ class ConvLayer final : public Layer {
   size_t dz_elems(const StageContext& c) const override { return px(c) * v_.cout; }
   void alloc_stash(StageContext& ctx) override {
     for (int k = 0; k < ctx.slots; ++k) {
-      // the forward's columns are kept for the weight gradient (no second im2col)
-      col_.push_back(alloc_n<bf16>(ctx, px(ctx) * v_.kp));
+      // explicit columns only where TMA's im2col mode cannot feed the GEMM
+      // (cin % 64 != 0: the RGB input); kept for the weight gradient
+      if (!implicit()) col_.push_back(alloc_n<bf16>(ctx, px(ctx) * v_.kp));
       if (v_.pool) yr_.push_back(alloc_n<bf16>(ctx, px(ctx) * v_.cout));  // post-ReLU, pre-pool output
     }
   }
   void forward(StageContext& ctx, int slot, const bf16* x, bf16* y) override {
     const int n = ctx.samples;
     const int rows = static_cast<int>(px(ctx));
-    im2col3x3(x, col_[slot], n, v_.h, v_.w, v_.cin, v_.kp, ctx.stream);
     bf16* out = v_.pool ? yr_[slot] : y;
-    GemmDesc d = plain(rows, v_.cout, v_.kp, col_[slot], v_.kp, false, w16_, v_.kp, false, out, v_.cout,
-                       kBias | kRelu);
+    GemmDesc d;
+    if (implicit()) {
+      // implicit GEMM: the A tiles are TMA im2col loads of x itself
+      d = plain(rows, v_.cout, v_.kp, x, v_.kp, false, w16_, v_.kp, false, out, v_.cout, kBias | kRelu);
+      conv_operand(d, 1, x, n);
+    } else {
+      im2col3x3(x, col_[slot], n, v_.h, v_.w, v_.cin, v_.kp, ctx.stream);
+      d = plain(rows, v_.cout, v_.kp, col_[slot], v_.kp, false, w16_, v_.kp, false, out, v_.cout, kBias | kRelu);
+    }
     d.bias = w32_ + static_cast<size_t>(v_.cout) * v_.kp;
     ctx.gemms.run(d, ctx.stream);
     if (v_.pool) maxpool2_fwd(out, y, n, v_.h, v_.w, v_.cout, ctx.stream);
@@ -431,11 +438,12 @@ class ConvLayer final : public Layer {
     else relu_bwd(ctx.cur_y, dy, ctx.conv_dz, static_cast<long long>(rows) * v_.cout, ctx.stream);
     float* gw = g32_;
     colsum_acc(ctx.conv_dz, gw + static_cast<size_t>(v_.cout) * v_.kp, rows, v_.cout, ctx.stream);
-    // dW += dz^T col (the forward's stashed columns)
-    (void)x;
-    ctx.gemms.run(plain(v_.cout, v_.kp, rows, ctx.conv_dz, v_.cout, true, col_[slot], v_.kp, true, gw, v_.kp,
-                        kOutF32Acc),
-                  ctx.stream);
+    // dW += dz^T col: the B tiles are TMA im2col loads of the stashed input
+    // (explicit columns from the forward for the RGB layer)
+    GemmDesc dw = plain(v_.cout, v_.kp, rows, ctx.conv_dz, v_.cout, true, implicit() ? x : col_[slot], v_.kp, true, gw,
+                        v_.kp, kOutF32Acc);
+    if (implicit()) conv_operand(dw, 2, x, n);
+    ctx.gemms.run(dw, ctx.stream);
     if (dx) {
       ctx.gemms.run(plain(rows, v_.kp, v_.cout, ctx.conv_dz, v_.cout, false, w16_, v_.kp, true, ctx.conv_dcol, v_.kp,
                           kOutBf16),
@@ -454,6 +462,15 @@ class ConvLayer final : public Layer {
 
  private:
   size_t px(const StageContext& c) const { return static_cast<size_t>(c.samples) * v_.h * v_.w; }
+  bool implicit() const { return v_.cin % 64 == 0; }
+  void conv_operand(GemmDesc& d, int which, const bf16* x, int n) const {
+    d.conv_x = x;
+    d.conv_operand = which;
+    d.conv_n = n;
+    d.conv_h = v_.h;
+    d.conv_w = v_.w;
+    d.conv_c = v_.cin;
+  }
   VggLayerShape v_;
   int index_;
   float* w32_ = nullptr;
