@@ -211,7 +211,27 @@ __global__ void relu_bwd_kernel(const bf16* __restrict__ y, const bf16* __restri
   }
 }
 
+__global__ void conv_weight_flip_kernel(const bf16* __restrict__ w, bf16* __restrict__ wt, int cin, int cout,
+                                        int kp) {
+  ptx::pdl_wait();
+  const long long total = static_cast<long long>(cin) * 9 * cout;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i / (9LL * cout));
+    const int r = static_cast<int>(i % (9LL * cout));
+    const int t = r / cout, co = r % cout;
+    wt[i] = w[static_cast<long long>(co) * kp + (8 - t) * cin + c];
+  }
+}
+
 }  // namespace
+
+void conv_weight_flip(const void* w, void* wt, int cin, int cout, int kp, cudaStream_t s) {
+  count_launch();
+  TimedLaunch timed_("conv_weight_flip", s);
+  launch_pdl(conv_weight_flip_kernel, dim3(grid_for(static_cast<long long>(cin) * 9 * cout, 256)), dim3(256), 0, s,
+             static_cast<const bf16*>(w), static_cast<bf16*>(wt), cin, cout, kp);
+}
 
 void im2col3x3(const void* x, void* col, int n, int h, int w, int c, int kp, cudaStream_t s) {
   if (kp < 9 * c || kp % 8) throw std::invalid_argument("im2col3x3: kp must be >= 9C and a multiple of 8");

@@ -20,5 +20,8 @@ void maxpool2_fwd(const void* x, void* y, int n, int h, int w, int c, cudaStream
 void maxpool2_relu_bwd(const void* x, const void* dy, void* dz, int n, int h, int w, int c, cudaStream_t s);
 // dz = dy * (y > 0)
 void relu_bwd(const void* y, const void* dy, void* dz, long long n, cudaStream_t s);
+// Weights of the transposed conv (backward data): wt[c][t*cout + co] =
+// w[co][(8 - t)*cin + c] (t = kh*3 + kw), so dx = conv3x3(dz, wt)
+void conv_weight_flip(const void* w, void* wt, int cin, int cout, int kp, cudaStream_t s);
 
 }  // namespace dpl

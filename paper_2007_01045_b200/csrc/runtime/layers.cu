@@ -404,7 +404,9 @@ class ConvLayer final : public Layer {
     init_params({{0, nw, 0, std::sqrt(6.0f / (9.0f * v_.cin))}, {nw, static_cast<size_t>(v_.cout), 1, 0.05f}},
                 index_, w32, w16, param_count(), seed, s);
   }
-  size_t col_elems(const StageContext& c) const override { return px(c) * v_.kp; }  // dcol scratch
+  size_t col_elems(const StageContext& c) const override {  // dcol scratch (explicit backward data only)
+    return implicit_dgrad() ? 0 : px(c) * v_.kp;
+  }
   size_t dz_elems(const StageContext& c) const override { return px(c) * v_.cout; }
   void alloc_stash(StageContext& ctx) override {
     for (int k = 0; k < ctx.slots; ++k) {
@@ -413,6 +415,7 @@ class ConvLayer final : public Layer {
       if (!implicit()) col_.push_back(alloc_n<bf16>(ctx, px(ctx) * v_.kp));
       if (v_.pool) yr_.push_back(alloc_n<bf16>(ctx, px(ctx) * v_.cout));  // post-ReLU, pre-pool output
     }
+    if (implicit_dgrad()) wt_ = alloc_n<bf16>(ctx, static_cast<size_t>(v_.cin) * 9 * v_.cout);
   }
   void forward(StageContext& ctx, int slot, const bf16* x, bf16* y) override {
     const int n = ctx.samples;
@@ -444,7 +447,20 @@ class ConvLayer final : public Layer {
                         v_.kp, kOutF32Acc);
     if (implicit()) conv_operand(dw, 2, x, n);
     ctx.gemms.run(dw, ctx.stream);
-    if (dx) {
+    if (dx && implicit_dgrad()) {
+      // backward data as a forward conv of dz with the flipped, transposed
+      // weights: dx = im2col(dz) wt^T, the A tiles TMA im2col loads of dz
+      conv_weight_flip(w16_, wt_, v_.cin, v_.cout, v_.kp, ctx.stream);
+      GemmDesc dd = plain(rows, v_.cin, 9 * v_.cout, ctx.conv_dz, 9 * v_.cout, false, wt_, 9 * v_.cout, false, dx,
+                          v_.cin, kOutBf16);
+      dd.conv_x = ctx.conv_dz;
+      dd.conv_operand = 1;
+      dd.conv_n = n;
+      dd.conv_h = v_.h;
+      dd.conv_w = v_.w;
+      dd.conv_c = v_.cout;
+      ctx.gemms.run(dd, ctx.stream);
+    } else if (dx) {
       ctx.gemms.run(plain(rows, v_.kp, v_.cout, ctx.conv_dz, v_.cout, false, w16_, v_.kp, true, ctx.conv_dcol, v_.kp,
                           kOutBf16),
                     ctx.stream);
@@ -463,6 +479,7 @@ class ConvLayer final : public Layer {
  private:
   size_t px(const StageContext& c) const { return static_cast<size_t>(c.samples) * v_.h * v_.w; }
   bool implicit() const { return v_.cin % 64 == 0; }
+  bool implicit_dgrad() const { return v_.cout % 64 == 0 && v_.cin % 8 == 0; }
   void conv_operand(GemmDesc& d, int which, const bf16* x, int n) const {
     d.conv_x = x;
     d.conv_operand = which;
@@ -478,6 +495,7 @@ class ConvLayer final : public Layer {
   bf16* w16_ = nullptr;
   std::vector<bf16*> yr_;
   std::vector<bf16*> col_;  // per slot: im2col columns of the forward
+  bf16* wt_ = nullptr;      // flipped / transposed weights for the backward-data conv
 };
 
 // y = x W^T + b (+ReLU), W [fout][fin]; takes / returns output / input gradients
