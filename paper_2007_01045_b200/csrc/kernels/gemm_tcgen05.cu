@@ -739,17 +739,25 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
 // leader's full barrier; the leader's commits multicast to both CTAs' empty /
 // tmem_full barriers; both CTAs' epilogue warps release the leader's
 // tmem_empty barrier.
+// Pair tile 256 x BN2 (BN2 = 256, or 128 for short-M / narrow shapes: half
+// the B bytes per stage, so a deeper ring covers the TMA latency).
+template <int BN2>
+struct PairCfg {
+  static constexpr int kBN = BN2;
+  static constexpr int kABytes = kBM * kBK * 2;        // 16 KB: this CTA's 128 rows of A
+  static constexpr int kBBytes = (kBN / 2) * kBK * 2;  // this CTA's half of B
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kTmemCols = 2 * kBN;            // double-buffered accumulator
+};
 namespace pair {
-constexpr int kBN = 256;
-constexpr int kABytes = kBM * kBK * 2;        // 16 KB: this CTA's 128 rows of A
-constexpr int kBBytes = (kBN / 2) * kBK * 2;  // 16 KB: this CTA's half of B
-constexpr int kStageBytes = kABytes + kBBytes;
 constexpr int kSmem = kSmemBudget;
 }  // namespace pair
 
+template <int BN2>
 __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __grid_constant__ GemmParams p) {
   if (threadIdx.x == 0) trace_mark(p, 0);
-  using namespace pair;
+  using Pc = PairCfg<BN2>;
+  constexpr int kBN = Pc::kBN, kABytes = Pc::kABytes, kBBytes = Pc::kBBytes, kStageBytes = Pc::kStageBytes;
   const int S = p.stages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -783,7 +791,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
     for (int i = 0; i < kEpiBars * kEpiWarps; ++i) ptx::mbar_init(&xbar[i], 1);
     ptx::fence_barrier_init();
   }
-  if (warp == 2) ptx::tmem_alloc_2sm<512>(tmem_base_slot);
+  if (warp == 2) ptx::tmem_alloc_2sm<Pc::kTmemCols>(tmem_base_slot);
   ptx::tc_fence_before();
   ptx::cluster_sync();
   ptx::tc_fence_after();
@@ -825,13 +833,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
           }
           if (p.conv_operand == 2) {
 #pragma unroll
-            for (int j = 0; j < 2; ++j)
+            for (int j = 0; j < kBN / 128; ++j)
               conv_tile_load<true>(p, &p.tma_b, sb + j * 64 * kBK * 2, &full[stage], kb * kBK, n0 + j * 64);
           } else if (!p.b_mn_major) {
             ptx::tma_load_3d_2sm(sb, &p.tma_b, &full[stage], kb * kBK, n0, z);
           } else {
 #pragma unroll
-            for (int j = 0; j < 2; ++j) ptx::tma_load_3d_2sm(sb + j * 64 * kBK * 2, &p.tma_b, &full[stage], n0 + j * 64, kb * kBK, z);
+            for (int j = 0; j < kBN / 128; ++j)
+              ptx::tma_load_3d_2sm(sb + j * 64 * kBK * 2, &p.tma_b, &full[stage], n0 + j * 64, kb * kBK, z);
           }
           if (t == first_tile && kb == kb0) trace_mark(p, 2);
           if (++stage == S) {
@@ -973,7 +982,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
   ptx::cluster_sync_relaxed();
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc_2sm<512>(tmem_base);
+    ptx::tmem_dealloc_2sm<Pc::kTmemCols>(tmem_base);
   }
   if (threadIdx.x == 0) trace_mark(p, 7);
 }
@@ -1120,7 +1129,11 @@ void GemmOp::prepare(const GemmDesc& d) {
     const char* e = std::getenv("DPL_GEMM_2SM");
     return !(e && e[0] == '0');
   }();
-  const bool two_sm = pair_enabled && !d.force_1sm && bn == 256 && d.M >= 256;
+  static const bool pair128 = [] {
+    const char* e = std::getenv("DPL_GEMM_PAIR128");
+    return !(e && e[0] == '0');
+  }();
+  const bool two_sm = pair_enabled && !d.force_1sm && d.M >= 256 && (bn == 256 || (bn == 128 && pair128));
   const int bm = two_sm ? 256 : kBM;
   GemmParams& p = params_;
   p = GemmParams{};
@@ -1210,15 +1223,15 @@ void GemmOp::prepare(const GemmDesc& d) {
               !two_in && !(x_in && aux);
     if (kind != kOutBf16 && (x_in || aux)) ok = false;
     if ((d.epi & kBias) && (d.N % 4 != 0 || reinterpret_cast<uintptr_t>(d.bias) % 16 != 0)) ok = false;
-    const int stage_bytes = two_sm ? pair::kStageBytes : (kBM + bn) * kBK * 2;
+    const int stage_bytes = two_sm ? (kBM + bn / 2) * kBK * 2 : (kBM + bn) * kBK * 2;
     const int ring = kSmemBudget - 2048;
     p.stages = std::min(kMaxStages, ring / stage_bytes);
     if (ok) {
       // carve the staging out of the ring, keeping >= 4 stages
-      const int per_warp = (two_sm ? pair::kBN : bn) / 64;  // chunks per epilogue warp per tile
+      const int per_warp = bn / 64;  // chunks per epilogue warp per tile
       p.epi_out_bytes = kind == kOutBf16 ? 2048 : 4096;
       p.epi_nx = x_in ? std::min(kMaxNx, per_warp) : (aux ? 2 : 1);
-      p.epi_tile_cols = two_sm ? pair::kBN : bn;
+      p.epi_tile_cols = bn;
       const int bias_bytes = (d.epi & kBias) ? p.epi_tile_cols * 4 : 0;
       for (;;) {
         // 1 KB multiple: every warp's chunk buffers stay swizzle-atom aligned
@@ -1256,7 +1269,8 @@ void GemmOp::prepare(const GemmDesc& d) {
     smem_ = pair::kSmem;
     static std::once_flag once;
     std::call_once(once, [] {
-      cudaFuncSetAttribute(gemm_bf16_tcgen05_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize, pair::kSmem);
+      cudaFuncSetAttribute(gemm_bf16_tcgen05_2sm<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, pair::kSmem);
+      cudaFuncSetAttribute(gemm_bf16_tcgen05_2sm<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, pair::kSmem);
     });
     return;
   }
@@ -1362,7 +1376,8 @@ void GemmOp::launch_kernel(cudaStream_t stream) const {
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_bf16_tcgen05_2sm, params_);
+    const cudaError_t e = bn_ == 256 ? cudaLaunchKernelEx(&cfg, gemm_bf16_tcgen05_2sm<256>, params_)
+                                     : cudaLaunchKernelEx(&cfg, gemm_bf16_tcgen05_2sm<128>, params_);
     if (e != cudaSuccess) throw std::runtime_error(std::string("dpl gemm: pair launch failed: ") + cudaGetErrorString(e));
     return;
   }

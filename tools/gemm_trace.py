@@ -16,7 +16,8 @@ one = "--1sm" in sys.argv
 shapes = {"o": (4096, 1024, 1024, "fwd", K.EPI_BIAS | K.EPI_RESID), "ffn1": (4096, 4096, 1024, "fwd", K.EPI_BIAS | K.EPI_GELU | K.EPI_AUX_OUT),
           "qkv": (4096, 3072, 1024, "fwd", K.EPI_BIAS), "ffn2": (4096, 1024, 4096, "fwd", K.EPI_BIAS | K.EPI_RESID),
           "plain": (4096, 1024, 1024, "fwd", 0), "wgrad_gpt": (1600, 6400, 1024, "wgrad", 0),
-          "wgrad_o": (1024, 1024, 4096, "wgrad", 0), "big": (8192, 8192, 8192, "fwd", 0)}
+          "wgrad_o": (1024, 1024, 4096, "wgrad", 0), "big": (8192, 8192, 8192, "fwd", 0),
+          "gpt_ffn2": (1024, 1600, 6400, "fwd", K.EPI_BIAS | K.EPI_RESID), "gpt_ffn2_plain": (1024, 1600, 6400, "fwd", 0)}
 M, N, Kd, kind, epi = shapes[which]
 tr = torch.zeros(148 * 16, dtype=torch.int64, device=dev)
 if kind == "fwd":
