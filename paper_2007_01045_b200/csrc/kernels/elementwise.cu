@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(256, 4)
 // Row kernel: one warp per row, pure streaming (no column reductions); x and
 // dy stay packed in registers, xhat and g*dy are recomputed in pass 2.
 template <int kMaxVec>
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(256, kMaxVec > 4 ? 2 : 4)  // h > 1024 (GPT-2): registers for x, dy without spills
     layernorm_bwd_rows_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
                               const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
                               const float* __restrict__ gamma, const __nv_bfloat16* __restrict__ dresid,
