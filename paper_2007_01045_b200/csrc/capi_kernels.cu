@@ -107,9 +107,21 @@ int dpl_k_attention_fwd(const void* qkv, void* ctx, long long ldc, float* lse, i
     d.seq = seq;
     d.heads = heads;
     d.causal = causal;
+    const auto st = static_cast<cudaStream_t>(stream);
+    void* ws = nullptr;
+    const size_t tiles = static_cast<size_t>(heads) * samples * (seq / 128);
+    const size_t part_bytes = tiles * 2 * 66 * 128 * sizeof(float);
+    if (causal) {  // split-schedule workspace, as the executor provides it
+      if (cudaMallocAsync(&ws, part_bytes + tiles * sizeof(int), st) != cudaSuccess)
+        throw std::runtime_error("attention_fwd: workspace allocation failed");
+      cudaMemsetAsync(static_cast<char*>(ws) + part_bytes, 0, tiles * sizeof(int), st);
+      d.fwd_part = static_cast<float*>(ws);
+      d.fwd_flags = reinterpret_cast<int*>(static_cast<char*>(ws) + part_bytes);
+    }
     dpl::AttentionOp op;
     op.prepare(d);
-    op.forward(static_cast<cudaStream_t>(stream));
+    op.forward(st);
+    if (ws) cudaFreeAsync(ws, st);
   });
 }
 

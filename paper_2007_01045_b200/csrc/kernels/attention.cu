@@ -30,6 +30,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "attention.h"
 #include "gemm.h"
@@ -52,6 +53,12 @@ struct AttnFwdParams {
   __nv_bfloat16* ctx;
   long long ldc;  // H
   float* lse;     // [z][S]
+  // Causal split schedule (n_items > 0): blockIdx = (z, item); item i covers
+  // key tiles [lo, hi) of query tile qt, half = 0 (whole range) or 1 / 2.
+  float* part;    // [z][S/128][2][66][128]: o[64], m, l per row, per half
+  int* flags;     // [z][S/128] tickets
+  int n_items;
+  unsigned char it_qt[32], it_lo[32], it_hi[32], it_half[32];
 };
 
 __device__ __forceinline__ float exp2_fast(float x) {
@@ -94,11 +101,23 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
   uint64_t* o_full = bars + 9;    // [2]
   uint64_t* o_empty = bars + 11;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  int* ticket = reinterpret_cast<int*>(bars + 15);
 
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
-  const int qt = blockIdx.x, z = blockIdx.y;
+  int qt, z, kv_lo, half = 0, n_kv;
+  if (p.n_items) {
+    z = blockIdx.x;
+    qt = p.it_qt[blockIdx.y];
+    kv_lo = p.it_lo[blockIdx.y];
+    n_kv = p.it_hi[blockIdx.y] - kv_lo;
+    half = p.it_half[blockIdx.y];
+  } else {
+    qt = blockIdx.x;
+    z = blockIdx.y;
+    kv_lo = 0;
+    n_kv = p.causal ? qt + 1 : p.S / kT;
+  }
   const int q0 = qt * kT;
-  const int n_kv = p.causal ? qt + 1 : p.S / kT;
   const int zk = p.z_count + z, zv = 2 * p.z_count + z;
 
   if (warp == 0 && lane == 0) {
@@ -134,10 +153,10 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
         const uint32_t ph = (j & 1) ^ 1;
         ptx::mbar_wait(k_empty, ph);
         ptx::mbar_arrive_expect_tx(k_full, kTileBytes);
-        ptx::tma_load_3d(sK, &p.qkv, k_full, 0, j * kT, zk);
+        ptx::tma_load_3d(sK, &p.qkv, k_full, 0, (kv_lo + j) * kT, zk);
         ptx::mbar_wait(v_empty, ph);
         ptx::mbar_arrive_expect_tx(v_full, kTileBytes);
-        ptx::tma_load_3d(sV, &p.qkv, v_full, 0, j * kT, zv);
+        ptx::tma_load_3d(sV, &p.qkv, v_full, 0, (kv_lo + j) * kT, zv);
       }
     }
   } else if (warp == 1) {
@@ -192,7 +211,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
         const uint32_t ph = j & 1;
         ptx::mbar_wait(s_full, ph);
         ptx::tc_fence_after();
-        const bool diag = p.causal && j == n_kv - 1;
+        const bool diag = p.causal && kv_lo + j == qt;
         const int lim = diag ? r : kT - 1;  // last unmasked key column of this row
         // pass 1: row max of the raw scores (scale > 0 commutes with max)
         float mx = -INFINITY;
@@ -261,6 +280,45 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
       }
       alpha_prev = alpha;
     }
+    bool write_out = true;
+    if (half) {
+      // Publish this half's (o, m, l); the CTA that takes ticket 1 merges
+      // the other half's partial and writes the output.
+      const int nq = p.S / kT;
+      const long long tile = static_cast<long long>(z) * nq + qt;
+      float* mine = p.part + (tile * 2 + (half - 1)) * 66 * kT;
+      const float* other = p.part + (tile * 2 + (2 - half)) * 66 * kT;
+#pragma unroll
+      for (int e = 0; e < kD; ++e) __stcg(mine + e * kT + r, o[e]);
+      __stcg(mine + 64 * kT + r, m);
+      __stcg(mine + 65 * kT + r, l);
+      __threadfence();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (quad == 0 && lane == 0) {
+        const int t = atomicAdd(p.flags + tile, 1);
+        if (t == 1) p.flags[tile] = 0;  // both halves in: ready for the next call
+        *ticket = t;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      write_out = *ticket == 1;
+      if (write_out) {  // merged in half order (1, 2) whichever CTA runs it: deterministic
+        __threadfence();
+        const bool first = half == 1;
+        const float mo = __ldcg(other + 64 * kT + r), lo = __ldcg(other + 65 * kT + r);
+        const float m1 = first ? m : mo, m2 = first ? mo : m;
+        const float l1 = first ? l : lo, l2 = first ? lo : l;
+        const float mm = fmaxf(m1, m2);
+        const float s1 = exp2_fast(m1 - mm), s2 = exp2_fast(m2 - mm);
+#pragma unroll
+        for (int e = 0; e < kD; ++e) {
+          const float ot = __ldcg(other + e * kT + r);
+          o[e] = fmaf(first ? o[e] : ot, s1, (first ? ot : o[e]) * s2);
+        }
+        l = fmaf(l1, s1, l2 * s2);
+        m = mm;
+      }
+    }
+    if (write_out) {
     const float inv = 1.f / l;
     const int b = z % p.B, h = z / p.B;
     __nv_bfloat16* out = p.ctx + static_cast<long long>(b * p.S + q) * p.ldc + h * kD;
@@ -274,6 +332,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
       reinterpret_cast<uint4*>(out)[u] = w;
     }
     p.lse[static_cast<long long>(z) * p.S + q] = (m + log2f(l)) * 0.69314718055994531f;
+    }
   }
 
   ptx::pdl_trigger();
@@ -644,9 +703,42 @@ void AttentionOp::forward(cudaStream_t s) const {
   p.ctx = static_cast<__nv_bfloat16*>(desc_.ctx);
   p.ldc = desc_.ldc;
   p.lse = desc_.lse;
+  p.part = desc_.fwd_part;
+  p.flags = desc_.fwd_flags;
+  p.n_items = 0;
+  const int nq = desc_.seq / kT;
+  static const bool split_on = [] {
+    const char* e = std::getenv("DPL_ATTN_SPLIT");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (split_on && desc_.causal && p.part && p.flags && nq <= 16) {
+    // Work items, longest first: query tiles with >= 4 key tiles split in two
+    // (the grid is one wave at small batch and the step waits on the longest CTA).
+    struct Item { int qt, lo, hi, half; };
+    std::vector<Item> items;
+    for (int qt = 0; qt < nq; ++qt) {
+      const int n = qt + 1;
+      if (n >= 4) {
+        items.push_back({qt, 0, n / 2, 1});
+        items.push_back({qt, n / 2, n, 2});
+      } else {
+        items.push_back({qt, 0, n, 0});
+      }
+    }
+    std::stable_sort(items.begin(), items.end(),
+                     [](const Item& x, const Item& y) { return x.hi - x.lo > y.hi - y.lo; });
+    p.n_items = static_cast<int>(items.size());
+    for (int i = 0; i < p.n_items; ++i) {
+      p.it_qt[i] = static_cast<unsigned char>(items[i].qt);
+      p.it_lo[i] = static_cast<unsigned char>(items[i].lo);
+      p.it_hi[i] = static_cast<unsigned char>(items[i].hi);
+      p.it_half[i] = static_cast<unsigned char>(items[i].half);
+    }
+  }
   count_launch();
   TimedLaunch timed_("attention_fwd", s, 4.0 * p.z_count * desc_.seq * desc_.seq * kD / (desc_.causal ? 2 : 1));
-  launch_pdl(attn_fwd_kernel, dim3(desc_.seq / kT, p.z_count), dim3(kFwdThreads), kFwdSmem, s, p);
+  const dim3 grid = p.n_items ? dim3(p.z_count, p.n_items) : dim3(nq, p.z_count);
+  launch_pdl(attn_fwd_kernel, grid, dim3(kFwdThreads), kFwdSmem, s, p);
 }
 
 void AttentionOp::backward(cudaStream_t s) const {

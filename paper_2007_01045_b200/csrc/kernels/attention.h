@@ -21,6 +21,12 @@ struct AttentionDesc {
   void* dqkv = nullptr;
   float* dsum = nullptr;
   float* dq_acc = nullptr;
+  // causal forward split (optional): query tiles with >= 4 key tiles run as
+  // two CTAs over halves of the key range, the second to finish merges.
+  // fwd_part [heads*B][S/128][2][66][128] fp32, fwd_flags [heads*B][S/128]
+  // int (zero before the first call; the merging CTA re-zeroes its entry).
+  float* fwd_part = nullptr;
+  int* fwd_flags = nullptr;
 };
 
 class AttentionOp {

@@ -442,6 +442,11 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
     const size_t z = static_cast<size_t>(spec_.heads) * ctx_.samples;
     ctx_.att_dsum = static_cast<float*>(mem_.alloc(z * spec_.seq * 4));
     ctx_.att_dq = static_cast<float*>(mem_.alloc(RH * 4));
+    if (spec_.causal) {
+      const size_t tiles = z * (spec_.seq / 128);
+      ctx_.att_part = static_cast<float*>(mem_.alloc(tiles * 2 * 66 * 128 * 4));
+      ctx_.att_flags = static_cast<int*>(mem_.alloc(tiles * 4));
+    }
     ctx_.ln_ws = static_cast<float*>(mem_.alloc(static_cast<size_t>(kLnBwdBlocks) * 4 * spec_.hidden * 4));
     ctx_.t_h = static_cast<bf16*>(mem_.alloc(RH * 2));
     ctx_.t_h2 = static_cast<bf16*>(mem_.alloc(RH * 2));

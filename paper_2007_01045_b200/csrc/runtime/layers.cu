@@ -328,6 +328,8 @@ class TransformerLayer final : public Layer {
       d.dqkv = ctx.t_qkv;
       d.dsum = ctx.att_dsum;
       d.dq_acc = ctx.att_dq;
+      d.fwd_part = ctx.att_part;
+      d.fwd_flags = ctx.att_flags;
       st.attn.prepare(d);
       st.attn_ready = true;
     }

@@ -86,6 +86,8 @@ struct StageContext {
   bf16* t_f = nullptr;      // [R][F]
   float* att_dsum = nullptr;  // attention backward workspaces: [z][S]
   float* att_dq = nullptr;    // [z][S][64]
+  float* att_part = nullptr;  // causal forward split partials, flags (AttentionDesc::fwd_part / fwd_flags)
+  int* att_flags = nullptr;
   float* ln_ws = nullptr;     // LayerNorm-backward partials [kLnBwdBlocks][2][H]
   bf16* conv_col = nullptr;   // VGG: im2col columns (max over the stage's convs)
   bf16* conv_dcol = nullptr;  // VGG: column gradients

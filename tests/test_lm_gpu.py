@@ -120,3 +120,23 @@ def test_lm_profile_and_host_tokens(cuda):
     assert prof["layers"][0]["param_bytes"] == base + (v * h + 128 * h) * 4
     assert prof["layers"][1]["param_bytes"] == base + (2 * h + v * h) * 4
     ex.close()
+
+
+def test_lm_causal_split_attention_step(cuda):
+    """seq 512: causal query tiles with >= 4 key tiles run as two CTAs whose
+    partials merge in the second to finish (attention.cu, fwd_part / fwd_flags).
+    The step matches the oracle and repeats (the tickets re-arm)."""
+    from oracle.executor_ref import full_batch_step
+    from parity_util import check_grads, check_loss
+    from paper_2007_01045_b200.runtime import Executor
+    lm = dict(LM, seq=512)
+    plan = {"stages": [{"layers": [0, 2], "gpus": [0], "replication": 1}]}
+    exact = full_batch_step(lm, 4)
+    emu = full_batch_step(lm, 4, bf16=True)
+    ex = Executor(lm, plan, 4, 4, lr=0.0, apply=False)
+    loss = ex.step()
+    check_loss(loss, emu, exact)
+    check_grads(ex, emu, exact, range(2), "gpt", 2)
+    losses = [ex.step() for _ in range(3)]
+    assert all(abs(l - loss) <= 1e-6 * abs(loss) for l in losses), (loss, losses)  # CE sums with atomics
+    ex.close()
