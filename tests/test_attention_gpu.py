@@ -20,7 +20,7 @@ def _ref(qkv, B, S, nh, causal):
 
 
 @pytest.mark.parametrize("B,S,nh,causal", [(2, 128, 2, False), (2, 512, 4, False), (3, 512, 2, True),
-                                           (1, 1024, 2, True), (4, 256, 16, False)])
+                                           (1, 1024, 2, True), (4, 256, 16, False), (2, 2048, 2, True)])
 def test_attention_forward(cuda, B, S, nh, causal):
     g = torch.Generator(device="cpu").manual_seed(B * S + nh)
     qkv = (torch.randn(3, nh, B, S, 64, generator=g) * 1.5).to(torch.bfloat16).to(cuda)
@@ -35,7 +35,7 @@ def test_attention_forward(cuda, B, S, nh, causal):
 
 
 @pytest.mark.parametrize("B,S,nh,causal", [(2, 128, 2, False), (2, 512, 4, False), (3, 512, 2, True),
-                                           (1, 1024, 2, True)])
+                                           (1, 1024, 2, True), (1, 1024, 25, True), (2, 2048, 2, True)])
 def test_attention_backward(cuda, B, S, nh, causal):
     g = torch.Generator(device="cpu").manual_seed(7 * B + S + nh)
     qkv = (torch.randn(3, nh, B, S, 64, generator=g) * 1.5).to(torch.bfloat16).to(cuda)
@@ -83,3 +83,28 @@ def test_attention_forward_causal_split_deterministic(cuda):
     err = (outs[0][0].float() - ro).abs().max().item()
     assert err < 2e-2 * ro.abs().max().item() + 1e-3, err
     assert (outs[0][1] - rl).abs().max().item() < 1e-2
+
+
+def test_attention_backward_causal_split_repeatable(cuda):
+    """GPT-2 shape at batch 1, after the split-schedule forward: dK and dV
+    are bit-identical across calls (dQ sums with atomics)."""
+    B, S, nh = 1, 1024, 25
+    H = nh * 64
+    g = torch.Generator(device="cpu").manual_seed(11)
+    qkv = (torch.randn(3, nh, B, S, 64, generator=g) * 1.5).to(torch.bfloat16).to(cuda)
+    dout = torch.randn(nh, B, S, 64, generator=g).to(torch.bfloat16).to(cuda)
+    ctx = torch.zeros(B * S, H, dtype=torch.bfloat16, device=cuda)
+    lse = torch.zeros(nh * B, S, device=cuda)
+    K.attention_fwd(qkv, ctx, lse, B, S, nh, H, True)
+    outs = []
+    for _ in range(3):
+        dqkv = torch.zeros(B * S, 3 * H, dtype=torch.bfloat16, device=cuda)
+        dsum = torch.zeros(nh * B, S, device=cuda)
+        dq_acc = torch.zeros(nh * B, S, 64, device=cuda)
+        K.attention_bwd(qkv, ctx, lse, dout, dqkv, dsum, dq_acc, B, S, nh, H, True)
+        torch.cuda.synchronize()
+        outs.append(dqkv)
+    for d in outs[1:]:
+        assert torch.equal(d[:, H:], outs[0][:, H:])
+        a, b = d[:, :H].float(), outs[0][:, :H].float()
+        assert ((a - b).norm() / b.norm()).item() < 1e-2  # bf16 rounding of atomically summed dQ
