@@ -393,7 +393,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
 
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
-  const int j = blockIdx.x, z = blockIdx.y;
+  // causal: blockIdx = (z, j) so the block scheduler hands out every head's
+  // longest key tile (j = 0 walks all query tiles) first and the short ones
+  // fill the tail of the >1-wave grid; non-causal: (j, z)
+  const int j = p.causal ? blockIdx.y : blockIdx.x, z = p.causal ? blockIdx.x : blockIdx.y;
   const int k0 = j * kT;
   const int n_q = p.S / kT;
   const int i_first = p.causal ? j : 0;
@@ -769,7 +772,8 @@ void AttentionOp::backward(cudaStream_t s) const {
   p.dqkv = static_cast<__nv_bfloat16*>(desc_.dqkv);
   p.ld = 3LL * desc_.heads * kD;
   p.H = desc_.heads * kD;
-  launch_pdl(attn_bwd_kernel, dim3(desc_.seq / kT, z_count), dim3(kBwdThreads), kBwdSmem, s, p);
+  const dim3 bgrid = desc_.causal ? dim3(z_count, desc_.seq / kT) : dim3(desc_.seq / kT, z_count);
+  launch_pdl(attn_bwd_kernel, bgrid, dim3(kBwdThreads), kBwdSmem, s, p);
   launch_pdl(attn_bwd_dq_kernel, dim3(std::min((rows + 15) / 16, 148 * 16)), dim3(256), 0, s,
              static_cast<const float*>(desc_.dq_acc), p.dqkv, p.ld, scale, desc_.seq, desc_.samples, rows);
 }
