@@ -1110,14 +1110,17 @@ void GemmOp::prepare(const GemmDesc& d) {
     if (d.N <= 64) {
       bn = 64;
     } else {
-      // minimise waves x tile width, charging the 128-wide tile ~30% more
+      // minimise waves x tile width, charging the 128-wide tile ~40% more
       // per FLOP (half the operand reuse per byte fetched; measured on B200:
-      // 4096x4096x1024 runs at 878 TF with BN=256 vs 713 TF with BN=128)
+      // 4096x4096x1024 runs at 878 TF with BN=256 vs 713 TF with BN=128, and
+      // at GPT-2's 1024-token shapes 1024x4800x1600 / 1024x6400x1600 the
+      // 256x256 pair beats the 256x128 pair by 10-24% despite a ragged
+      // second wave: tools/gemm_graph_bench.py --T 1024 --H 1600 --F 6400)
       const int sms = num_sms();
       double best = -1;
       for (int cand : {256, 128}) {
         const long long tiles = static_cast<long long>(ceil_div(d.M, kBM)) * ceil_div(d.N, cand) * d.batch;
-        const double cost = static_cast<double>((tiles + sms - 1) / sms) * cand * (cand == 128 ? 1.3 : 1.0);
+        const double cost = static_cast<double>((tiles + sms - 1) / sms) * cand * (cand == 128 ? 1.4 : 1.0);
         if (best < 0 || cost < best) {
           best = cost;
           bn = cand;

@@ -106,7 +106,8 @@ def main():
                     j = i % nb
                     torch.matmul(A[j].T, B[j], out=C16[j])
             row = {"T": T, "gemm": name, "M": M, "N": N, "K": Kd}
-            for vname, v in (("ours", {}), ("1sm", {"force_1sm": True}), ("bn128", {"force_bn": 128, "force_1sm": True})):
+            for vname, v in (("ours", {}), ("1sm", {"force_1sm": True}), ("bn128", {"force_bn": 128, "force_1sm": True}),
+                             ("pair256", {"force_bn": 256}), ("pair128", {"force_bn": 128})):
                 try:
                     t = graph_time(lambda i: ours(i, v))
                     row[vname] = round(fl / t / 1e12, 1)
