@@ -1117,10 +1117,14 @@ void GemmOp::prepare(const GemmDesc& d) {
       // 256x256 pair beats the 256x128 pair by 10-24% despite a ragged
       // second wave: tools/gemm_graph_bench.py --T 1024 --H 1600 --F 6400)
       const int sms = num_sms();
+      static const double narrow_cost = [] {  // DPL_GEMM_BN128_COST: A/B knob
+        const char* e = std::getenv("DPL_GEMM_BN128_COST");
+        return e ? std::atof(e) : 1.4;
+      }();
       double best = -1;
       for (int cand : {256, 128}) {
         const long long tiles = static_cast<long long>(ceil_div(d.M, kBM)) * ceil_div(d.N, cand) * d.batch;
-        const double cost = static_cast<double>((tiles + sms - 1) / sms) * cand * (cand == 128 ? 1.4 : 1.0);
+        const double cost = static_cast<double>((tiles + sms - 1) / sms) * cand * (cand == 128 ? narrow_cost : 1.0);
         if (best < 0 || cost < best) {
           best = cost;
           bn = cand;
@@ -1136,7 +1140,11 @@ void GemmOp::prepare(const GemmDesc& d) {
     const char* e = std::getenv("DPL_GEMM_PAIR128");
     return !(e && e[0] == '0');
   }();
-  const bool two_sm = pair_enabled && !d.force_1sm && d.M >= 256 && (bn == 256 || (bn == 128 && pair128));
+  // 256x128 pairs help the 1024-row transformer GEMMs but not the implicit
+  // convolutions (VGG-19 N=1: 3719 vs 3889 samples/s with them), which keep
+  // the 1-SM 128x128 tile
+  const bool two_sm = pair_enabled && !d.force_1sm && d.M >= 256 &&
+                      (bn == 256 || (bn == 128 && pair128 && !d.conv_operand));
   const int bm = two_sm ? 256 : kBM;
   GemmParams& p = params_;
   p = GemmParams{};
