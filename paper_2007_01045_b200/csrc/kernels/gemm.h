@@ -58,7 +58,7 @@ struct GemmDesc {
   void* aux_out = nullptr;
   int force_bn = 0;  // 0 = heuristic; else 64/128/256
   int force_1sm = 0; // 1 = never use the CTA-pair kernel
-  unsigned long long* trace = nullptr;  // per-CTA phase timestamps (16 per CTA), diagnostics
+  unsigned long long* trace = nullptr;  // per-CTA phase timestamps (64 words per CTA), diagnostics
   float* colsum = nullptr;              // kColSum target (fp32, N)
   // implicit-GEMM 3x3 / pad-1 convolution over NHWC conv_x [n][h][w][c] (c % 64 == 0):
   //   conv_operand 1: A[M = n*h*w][K = 9c] are its im2col columns (K-major, A unused)

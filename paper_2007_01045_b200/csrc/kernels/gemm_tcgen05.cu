@@ -91,9 +91,32 @@ __device__ __forceinline__ void conv_tile_load(const GemmParams& p, const CUtens
 }
 
 // diagnostics: phase timestamps per CTA (GemmDesc::trace)
+// 64 words per CTA: slots 0-15 the phase marks below, 16 + 4 j + {0..3} tile
+// j's (j < 11) MMA start / last commit / epilogue start / epilogue end, 63 the
+// %globaltimer at entry (ns, aligns CTAs)
+constexpr int kTraceWords = 64;
 __device__ __forceinline__ void trace_mark(const GemmParams& p, int slot) {
   if (p.trace) {
-    p.trace[blockIdx.x * 16 + slot] = clock64();  // SM cycles (compare within one CTA)
+    p.trace[blockIdx.x * kTraceWords + slot] = clock64();  // SM cycles (compare within one CTA)
+  }
+}
+__device__ __forceinline__ void trace_tile(const GemmParams& p, int j, int k) {
+  if (p.trace && j < 11) p.trace[blockIdx.x * kTraceWords + 16 + 4 * j + k] = clock64();
+}
+__device__ __forceinline__ void trace_exit(const GemmParams& p) {
+  if (p.trace) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[blockIdx.x * kTraceWords + 62] = t;
+    p.trace[blockIdx.x * kTraceWords + 7] = clock64();
+  }
+}
+__device__ __forceinline__ void trace_entry(const GemmParams& p) {
+  if (p.trace) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[blockIdx.x * kTraceWords + 63] = t;
+    p.trace[blockIdx.x * kTraceWords] = clock64();
   }
 }
 
@@ -498,7 +521,7 @@ __device__ __forceinline__ void epi_tile_tma(const GemmParams& p, EpiTma& e, uin
 
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_constant__ GemmParams p) {
-  if (threadIdx.x == 0) trace_mark(p, 0);
+  if (threadIdx.x == 0) trace_entry(p);
   using C = Cfg<BN>;
   const int S = p.stages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -605,7 +628,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      int jt = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++jt) {
         const int ks = t % p.k_splits;
         const int kb0 = ks * p.kb_per_split;
         const int kb1 = min(p.num_k_blocks, kb0 + p.kb_per_split);
@@ -616,6 +640,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
           if (t == static_cast<int>(blockIdx.x) && kb == kb0) trace_mark(p, 3);
+          if (kb == kb0) trace_tile(p, jt, 0);
           const uint32_t sa = ptx::smem_addr(smem_a + stage * C::kABytes);
           const uint32_t sb = ptx::smem_addr(smem_b + stage * C::kBBytes);
 #pragma unroll
@@ -632,6 +657,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
         }
         ptx::mma_commit(&tmem_full[acc]);
         trace_mark(p, 4);
+        trace_tile(p, jt, 1);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -645,7 +671,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
     EpiTma e{smem_epi + (warp - 4) * p.epi_warp_bytes, xbar + kEpiBars * (warp - 4), 0, 0};
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+    int jt = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++jt) {
       const int tt = t / p.k_splits;
       const int z = tt / tiles_per_z;
       const int r = tt % tiles_per_z;
@@ -656,9 +683,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
       ptx::mbar_wait(&tmem_full[acc], acc_phase);
       ptx::tc_fence_after();
       if (warp == 4 && ptx::lane_id() == 0 && t == static_cast<int>(blockIdx.x)) trace_mark(p, 5);
+      if (warp == 4 && ptx::lane_id() == 0) trace_tile(p, jt, 2);
       epi_tile_tma<BN / 64>(p, e, tmem_base + ((quad * 32) << 16) + acc * BN, z, row0, nb * BN, half);
       ptx::tc_fence_before();
       if (warp == 4 && ptx::lane_id() == 0) trace_mark(p, 6);
+      if (warp == 4 && ptx::lane_id() == 0) trace_tile(p, jt, 3);
       ptx::mbar_arrive(&tmem_empty[acc]);
       if (++acc == 2) {
         acc = 0;
@@ -726,7 +755,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
     ptx::tc_fence_after();
     ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
   }
-  if (threadIdx.x == 0) trace_mark(p, 7);
+  if (threadIdx.x == 0) trace_exit(p);
 }
 
 
@@ -755,7 +784,7 @@ constexpr int kSmem = kSmemBudget;
 
 template <int BN2>
 __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __grid_constant__ GemmParams p) {
-  if (threadIdx.x == 0) trace_mark(p, 0);
+  if (threadIdx.x == 0) trace_entry(p);
   using Pc = PairCfg<BN2>;
   constexpr int kBN = Pc::kBN, kABytes = Pc::kABytes, kBBytes = Pc::kBBytes, kStageBytes = Pc::kStageBytes;
   const int S = p.stages;
@@ -861,7 +890,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = pair_id; t < p.num_tiles; t += n_pairs) {
+      int jt = 0;
+      for (int t = pair_id; t < p.num_tiles; t += n_pairs, ++jt) {
         const int ks = t % p.k_splits;
         const int kb0 = ks * p.kb_per_split;
         const int kb1 = min(p.num_k_blocks, kb0 + p.kb_per_split);
@@ -872,6 +902,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
           if (t == pair_id && kb == kb0) trace_mark(p, 3);
+          if (kb == kb0) trace_tile(p, jt, 0);
           const uint32_t sa = ptx::smem_addr(smem_a + stage * kABytes);
           const uint32_t sb = ptx::smem_addr(smem_b + stage * kBBytes);
 #pragma unroll
@@ -888,6 +919,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
         }
         ptx::mma_commit_2sm(&tmem_full[acc]);
         trace_mark(p, 4);
+        trace_tile(p, jt, 1);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -900,7 +932,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
     EpiTma e{smem_epi + (warp - 4) * p.epi_warp_bytes, xbar + kEpiBars * (warp - 4), 0, 0};
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = pair_id; t < p.num_tiles; t += n_pairs) {
+    int jt = 0;
+    for (int t = pair_id; t < p.num_tiles; t += n_pairs, ++jt) {
       const int tt = t / p.k_splits;
       const int z = tt / tiles_per_z;
       const int r = tt % tiles_per_z;
@@ -911,10 +944,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
       ptx::mbar_wait(&tmem_full[acc], acc_phase);
       ptx::tc_fence_after();
       if (warp == 4 && lane == 0 && t == pair_id) trace_mark(p, 5);
+      if (warp == 4 && lane == 0) trace_tile(p, jt, 2);
       epi_tile_tma<kBN / 64>(p, e, tmem_base + ((quad * 32) << 16) + acc * kBN, z, row0, nb * kBN, half);
       ptx::tc_fence_before();
       __syncwarp();
       if (warp == 4 && lane == 0) trace_mark(p, 6);
+      if (warp == 4 && lane == 0) trace_tile(p, jt, 3);
       if (lane == 0) {
         if (leader) ptx::mbar_arrive(&tmem_empty[acc]);
         else ptx::mbar_arrive_cluster(&tmem_empty[acc], 0);
@@ -984,7 +1019,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
     ptx::tc_fence_after();
     ptx::tmem_dealloc_2sm<Pc::kTmemCols>(tmem_base);
   }
-  if (threadIdx.x == 0) trace_mark(p, 7);
+  if (threadIdx.x == 0) trace_exit(p);
 }
 
 // ---------------------------------------------------------------- host side
@@ -1178,7 +1213,9 @@ void GemmOp::prepare(const GemmDesc& d) {
   p.num_k_blocks = ceil_div(d.K, kBK);
   p.k_splits = 1;
   p.kb_per_split = p.num_k_blocks;
-  if ((d.epi & kOutMask) == kOutF32Acc) {
+  if ((d.epi & kOutMask) == kOutF32Acc && d.epi != kOutF32Acc)
+    throw std::invalid_argument("dpl gemm: fp32 accumulation takes no other epilogue flags");
+  if (d.epi == kOutF32Acc) {
     // too few tiles for the SMs: split K (>= 8 k-blocks per split) and let
     // the fp32 accumulator absorb the partial sums atomically
     const int sms = two_sm ? num_sms() / 2 : num_sms();

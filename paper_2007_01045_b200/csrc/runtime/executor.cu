@@ -140,6 +140,13 @@ using Route = pipeplan::SplitConcatRoute;
 // after the flag banks: {ping u32, pong u32, peer_time u64} for clock calibration
 constexpr size_t kCalibBytes = 256;
 
+// stream memory operations (cuStreamWaitValue32) usable, process-wide
+bool& memops_flag() {
+  static bool ok = true;
+  return ok;
+}
+bool memops_ok() { return memops_flag(); }
+
 struct BlockEvents {
   cudaEvent_t start = nullptr, end = nullptr;
 };
@@ -166,9 +173,8 @@ class Executor {
     kernel_timer().used = 0;
     // the profiled graph is captured afresh so its event records are current
     for (auto it = graphs_.begin(); it != graphs_.end();) {
-      if (it->first.profile) {
-        cudaGraphExecDestroy(it->second);
-        graph_kernels_.erase(graph_kernels_.begin() + (it - graphs_.begin()));
+      if (it->key.profile) {
+        it->destroy();
         it = graphs_.erase(it);
       } else {
         ++it;
@@ -180,6 +186,7 @@ class Executor {
   std::string timeline_json() const;
   void read_tensor(const std::string& name, bool grad, void* host, size_t bytes);
   std::string info() const;
+  long long graph_count() const;
 
  private:
   // --- configuration
@@ -246,17 +253,51 @@ class Executor {
   float last_loss_ = NAN;
   float* loss_host_ = nullptr;  // pinned
   bool use_graph_ = true, capturing_ = false;
+  // One captured step per (flag bank, host inputs present, host targets
+  // present, profiling).  Host buffers are not part of the key: the graph's
+  // host->device copy nodes are re-pointed in place
+  // (cudaGraphExecMemcpyNodeSetParams1D) when a caller passes a different
+  // pinned buffer, so a data loader rotating buffers never re-captures.
   struct GraphKey {
     int bank;
-    const void* in;
-    const void* tgt;
-    bool profile;
+    bool in, tgt, profile;
     bool operator==(const GraphKey& o) const {
       return bank == o.bank && in == o.in && tgt == o.tgt && profile == o.profile;
     }
   };
-  std::vector<std::pair<GraphKey, cudaGraphExec_t>> graphs_;
-  std::vector<long long> graph_kernels_;  // kernel nodes of graphs_[i] (launch accounting per replay)
+  struct HostCopy {
+    cudaGraphNode_t node;
+    int which;      // 0 input, 1 target
+    size_t offset;  // bytes from the start of the host buffer
+    void* dst;
+    size_t bytes;
+  };
+  struct GraphEntry {
+    GraphKey key;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    long long kernels = 0;  // kernel nodes (launch accounting per replay)
+    std::vector<HostCopy> copies;
+    const void* src[2] = {nullptr, nullptr};  // host buffers the copy nodes currently read
+    void destroy() {
+      if (exec) cudaGraphExecDestroy(exec);
+      if (graph) cudaGraphDestroy(graph);
+      exec = nullptr;
+      graph = nullptr;
+    }
+  };
+  std::vector<GraphEntry> graphs_;
+  // pageable host inputs are staged through executor-owned pinned buffers
+  void* staging_[2] = {nullptr, nullptr};
+  size_t staging_bytes_[2] = {0, 0};
+  const void* stage_host(const void* p, int which);
+ public:
+  // host bytes of this rank's inputs / targets for one step ([M][slice]), 0 if none
+  size_t input_bytes() const;
+  size_t target_bytes() const;
+
+ private:
+  void capture_step(GraphEntry& g, const void* host_input, const void* host_target);
   void enqueue_step(const void* host_input, const void* host_target);
   // this rank's gradients of one parameter block are final: AllReduce over
   // the replica group and apply on the reduce stream
@@ -333,15 +374,27 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
   if (M_ < 1 || gbs_ % M_ != 0) throw std::invalid_argument("dpl exec: GBS must be a multiple of M");
   B_ = gbs_ / M_;
 
-  // plan checks: contiguous cover of the model's layers, disjoint devices
+  // plan checks (the profile-independent part of PipelinePlan::validate,
+  // model.cpp:100-131): contiguous cover of the model's layers, non-empty,
+  // non-negative and pairwise disjoint device sets
   S_ = plan_.compute_stage_count();
   if (S_ < 1) throw std::invalid_argument("dpl exec: empty plan");
   int expect = 0;
   k_ = -1;
+  std::vector<int> owner(static_cast<size_t>(std::max(world_, 1)), -1);
   for (int k = 0; k < S_; ++k) {
     const pipeplan::Stage& st = plan_.stages[k];
     if (st.layer_lo != expect || st.layer_hi <= st.layer_lo)
       throw std::invalid_argument("dpl exec: plan stages must partition the layers");
+    if (st.devices.empty()) throw std::invalid_argument("dpl exec: stage " + std::to_string(k) + " has no GPUs");
+    for (int g : st.devices) {
+      if (g < 0) throw std::invalid_argument("dpl exec: negative GPU id in the plan");
+      if (g < world_) {
+        if (owner[g] >= 0)
+          throw std::invalid_argument("dpl exec: GPU " + std::to_string(g) + " appears in more than one stage slot");
+        owner[g] = k;
+      }
+    }
     expect = st.layer_hi;
     // replica j owns samples [B*j/r, B*(j+1)/r) of every micro-batch
     // (uneven when r does not divide B, as the planner's
@@ -374,6 +427,18 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
     phi_expanded_.resize(Se);
     for (int x = 0; x < Se; ++x) phi_expanded_[x] = std::min(Se - x, M_);
   }
+  // every rank checks the whole vector (check_phi, simulator.cpp:118-133, after
+  // clamping to M): a phi that grows toward the top stage or is < 1 would
+  // deadlock the ranks' flag waits rather than fail
+  if (static_cast<int>(phi_expanded_.size()) != Se)
+    throw std::invalid_argument("dpl exec: phi must have one entry per expanded stage");
+  for (int x = 0; x < Se; ++x) {
+    const int px = std::min(phi_expanded_[x], M_);
+    if (phi_expanded_[x] < 1) throw std::invalid_argument("dpl exec: phi entries must be >= 1");
+    if (x > 0 && px > std::min(phi_expanded_[x - 1], M_))
+      throw std::invalid_argument("dpl exec: phi must be non-increasing toward the top stage");
+  }
+  if (phi_expanded_.back() != 1) throw std::invalid_argument("dpl exec: phi of the topmost stage must be 1");
   phi_ = gpipe_ ? M_ : std::min(phi_expanded_[2 * k_], M_);
   chain_ = pipeplan::stage_chain(M_, phi_, gpipe_ ? pipeplan::ScheduleKind::gpipe : pipeplan::ScheduleKind::dapple);
   // live micro-batches per stage = phi (DAPPLE) or M (GPipe); with
@@ -563,9 +628,8 @@ void Executor::disconnect() {
   cudaSetDevice(device_);
   cudaDeviceSynchronize();
   // captured steps reference the communicator and the peer mappings
-  for (auto& g : graphs_) cudaGraphExecDestroy(g.second);
+  for (auto& g : graphs_) g.destroy();
   graphs_.clear();
-  graph_kernels_.clear();
   if (comm_) {
     ncclCommDestroy(comm_);
     comm_ = nullptr;
@@ -579,8 +643,54 @@ void Executor::disconnect() {
 Executor::~Executor() {
   disconnect();
   if (loss_host_) cudaFreeHost(loss_host_);
+  for (void* p : staging_)
+    if (p) cudaFreeHost(p);
+  for (cudaEvent_t e : {ev_begin_, ev_end_, ev_reduce_done_, ev_sa_done_, ev_sg_done_, ev_fork_, ev_last_bwd_,
+                        emb_done_, head_done_})
+    if (e) cudaEventDestroy(e);
+  for (auto* v : {&fwd_ev_, &bwd_ev_, &send_fwd_ev_, &send_bwd_ev_})
+    for (BlockEvents& b : *v) {
+      if (b.start) cudaEventDestroy(b.start);
+      if (b.end) cudaEventDestroy(b.end);
+    }
+  for (auto* v : {&layer_done_, &fwd_done_, &bwd_done_})
+    for (cudaEvent_t e : *v)
+      if (e) cudaEventDestroy(e);
   for (cudaStream_t s : {compute_, send_act_, send_grad_s_, reduce_})
     if (s) cudaStreamDestroy(s);
+}
+
+size_t Executor::input_bytes() const {
+  if (k_ != 0) return 0;
+  if (emb_) return static_cast<size_t>(M_) * ctx_.rows * 4;  // token ids
+  return static_cast<size_t>(M_) * in_elems() * 2;
+}
+
+size_t Executor::target_bytes() const {
+  if (k_ != S_ - 1) return 0;
+  if (head_) return static_cast<size_t>(M_) * ctx_.rows * 4;        // next-token ids
+  if (classify()) return static_cast<size_t>(M_) * ctx_.samples * 4;  // class labels
+  return static_cast<size_t>(M_) * out_elems() * 2;
+}
+
+// Pinned (or registered) host memory is used in place; pageable memory is
+// copied into an executor-owned pinned buffer first (a captured step can
+// only read page-locked memory).
+const void* Executor::stage_host(const void* p, int which) {
+  if (!p) return nullptr;
+  const size_t bytes = which == 0 ? input_bytes() : target_bytes();
+  if (bytes == 0) return nullptr;  // this rank consumes no such tensor
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) == cudaSuccess && a.type == cudaMemoryTypeHost) return p;
+  cudaGetLastError();
+  if (staging_bytes_[which] < bytes) {
+    if (staging_[which]) DPL_CUDA(cudaFreeHost(staging_[which]));
+    staging_[which] = nullptr;
+    DPL_CUDA(cudaMallocHost(&staging_[which], bytes));
+    staging_bytes_[which] = bytes;
+  }
+  std::memcpy(staging_[which], p, bytes);
+  return staging_[which];
 }
 
 size_t Executor::export_blob(void* blob, size_t cap) {
@@ -660,13 +770,12 @@ void Executor::nccl_init(const void* id) {
 }
 
 void Executor::wait_flag(cudaStream_t s, uint32_t* flag, uint32_t value) {
-  static bool memops_ok = true;
-  if (memops_ok) {
+  if (memops_ok()) {
     if (StreamValueFn fn = wait_value_fn()) {
       const CUresult rc = fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flag), value, 0x0 /*GEQ*/);
       if (rc == CUDA_SUCCESS) return;
     }
-    memops_ok = false;  // not available / not capturable: one-thread acquire spin on this stream
+    memops_flag() = false;  // not available / not capturable: one-thread acquire spin on this stream
   }
   count_launch();
   wait_kernel<<<1, 1, 0, s>>>(flag, value);
@@ -885,68 +994,106 @@ void Executor::enqueue_step(const void* host_input, const void* host_target) {
   DPL_CUDA(cudaMemsetAsync(flags(), 0, 2 * static_cast<size_t>(world_) * 4, compute_));
 }
 
+// Captures enqueue_step into g.  A stream memory op that cannot be captured
+// invalidates the capture; wait_flag then switches to its kernel form and the
+// capture is retried once.  Any other failure is rethrown as is.
+void Executor::capture_step(GraphEntry& g, const void* host_input, const void* host_target) {
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    cudaGraph_t graph = nullptr;
+    const long long counted0 = launch_count();
+    const bool memops_before = memops_ok();
+    DPL_CUDA(cudaStreamBeginCapture(compute_, cudaStreamCaptureModeRelaxed));
+    capturing_ = true;
+    kernel_timer().capturing = true;
+    std::string error;
+    try {
+      enqueue_step(host_input, host_target);
+    } catch (const std::exception& e) {
+      error = e.what();
+    }
+    capturing_ = false;
+    kernel_timer().capturing = false;
+    const cudaError_t end = cudaStreamEndCapture(compute_, &graph);
+    // captured launches are not executions: the kernel nodes are counted on
+    // every replay instead
+    count_launch(counted0 - launch_count());
+    if (error.empty() && end == cudaSuccess && graph) {
+      g.graph = graph;
+      DPL_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
+      size_t n_nodes = 0;
+      DPL_CUDA(cudaGraphGetNodes(graph, nullptr, &n_nodes));
+      std::vector<cudaGraphNode_t> nodes(n_nodes);
+      DPL_CUDA(cudaGraphGetNodes(graph, nodes.data(), &n_nodes));
+      const void* bases[2] = {host_input, host_target};
+      const size_t sizes[2] = {input_bytes(), target_bytes()};
+      g.kernels = 0;
+      for (cudaGraphNode_t nd : nodes) {
+        // stream memory-op nodes (the flag waits) have no runtime-API type:
+        // the query fails for them, which is fine -- only kernels and host
+        // copies matter here
+        cudaGraphNodeType t;
+        if (cudaGraphNodeGetType(nd, &t) != cudaSuccess) {
+          cudaGetLastError();
+          continue;
+        }
+        if (t == cudaGraphNodeTypeKernel) ++g.kernels;
+        if (t != cudaGraphNodeTypeMemcpy) continue;
+        cudaMemcpy3DParms mp{};
+        if (cudaGraphMemcpyNodeGetParams(nd, &mp) != cudaSuccess) {
+          cudaGetLastError();
+          continue;
+        }
+        const char* src = static_cast<const char*>(mp.srcPtr.ptr);
+        for (int w = 0; w < 2; ++w) {
+          const char* b = static_cast<const char*>(bases[w]);
+          if (b && src >= b && src < b + sizes[w])
+            g.copies.push_back({nd, w, static_cast<size_t>(src - b), mp.dstPtr.ptr, mp.extent.width});
+        }
+      }
+      g.src[0] = host_input;
+      g.src[1] = host_target;
+      return;
+    }
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    const bool retry = memops_before && !memops_ok();  // the flag waits fell back to kernels
+    if (!retry || attempt == 1)
+      throw std::runtime_error("dpl exec: step capture failed: " +
+                               (error.empty() ? std::string(cudaGetErrorString(end)) : error));
+  }
+}
+
 float Executor::step(const void* host_input, const void* host_target) {
   DPL_CUDA(cudaSetDevice(device_));
+  host_input = stage_host(host_input, 0);
+  host_target = stage_host(host_target, 1);
   const bool profiling = ctx_.gemms.profile.enabled || kernel_timer().enabled;
   if (!use_graph_) {
     enqueue_step(host_input, host_target);
   } else {
     // a profiled step is its own graph (per-launch timing events inside);
     // its records are re-registered on every capture
-    const GraphKey key{bank_, host_input, host_target, profiling};
-    cudaGraphExec_t exec = nullptr;
-    long long kernels = 0;
-    for (size_t gi = 0; gi < graphs_.size(); ++gi)
-      if (graphs_[gi].first == key) {
-        exec = graphs_[gi].second;
-        kernels = graph_kernels_[gi];
-      }
-    // capture (a stream memory op that cannot be captured invalidates the
-    // capture; wait_flag then switches to its kernel form and we retry once)
-    for (int attempt = 0; !exec && attempt < 2; ++attempt) {
-      cudaGraph_t graph = nullptr;
-      const long long counted0 = launch_count();
-      DPL_CUDA(cudaStreamBeginCapture(compute_, cudaStreamCaptureModeRelaxed));
-      capturing_ = true;
-      kernel_timer().capturing = true;
-      bool ok = true;
-      try {
-        enqueue_step(host_input, host_target);
-      } catch (...) {
-        ok = false;
-      }
-      capturing_ = false;
-      kernel_timer().capturing = false;
-      const cudaError_t end = cudaStreamEndCapture(compute_, &graph);
-      // captured launches are not executions: the kernel nodes are counted
-      // on every replay instead
-      count_launch(counted0 - launch_count());
-      if (ok && end == cudaSuccess && graph) {
-        DPL_CUDA(cudaGraphInstantiate(&exec, graph, 0));
-        size_t n_nodes = 0;
-        DPL_CUDA(cudaGraphGetNodes(graph, nullptr, &n_nodes));
-        std::vector<cudaGraphNode_t> nodes(n_nodes);
-        DPL_CUDA(cudaGraphGetNodes(graph, nodes.data(), &n_nodes));
-        kernels = 0;
-        for (cudaGraphNode_t nd : nodes) {
-          // stream memory-op nodes (the flag waits) have no runtime-API type:
-          // the query fails for them, which is fine -- only kernels count
-          cudaGraphNodeType t;
-          if (cudaGraphNodeGetType(nd, &t) == cudaSuccess) {
-            if (t == cudaGraphNodeTypeKernel) ++kernels;
-          } else {
-            cudaGetLastError();
-          }
-        }
-        graphs_.push_back({key, exec});
-        graph_kernels_.push_back(kernels);
-      }
-      if (graph) cudaGraphDestroy(graph);
-      cudaGetLastError();
-      if (!exec && attempt == 1) throw std::runtime_error("dpl exec: step capture failed");
+    const GraphKey key{bank_, host_input != nullptr, host_target != nullptr, profiling};
+    GraphEntry* g = nullptr;
+    for (GraphEntry& e : graphs_)
+      if (e.key == key) g = &e;
+    if (!g) {
+      GraphEntry fresh;
+      fresh.key = key;
+      capture_step(fresh, host_input, host_target);
+      graphs_.push_back(std::move(fresh));
+      g = &graphs_.back();
     }
-    DPL_CUDA(cudaGraphLaunch(exec, compute_));
-    count_launch(kernels);
+    const void* now[2] = {host_input, host_target};
+    for (const HostCopy& c : g->copies)
+      if (now[c.which] != g->src[c.which])
+        DPL_CUDA(cudaGraphExecMemcpyNodeSetParams1D(g->exec, c.node, c.dst,
+                                                     static_cast<const char*>(now[c.which]) + c.offset, c.bytes,
+                                                     cudaMemcpyHostToDevice));
+    g->src[0] = host_input;
+    g->src[1] = host_target;
+    DPL_CUDA(cudaGraphLaunch(g->exec, compute_));
+    count_launch(g->kernels);
   }
   DPL_CUDA(cudaStreamSynchronize(compute_));
   DPL_CUDA(cudaGetLastError());
@@ -958,7 +1105,7 @@ float Executor::step(const void* host_input, const void* host_target) {
   return loss;
 }
 
-
+long long Executor::graph_count() const { return static_cast<long long>(graphs_.size()); }
 
 std::string Executor::timeline_json() const {
   auto ms = [&](cudaEvent_t e) {
@@ -1224,6 +1371,11 @@ std::string Executor::info() const {
   v["device_bytes"] = static_cast<long long>(mem_.total());
   v["flops_per_step"] = flops_per_step_;
   v["gemm_plans"] = static_cast<long long>(ctx_.gemms.size());
+  v["input_bytes"] = static_cast<long long>(input_bytes());
+  v["target_bytes"] = static_cast<long long>(target_bytes());
+  v["input_dtype"] = emb_ ? "int32" : "bfloat16";
+  v["target_dtype"] = (head_ || classify()) ? "int32" : "bfloat16";
+  v["graphs"] = graph_count();
   Value chain = Value::array();
   for (const auto& c : chain_) chain.push_back(std::string(c.kind == pipeplan::BlockKind::forward ? "F" : "B") +
                                                std::to_string(c.micro_batch));

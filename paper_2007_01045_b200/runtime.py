@@ -96,10 +96,46 @@ class Executor:
         ([M][rows][H] bf16), or None to generate the seeded synthetic data on
         the device.  Returns the global-batch loss on last-stage ranks."""
         loss = ctypes.c_float(float("nan"))
-        pin = None if host_input is None else ctypes.c_void_p(host_input.data_ptr())
-        pt = None if host_target is None else ctypes.c_void_p(host_target.data_ptr())
+        pin = self._host_arg(host_input, "input")
+        pt = self._host_arg(host_target, "target")
         check(lib().dpl_exec_step(self._h, pin, pt, ctypes.byref(loss)))
         return loss.value
+
+    def _host_arg(self, t, which: str):
+        """Validates one step's host tensor (this rank's slices of every
+        micro-batch) and returns its address.  Pinned memory is read in place
+        by the captured step; pageable memory is staged by the library."""
+        if t is None:
+            return None
+        want = self.info[f"{which}_bytes"]
+        if want == 0:  # this rank's stage does not consume it (e.g. targets on stage 0)
+            return None
+        import numpy as np
+        import torch
+        if isinstance(t, np.ndarray):
+            t = torch.from_numpy(t)
+        if not isinstance(t, torch.Tensor):
+            raise TypeError(f"{which}: expected a torch.Tensor or numpy array, got {type(t).__name__}")
+        if t.device.type != "cpu":
+            raise ValueError(f"{which}: host tensor expected, got device {t.device}")
+        dtype = {"int32": torch.int32, "bfloat16": torch.bfloat16}[self.info[f"{which}_dtype"]]
+        if t.dtype != dtype:
+            raise TypeError(f"{which}: dtype {t.dtype}, expected {dtype}")
+        if not t.is_contiguous():
+            raise ValueError(f"{which}: tensor must be contiguous")
+        if t.numel() * t.element_size() != want:
+            raise ValueError(f"{which}: {t.numel() * t.element_size()} bytes, expected {want} "
+                             f"([M={self.M}] x this replica's slice)")
+        if dtype == torch.int32:
+            hi = self.model.get("vocab") if (which == "input" or self.model.get("vocab")) else self.model.get("classes")
+            lo_v, hi_v = int(t.min()), int(t.max())
+            if lo_v < 0 or (hi and hi_v >= hi):
+                raise ValueError(f"{which}: ids must lie in [0, {hi}), got [{lo_v}, {hi_v}]")
+        return ctypes.c_void_p(t.data_ptr())
+
+    def graphs(self) -> int:
+        """Captured step graphs held (one per flag bank x host-data mode)."""
+        return self._info()["graphs"]
 
     def gemm_profile(self, enable: bool):
         check(lib().dpl_exec_gemm_profile(self._h, int(enable)))
