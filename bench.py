@@ -1,15 +1,16 @@
 #!/usr/bin/env python
 """bench.py -- DAPPLE synchronous pipelined-DP training step on B200.
 
-Workload (BASELINE.json configs[1]): BERT-48 encoder, hidden 1024, seq 512,
-16 heads, FFN 4096, bf16, MSE regression head, synthetic data, M = 8
-micro-batches, each stage replica owning an 8-sample (4096-token) slice of
-every micro-batch.  Plans:
+Workload (BASELINE.json configs[1], C2): BERT-48 encoder, hidden 1024, seq
+512, 16 heads, FFN 4096, bf16, MSE regression head, synthetic data, global
+batch 64 at every N (strong scaling), M = 8 micro-batches of 8 samples.  Plans:
   N = 1   [0,48) x1                         (the step: 8 micro-batches accumulated)
-  N >= 2  [0,24) x N/2 | [24,48) x N/2      (BASELINE's 2-stage shape; 2 x 4 at N = 8)
-so the global batch is 64 samples per replica group (GBS = 64 * N / S).
+  N >= 2  the host planner's plan (bit-exact to the reference planner) on
+          B200 layer profiles taken at the plan's own replica slice sizes,
+          per_gpu_memory_gb 12 so that pure DP is infeasible (C2: 2 stages x
+          4 replicas at N = 8, 2-sample replica slices).
 --model gpt2-1.5b (configs[3], C4): GPT-2 1.5B with token embedding and
-causal-LM cross-entropy head (vocab 50304), a straight N-stage pipeline,
+causal-LM cross-entropy head (vocab 50257), a straight N-stage pipeline,
 M = 32 micro-batches of 1 sample (GBS 32 at every N: strong scaling).
 
 Metric: training samples/s of the whole job (value: device-timed, inputs
@@ -37,8 +38,8 @@ sys.path.insert(0, ROOT)
 
 MODELS = {
     "bert48": dict(kind="bert", layers=48, hidden=1024, heads=16, ffn=4096, seq=512),
-    # C4: GPT-2 1.5B, causal-LM cross-entropy over the padded 50304-token vocabulary
-    "gpt2-1.5b": dict(kind="gpt", layers=48, hidden=1600, heads=25, ffn=6400, seq=1024, vocab=50304),
+    # C4: GPT-2 1.5B, causal-LM cross-entropy over the 50257-token vocabulary (projection stored padded to 50264 rows, padding masked)
+    "gpt2-1.5b": dict(kind="gpt", layers=48, hidden=1600, heads=25, ffn=6400, seq=1024, vocab=50257),
     "mlp16": dict(kind="mlp", layers=16, hidden=1024),
     # C3: VGG-19 on 224x224 images, 1000-class cross-entropy (convs as im2col + tcgen05 GEMM)
     "vgg19": dict(kind="vgg", layers=19, image=224, width=64, fc=4096, classes=1000),
@@ -79,10 +80,43 @@ def flops_per_sample(m: dict) -> float:
 
 # per-workload defaults (BASELINE.json configs): C2 BERT-48 2 stages x N/2,
 # M=8; C4 GPT-2 a straight N-stage pipeline, M=32 micro-batches of 1 sample
-DEFAULTS = {"bert48": dict(micro_batches=8, slice=8, straight=False),
+DEFAULTS = {"bert48": dict(micro_batches=8, slice=8, straight=False, global_batch=64),
             "gpt2-1.5b": dict(micro_batches=32, slice=1, straight=True),
             "mlp16": dict(micro_batches=8, slice=8, straight=False),
             "vgg19": dict(micro_batches=8, slice=24, straight=False)}
+
+
+def plan_fixed_point(model: dict, profiles: dict, mb: int, cluster: dict, m: int, max_iter: int = 4):
+    """The host planner's plan (pipeplan.plan, bit-exact to the reference's
+    planner.cpp:306-421) on B200 layer profiles taken at the plan's OWN
+    replica slice sizes: the reference cost model divides a stage's time by r
+    (model.cpp:228-230), which assumes perfect strong scaling of a layer over
+    smaller slices; so profile at mb, plan, profile every layer at the slice
+    its stage runs (times x r, slice_profile), re-plan, until the plan stops
+    changing.  At the fixed point the planner's est / sim L for its own plan
+    are computed from the times its replicas actually run at."""
+    from paper_2007_01045_b200 import pipeplan
+    prof = profiles[mb]
+    history = []
+    plan = None
+    for it in range(max_iter):
+        res = pipeplan.plan(prof, cluster, m)["plan"]
+        history.append({"stages": [[s["layers"], s["gpus"]] for s in res["stages"]], "phi": res.get("phi"),
+                        "est_ms": res.get("est_latency_us", 0) / 1e3, "sim_ms": res.get("sim_latency_us", 0) / 1e3})
+        if plan is not None and [s["layers"] for s in res["stages"]] == [s["layers"] for s in plan["stages"]] and \
+                [s["gpus"] for s in res["stages"]] == [s["gpus"] for s in plan["stages"]]:
+            plan = res
+            break
+        plan = res
+        for st in plan["stages"]:
+            size = -(-mb // len(st["gpus"]))
+            if size not in profiles:
+                profiles[size] = profile_model(model, size)
+        prof = slice_profile(profiles, plan, mb)
+    fixed = len(history) >= 2 and history[-1]["stages"] == history[-2]["stages"]
+    return plan, {"iterations": history, "fixed_point": fixed, "per_gpu_memory_gb": cluster["per_gpu_memory_gb"],
+                  "est_latency_ms": plan.get("est_latency_us", 0) / 1e3,
+                  "sim_latency_ms": plan.get("sim_latency_us", 0) / 1e3}
 
 
 def make_plan(n: int, layers: int, straight: bool = False, kind: str = "") -> dict:
@@ -250,10 +284,47 @@ def host_batches(model: dict, plan: dict, rank: int, m: int, B: int, seed: int):
     return inp, tgt
 
 
-def b200_cluster(n: int, mem_gb: float = 180.0) -> dict:
-    # NVLink 5 through NVSwitch: measured 770 GB/s peer copy (B200_PROFILING.md)
-    return {"seps": [n], "intra_bw_gbps": 770.0, "inter_bw_gbps": 50.0, "intra_latency_us": 5.0,
+def b200_cluster(n: int, mem_gb: float = 180.0, link: dict | None = None) -> dict:
+    """ClusterSpec of one NVSwitch node (model.cpp:175-199 units).  intra_bw /
+    intra_latency come from this run's peer-copy sweep (calibrate_link) when
+    there is a second GPU, else the recipe's measured 770 GB/s peer copy
+    (B200_PROFILING.md); inter_* is unused on one node but must be > 0."""
+    bw, lat = (link["bw_gbps"], link["latency_us"]) if link else (770.0, 5.0)
+    return {"seps": [n], "intra_bw_gbps": bw, "inter_bw_gbps": 50.0, "intra_latency_us": lat,
             "inter_latency_us": 10.0, "per_gpu_memory_gb": mem_gb}
+
+
+def calibrate_link(reps: int = 20) -> dict:
+    """Peer copies cuda:0 -> cuda:1 over NVLink (copy engines, the path the
+    Split-Concat hand-off takes) at 256 KiB .. 64 MiB, timed with CUDA events;
+    least-squares fit t = latency + bytes / bw (costmodel.cpp:52-71's flow
+    model).  Rank 0 only, before the executors exist."""
+    import torch
+    sizes = [1 << 18, 1 << 20, 1 << 22, 1 << 24, 1 << 26]
+    src = torch.empty(sizes[-1], dtype=torch.uint8, device="cuda:0")
+    dst = torch.empty(sizes[-1], dtype=torch.uint8, device="cuda:1")
+    pts = []
+    for n in sizes:
+        for _ in range(3):
+            dst[:n].copy_(src[:n], non_blocking=True)
+        torch.cuda.synchronize(0)
+        torch.cuda.synchronize(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            dst[:n].copy_(src[:n], non_blocking=True)
+        b.record()
+        b.synchronize()
+        pts.append((n, a.elapsed_time(b) * 1e-3 / reps))
+    xs = [n for n, _ in pts]
+    ys = [t for _, t in pts]
+    mx, my = statistics.mean(xs), statistics.mean(ys)
+    slope = sum((x - mx) * (y - my) for x, y in zip(xs, ys)) / sum((x - mx) ** 2 for x in xs)
+    lat = max(my - slope * mx, 0.0)
+    return {"bw_gbps": 1.0 / slope / 1e9, "latency_us": lat * 1e6,
+            "points": [{"bytes": n, "us": t * 1e6, "gbps": n / t / 1e9} for n, t in pts],
+            "how": "cuda:0 -> cuda:1 tensor copies (cudaMemcpyPeerAsync, copy engines), CUDA events, "
+                   f"{reps} back to back per size; fit t = latency + bytes / bw"}
 
 
 def profile_model(model: dict, mb: int, reps: int = 5) -> dict:
@@ -334,6 +405,85 @@ def predicted_latency(plan, profile, cluster, m, n, schedule="dapple"):
             "sim_bubble": 1.0 - busy / (n * sim["latency"]), "pivot": est["pivot"]}
 
 
+def planner_cpu_times(profile: dict, cluster: dict, m: int, plan_json: dict) -> dict:
+    """the reference's own plan() and
+    simulate_plan() (oracle/_ref/ref_cli, compiled from /root/reference) on
+    this run's profile and cluster, timed on this host beside the new host
+    planner (sequential and parallel search) for the same request; the plans
+    must be identical."""
+    from oracle import refproc  # checker / CPU baseline only
+    req = {"op": "plan", "profile": profile, "cluster": cluster, "M": m}
+    sim = {"op": "simulate_plan", "plan": plan_json, "profile": profile, "cluster": cluster, "M": m}
+    out = {"cores": os.cpu_count(), "M": m, "layers": len(profile["layers"]), "gpus": cluster["seps"]}
+    from paper_2007_01045_b200 import pipeplan
+    t = time.perf_counter()
+    mine = pipeplan.call("plan", profile=profile, cluster=cluster, M=m, threads=1)
+    out["ours_plan_seq_s"] = time.perf_counter() - t
+    t = time.perf_counter()
+    mine_par = pipeplan.call("plan", profile=profile, cluster=cluster, M=m, threads=os.cpu_count())
+    out["ours_plan_par_s"] = time.perf_counter() - t
+    t = time.perf_counter()
+    mine_sim = pipeplan.simulate_plan(plan_json, profile, cluster, m)
+    out["ours_simulate_s"] = time.perf_counter() - t
+    if not refproc.available():
+        out["reference"] = "oracle/_ref/ref_cli not built (needs /root/reference at build time)"
+        return out
+    ref = refproc.ReferenceProcess()
+    try:
+        t = time.perf_counter()
+        theirs = ref.call(req)
+        out["reference_plan_s"] = time.perf_counter() - t
+        t = time.perf_counter()
+        theirs_sim = ref.call(sim)
+        out["reference_simulate_s"] = time.perf_counter() - t
+    finally:
+        ref.close()
+    out["identical_plan"] = theirs.get("plan") == mine.get("plan") == mine_par.get("plan")
+    out["identical_sim_latency"] = theirs_sim.get("latency") == mine_sim.get("latency")
+    return out
+
+
+def comm_stats(tls: list, link: dict | None) -> dict:
+    """Split-Concat and replica-AllReduce traffic of one measured step (every
+    rank's timeline): bytes moved and the achieved rate against the link.
+    Split-Concat: each send block moves send_bytes (forward) / send_back_bytes
+    (backward) from one rank.  AllReduce: bus bandwidth 2(r-1)/r x bytes / t
+    per parameter block (the ring formula costmodel.cpp:41-50 charges)."""
+    link_bw = link["bw_gbps"] if link else 770.0
+    sc_bytes, sc_rates, sc_time = 0, [], 0.0
+    ar_bytes, ar_rates, ar_time, impl = 0, [], 0.0, "none"
+    for tl in tls:
+        x0 = 2 * tl["stage"]
+        for x, i, kind, st, en in tl["blocks"]:
+            if x == x0 or st < 0 or en <= st:
+                continue
+            nbytes = tl.get("send_bytes", 0) if kind == 0 else tl.get("send_back_bytes", 0)
+            if nbytes:
+                sc_bytes += nbytes
+                sc_time += en - st
+                sc_rates.append(nbytes / (en - st) / 1e9)
+        r = tl.get("replication", 1)
+        for blk, st, en, nbytes in tl.get("allreduce", []):
+            if en > st and r > 1:
+                impl = tl.get("allreduce_impl", impl)
+                ar_bytes += nbytes
+                ar_time += en - st
+                ar_rates.append(2.0 * (r - 1) / r * nbytes / (en - st) / 1e9)
+    out = {"link_gbps": link_bw, "link_source": "this run's peer-copy fit" if link else "B200_PROFILING.md 770 GB/s"}
+    if sc_rates:
+        med = statistics.median(sc_rates)
+        out["splitconcat"] = {"bytes_per_step": sc_bytes, "sends": len(sc_rates), "gbps_median": med,
+                              "gbps_aggregate": sc_bytes / sc_time / 1e9, "frac_of_link": med / link_bw,
+                              "frac_of_nvlink_nominal": med / 900.0}
+    if ar_rates:
+        med = statistics.median(ar_rates)
+        out["allreduce"] = {"impl": impl, "bytes_per_step": ar_bytes, "blocks": len(ar_rates),
+                            "busbw_gbps_median": med, "busbw_gbps_aggregate": sum(ar_rates) / len(ar_rates),
+                            "frac_of_link": med / link_bw, "frac_of_nvlink_nominal": med / 900.0,
+                            "seconds_per_step_max_rank": ar_time / max(1, len(tls))}
+    return out
+
+
 def cpu_baseline(model: dict, budget_layers: int | None = None) -> dict:
     """The oracle's CPU step (numpy, all host cores) on a bounded sample:
     one sample through `budget_layers` layers, fwd + bwd + SGD."""
@@ -396,10 +546,14 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-layers", type=int, default=8)
     ap.add_argument("--seed", type=int, default=1234)
-    ap.add_argument("--plan", default="forced", choices=["forced", "planner"],
-                    help="forced: [0,L)x1 / 2 stages x N/2; planner: the host planner's plan for the B200 profile")
-    ap.add_argument("--mem-gb", type=float, default=180.0, help="per_gpu_memory_gb given to the planner")
-    ap.add_argument("--global-batch", type=int, default=0, help="default: M x slice x (N/2 or 1)")
+    ap.add_argument("--plan", default="auto", choices=["auto", "forced", "planner"],
+                    help="forced: [0,L)x1 / 2 stages x N/2 / straight; planner: the host planner's plan for the B200 "
+                         "profile (profiled at its own replica slice sizes until the plan is a fixed point); "
+                         "auto: planner for BERT-48 at N >= 2 (C2), forced otherwise")
+    ap.add_argument("--mem-gb", type=float, default=None,
+                    help="per_gpu_memory_gb given to the planner (default: 12 for BERT-48 -- pure DP needs 8 x P = "
+                         "19.3 GB, so the planner must pipeline, as C2 does; 180 otherwise)")
+    ap.add_argument("--global-batch", type=int, default=0, help="default: the workload's (BERT-48: 64 at every N)")
     ap.add_argument("--no-profile", action="store_true", help="skip the pre-run B200 layer profile")
     ap.add_argument("--schedule", default="dapple", choices=["dapple", "gpipe"])
     ap.add_argument("--recompute", action="store_true")
@@ -425,17 +579,26 @@ def main():
     model = MODELS[args.model]
     M = args.micro_batches
     straight = dflt["straight"]
-    strong = straight or model["kind"] == "vgg"  # fixed global batch at every N
-    gbs = args.global_batch or M * args.slice * (1 if straight or model["kind"] == "vgg" else max(1, world // 2))
-    cluster = b200_cluster(world, args.mem_gb)
+    strong = straight or model["kind"] == "vgg" or "global_batch" in dflt  # fixed global batch at every N
+    gbs = args.global_batch or dflt.get("global_batch") or M * args.slice
+    if args.plan == "auto":
+        args.plan = "planner" if args.model == "bert48" and world >= 2 else "forced"
+    if args.mem_gb is None:
+        args.mem_gb = 12.0 if args.model == "bert48" else 180.0
+    # NVLink calibration (peer-copy sweep on rank 0) feeds the cluster's intra_bw / intra_latency
+    link = calibrate_link() if rank == 0 and world >= 2 else None
+    link = broadcast(link, world)
+    cluster = b200_cluster(world, args.mem_gb, link)
     # pre-run B200 layer profile at the micro-batch size: the planner's input
     # and the source of the predicted L (a real prediction, made before the run)
     mb = gbs // M
     profiles = {}  # samples -> B200 layer profile at that size
+    planner_info = None
     if not args.no_profile or args.plan == "planner":
         profiles[mb] = profile_model(model, mb) if rank == 0 else None
     if args.plan == "planner":
-        plan = pipeplan.plan(profiles[mb], cluster, M)["plan"] if rank == 0 else None
+        if rank == 0:
+            plan, planner_info = plan_fixed_point(model, profiles, mb, cluster, M)
         plan = broadcast(plan, world)
     else:
         plan = make_plan(world, model["layers"], straight, model["kind"])
@@ -504,12 +667,17 @@ def main():
     e2e = None
     if not args.no_e2e:
         inp, tgt = host_batches(model, plan, rank, M, gbs // M, args.seed)
-        for _ in range(2):  # warm the H2D path: one captured graph per flag bank (banks alternate by step)
-            ex.step(inp, tgt)
+        # three pinned buffer pairs in rotation, as a data loader hands them in:
+        # the captured step's copy nodes are re-pointed, never re-captured
+        bufs = [(inp, tgt)] + [(None if inp is None else inp.clone().pin_memory(),
+                                None if tgt is None else tgt.clone().pin_memory()) for _ in range(2)]
+        for k in range(2):  # warm the H2D path: one captured graph per flag bank (banks alternate by step)
+            ex.step(*bufs[k])
+        graphs_before = ex.graphs()
         barrier(world)
         t0 = time.perf_counter()
-        for _ in range(args.steps):
-            ex.step(inp, tgt)  # H2D of the step's inputs/targets, D2H of the loss
+        for k in range(args.steps):
+            ex.step(*bufs[k % 3])  # H2D of the step's inputs/targets, D2H of the loss
         torch.cuda.synchronize()
         barrier(world)
         t_e2e = time.perf_counter() - t0
@@ -519,7 +687,8 @@ def main():
         sums = gather((h2d, d2h, t_e2e), world)
         e2e = {"value": args.steps * gbs / max(s[2] for s in sums), "unit": "samples/s",
                "h2d_bytes_per_step": sum(s[0] for s in sums), "d2h_bytes_per_step": sum(s[1] for s in sums),
-               "timing": "wall clock between barriers, pinned host buffers"}
+               "timing": "wall clock between barriers, 3 pinned host buffer pairs in rotation",
+               "captures_during_timed_steps": ex.graphs() - graphs_before}
 
     info = ex.info
     ex.close()
@@ -589,7 +758,12 @@ def main():
         "schedule": {"kind": args.schedule, "recompute": args.recompute, "stash_slots": info["stash_slots"],
                      "peak_activations_measured": exported["peak_activations"],
                      "device_bytes": info.get("device_bytes")},
+        "comm": comm_stats([all_tls[r][-1] for r in range(world)], link),
+        "link_calibration": link,
         "latency": {"measured_ms": measured_ms,
+                    "planner": None if planner_info is None else {
+                        **planner_info, "measured_over_planner_sim": measured_ms / planner_info["sim_latency_ms"],
+                        "measured_over_planner_est": measured_ms / planner_info["est_latency_ms"]},
                     "predicted": None if pred is None else {
                         **pred, "measured_over_sim": measured_ms / pred["sim_ms"],
                         "profile": "B200 layer profiles taken before the run (Executor.layer_profile) at "
@@ -610,6 +784,15 @@ def main():
     }
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(model, budget_layers=min(model["layers"], 48))
+        if profile is not None:
+            # the reference planner + simulator beside the new host planner on
+            # the C2 planning problem built from this run's B200 profile
+            try:
+                c2 = b200_cluster(8, 12.0)
+                c2_plan = pipeplan.plan(profile, c2, M)["plan"]
+                line["cpu_baseline"]["planner"] = planner_cpu_times(profile, c2, M, c2_plan)
+            except Exception as e:  # noqa: BLE001 -- a missing checker must not cost the line
+                line["cpu_baseline"]["planner"] = {"error": str(e)[:200]}
     print(json.dumps(line), flush=True)
 
 

@@ -125,6 +125,10 @@ int dpl_k_sgd_apply(float* w32, float* g, void* w16, long long n, float lr, void
 int dpl_k_fill_tokens(int* dst, long long n, uint64_t seed, uint64_t tensor, long long idx0, int vocab, void* stream);
 int dpl_k_embed_fwd(const int* tok, const void* wte, const void* wpe, void* x, int rows, int seq, int h, void* stream);
 int dpl_k_embed_bwd(const int* tok, const void* dx, float* gwte, float* gwpe, int rows, int seq, int h, void* stream);
+/* the same over rows of stride ld >= vocab (ld % 8 == 0): columns past vocab
+ * are padding, excluded from the softmax, gradient 0 */
+int dpl_k_cross_entropy_padded(void* logits, const int* tgt, float* loss_acc, int rows, int vocab, int ld,
+                               float grad_scale, void* stream);
 int dpl_k_cross_entropy(void* logits, const int* tgt, float* loss_acc, int rows, int vocab, float grad_scale,
                         void* stream);
 /* VGG convolution support (config C3; NHWC bf16, 3x3 stride-1 pad-1 convs as
@@ -152,13 +156,18 @@ typedef struct dpl_exec dpl_exec; /* one per process / GPU */
  * world size.  Allocates parameters, gradients, activation stash and
  * Split-Concat receive buffers on `device`. */
 int dpl_exec_create(const char* config_json, int device, dpl_exec** out);
-/* Opaque blob this rank must share with every other rank (CUDA IPC handles
- * of its receive buffers and flag words); dpl_exec_connect takes the blobs
- * of all ranks, concatenated in rank order. */
+/* Opaque blob (<= 256 bytes) this rank must share with every other rank:
+ * CUDA IPC handles of its receive region (activations, gradients, flag
+ * words, loss) and of its fp32 gradients, plus process id / device / raw
+ * pointers so ranks living in one process (several ranks on one GPU) map
+ * each other without IPC.  dpl_exec_connect takes the blobs of all ranks,
+ * concatenated in rank order. */
 int dpl_exec_export(dpl_exec* ex, void* blob, size_t cap, size_t* len);
 int dpl_exec_connect(dpl_exec* ex, const void* blobs, size_t blob_len, int world);
-/* NCCL: rank 0 of each stage group creates the id (128 bytes), the group
- * shares it, then every member initialises its communicator. */
+/* NCCL (config "allreduce": "nccl" only; the default "peer" reduces the
+ * replica group over peer memory): rank 0 of each stage group creates the id
+ * (128 bytes), the group shares it, then every member initialises its
+ * communicator. */
 int dpl_exec_nccl_id(void* id128);
 int dpl_exec_nccl_init(dpl_exec* ex, const void* id128);
 /* One synchronous DAPPLE step: phi warm-up forwards, 1F1B steady state,
@@ -166,11 +175,25 @@ int dpl_exec_nccl_init(dpl_exec* ex, const void* id128);
  * generated on device from the seed).  *loss gets the global-batch loss on
  * last-stage ranks (NaN elsewhere). */
 int dpl_exec_step(dpl_exec* ex, const void* host_input, const void* host_target, float* loss);
+/* The same step split in two: launch enqueues it (a CUDA-graph replay) and
+ * returns, finish waits for it.  Ranks sharing one process launch every
+ * rank's step before finishing any. */
+int dpl_exec_step_launch(dpl_exec* ex, const void* host_input, const void* host_target);
+/* Captures and instantiates the step graphs (both flag banks, device data)
+ * ahead of the first step; ranks sharing one process call it on every rank
+ * before any rank steps. */
+int dpl_exec_prepare(dpl_exec* ex);
+int dpl_exec_step_finish(dpl_exec* ex, float* loss);
 /* Measured timeline of the last step as JSON (same layout as the
  * simulator's Timeline, seconds), plus per-block kernel times. */
 const char* dpl_exec_timeline(dpl_exec* ex);
 /* Copies a parameter / gradient tensor (by name) to host, for parity. */
 int dpl_exec_read_tensor(dpl_exec* ex, const char* name, int grad, void* host, size_t bytes);
+/* Parity probes (executor created with "probe": true): the last
+ * micro-batch's input "x", output "y", backward intermediate "aux" (pooling
+ * convs: pre-pool output), output gradient "dy" or input gradient "dx" of a
+ * layer on this stage, bf16, for teacher-forced layer checks. */
+int dpl_exec_read_probe(dpl_exec* ex, int layer, const char* which, void* host, size_t bytes);
 int dpl_exec_info(dpl_exec* ex, char* buf, size_t cap);
 /* Cross-GPU timer calibration (collective over phases 1..world-1, a host
  * barrier between the responder's call and rank 0's): on rank 0 returns the

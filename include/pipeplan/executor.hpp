@@ -48,6 +48,9 @@ struct ExecOptions {
   /// Keep only stage inputs; each backward block re-runs the stage forward
   /// (the executed counterpart of apply_recompute, simulator.cpp:216-221).
   bool recompute = false;
+  /// Replica-group gradient AllReduce: "peer" (one reduce kernel over the
+  /// replicas' peer-mapped gradients, collective.cu) or "nccl".
+  std::string allreduce = "peer";
   /// Plumbing for world > 1: all-gather of one byte string per rank
   /// (CUDA-IPC handles, NCCL ids, timelines), e.g. over torch.distributed
   /// or MPI.  Must be collective and return the strings in rank order.

@@ -61,6 +61,7 @@ _PROTOS = {
     "dpl_k_embed_fwd": (_I, [_VP, _VP, _VP, _VP, _I, _I, _I, _VP]),
     "dpl_k_embed_bwd": (_I, [_VP, _VP, _VP, _VP, _I, _I, _I, _VP]),
     "dpl_k_cross_entropy": (_I, [_VP, _VP, _VP, _I, _I, _F, _VP]),
+    "dpl_k_cross_entropy_padded": (_I, [_VP, _VP, _VP, _I, _I, _I, _F, _VP]),
     "dpl_k_im2col3x3": (_I, [_VP, _VP, _I, _I, _I, _I, _I, _VP]),
     "dpl_k_col2im3x3": (_I, [_VP, _VP, _I, _I, _I, _I, _I, _VP]),
     "dpl_k_maxpool2_fwd": (_I, [_VP, _VP, _I, _I, _I, _I, _VP]),
@@ -75,9 +76,13 @@ _PROTOS = {
     "dpl_exec_nccl_id": (_I, [_VP]),
     "dpl_exec_nccl_init": (_I, [_VP, _VP]),
     "dpl_exec_step": (_I, [_VP, _VP, _VP, ctypes.POINTER(_F)]),
+    "dpl_exec_step_launch": (_I, [_VP, _VP, _VP]),
+    "dpl_exec_step_finish": (_I, [_VP, ctypes.POINTER(_F)]),
+    "dpl_exec_prepare": (_I, [_VP]),
     "dpl_exec_timeline": (ctypes.c_char_p, [_VP]),
     "dpl_exec_read_tensor": (_I, [_VP, ctypes.c_char_p, _I, _VP, ctypes.c_size_t]),
     "dpl_exec_info": (_I, [_VP, ctypes.c_char_p, ctypes.c_size_t]),
+    "dpl_exec_read_probe": (_I, [_VP, _I, ctypes.c_char_p, _VP, ctypes.c_size_t]),
     "dpl_exec_clock_calibrate": (_I, [_VP, _I, ctypes.POINTER(_LL)]),
     "dpl_exec_gemm_profile": (_I, [_VP, _I]),
     "dpl_exec_gemm_profile_json": (ctypes.c_char_p, [_VP]),

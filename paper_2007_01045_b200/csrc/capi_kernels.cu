@@ -195,6 +195,13 @@ int dpl_k_embed_bwd(const int* tok, const void* dx, float* gwte, float* gwpe, in
   return guarded([&] { dpl::embed_bwd(tok, dx, gwte, gwpe, rows, seq, h, static_cast<cudaStream_t>(stream)); });
 }
 
+int dpl_k_cross_entropy_padded(void* logits, const int* tgt, float* loss_acc, int rows, int vocab, int ld,
+                               float grad_scale, void* stream) {
+  return guarded([&] {
+    dpl::cross_entropy_fwd_bwd(logits, tgt, loss_acc, rows, vocab, grad_scale, static_cast<cudaStream_t>(stream), ld);
+  });
+}
+
 int dpl_k_cross_entropy(void* logits, const int* tgt, float* loss_acc, int rows, int vocab, float grad_scale,
                         void* stream) {
   return guarded(

@@ -19,6 +19,10 @@
 #include "pipeplan/simulator.hpp"
 
 using dpl::json::Value;
+
+namespace pipeplan {
+int& planner_threads_override();  // planner.cpp (not part of the reference API)
+}
 using namespace pipeplan;
 
 namespace dpl {
@@ -127,6 +131,10 @@ Value dispatch(const Value& req) {
     opts.optimizer_multiplier = dbl_of(req, "optimizer_multiplier", 8.0);
     SearchReport rep;
     const bool want = bool_of(req, "report");
+    struct ThreadsScope {  // optional "threads": worker count of this search only (1 = sequential)
+      explicit ThreadsScope(int n) { planner_threads_override() = n; }
+      ~ThreadsScope() { planner_threads_override() = 0; }
+    } threads_scope(int_of(req, "threads", 0));
     const PipelinePlan p = plan(prof, cl, int_of(req, "M", 1), opts, want ? &rep : nullptr);
     out["plan"] = plan_json(p, prof, cl);
     if (want) {

@@ -82,6 +82,8 @@ struct alignas(64) GemmParams {
   int epi_out_bytes;   // one output chunk buffer (2 KB bf16 / 4 KB fp32)
   int epi_nx;          // extra-tensor chunk buffers per warp
   int epi_tile_cols;   // columns of one CTA tile (bias slice staged per warp)
+  int epi_groups;      // 64-column-group TMA epilogue (epi_tile_tma_g); 0: 32-column chunks
+  int epi_plain;       // output / extra maps address one [M][ldc] matrix per z (no column / batch split)
   float* colsum;       // kColSum target (TMA epilogue; otherwise a colsum pass after the GEMM)
   int conv_operand, conv_h, conv_w, conv_c;  // implicit-GEMM convolution operand (GemmDesc)
   int M, N, K, batch;

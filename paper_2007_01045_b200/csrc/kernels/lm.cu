@@ -114,24 +114,32 @@ __device__ __forceinline__ void ms_merge(float& m, float& s, float m2, float s2)
   m = mn;
 }
 
+// Row stride `ld` (a multiple of 8) may exceed the vocabulary: columns
+// [vocab, ld) are padding (e.g. GPT-2's 50257 stored as 50264) -- excluded
+// from the softmax and given a zero gradient.
 __global__ void __launch_bounds__(kCeThreads) ce_kernel(__nv_bfloat16* __restrict__ logits,
                                                         const int* __restrict__ tgt, float* __restrict__ loss_acc,
-                                                        int vocab, float grad_scale) {
+                                                        int vocab, int ld, float grad_scale) {
   ptx::pdl_wait();
   const int r = blockIdx.x;
-  __nv_bfloat16* row = logits + static_cast<size_t>(r) * vocab;
+  __nv_bfloat16* row = logits + static_cast<size_t>(r) * ld;
   const uint4* rv = reinterpret_cast<const uint4*>(row);
-  const int nvec = vocab / 8;
+  const int nvec = ld / 8;
   float m = -FLT_MAX, s = 0.f;
   for (int v = threadIdx.x; v < nvec; v += kCeThreads) {
     float f[8];
     unpack8(rv[v], f);
+    if (v * 8 + 8 > vocab) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (v * 8 + e >= vocab) f[e] = -FLT_MAX;
+    }
     float lm = f[0];
 #pragma unroll
     for (int e = 1; e < 8; ++e) lm = fmaxf(lm, f[e]);
     float ls = 0.f;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) ls += __expf(f[e] - lm);
+    for (int e = 0; e < 8; ++e) ls += f[e] == -FLT_MAX ? 0.f : __expf(f[e] - lm);
     ms_merge(m, s, lm, ls);
   }
 #pragma unroll
@@ -172,7 +180,7 @@ __global__ void __launch_bounds__(kCeThreads) ce_kernel(__nv_bfloat16* __restric
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const float p = __expf(f[e] - mm) * inv;
-      f[e] = (p - (v * 8 + e == t ? 1.f : 0.f)) * grad_scale;
+      f[e] = v * 8 + e < vocab ? (p - (v * 8 + e == t ? 1.f : 0.f)) * grad_scale : 0.f;
     }
     wv[v] = pack8(f);
   }
@@ -205,12 +213,14 @@ void embed_bwd(const int* tok, const void* dx, float* gwte, float* gwpe, int row
 }
 
 void cross_entropy_fwd_bwd(void* logits, const int* tgt, float* loss_acc, int rows, int vocab, float grad_scale,
-                           cudaStream_t s) {
-  if (vocab % 8) throw std::invalid_argument("cross_entropy: vocab must be a multiple of 8");
+                           cudaStream_t s, int ld) {
+  if (ld == 0) ld = vocab;
+  if (ld % 8 || vocab < 1 || vocab > ld)
+    throw std::invalid_argument("cross_entropy: row stride must be a multiple of 8 and >= vocab");
   count_launch();
   TimedLaunch timed_("cross_entropy", s);
   launch_pdl(ce_kernel, dim3(rows), dim3(kCeThreads), 0, s, static_cast<__nv_bfloat16*>(logits), tgt, loss_acc, vocab,
-             grad_scale);
+             ld, grad_scale);
 }
 
 }  // namespace dpl

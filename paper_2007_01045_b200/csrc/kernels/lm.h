@@ -16,9 +16,10 @@ void fill_tokens(int* dst, long long n, uint64_t seed, uint64_t tensor, long lon
 void embed_fwd(const int* tok, const void* wte, const void* wpe, void* x, int rows, int seq, int h, cudaStream_t s);
 // gwte[tok[r]] += dx[r] ; gwpe[r % seq] += dx[r]   (fp32 vector atomics)
 void embed_bwd(const int* tok, const void* dx, float* gwte, float* gwpe, int rows, int seq, int h, cudaStream_t s);
-// Per row r of logits [rows][vocab] (bf16): loss_acc += logsumexp(row) - row[tgt[r]]
-// and, in place, row <- bf16((softmax(row) - onehot(tgt[r])) * grad_scale).
+// Per row r of logits [rows][ld] (bf16; ld = vocab rounded up to 8, 0 = vocab):
+// loss_acc += logsumexp(row[:vocab]) - row[tgt[r]] and, in place,
+// row <- bf16((softmax(row[:vocab]) - onehot(tgt[r])) * grad_scale), padding 0.
 void cross_entropy_fwd_bwd(void* logits, const int* tgt, float* loss_acc, int rows, int vocab, float grad_scale,
-                           cudaStream_t s);
+                           cudaStream_t s, int ld = 0);
 
 }  // namespace dpl

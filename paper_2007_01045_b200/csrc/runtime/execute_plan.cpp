@@ -56,11 +56,12 @@ PlanExecution execute_plan(const PipelinePlan& plan, const ModelProfile& profile
   cfg["apply"] = opts.apply;
   cfg["schedule"] = opts.schedule == ScheduleKind::gpipe ? "gpipe" : "dapple";
   cfg["recompute"] = opts.recompute;
+  cfg["allreduce"] = opts.allreduce;
   dpl_exec* ex = nullptr;
   ok(dpl_exec_create(cfg.dump().c_str(), opts.device, &ex));
   try {
     if (opts.world > 1) {
-      char blob[64];
+      char blob[256];
       size_t len = 0;
       ok(dpl_exec_export(ex, blob, sizeof blob, &len));
       std::string all;
@@ -72,13 +73,14 @@ PlanExecution execute_plan(const PipelinePlan& plan, const ModelProfile& profile
         if (std::find(s.devices.begin(), s.devices.end(), opts.rank) != s.devices.end()) mine = &s;
       if (!mine) throw std::invalid_argument("execute_plan: rank not in plan");
       std::string id;
-      if (mine->replication() > 1 && mine->devices.front() == opts.rank) {
+      const bool nccl = mine->replication() > 1 && opts.allreduce == "nccl";
+      if (nccl && mine->devices.front() == opts.rank) {
         char buf[128];
         ok(dpl_exec_nccl_id(buf));
         id.assign(buf, sizeof buf);
       }
       const std::vector<std::string> ids = gather(opts, id);
-      if (mine->replication() > 1) ok(dpl_exec_nccl_init(ex, ids[mine->devices.front()].data()));
+      if (nccl) ok(dpl_exec_nccl_init(ex, ids[mine->devices.front()].data()));
     }
     float loss = std::nanf("");
     ok(dpl_exec_step(ex, nullptr, nullptr, &loss));

@@ -10,7 +10,7 @@
 //   compute   the stage's F/B chain (all tcgen05 GEMMs + stage kernels)
 //   send_act  Split-Concat forward hand-off  (peer copies over NVLink)
 //   send_grad Split-Concat backward hand-off
-//   reduce    per-layer NCCL AllReduce of the replica group + SGD apply
+//   reduce    per-layer replica AllReduce (peer memory, or NCCL) + SGD apply
 //
 // Cross-GPU dependencies never involve the host: a sender pushes its rows
 // straight into the receiver's buffer (cudaMemcpyAsync to a CUDA-IPC
@@ -33,12 +33,14 @@
 #include <cstring>
 #include <memory>
 #include <sstream>
+#include <unistd.h>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "dapple.h"
 #include "host/json.hpp"
+#include "kernels/collective.h"
 #include "kernels/elementwise.h"
 #include "kernels/lm.h"
 #include "layers.h"
@@ -137,8 +139,23 @@ __global__ void stamp_kernel(unsigned long long* out) {
 
 using Route = pipeplan::SplitConcatRoute;
 
-// after the flag banks: {ping u32, pong u32, peer_time u64} for clock calibration
+// after the flag banks: {ping u32, pong u32, peer_time u64} for clock calibration,
+// then the step's loss accumulator (a peer-reduced block on replicated last stages)
 constexpr size_t kCalibBytes = 256;
+
+// What a rank publishes so its peers can reach its receive region and (for
+// replica peers) its fp32 gradients: CUDA-IPC handles for other processes,
+// plain pointers for ranks living in the same process (one per GPU, or
+// several ranks sharing one GPU in tests).
+struct PeerBlob {
+  cudaIpcMemHandle_t recv;
+  cudaIpcMemHandle_t grads;
+  long long pid;
+  int device;
+  int pad;
+  unsigned long long recv_ptr;
+  unsigned long long grads_ptr;
+};
 
 // stream memory operations (cuStreamWaitValue32) usable, process-wide
 bool& memops_flag() {
@@ -162,9 +179,13 @@ class Executor {
   void connect(const uint8_t* blobs, size_t blob_len, int world);
   void nccl_init(const void* id);
   void disconnect();
+  bool shares_gpu() const;
   // ns to add to this rank's %globaltimer to express it on rank 0's timer
   long long calibrate_clock(int phase);
   float step(const void* host_input, const void* host_target);
+  void step_launch(const void* host_input, const void* host_target);
+  float step_finish();
+  void prepare_graphs();
   void set_gemm_profile(bool on) {
     ctx_.gemms.profile.enabled = on;
     ctx_.gemms.profile.reset();
@@ -185,6 +206,8 @@ class Executor {
   std::string layer_profile_json(int reps);
   std::string timeline_json() const;
   void read_tensor(const std::string& name, bool grad, void* host, size_t bytes);
+  // one probe tensor (bf16) of a layer of this stage: x | y | aux | dy | dx
+  void read_probe(int layer, const std::string& which, void* host, size_t bytes);
   std::string info() const;
   long long graph_count() const;
 
@@ -206,6 +229,18 @@ class Executor {
   bool gpipe_ = false;      // all-forward-first chain (simulator.cpp:161-167)
   bool recompute_ = false;  // re-run the stage forward inside each backward (simulator.cpp:216-221)
   int stash_slots_ = 1;     // layer-internal activation sets kept alive
+  // parity probes (config "probe"): every layer's input, output, backward
+  // intermediate, output gradient and input gradient of the LAST micro-batch,
+  // copied aside so tests can teacher-force the oracle layer by layer
+  bool probe_ = false;
+  struct Probe {
+    bf16 *x = nullptr, *y = nullptr, *aux = nullptr, *dy = nullptr, *dx = nullptr;
+    size_t nx = 0, ny = 0, naux = 0;
+  };
+  std::vector<Probe> probes_;
+  void probe_copy(bf16* dst, const bf16* src, size_t n) {
+    if (dst && src && n) DPL_CUDA(cudaMemcpyAsync(dst, src, n * 2, cudaMemcpyDeviceToDevice, compute_));
+  }
 
   // --- device state
   DeviceMemory mem_;
@@ -237,7 +272,13 @@ class Executor {
   //   [recv_act M x R x H][recv_grad M x R x H][flags: bank[2] x {act[world], grad[world]}]
   uint8_t* recv_ = nullptr;
   size_t recv_bytes_ = 0, recv_grad_off_ = 0, flags_off_ = 0;
-  std::vector<uint8_t*> peer_recv_;  // by rank (IPC-mapped), null if unused
+  std::vector<uint8_t*> peer_recv_;  // by rank (IPC-mapped or same-process), null if unused
+  std::vector<float*> peer_g32_;     // by rank: replica peers' fp32 gradients (peer AllReduce)
+  std::vector<void*> ipc_opened_;    // mappings to close on disconnect
+  std::vector<char> colocated_;      // by rank: same process and same GPU as this rank
+  std::vector<int> group_;           // global ranks of this stage's replicas, replica order
+  bool peer_ar_ = true;              // replica AllReduce over peer memory (false: NCCL)
+  int nblk_ = 1;                     // parameter blocks per stage in the flag layout (layers + emb + head + loss)
   long long clock_offset_ns_ = 0;
   std::vector<int> peer_samples_;    // samples per micro-batch slice of each rank
   std::vector<int> peer_stage_;      // stage of each rank
@@ -247,8 +288,11 @@ class Executor {
   cudaEvent_t ev_begin_ = nullptr, ev_end_ = nullptr, ev_reduce_done_ = nullptr;
   cudaEvent_t ev_sa_done_ = nullptr, ev_sg_done_ = nullptr, ev_fork_ = nullptr, ev_last_bwd_ = nullptr;
   std::vector<BlockEvents> fwd_ev_, bwd_ev_, send_fwd_ev_, send_bwd_ev_;
+  std::vector<BlockEvents> ar_ev_;        // per parameter block: the replica AllReduce on the reduce stream
+  std::vector<long long> ar_bytes_;       // fp32 bytes reduced per block (0: not reduced this step)
   std::vector<cudaEvent_t> layer_done_, fwd_done_, bwd_done_;
   long long steps_done_ = 0;
+  bool launched_ = false;
   int bank_ = 0;
   float last_loss_ = NAN;
   float* loss_host_ = nullptr;  // pinned
@@ -301,7 +345,9 @@ class Executor {
   void enqueue_step(const void* host_input, const void* host_target);
   // this rank's gradients of one parameter block are final: AllReduce over
   // the replica group and apply on the reduce stream
-  void reduce_apply(cudaEvent_t ready, size_t off, size_t n);
+  void reduce_apply(cudaEvent_t ready, size_t off, size_t n, int blk);
+  // peer-memory AllReduce of one block over the replica group on the reduce stream
+  void peer_allreduce(float* mine, const std::vector<float*>& peers, size_t n, int blk);
   double flops_per_step_ = 0.0;
 
   // --- helpers
@@ -318,8 +364,17 @@ class Executor {
   bf16* recv_grad(int i) const {
     return reinterpret_cast<bf16*>(recv_ + recv_grad_off_) + static_cast<size_t>(i) * out_elems();
   }
-  // flag bank of the current step (parity)
-  uint32_t* flags() const { return reinterpret_cast<uint32_t*>(recv_ + flags_off_) + bank_ * 2 * world_; }
+  // flag bank of the current step (parity): [act world][grad world][ar_ready nblk x world][ar_done nblk x world]
+  size_t bank_words() const { return 2 * static_cast<size_t>(world_) * (1 + nblk_); }
+  uint32_t* flags() const { return reinterpret_cast<uint32_t*>(recv_ + flags_off_) + bank_ * bank_words(); }
+  // flag word of (bank, region, index) in any rank's receive region
+  uint32_t* flag_at(uint8_t* region, int rank, size_t word) const {
+    return reinterpret_cast<uint32_t*>(region + layout_flags_off(rank)) + bank_ * bank_words() + word;
+  }
+  size_t ar_word(int done, int blk, int src) const {
+    return 2 * static_cast<size_t>(world_) + (static_cast<size_t>(done) * nblk_ + blk) * world_ + src;
+  }
+  size_t loss_off(int rank) const { return layout_flags_off(rank) + 2 * bank_words() * 4 + kCalibBytes; }
   // receive-region layout of any rank (from the plan): [recv_act M x s x E_in][recv_grad M x s x E_out][flags]
   size_t layout_grad_off(int rank) const;
   size_t layout_flags_off(int rank) const;
@@ -356,8 +411,7 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
     spec_.seq = 1;
     spec_.hidden = spec_.classes;
   }
-  if (spec_.vocab > 0 && (spec_.kind != "gpt" || spec_.vocab % 8 != 0))
-    throw std::invalid_argument("dpl exec: vocab needs kind gpt and a multiple of 8");
+  if (spec_.vocab > 0 && spec_.kind != "gpt") throw std::invalid_argument("dpl exec: vocab needs kind gpt");
 
   plan_ = pipeplan::plan_from_json(cfg.at("plan").is_string() ? cfg.at("plan").as_string() : cfg.at("plan").dump());
   M_ = static_cast<int>(cfg.at("M").as_int());
@@ -371,6 +425,12 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
   if (cfg.contains("graph")) use_graph_ = cfg.at("graph").as_bool();
   if (cfg.contains("schedule")) gpipe_ = cfg.at("schedule").as_string() == "gpipe";
   if (cfg.contains("recompute")) recompute_ = cfg.at("recompute").as_bool();
+  if (cfg.contains("probe")) probe_ = cfg.at("probe").as_bool();
+  if (cfg.contains("allreduce")) {
+    const std::string ar = cfg.at("allreduce").as_string();
+    if (ar != "peer" && ar != "nccl") throw std::invalid_argument("dpl exec: allreduce must be peer or nccl");
+    peer_ar_ = ar == "peer";
+  }
   if (M_ < 1 || gbs_ % M_ != 0) throw std::invalid_argument("dpl exec: GBS must be a multiple of M");
   B_ = gbs_ / M_;
 
@@ -416,6 +476,10 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
   r_ = mine.replication();
   lo_ = mine.layer_lo;
   hi_ = mine.layer_hi;
+  group_ = mine.devices;  // sorted (plan_from_json): replica j is devices[j]
+  if (r_ > kMaxReplicas) throw std::invalid_argument("dpl exec: at most 16 replicas per stage");
+  // parameter blocks of the widest stage (layers + embedding + LM head + loss): every rank can lay out any rank's flags
+  for (int k = 0; k < S_; ++k) nblk_ = std::max(nblk_, plan_.stages[k].layer_hi - plan_.stages[k].layer_lo + 3);
 
   // phi resolution, planner.cpp:501-508 (preset A is cost-independent)
   const int Se = 2 * S_ - 1;
@@ -549,10 +613,23 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
     tgt_tok_.push_back(static_cast<int*>(mem_.alloc(smp * 4)));
   if (k_ > 0)
     for (int i = 0; i < M_; ++i) send_grad_.push_back(static_cast<bf16*>(mem_.alloc(in_elems() * 2)));
+  if (probe_) {
+    probes_.resize(L());
+    for (int li = 0; li < L(); ++li) {
+      Probe& p = probes_[li];
+      p.nx = smp * elems(lo_ + li);
+      p.ny = smp * elems(lo_ + li + 1);
+      p.naux = layers_[li]->probe_aux_elems(ctx_);
+      p.x = static_cast<bf16*>(mem_.alloc(p.nx * 2));
+      p.dx = static_cast<bf16*>(mem_.alloc(p.nx * 2));
+      p.y = static_cast<bf16*>(mem_.alloc(p.ny * 2));
+      p.dy = static_cast<bf16*>(mem_.alloc(p.ny * 2));
+      if (p.naux) p.aux = static_cast<bf16*>(mem_.alloc(p.naux * 2));
+    }
+  }
   if (emb_) gmax = std::max(gmax, in_elems());
   gbuf_[0] = static_cast<bf16*>(mem_.alloc(gmax * 2));
   gbuf_[1] = static_cast<bf16*>(mem_.alloc(gmax * 2));
-  loss_acc_ = static_cast<float*>(mem_.alloc(4));
   t0_ = static_cast<unsigned long long*>(mem_.alloc(8));
 
   // receive region: one allocation so a single IPC handle covers it
@@ -566,9 +643,12 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
     }
   recv_grad_off_ = layout_grad_off(rank_);
   flags_off_ = layout_flags_off(rank_);
-  recv_bytes_ = flags_off_ + 4 * static_cast<size_t>(world_) * 4 + kCalibBytes;
+  recv_bytes_ = loss_off(rank_) + 256;
   recv_ = static_cast<uint8_t*>(mem_.alloc(recv_bytes_));
+  loss_acc_ = reinterpret_cast<float*>(recv_ + loss_off(rank_));
   peer_recv_.assign(world_, nullptr);
+  peer_g32_.assign(world_, nullptr);
+  colocated_.assign(world_, 0);
 
   // events
   auto mk = [](cudaEvent_t* e) { DPL_CUDA(cudaEventCreate(e)); };
@@ -591,6 +671,12 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
     }
   layer_done_.resize(L());
   for (auto& e : layer_done_) mk_nt(&e);
+  ar_ev_.resize(nblk_);
+  ar_bytes_.assign(nblk_, 0);
+  for (BlockEvents& b : ar_ev_) {
+    mk(&b.start);
+    mk(&b.end);
+  }
   mk_nt(&emb_done_);
   mk_nt(&head_done_);
   fwd_done_.resize(M_);
@@ -634,10 +720,10 @@ void Executor::disconnect() {
     ncclCommDestroy(comm_);
     comm_ = nullptr;
   }
-  for (uint8_t*& p : peer_recv_) {
-    if (p) cudaIpcCloseMemHandle(p);
-    p = nullptr;
-  }
+  for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
+  ipc_opened_.clear();
+  for (uint8_t*& p : peer_recv_) p = nullptr;
+  for (float*& p : peer_g32_) p = nullptr;
 }
 
 Executor::~Executor() {
@@ -648,7 +734,7 @@ Executor::~Executor() {
   for (cudaEvent_t e : {ev_begin_, ev_end_, ev_reduce_done_, ev_sa_done_, ev_sg_done_, ev_fork_, ev_last_bwd_,
                         emb_done_, head_done_})
     if (e) cudaEventDestroy(e);
-  for (auto* v : {&fwd_ev_, &bwd_ev_, &send_fwd_ev_, &send_bwd_ev_})
+  for (auto* v : {&fwd_ev_, &bwd_ev_, &send_fwd_ev_, &send_bwd_ev_, &ar_ev_})
     for (BlockEvents& b : *v) {
       if (b.start) cudaEventDestroy(b.start);
       if (b.end) cudaEventDestroy(b.end);
@@ -694,15 +780,27 @@ const void* Executor::stage_host(const void* p, int which) {
 }
 
 size_t Executor::export_blob(void* blob, size_t cap) {
-  cudaIpcMemHandle_t h;
-  DPL_CUDA(cudaIpcGetMemHandle(&h, recv_));
-  if (cap < sizeof h) throw std::invalid_argument("dpl exec: export buffer too small");
-  std::memcpy(blob, &h, sizeof h);
-  return sizeof h;
+  if (cap < sizeof(PeerBlob)) throw std::invalid_argument("dpl exec: export buffer too small");
+  PeerBlob b{};
+  DPL_CUDA(cudaIpcGetMemHandle(&b.recv, recv_));
+  DPL_CUDA(cudaIpcGetMemHandle(&b.grads, g32_));
+  b.pid = static_cast<long long>(getpid());
+  b.device = device_;
+  b.recv_ptr = reinterpret_cast<unsigned long long>(recv_);
+  b.grads_ptr = reinterpret_cast<unsigned long long>(g32_);
+  std::memcpy(blob, &b, sizeof b);
+  return sizeof b;
 }
 
 void Executor::connect(const uint8_t* blobs, size_t blob_len, int world) {
   if (world != world_) throw std::invalid_argument("dpl exec: world size mismatch");
+  if (blob_len < sizeof(PeerBlob)) throw std::invalid_argument("dpl exec: peer blobs too short");
+  auto blob = [&](int p) {
+    PeerBlob b;
+    std::memcpy(&b, blobs + static_cast<size_t>(p) * blob_len, sizeof b);
+    return b;
+  };
+  const long long me = static_cast<long long>(getpid());
   std::vector<int> peers;
   for (const Route& r : out_routes_) peers.push_back(r.dst_gpu);
   for (const Route& r : in_routes_) peers.push_back(r.src_gpu);
@@ -711,23 +809,59 @@ void Executor::connect(const uint8_t* blobs, size_t blob_len, int world) {
   } else {
     peers.push_back(0);
   }
+  for (int p : group_) peers.push_back(p);
+  for (int p = 0; p < world_; ++p) {
+    const PeerBlob b = blob(p);
+    colocated_[p] = b.pid == me && b.device == device_;
+  }
   for (int p : peers) {
     if (p == rank_ || peer_recv_[p]) continue;
-    cudaIpcMemHandle_t h;
-    std::memcpy(&h, blobs + static_cast<size_t>(p) * blob_len, sizeof h);
+    const PeerBlob b = blob(p);
+    if (b.pid == me) {
+      // a rank of this process: plain pointers (peer access for another GPU)
+      if (b.device != device_) {
+        const cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) DPL_CUDA(e);
+        cudaGetLastError();
+      }
+      peer_recv_[p] = reinterpret_cast<uint8_t*>(b.recv_ptr);
+      peer_g32_[p] = reinterpret_cast<float*>(b.grads_ptr);
+      continue;
+    }
     void* ptr = nullptr;
-    DPL_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    DPL_CUDA(cudaIpcOpenMemHandle(&ptr, b.recv, cudaIpcMemLazyEnablePeerAccess));
     peer_recv_[p] = static_cast<uint8_t*>(ptr);
+    ipc_opened_.push_back(ptr);
+    if (std::find(group_.begin(), group_.end(), p) != group_.end() && peer_ar_) {
+      DPL_CUDA(cudaIpcOpenMemHandle(&ptr, b.grads, cudaIpcMemLazyEnablePeerAccess));
+      peer_g32_[p] = static_cast<float*>(ptr);
+      ipc_opened_.push_back(ptr);
+    }
   }
+  peer_g32_[rank_] = g32_;
+  // the flag waits of ranks sharing one GPU must stay stream memory
+  // operations: a spinning wait kernel could starve the kernel that would
+  // release it
+  for (int p = 0; p < world_; ++p)
+    if (p != rank_ && colocated_[p] && !memops_ok())
+      throw std::runtime_error("dpl exec: ranks sharing a GPU need stream memory operations (cuStreamWaitValue32)");
+}
+
+bool Executor::shares_gpu() const {
+  for (int p = 0; p < world_; ++p)
+    if (p != rank_ && colocated_[p]) return true;
+  return false;
 }
 
 // Called collectively: phase p (1..world-1) calibrates rank p against rank 0;
 // the host side barriers between phases.  Returns this rank's offset.
 long long Executor::calibrate_clock(int phase) {
   if (world_ == 1 || (rank_ != 0 && rank_ != phase)) return clock_offset_ns_;
+  // ranks on one GPU share its timer (and must not run the spinning ping-pong)
+  if (colocated_[rank_ == 0 ? phase : 0]) return 0;
   constexpr int kRounds = 64;
   auto calib = [&](uint8_t* region, int rank) {
-    uint8_t* base = region + layout_flags_off(rank) + 4 * static_cast<size_t>(world_) * 4;
+    uint8_t* base = region + layout_flags_off(rank) + 2 * bank_words() * 4;
     return base;
   };
   DPL_CUDA(cudaSetDevice(device_));
@@ -763,7 +897,9 @@ long long Executor::calibrate_clock(int phase) {
 }
 
 void Executor::nccl_init(const void* id) {
-  if (r_ == 1) return;
+  if (r_ == 1 || peer_ar_) return;
+  for (int p : group_)
+    if (p != rank_ && colocated_[p]) throw std::runtime_error("dpl exec: NCCL cannot reduce over ranks sharing a GPU");
   ncclUniqueId uid;
   std::memcpy(&uid, id, sizeof uid);
   DPL_NCCL(ncclCommInitRank(&comm_, r_, uid, rep_));
@@ -775,6 +911,10 @@ void Executor::wait_flag(cudaStream_t s, uint32_t* flag, uint32_t value) {
       const CUresult rc = fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flag), value, 0x0 /*GEQ*/);
       if (rc == CUDA_SUCCESS) return;
     }
+    // a spinning wait kernel could starve the kernel of a rank sharing this
+    // GPU that would release it: those ranks need stream memory operations
+    if (shares_gpu())
+      throw std::runtime_error("dpl exec: ranks sharing a GPU need stream memory operations (cuStreamWaitValue32)");
     memops_flag() = false;  // not available / not capturable: one-thread acquire spin on this stream
   }
   count_launch();
@@ -798,9 +938,16 @@ void Executor::forward(int i, uint32_t base) {
   }
   record(fwd_ev_[i].start, compute_);
   if (emb_) emb_->forward(ctx_, tok_[slot], in_[slot]);
+  const bool probe = probe_ && i == M_ - 1;
   for (int li = 0; li < L(); ++li) {
     bf16* y = li + 1 < L() ? act_[li + 1][ss] : out_[i];
     layers_[li]->forward(ctx_, ss, x, y);
+    if (probe) {
+      Probe& p = probes_[li];
+      probe_copy(p.x, x, p.nx);
+      probe_copy(p.y, y, p.ny);
+      probe_copy(p.aux, layers_[li]->probe_aux(ss), p.naux);
+    }
     x = y;
   }
   if (head_) {
@@ -827,7 +974,7 @@ void Executor::forward(int i, uint32_t base) {
       uint8_t* peer = peer_recv_[r.dst_gpu];
       bf16* dst = reinterpret_cast<bf16*>(peer) + static_cast<size_t>(i) * peer_samples_[r.dst_gpu] * eb + r.dst_row;
       DPL_CUDA(cudaMemcpyAsync(dst, out_[i] + r.src_row, r.rows * 2, cudaMemcpyDeviceToDevice, send_act_));
-      uint32_t* flag = reinterpret_cast<uint32_t*>(peer + layout_flags_off(r.dst_gpu)) + bank_ * 2 * world_ + rank_;
+      uint32_t* flag = flag_at(peer, r.dst_gpu, rank_);
       signal(send_act_, flag, base + i + 1);
     }
     record(send_fwd_ev_[i].end, send_act_);
@@ -848,7 +995,7 @@ void Executor::backward(int i, uint32_t base) {
   const bool last_mb = i == M_ - 1;
   if (head_) {
     head_->backward(ctx_, slot, out_[i], dloss_[slot]);
-    if (last_mb) reduce_apply(head_done_, head_off_, head_->param_count());
+    if (last_mb) reduce_apply(head_done_, head_off_, head_->param_count(), L() + 1);
   }
   if (recompute_) {
     // the backward block first re-runs the stage forward (B' = B + F)
@@ -872,15 +1019,17 @@ void Executor::backward(int i, uint32_t base) {
       dx = gbuf_[pp];
     }
     ctx_.cur_y = li + 1 < L() ? act_[li + 1][ss] : (recompute_ ? rc_out_ : out_[i]);
+    if (probe_ && last_mb) probe_copy(probes_[li].dy, dy, probes_[li].ny);
     layers_[li]->backward(ctx_, ss, x, dy, dx);
+    if (probe_ && last_mb) probe_copy(probes_[li].dx, dx, probes_[li].nx);
     dy = dx;
     // this layer's gradients are final: AllReduce + apply while the
     // remaining layers' backward runs
-    if (last_mb) reduce_apply(layer_done_[li], param_off_[li], layers_[li]->param_count());
+    if (last_mb) reduce_apply(layer_done_[li], param_off_[li], layers_[li]->param_count(), li);
   }
   if (emb_) {
     emb_->backward(ctx_, tok_[slot], dy);
-    if (last_mb) reduce_apply(emb_done_, emb_off_, emb_->param_count());
+    if (last_mb) reduce_apply(emb_done_, emb_off_, emb_->param_count(), L());
   }
   record(bwd_ev_[i].end, compute_);
   if (k_ > 0) {
@@ -893,19 +1042,54 @@ void Executor::backward(int i, uint32_t base) {
       bf16* dst = reinterpret_cast<bf16*>(peer + layout_grad_off(r.src_gpu)) +
                   static_cast<size_t>(i) * peer_samples_[r.src_gpu] * eb + r.src_row;
       DPL_CUDA(cudaMemcpyAsync(dst, send_grad_[i] + r.dst_row, r.rows * 2, cudaMemcpyDeviceToDevice, send_grad_s_));
-      uint32_t* flag =
-          reinterpret_cast<uint32_t*>(peer + layout_flags_off(r.src_gpu)) + bank_ * 2 * world_ + world_ + rank_;
+      uint32_t* flag = flag_at(peer, r.src_gpu, world_ + rank_);
       signal(send_grad_s_, flag, base + i + 1);
     }
     record(send_bwd_ev_[i].end, send_grad_s_);
   }
 }
 
-void Executor::reduce_apply(cudaEvent_t ready, size_t off, size_t n) {
+void Executor::reduce_apply(cudaEvent_t ready, size_t off, size_t n, int blk) {
   DPL_CUDA(cudaEventRecord(ready, compute_));
   DPL_CUDA(cudaStreamWaitEvent(reduce_, ready, 0));
-  if (comm_) DPL_NCCL(ncclAllReduce(g32_ + off, g32_ + off, n, ncclFloat, ncclSum, comm_, reduce_));
+  if (r_ > 1) {
+    record(ar_ev_[blk].start, reduce_);
+    ar_bytes_[blk] = static_cast<long long>(n) * 4;
+  }
+  if (r_ > 1 && peer_ar_) {
+    std::vector<float*> peers(r_);
+    for (int j = 0; j < r_; ++j) peers[j] = peer_g32_[group_[j]] + off;
+    peer_allreduce(g32_ + off, peers, n, blk);
+  } else if (r_ > 1) {
+    if (!comm_) throw std::runtime_error("dpl exec: replicated stage without an NCCL communicator");
+    DPL_NCCL(ncclAllReduce(g32_ + off, g32_ + off, n, ncclFloat, ncclSum, comm_, reduce_));
+  }
+  if (r_ > 1) record(ar_ev_[blk].end, reduce_);
   if (apply_) sgd_apply(w32_ + off, g32_ + off, w16_ + off, static_cast<long long>(n), lr_, reduce_);
+}
+
+// Two flag rounds around one kernel (collective.cu): every replica announces
+// that its block is final, replica j reduces chunk j across the group and
+// stores the sum into every replica, and each replica waits until all
+// chunks have landed before anything (SGD) reads the block.
+void Executor::peer_allreduce(float* mine, const std::vector<float*>& peers, size_t n, int blk) {
+  (void)mine;
+  if (static_cast<int>(peers.size()) != r_) throw std::logic_error("dpl exec: replica pointers");
+  ReplicaPtrs rp{};
+  for (int j = 0; j < r_; ++j) {
+    if (!peers[j]) throw std::runtime_error("dpl exec: replica peer gradients not mapped (connect first)");
+    rp.g[j] = peers[j];
+  }
+  for (int round = 0; round < 2; ++round) {
+    if (round == 1) replica_allreduce_chunk(rp, r_, static_cast<long long>(n), rep_, reduce_);
+    FlagPtrs fp{};
+    int nf = 0;
+    for (int p : group_)
+      if (p != rank_) fp.f[nf++] = flag_at(peer_recv_[p], p, ar_word(round, blk, rank_));
+    signal_peers(fp, nf, 1u, reduce_);
+    for (int p : group_)
+      if (p != rank_) wait_flag(reduce_, flags() + ar_word(round, blk, p), 1u);
+  }
 }
 
 void Executor::enqueue_step(const void* host_input, const void* host_target) {
@@ -975,12 +1159,21 @@ void Executor::enqueue_step(const void* host_input, const void* host_target) {
       backward(i, base);
     }
   }
-  if (k_ == S_ - 1 && comm_) {
+  if (k_ == S_ - 1 && r_ > 1) {
     // sync (non-timing) event: timing events are external nodes in a
     // captured step and cannot carry dependencies
     DPL_CUDA(cudaEventRecord(ev_last_bwd_, compute_));
     DPL_CUDA(cudaStreamWaitEvent(reduce_, ev_last_bwd_, 0));
-    DPL_NCCL(ncclAllReduce(loss_acc_, loss_acc_, 1, ncclFloat, ncclSum, comm_, reduce_));
+    if (peer_ar_) {
+      std::vector<float*> peers(r_);
+      for (int j = 0; j < r_; ++j)
+        peers[j] = group_[j] == rank_ ? loss_acc_
+                                      : reinterpret_cast<float*>(peer_recv_[group_[j]] + loss_off(group_[j]));
+      peer_allreduce(loss_acc_, peers, 1, L() + 2);
+    } else {
+      if (!comm_) throw std::runtime_error("dpl exec: replicated stage without an NCCL communicator");
+      DPL_NCCL(ncclAllReduce(loss_acc_, loss_acc_, 1, ncclFloat, ncclSum, comm_, reduce_));
+    }
   }
   DPL_CUDA(cudaEventRecord(ev_reduce_done_, reduce_));
   DPL_CUDA(cudaEventRecord(ev_sa_done_, send_act_));
@@ -991,7 +1184,7 @@ void Executor::enqueue_step(const void* host_input, const void* host_target) {
   record(ev_end_, compute_);
   if (k_ == S_ - 1) DPL_CUDA(cudaMemcpyAsync(loss_host_, loss_acc_, 4, cudaMemcpyDeviceToHost, compute_));
   // clear this step's flag bank (signalled again two steps from now)
-  DPL_CUDA(cudaMemsetAsync(flags(), 0, 2 * static_cast<size_t>(world_) * 4, compute_));
+  DPL_CUDA(cudaMemsetAsync(flags(), 0, bank_words() * 4, compute_));
 }
 
 // Captures enqueue_step into g.  A stream memory op that cannot be captured
@@ -1064,7 +1257,15 @@ void Executor::capture_step(GraphEntry& g, const void* host_input, const void* h
 }
 
 float Executor::step(const void* host_input, const void* host_target) {
+  step_launch(host_input, host_target);
+  return step_finish();
+}
+
+// Enqueues one step (a graph replay) without waiting for it: ranks sharing
+// this process launch every rank's step before finishing any of them.
+void Executor::step_launch(const void* host_input, const void* host_target) {
   DPL_CUDA(cudaSetDevice(device_));
+  if (launched_) throw std::logic_error("dpl exec: step_launch twice without step_finish");
   host_input = stage_host(host_input, 0);
   host_target = stage_host(host_target, 1);
   const bool profiling = ctx_.gemms.profile.enabled || kernel_timer().enabled;
@@ -1095,6 +1296,13 @@ float Executor::step(const void* host_input, const void* host_target) {
     DPL_CUDA(cudaGraphLaunch(g->exec, compute_));
     count_launch(g->kernels);
   }
+  launched_ = true;
+}
+
+float Executor::step_finish() {
+  if (!launched_) throw std::logic_error("dpl exec: step_finish without step_launch");
+  launched_ = false;
+  DPL_CUDA(cudaSetDevice(device_));
   DPL_CUDA(cudaStreamSynchronize(compute_));
   DPL_CUDA(cudaGetLastError());
   ++steps_done_;
@@ -1106,6 +1314,35 @@ float Executor::step(const void* host_input, const void* host_target) {
 }
 
 long long Executor::graph_count() const { return static_cast<long long>(graphs_.size()); }
+
+// Captures and instantiates the device-data step graphs of both flag banks
+// now, so later steps only launch.  Ranks sharing one process must do this
+// before any of them runs a step: a capture / instantiation while another
+// rank's step is blocked on this rank can synchronise the context.
+void Executor::prepare_graphs() {
+  if (!use_graph_) return;
+  DPL_CUDA(cudaSetDevice(device_));
+  const bool profiling = ctx_.gemms.profile.enabled || kernel_timer().enabled;
+  const int saved = bank_;
+  for (int b = 0; b < 2; ++b) {
+    const GraphKey key{b, false, false, profiling};
+    bool have = false;
+    for (const GraphEntry& e : graphs_) have = have || e.key == key;
+    if (have) continue;
+    bank_ = b;
+    GraphEntry fresh;
+    fresh.key = key;
+    try {
+      capture_step(fresh, nullptr, nullptr);
+    } catch (...) {
+      bank_ = saved;
+      throw;
+    }
+    graphs_.push_back(std::move(fresh));
+  }
+  bank_ = saved;
+  DPL_CUDA(cudaDeviceSynchronize());
+}
 
 std::string Executor::timeline_json() const {
   auto ms = [&](cudaEvent_t e) {
@@ -1146,6 +1383,26 @@ std::string Executor::timeline_json() const {
   if (k_ > 0)
     for (int i = 0; i < M_; ++i) add(2 * k_ - 1, i, 1, send_bwd_ev_[i]);
   out["blocks"] = std::move(blocks);
+  // replica AllReduce per parameter block: [block, start_s, end_s, fp32 bytes]
+  Value ars = Value::array();
+  for (int b = 0; b < nblk_; ++b) {
+    if (!ar_bytes_[b]) continue;
+    Value row = Value::array();
+    row.push_back(b);
+    row.push_back(ms(ar_ev_[b].start));
+    row.push_back(ms(ar_ev_[b].end));
+    row.push_back(ar_bytes_[b]);
+    ars.push_back(std::move(row));
+  }
+  out["allreduce"] = std::move(ars);
+  out["replication"] = r_;
+  out["allreduce_impl"] = r_ > 1 ? (peer_ar_ ? "peer" : "nccl") : "none";
+  // Split-Concat bytes of one micro-batch hand-off out of / into this rank
+  long long sent = 0, sent_back = 0;
+  for (const Route& r : out_routes_) sent += r.rows * 2;
+  for (const Route& r : in_routes_) sent_back += r.rows * 2;
+  out["send_bytes"] = sent;          // activations, per forward send block
+  out["send_back_bytes"] = sent_back;  // activation gradients, per backward send block
   return out.dump();
 }
 
@@ -1182,6 +1439,20 @@ void Executor::read_tensor(const std::string& name, bool grad, void* host, size_
     return;
   }
   throw std::invalid_argument("dpl exec: unknown tensor " + name);
+}
+
+void Executor::read_probe(int layer, const std::string& which, void* host, size_t bytes) {
+  if (!probe_) throw std::invalid_argument("dpl exec: executor built without \"probe\"");
+  if (layer < lo_ || layer >= hi_) throw std::out_of_range("dpl exec: layer not on this stage");
+  const Probe& p = probes_[layer - lo_];
+  const bf16* src = which == "x" ? p.x : which == "y" ? p.y : which == "aux" ? p.aux : which == "dy" ? p.dy
+                    : which == "dx" ? p.dx : nullptr;
+  const size_t n = which == "x" || which == "dx" ? p.nx : which == "aux" ? p.naux : p.ny;
+  if (!src) throw std::invalid_argument("dpl exec: no probe '" + which + "' for layer " + std::to_string(layer));
+  if (bytes != n * 2) throw std::invalid_argument("dpl exec: probe size mismatch (" + std::to_string(n * 2) + " bytes)");
+  DPL_CUDA(cudaSetDevice(device_));
+  DPL_CUDA(cudaDeviceSynchronize());
+  DPL_CUDA(cudaMemcpy(host, src, bytes, cudaMemcpyDeviceToHost));
 }
 
 // B200 layer profiler (the reference only ingests
@@ -1452,6 +1723,21 @@ int dpl_exec_step(dpl_exec* ex, const void* host_input, const void* host_target,
   });
 }
 
+int dpl_exec_step_launch(dpl_exec* ex, const void* host_input, const void* host_target) {
+  return exec_guard([&] { ex->impl->step_launch(host_input, host_target); });
+}
+
+int dpl_exec_prepare(dpl_exec* ex) {
+  return exec_guard([&] { ex->impl->prepare_graphs(); });
+}
+
+int dpl_exec_step_finish(dpl_exec* ex, float* loss) {
+  return exec_guard([&] {
+    const float l = ex->impl->step_finish();
+    if (loss) *loss = l;
+  });
+}
+
 const char* dpl_exec_timeline(dpl_exec* ex) {
   try {
     ex->reply = ex->impl->timeline_json();
@@ -1463,6 +1749,10 @@ const char* dpl_exec_timeline(dpl_exec* ex) {
 
 int dpl_exec_read_tensor(dpl_exec* ex, const char* name, int grad, void* host, size_t bytes) {
   return exec_guard([&] { ex->impl->read_tensor(name, grad != 0, host, bytes); });
+}
+
+int dpl_exec_read_probe(dpl_exec* ex, int layer, const char* which, void* host, size_t bytes) {
+  return exec_guard([&] { ex->impl->read_probe(layer, which, host, bytes); });
 }
 
 int dpl_exec_info(dpl_exec* ex, char* buf, size_t cap) {

@@ -410,6 +410,8 @@ class ConvLayer final : public Layer {
     return implicit_dgrad() ? 0 : px(c) * v_.kp;
   }
   size_t dz_elems(const StageContext& c) const override { return px(c) * v_.cout; }
+  const bf16* probe_aux(int slot) const override { return v_.pool ? yr_[slot] : nullptr; }
+  size_t probe_aux_elems(const StageContext& c) const override { return v_.pool ? px(c) * v_.cout : 0; }
   void alloc_stash(StageContext& ctx) override {
     for (int k = 0; k < ctx.slots; ++k) {
       // explicit columns only where TMA's im2col mode cannot feed the GEMM
@@ -602,7 +604,7 @@ void LmHead::alloc_stash(StageContext& ctx, int slots) {
     st.xn = alloc_n<bf16>(ctx, R * h_);
     st.mean = alloc_n<float>(ctx, R);
     st.rstd = alloc_n<float>(ctx, R);
-    st.dlogits = alloc_n<bf16>(ctx, R * static_cast<size_t>(v_));
+    st.dlogits = alloc_n<bf16>(ctx, R * static_cast<size_t>(vp_));
     slots_.push_back(st);
   }
   dxn_ = alloc_n<bf16>(ctx, R * h_);
@@ -613,16 +615,16 @@ void LmHead::forward(StageContext& ctx, int slot, const bf16* y, const int* tgt,
   const int R = ctx.rows;
   layernorm_fwd(y, w32_, w32_ + h_, st.xn, st.mean, st.rstd, R, h_, eps_, ctx.stream);
   // logits [R][V] = xn Wout^T  (tcgen05, bf16 out)
-  ctx.gemms.run(plain(R, v_, h_, st.xn, h_, false, w16_ + 2 * h_, h_, false, st.dlogits, v_, kOutBf16), ctx.stream);
-  cross_entropy_fwd_bwd(st.dlogits, tgt, loss_acc, R, v_, grad_scale, ctx.stream);
+  ctx.gemms.run(plain(R, vp_, h_, st.xn, h_, false, w16_ + 2 * h_, h_, false, st.dlogits, vp_, kOutBf16), ctx.stream);
+  cross_entropy_fwd_bwd(st.dlogits, tgt, loss_acc, R, v_, grad_scale, ctx.stream, vp_);
 }
 
 void LmHead::backward(StageContext& ctx, int slot, const bf16* y, bf16* dy) {
   const Slot& st = slots_[slot];
   const int R = ctx.rows;
   // dWout += dlogits^T xn ; dxn = dlogits Wout
-  ctx.gemms.run(plain(v_, h_, R, st.dlogits, v_, true, st.xn, h_, true, g32_ + 2 * h_, h_, kOutF32Acc), ctx.stream);
-  ctx.gemms.run(plain(R, h_, v_, st.dlogits, v_, false, w16_ + 2 * h_, h_, true, dxn_, h_, kOutBf16), ctx.stream);
+  ctx.gemms.run(plain(vp_, h_, R, st.dlogits, vp_, true, st.xn, h_, true, g32_ + 2 * h_, h_, kOutF32Acc), ctx.stream);
+  ctx.gemms.run(plain(R, h_, vp_, st.dlogits, vp_, false, w16_ + 2 * h_, h_, true, dxn_, h_, kOutBf16), ctx.stream);
   layernorm_bwd(dxn_, y, st.mean, st.rstd, w32_, nullptr, dy, g32_, g32_ + h_, R, h_, ctx.stream, ctx.ln_ws);
 }
 

@@ -119,6 +119,10 @@ class Layer {
   // scratch the layer needs in StageContext (VGG): columns, dz (elements)
   virtual size_t col_elems(const StageContext&) const { return 0; }
   virtual size_t dz_elems(const StageContext&) const { return 0; }
+  // a stashed intermediate the backward reads besides x / y (parity probes):
+  // the post-ReLU pre-pool conv output of a pooling VGG layer
+  virtual const bf16* probe_aux(int) const { return nullptr; }
+  virtual size_t probe_aux_elems(const StageContext&) const { return 0; }
 };
 
 std::unique_ptr<Layer> make_layer(const ModelSpec& spec, int global_index);
@@ -146,8 +150,12 @@ class TokenEmbedding {
 
 class LmHead {
  public:
-  explicit LmHead(const ModelSpec& spec) : v_(spec.vocab), h_(spec.hidden), eps_(spec.ln_eps) {}
-  size_t param_count() const { return 2 * static_cast<size_t>(h_) + static_cast<size_t>(v_) * h_; }
+  // the vocabulary projection is stored with vp_ = vocab rounded up to 8 rows
+  // (50257 -> 50264 for GPT-2): the padding rows stay zero, their logits are
+  // masked out of the softmax and get no gradient
+  explicit LmHead(const ModelSpec& spec)
+      : v_(spec.vocab), vp_((spec.vocab + 7) / 8 * 8), h_(spec.hidden), eps_(spec.ln_eps) {}
+  size_t param_count() const { return 2 * static_cast<size_t>(h_) + static_cast<size_t>(vp_) * h_; }
   void bind(float* w32, float* g32, bf16* w16, uint64_t seed, cudaStream_t s);
   void alloc_stash(StageContext& ctx, int slots);
   // y: the last block's output; accumulates sum_rows CE into loss_acc and
@@ -160,7 +168,7 @@ class LmHead {
   std::vector<Layer::Named> tensors() const;
 
  private:
-  int v_, h_;
+  int v_, vp_, h_;
   float eps_;
   float* w32_ = nullptr;
   float* g32_ = nullptr;
@@ -169,7 +177,7 @@ class LmHead {
     bf16* xn;
     float* mean;
     float* rstd;
-    bf16* dlogits;  // [R][V]: logits, then in place their gradient
+    bf16* dlogits;  // [R][Vp]: logits, then in place their gradient
   };
   std::vector<Slot> slots_;
   bf16* dxn_ = nullptr;

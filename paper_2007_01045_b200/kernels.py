@@ -82,6 +82,11 @@ def embed_bwd(tok, dx, gwte, gwpe, rows, seq, h):
     check(lib().dpl_k_embed_bwd(_ptr(tok), _ptr(dx), _ptr(gwte), _ptr(gwpe), rows, seq, h, _stream()))
 
 
+def cross_entropy_padded(logits, tgt, loss_acc, rows, vocab, ld, grad_scale):
+    check(lib().dpl_k_cross_entropy_padded(_ptr(logits), _ptr(tgt), _ptr(loss_acc), rows, vocab, ld, grad_scale,
+                                           _stream()))
+
+
 def cross_entropy(logits, tgt, loss_acc, rows, vocab, grad_scale):
     """In place: logits rows -> (softmax - onehot(tgt)) * grad_scale; loss_acc += sum CE."""
     check(lib().dpl_k_cross_entropy(_ptr(logits), _ptr(tgt), _ptr(loss_acc), rows, vocab, grad_scale, _stream()))

@@ -14,26 +14,29 @@ from typing import Optional
 
 from ._lib import check, lib
 
-BLOB_BYTES = 64  # cudaIpcMemHandle_t
+BLOB_BYTES = 256  # PeerBlob (executor.cu): IPC handles + pid / device / pointers
 
 
 class Executor:
     def __init__(self, model: dict, plan, micro_batches: int, gbs: int, *, lr: float = 1e-3, seed: int = 1234,
                  rank: int = 0, world: int = 1, device: Optional[int] = None, apply: bool = True,
-                 timeline: bool = True, schedule: str = "dapple", recompute: bool = False):
+                 timeline: bool = True, schedule: str = "dapple", recompute: bool = False,
+                 allreduce: Optional[str] = None, connect: bool = True, probe: bool = False):
         self.plan = json.loads(plan) if isinstance(plan, str) else plan
         self.model, self.M, self.gbs = model, micro_batches, gbs
         self.rank, self.world = rank, world
         self.device = rank if device is None else device
+        self.allreduce = allreduce or os.environ.get("DPL_ALLREDUCE", "peer")
         cfg = {"model": model, "plan": self.plan, "M": micro_batches, "gbs": gbs, "lr": lr, "seed": seed,
                "rank": rank, "world": world, "apply": apply, "timeline": timeline,
-               "schedule": schedule, "recompute": recompute,
+               "schedule": schedule, "recompute": recompute, "allreduce": self.allreduce, "probe": probe,
                "graph": os.environ.get("DPL_GRAPH", "1") != "0"}
         h = ctypes.c_void_p()
         check(lib().dpl_exec_create(json.dumps(cfg).encode(), self.device, ctypes.byref(h)))
         self._h = h
         self.info = self._info()
-        if world > 1:
+        self.clock_offsets_ns = [0] * world
+        if world > 1 and connect:
             self._connect()
 
     # ----------------------------------------------------------- plumbing
@@ -42,26 +45,32 @@ class Executor:
         check(lib().dpl_exec_info(self._h, buf, len(buf)))
         return json.loads(buf.value.decode())
 
-    def _connect(self):
-        import torch.distributed as dist
+    def export(self) -> bytes:
         blob = ctypes.create_string_buffer(BLOB_BYTES)
         n = ctypes.c_size_t()
         check(lib().dpl_exec_export(self._h, blob, BLOB_BYTES, ctypes.byref(n)))
+        return bytes(blob.raw[:BLOB_BYTES])
+
+    def connect_blobs(self, blobs: list):
+        check(lib().dpl_exec_connect(self._h, b"".join(blobs), BLOB_BYTES, self.world))
+
+    def _connect(self):
+        import torch.distributed as dist
         blobs = [None] * self.world
-        dist.all_gather_object(blobs, bytes(blob.raw[:BLOB_BYTES]))
-        joined = b"".join(blobs)
-        check(lib().dpl_exec_connect(self._h, joined, BLOB_BYTES, self.world))
-        # one NCCL communicator per stage replica group; its first GPU makes the id
+        dist.all_gather_object(blobs, self.export())
+        self.connect_blobs(blobs)
+        # NCCL mode: one communicator per stage replica group; its first GPU makes the id
         stage = self.plan["stages"][self.info["stage"]]
         leader = sorted(stage["gpus"])[0]
+        nccl = self.allreduce == "nccl" and len(stage["gpus"]) > 1
         my_id = None
-        if self.rank == leader and len(stage["gpus"]) > 1:
+        if self.rank == leader and nccl:
             idbuf = ctypes.create_string_buffer(128)
             check(lib().dpl_exec_nccl_id(idbuf))
             my_id = bytes(idbuf.raw)
         ids = [None] * self.world
         dist.all_gather_object(ids, my_id)
-        if len(stage["gpus"]) > 1:
+        if nccl:
             check(lib().dpl_exec_nccl_init(self._h, ids[leader]))
         self.clock_offsets_ns = self._calibrate_clocks()
 
@@ -137,6 +146,18 @@ class Executor:
         """Captured step graphs held (one per flag bank x host-data mode)."""
         return self._info()["graphs"]
 
+    def step_launch(self, host_input=None, host_target=None):
+        """Enqueues one step and returns at once (see LocalRanks)."""
+        self._keep = (host_input, host_target)
+        check(lib().dpl_exec_step_launch(self._h, self._host_arg(host_input, "input"),
+                                         self._host_arg(host_target, "target")))
+
+    def step_finish(self) -> float:
+        loss = ctypes.c_float(float("nan"))
+        check(lib().dpl_exec_step_finish(self._h, ctypes.byref(loss)))
+        self._keep = None
+        return loss.value
+
     def gemm_profile(self, enable: bool):
         check(lib().dpl_exec_gemm_profile(self._h, int(enable)))
 
@@ -164,6 +185,16 @@ class Executor:
                                          out.ctypes.data_as(ctypes.c_void_p), out.nbytes))
         return out
 
+    def probe(self, layer: int, which: str, count: int):
+        """Teacher-forcing probe (Executor(..., probe=True)): the last
+        micro-batch's x / y / aux / dy / dx of `layer`, as float32."""
+        import numpy as np
+        import torch
+        out = torch.empty(count, dtype=torch.bfloat16)
+        check(lib().dpl_exec_read_probe(self._h, layer, which.encode(), ctypes.c_void_p(out.data_ptr()),
+                                        count * 2))
+        return out.float().numpy().astype(np.float64)
+
     def close(self):
         """Collective when world > 1: unmap peers, barrier, then free."""
         if getattr(self, "_h", None):
@@ -183,6 +214,66 @@ class Executor:
             except Exception:
                 pass
             self._h = None
+
+
+class LocalRanks:
+    """Every rank of a plan in this one process (several ranks may share one
+    GPU, e.g. all on cuda:0): the ranks map each other's receive regions and
+    gradients with plain pointers instead of CUDA IPC, their flag waits stay
+    stream memory operations, and the replica AllReduce runs over the shared
+    memory (collective.cu) -- the same step program as one process per GPU,
+    so the Split-Concat hand-off, the cross-rank flag chain and the replica
+    reduction are exercised on a single device.  A step launches every
+    rank's captured step, then waits for all of them."""
+
+    def __init__(self, model: dict, plan, micro_batches: int, gbs: int, *, devices=None, **kw):
+        # Before CUDA initialises: kernels loaded eagerly (lazy loading
+        # synchronises the context on a kernel's first launch, deadlocking
+        # ranks that wait on each other) and one hardware work queue per
+        # stream (ranks' blocked flag waits must not sit in front of another
+        # rank's work).
+        want = {"CUDA_MODULE_LOADING": "EAGER", "CUDA_DEVICE_MAX_CONNECTIONS": "32"}
+        if any(os.environ.get(k) != v for k, v in want.items()):
+            import torch
+            if torch.cuda.is_initialized():
+                raise RuntimeError("LocalRanks needs CUDA_MODULE_LOADING=EAGER and CUDA_DEVICE_MAX_CONNECTIONS=32 "
+                                   "set before CUDA initialises")
+            os.environ.update(want)
+        plan = json.loads(plan) if isinstance(plan, str) else plan
+        world = 1 + max(g for s in plan["stages"] for g in s["gpus"])
+        devices = devices or [0] * world
+        if kw.get("allreduce", "peer") != "peer":
+            raise ValueError("LocalRanks reduce over shared memory (allreduce='peer')")
+        self.ranks = [Executor(model, plan, micro_batches, gbs, rank=r, world=world, device=devices[r],
+                               allreduce="peer", connect=False, **kw) for r in range(world)]
+        blobs = [ex.export() for ex in self.ranks]
+        for ex in self.ranks:
+            ex.connect_blobs(blobs)
+        # every rank's step graphs exist before any rank runs
+        for ex in self.ranks:
+            check(lib().dpl_exec_prepare(ex._h))
+        self.world = world
+
+    def step(self, inputs=None, targets=None) -> list:
+        """One step on every rank; returns the per-rank losses (NaN except on
+        last-stage ranks)."""
+        inputs = inputs or [None] * self.world
+        targets = targets or [None] * self.world
+        for ex, x, t in zip(self.ranks, inputs, targets):
+            ex.step_launch(x, t)
+        return [ex.step_finish() for ex in self.ranks]
+
+    def timelines(self) -> list:
+        return [ex.timeline() for ex in self.ranks]
+
+    def close(self):
+        for ex in self.ranks:  # unmap peers everywhere before anyone frees
+            if getattr(ex, "_h", None):
+                check(lib().dpl_exec_disconnect(ex._h))
+        for ex in self.ranks:
+            if getattr(ex, "_h", None):
+                lib().dpl_exec_destroy(ex._h)
+                ex._h = None
 
 
 def merge_timelines(parts: list, micro_batches: int, stages: int) -> dict:

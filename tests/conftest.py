@@ -3,6 +3,15 @@ import sys
 
 import pytest
 
+# Kernels are loaded eagerly: with lazy loading the first launch of a kernel
+# synchronises the CUDA context, which deadlocks ranks that share one GPU in
+# this process (runtime.LocalRanks) while another rank's step waits on them.
+# Must be set before anything initialises CUDA.
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+# one hardware work queue per stream for the same reason: a rank's blocked
+# flag wait must not sit in front of another rank's work
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

@@ -16,9 +16,9 @@ from paper_2007_01045_b200.runtime import merge_timelines  # noqa: E402
 def test_flops_per_sample_match_survey():
     assert bench.flops_per_sample(bench.MODELS["bert48"]) == pytest.approx(2.010e12, rel=1e-3)
     assert bench.flops_per_sample(bench.MODELS["vgg19"]) == pytest.approx(117.8e9, rel=1e-3)
-    # GPT-2: 67,993,600 FLOP/token/layer x48 + head, x3 x1024 tokens (head at V = 50304)
+    # GPT-2: 67,993,600 FLOP/token/layer x48 + head, x3 x1024 tokens (head at V = 50257)
     gpt = bench.flops_per_sample(bench.MODELS["gpt2-1.5b"])
-    assert gpt == pytest.approx(3 * 1024 * (48 * 67_993_600 + 2 * 1600 * 50304), rel=1e-9)
+    assert gpt == pytest.approx(3 * 1024 * (48 * 67_993_600 + 2 * 1600 * 50257), rel=1e-9)
 
 
 @pytest.mark.parametrize("n", [1, 2, 4, 8])
@@ -69,3 +69,59 @@ def test_merge_timelines_aligns_ranks_and_computes_bubble():
     assert m["latency"] == pytest.approx(0.010)  # first forward at 0 -> last rank done at 10 ms
     busy = (0.001 + 0.001 + 0.002 + 0.002) + (0.001 + 0.002 + 0.001 + 0.002)
     assert m["bubble"] == pytest.approx(1 - busy / (2 * 0.010))
+
+
+def test_comm_stats_rates():
+    """Split-Concat GB/s from send blocks and AllReduce bus bandwidth per block."""
+    tl0 = {"stage": 0, "replication": 2, "allreduce_impl": "peer", "send_bytes": 8 << 20, "send_back_bytes": 0,
+           "blocks": [[0, 0, 0, 0.0, 1.0], [1, 0, 0, 1.0, 1.0 + 0.01]],
+           "allreduce": [[0, 2.0, 2.0 + 0.001, 100_000_000]]}
+    tl1 = {"stage": 1, "replication": 1, "send_bytes": 0, "send_back_bytes": 4 << 20,
+           "blocks": [[2, 0, 0, 1.1, 1.2], [1, 0, 1, 1.3, 1.3 + 0.004]], "allreduce": []}
+    c = bench.comm_stats([tl0, tl1], {"bw_gbps": 800.0, "latency_us": 3.0})
+    assert c["splitconcat"]["sends"] == 2
+    assert c["splitconcat"]["gbps_median"] == pytest.approx(((8 << 20) / 0.01 + (4 << 20) / 0.004) / 2 / 1e9)
+    ar = c["allreduce"]
+    assert ar["impl"] == "peer" and ar["blocks"] == 1
+    assert ar["busbw_gbps_median"] == pytest.approx(2 * 1 / 2 * 1e8 / 0.001 / 1e9)
+    assert ar["frac_of_link"] == pytest.approx(ar["busbw_gbps_median"] / 800.0)
+
+
+def test_planner_cpu_times_match_reference():
+    """The CPU baseline's planner leg: the reference's plan() (oracle/_ref) and
+    the new host planner give the same plan for the same request."""
+    from oracle import refproc
+    if not refproc.available():
+        pytest.skip("oracle/_ref not built")
+    prof = {"profile_batch_size": 8, "layers": [
+        {"fwd_time_us": 100.0 + 7 * i, "bwd_time_us": 210.0, "activation_bytes": 1 << 23, "param_bytes": 50 << 20}
+        for i in range(24)]}
+    cl = bench.b200_cluster(4, 4.0)
+    from paper_2007_01045_b200 import pipeplan
+    plan = pipeplan.plan(prof, cl, 8)["plan"]
+    out = bench.planner_cpu_times(prof, cl, 8, plan)
+    assert out["identical_plan"] and out["identical_sim_latency"]
+    assert out["reference_plan_s"] > 0 and out["ours_plan_par_s"] > 0
+
+
+def test_plan_fixed_point_replans_on_slice_profiles(monkeypatch):
+    """plan_fixed_point re-profiles at the chosen plan's slice sizes until
+    the plan repeats (fake profiler: per-sample cost with a fixed overhead, so
+    smaller slices are less efficient than the planner's ÷r assumes)."""
+    calls = []
+
+    def fake_profile(model, samples, reps=5):
+        calls.append(samples)
+        return {"profile_batch_size": samples, "layers": [
+            {"fwd_time_us": 50.0 + 10.0 * samples, "bwd_time_us": 100.0 + 20.0 * samples,
+             "activation_bytes": samples << 20, "param_bytes": 50 << 20} for _ in range(24)]}
+
+    monkeypatch.setattr(bench, "profile_model", fake_profile)
+    profiles = {8: fake_profile(None, 8)}
+    plan, info = bench.plan_fixed_point({"layers": 24}, profiles, 8, bench.b200_cluster(4, 6.0), 8)
+    assert info["fixed_point"]
+    last = info["iterations"][-1]
+    assert last["stages"] == [[s["layers"], s["gpus"]] for s in plan["stages"]]
+    assert info["sim_latency_ms"] > 0
+    for st in plan["stages"]:
+        assert -(-8 // len(st["gpus"])) in profiles

@@ -66,7 +66,33 @@ def test_cross_entropy_fwd_bwd(cuda, rows, v):
     assert err <= 0.01 * (dref * scale).abs().max().item()
 
 
+@pytest.mark.parametrize("rows,v", [(64, 1001), (300, 50257), (8, 1)])
+def test_cross_entropy_padded_vocab(cuda, rows, v):
+    """Rows of stride ld = v rounded up to 8 (C4's 50257 stored as 50264):
+    the padding columns hold garbage that must not enter the softmax and get
+    a zero gradient."""
+    ld = (v + 7) // 8 * 8
+    logits = _rand(rows, ld, dev=cuda, seed=7, scale=8.0)
+    logits[:, v:] = 30.0  # would dominate the softmax if not masked
+    g = torch.Generator(device="cpu").manual_seed(8)
+    tgt = torch.randint(0, v, (rows,), generator=g, dtype=torch.int32).to(cuda)
+    lf = logits[:, :v].float().requires_grad_(True)
+    ref = torch.nn.functional.cross_entropy(lf, tgt.long(), reduction="sum")
+    (dref,) = torch.autograd.grad(ref, lf)
+    scale = 1.0 / rows
+    acc = torch.zeros(1, device=cuda)
+    work = logits.clone()
+    K.cross_entropy_padded(work, tgt, acc, rows, v, ld, scale)
+    torch.cuda.synchronize()
+    assert abs(acc.item() - ref.item()) <= 1e-4 * abs(ref.item()) + 1e-3
+    err = (work[:, :v].float() - dref * scale).abs().max().item()
+    assert err <= 0.01 * (dref * scale).abs().max().item() + 1e-6
+    assert bool((work[:, v:] == 0).all())
+
+
 LM = dict(kind="gpt", layers=2, hidden=256, heads=4, ffn=1024, seq=128, vocab=1000)
+# vocabulary not a multiple of 8 (padded projection rows, masked logits)
+LM_ODD = dict(kind="gpt", layers=2, hidden=256, heads=4, ffn=1024, seq=128, vocab=1001)
 
 
 def _check_lm_tensors(ex, emu, exact, stage_first, stage_last):
@@ -81,17 +107,19 @@ def _check_lm_tensors(ex, emu, exact, stage_first, stage_last):
         assert rel_fro(got, exact.grads[(owner, name)]) < FP64_GRAD_RTOL
 
 
-@pytest.mark.parametrize("schedule,recompute", [("dapple", False), ("gpipe", True)])
-def test_lm_single_gpu_step_matches_oracle(cuda, schedule, recompute):
+@pytest.mark.parametrize("schedule,recompute,model", [("dapple", False, "LM"), ("gpipe", True, "LM"),
+                                                      ("dapple", False, "LM_ODD")])
+def test_lm_single_gpu_step_matches_oracle(cuda, schedule, recompute, model):
     from oracle.executor_ref import full_batch_step
     from parity_util import check_grads, check_loss
     from paper_2007_01045_b200.runtime import Executor
     plan = {"stages": [{"layers": [0, 2], "gpus": [0], "replication": 1}]}
-    exact = full_batch_step(LM, 8)
-    emu = full_batch_step(LM, 8, bf16=True)
-    ex = Executor(LM, plan, 4, 8, lr=1e-3, apply=False, schedule=schedule, recompute=recompute)
+    model = {"LM": LM, "LM_ODD": LM_ODD}[model]
+    exact = full_batch_step(model, 8)
+    emu = full_batch_step(model, 8, bf16=True)
+    ex = Executor(model, plan, 4, 8, lr=1e-3, apply=False, schedule=schedule, recompute=recompute)
     loss = ex.step()
-    assert abs(loss - np.log(1000)) < 1.0  # near-uniform predictions at init
+    assert abs(loss - np.log(model["vocab"])) < 1.0  # near-uniform predictions at init
     check_loss(loss, emu, exact)
     check_grads(ex, emu, exact, range(2), "gpt", 2)
     _check_lm_tensors(ex, emu, exact, True, True)

@@ -57,12 +57,12 @@ for i, n in enumerate(names):
 # per-tile timeline: SM clock -> ns via each CTA's entry / exit globaltimer
 clk = (full[:, 7] - full[:, 0]) / np.maximum(full[:, 62] - full[:, 63], 1)  # cycles per ns
 t0 = full[:, 63].min()
-print(f"  SM clock ~{np.median(clk):.2f} GHz; kernel span {(full[:, 62].max() - t0) / 1e3:.2f} us")
+print(f"  ring stages {int(full[0, 61])}; SM clock ~{np.median(clk):.2f} GHz; kernel span {(full[:, 62].max() - t0) / 1e3:.2f} us")
 rows = []
 for c in range(full.shape[0]):
     ent = (full[c, 63] - t0) / 1e3
     tiles = []
-    for j in range(11):
+    for j in range(6):
         v = full[c, 16 + 4 * j:20 + 4 * j]
         if v[0] <= 0:
             break
@@ -76,5 +76,20 @@ for c in list(range(0, len(rows), max(1, len(rows) // 8))):
 mma = [b - a for _, tiles, _ in rows for a, b, _, _ in tiles]
 epi = [e1 - e0 for _, tiles, _ in rows for _, _, e0, e1 in tiles if e1 == e1]
 gap = [tiles[j + 1][0] - tiles[j][1] for _, tiles, _ in rows for j in range(len(tiles) - 1)]
+kb = -(-Kd // 64)
+print(f"  cycles per 64-wide k-block: median {np.median(mma) * 1e3 * np.median(clk) / kb:.0f} (MMA floor 512 for 256-wide tiles)")
 print(f"  mma span per tile: median {np.median(mma):.2f} us; epilogue per tile: median {np.median(epi):.2f} us;"
       f" gap mma_end -> next mma_start: median {np.median(gap) if gap else 0:.2f} us")
+
+steps = ["tmem_ld", "wait_ld", "wait_store_read", "stage_sts", "fence", "store_issue"]
+for j in range(2):
+    sl = full[:, 40 + 8 * j:46 + 8 * j]
+    ok = sl[:, 0] > 0
+    if ok.any():
+        d = np.diff(sl[ok], axis=1)
+        print(f"  chunk {j} of warp 4 (cycles): " + ", ".join(f"{steps[k + 1]} {np.median(d[:, k]):.0f}" for k in range(5)))
+    if j == 0:
+        nxt = full[:, 48]
+        ok2 = (nxt > 0) & (sl[:, 5] > 0)
+        if ok2.any():
+            print(f"  chunk 0 store issued -> chunk 1 start: {np.median(nxt[ok2] - sl[ok2, 5]):.0f} cycles")
