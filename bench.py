@@ -41,6 +41,10 @@ MODELS = {
     # C4: GPT-2 1.5B, causal-LM cross-entropy over the 50257-token vocabulary (projection stored padded to 50264 rows, padding masked)
     "gpt2-1.5b": dict(kind="gpt", layers=48, hidden=1600, heads=25, ffn=6400, seq=1024, vocab=50257),
     "mlp16": dict(kind="mlp", layers=16, hidden=1024),
+    # C5's XLNet-36 (Table I: 36 uniform transformer blocks) executed as
+    # a BERT-style encoder of that depth; its plans come from the host planner
+    # on this model's own B200 profile (--plan planner), measured L vs est / sim L
+    "xlnet36": dict(kind="bert", layers=36, hidden=1024, heads=16, ffn=4096, seq=512),
     # C3: VGG-19 on 224x224 images, 1000-class cross-entropy (convs as im2col + tcgen05 GEMM)
     "vgg19": dict(kind="vgg", layers=19, image=224, width=64, fc=4096, classes=1000),
 }
@@ -83,6 +87,7 @@ def flops_per_sample(m: dict) -> float:
 DEFAULTS = {"bert48": dict(micro_batches=8, slice=8, straight=False, global_batch=64),
             "gpt2-1.5b": dict(micro_batches=32, slice=1, straight=True),
             "mlp16": dict(micro_batches=8, slice=8, straight=False),
+            "xlnet36": dict(micro_batches=16, slice=8, straight=False, global_batch=128),
             "vgg19": dict(micro_batches=8, slice=24, straight=False)}
 
 

@@ -1523,7 +1523,12 @@ void GemmOp::prepare(const GemmDesc& d) {
     }();
     const int c_inner = d.ndiv >= d.N ? d.N : d.ndiv;
     // a 64-column box must not straddle a column split of the output addressing
-    const bool groups = groups_enabled && bn >= 128 && (c_inner == d.N || c_inner % 64 == 0);
+    // 64-column groups pay off for bf16 outputs without an extra tensor (qkv,
+    // plain dgrads: fewer, larger stores); the residual / activation-input /
+    // aux-output and fp32 paths keep the 32-column chunks, whose smaller
+    // staging leaves the ring a stage deeper (tools/gemm_graph_bench.py, r02)
+    const bool groups = groups_enabled && bn >= 128 && (c_inner == d.N || c_inner % 64 == 0) && kind == kOutBf16 &&
+                        !x_in && !aux;
     p.stages = std::min(kMaxStages, ring / stage_bytes);
     static const int max_stages = [] {  // DPL_GEMM_MAX_STAGES: diagnostic cap on the ring depth
       const char* e = std::getenv("DPL_GEMM_MAX_STAGES");

@@ -83,10 +83,15 @@ def test_local_ranks_measured_block_order(cuda):
     finally:
         lr.close()
     blk = {(x, i, k): (s, e) for x, i, k, s, e in tl["blocks"]}
+    # the receiver is released by the flag store inside the send block, so its
+    # block starts after the send started (the send's end event is recorded a
+    # little after the flag store)
     eps = 2e-6  # event resolution
     for i in range(M):
-        assert blk[(2, i, 0)][0] >= blk[(1, i, 0)][1] - eps  # F_i on stage 1 after the activation send
-        assert blk[(0, i, 1)][0] >= blk[(1, i, 1)][1] - eps  # B_i on stage 0 after the gradient send
+        assert blk[(2, i, 0)][0] >= blk[(1, i, 0)][0] - eps  # F_i on stage 1 after its activation send began
+        assert blk[(0, i, 1)][0] >= blk[(1, i, 1)][0] - eps  # B_i on stage 0 after its gradient send began
+        assert blk[(1, i, 0)][0] >= blk[(0, i, 0)][1] - eps  # the send follows F_i on stage 0
+        assert blk[(1, i, 1)][0] >= blk[(2, i, 1)][1] - eps  # the gradient send follows B_i on stage 1
     # stage 0 runs phi = 2 forwards before its first backward
     f = sorted((blk[(0, i, 0)][0], i) for i in range(M))
     b0 = blk[(0, 0, 1)][0]
