@@ -58,7 +58,7 @@ struct GemmDesc {
   void* aux_out = nullptr;
   int force_bn = 0;  // 0 = heuristic; else 64/128/256
   int force_1sm = 0; // 1 = never use the CTA-pair kernel
-  unsigned long long* trace = nullptr;  // per-CTA phase timestamps (64 words per CTA), diagnostics
+  unsigned long long* trace = nullptr;  // per-CTA phase timestamps (16 per CTA), diagnostics
   float* colsum = nullptr;              // kColSum target (fp32, N)
   // implicit-GEMM 3x3 / pad-1 convolution over NHWC conv_x [n][h][w][c] (c % 64 == 0):
   //   conv_operand 1: A[M = n*h*w][K = 9c] are its im2col columns (K-major, A unused)
@@ -82,8 +82,6 @@ struct alignas(64) GemmParams {
   int epi_out_bytes;   // one output chunk buffer (2 KB bf16 / 4 KB fp32)
   int epi_nx;          // extra-tensor chunk buffers per warp
   int epi_tile_cols;   // columns of one CTA tile (bias slice staged per warp)
-  int epi_groups;      // 64-column-group TMA epilogue (epi_tile_tma_g); 0: 32-column chunks
-  int epi_plain;       // output / extra maps address one [M][ldc] matrix per z (no column / batch split)
   float* colsum;       // kColSum target (TMA epilogue; otherwise a colsum pass after the GEMM)
   int conv_operand, conv_h, conv_w, conv_c;  // implicit-GEMM convolution operand (GemmDesc)
   int M, N, K, batch;

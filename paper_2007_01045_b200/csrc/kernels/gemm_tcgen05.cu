@@ -91,34 +91,9 @@ __device__ __forceinline__ void conv_tile_load(const GemmParams& p, const CUtens
 }
 
 // diagnostics: phase timestamps per CTA (GemmDesc::trace)
-// 64 words per CTA: slots 0-15 the phase marks below, 16 + 4 j + {0..3} tile
-// j's (j < 6) MMA start / last commit / epilogue start / epilogue end, 40-55
-// the steps of the first two TMA-epilogue chunks of warp 4, 61 the ring depth,
-// 62 / 63 the %globaltimer at exit / entry (ns, aligns CTAs)
-constexpr int kTraceWords = 64;
 __device__ __forceinline__ void trace_mark(const GemmParams& p, int slot) {
   if (p.trace) {
-    p.trace[blockIdx.x * kTraceWords + slot] = clock64();  // SM cycles (compare within one CTA)
-  }
-}
-__device__ __forceinline__ void trace_tile(const GemmParams& p, int j, int k) {
-  if (p.trace && j < 6) p.trace[blockIdx.x * kTraceWords + 16 + 4 * j + k] = clock64();
-}
-__device__ __forceinline__ void trace_exit(const GemmParams& p) {
-  if (p.trace) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    p.trace[blockIdx.x * kTraceWords + 62] = t;
-    p.trace[blockIdx.x * kTraceWords + 7] = clock64();
-  }
-}
-__device__ __forceinline__ void trace_entry(const GemmParams& p) {
-  if (p.trace) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    p.trace[blockIdx.x * kTraceWords + 63] = t;
-    p.trace[blockIdx.x * kTraceWords + 61] = p.stages;
-    p.trace[blockIdx.x * kTraceWords] = clock64();
+    p.trace[blockIdx.x * 16 + slot] = clock64();  // SM cycles (compare within one CTA)
   }
 }
 
@@ -378,8 +353,6 @@ __device__ __forceinline__ void epi_tile_prefetch(const GemmParams& p, EpiTma& e
 
 #define EPI_MARK(J, K) \
   if (threadIdx.x == 128 && e.seq < 2 && (J) < 2) trace_mark(p, 8 + (J) * 4 + (K))
-#define EPI_MARK2(J, K) \
-  if (threadIdx.x == 128 && e.seq < 2 && (J) < 2) trace_mark(p, 40 + (J) * 8 + (K))
 
 template <int kPerWarp>
 __device__ __forceinline__ void epi_tile_tma(const GemmParams& p, EpiTma& e, uint32_t tbase, int z, int row0, int col0,
@@ -399,11 +372,9 @@ __device__ __forceinline__ void epi_tile_tma(const GemmParams& p, EpiTma& e, uin
     const int c = half + 2 * j;
     const int n0 = col0 + c * 32;
     uint32_t raw[32];
-    EPI_MARK2(j, 0);
     ptx::tmem_ld_32x32b_x32(tbase + c * 32, raw);
     ptx::tmem_wait_ld();
     EPI_MARK(j, 0);
-    EPI_MARK2(j, 1);
     if (n0 >= p.N) {  // chunk entirely right of the matrix (no load was issued for it)
       ++e.seq;
       continue;
@@ -458,7 +429,6 @@ __device__ __forceinline__ void epi_tile_tma(const GemmParams& p, EpiTma& e, uin
     // output buffer ob (and the aux buffer) were last read by the bulk store two chunks ago
     if (lane == 0) ptx::bulk_wait_read<1>();
     __syncwarp();
-    EPI_MARK2(j, 2);
     if (epi & kAuxOut) {
       uint8_t* abuf = epi_xbuf(p, e, ob);
 #pragma unroll
@@ -512,10 +482,8 @@ __device__ __forceinline__ void epi_tile_tma(const GemmParams& p, EpiTma& e, uin
         if (n0 + static_cast<int>(lane) < p.N) atomicAdd(p.colsum + n0 + lane, cs);
       }
     }
-    EPI_MARK2(j, 3);
     ptx::fence_proxy_async_smem();
     __syncwarp();
-    EPI_MARK2(j, 4);
     if (lane == 0) {
       int cc[5];
       epi_coords(p, z, row0, n0, cc);
@@ -524,236 +492,13 @@ __device__ __forceinline__ void epi_tile_tma(const GemmParams& p, EpiTma& e, uin
       if (epi & kAuxOut) ptx::tma_store_5d(&p.tma_x, epi_xbuf(p, e, ob), cc[0], cc[1], cc[2], cc[3], cc[4]);
       ptx::bulk_commit();
     }
-    EPI_MARK2(j, 5);
-    ++e.seq;
-  }
-}
-
-// ---------------------------------------------------------------- TMA epilogue, 64-column groups
-// The default epilogue for 128- and 256-wide tiles.  Per epilogue warp and
-// tile: groups g = half + 2 j (64 columns each) of its 32 TMEM lanes.  Per
-// group: two TMEM loads (64 fp32 columns per lane, one wait; the next group's
-// loads are issued before this group is processed), the epilogue math over
-// 64 independent values, one staging pass into a 32 x 128-byte
-// SWIZZLE_128B buffer and ONE bulk tensor store (bf16: box 64 x 32; fp32: two
-// 32 x 32 boxes) -- half the stores, fences and waits of the 32-column
-// chunks, with the integer coordinate math hoisted.
-//   bf16 group: 32 rows x 128 B; unit q of row r at r*128 + ((q ^ (r & 7)) << 4)
-//   fp32 group: two such 4 KB halves (columns 0-31, 32-63)
-constexpr int kGroupBytes = 32 * 128;
-
-__device__ __forceinline__ void epi_coords_g(const GemmParams& p, int z, int m, int n, int (&c)[5]) {
-  if (p.epi_plain) {  // C is one [M][ldc] matrix per z: no column / batch split to undo
-    c[0] = n;
-    c[1] = m;
-    c[2] = 0;
-    c[3] = 0;
-    c[4] = z;
-  } else {
-    epi_coords(p, z, m, n, c);
-  }
-}
-
-__device__ __forceinline__ uint8_t* epi_gxbuf(const GemmParams& p, const EpiTma& e, int b) {
-  return e.region + p.epi_out_bytes + b * kGroupBytes;
-}
-
-// lane 0: bulk-load the extra input (residual / activation input) of the
-// 64-column group at (row0, n0) into x buffer b
-__device__ __forceinline__ void epi_issue_gx(const GemmParams& p, EpiTma& e, int b, int z, int row0, int n0) {
-  int c[5];
-  epi_coords_g(p, z, row0, n0, c);
-  ptx::mbar_arrive_expect_tx(&e.xbar[b], kGroupBytes);
-  ptx::tma_load_5d(epi_gxbuf(p, e, b), &p.tma_x, &e.xbar[b], c[0], c[1], c[2], c[3], c[4]);
-}
-
-template <int kGroups>
-__device__ __forceinline__ void epi_tile_prefetch_g(const GemmParams& p, EpiTma& e, int z, int row0, int col0,
-                                                    int half) {
-  const bool bias = (p.epi & kBias) != 0;
-  const bool x_in = epi_has_x_in(p);
-  if (!x_in && !bias) return;
-  ptx::fence_proxy_async_smem();
-  __syncwarp();
-  if (ptx::lane_id() != 0) return;
-  if (bias) {
-    const int cols = min(p.epi_tile_cols, p.N - col0);
-    const uint32_t bytes = static_cast<uint32_t>((cols * 4 + 15) & ~15);
-    ptx::mbar_arrive_expect_tx(&e.xbar[kMaxNx], bytes);
-    ptx::bulk_load(epi_bias(p, e), p.bias + col0, bytes, &e.xbar[kMaxNx]);
-  }
-  if (!x_in) return;
-#pragma unroll
-  for (int j = 0; j < kGroups; ++j) {
-    const int n0 = col0 + (half + 2 * j) * 64;
-    if (j < p.epi_nx && n0 < p.N) epi_issue_gx(p, e, (e.seq + j) % p.epi_nx, z, row0, n0);
-  }
-}
-
-__device__ __forceinline__ void pack_bf16x8(const float* v, uint4& w) {
-  uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
-    wp[k] = *reinterpret_cast<uint32_t*>(&h);
-  }
-}
-
-template <int kGroups>
-__device__ __forceinline__ void epi_tile_tma_g(const GemmParams& p, EpiTma& e, uint32_t tbase, int z, int row0,
-                                               int col0, int half) {
-  const uint32_t lane = ptx::lane_id();
-  const uint32_t epi = p.epi;
-  const bool x_in = epi_has_x_in(p);
-  const uint32_t kind = epi & kOutMask;
-  const bool f32 = kind != kOutBf16;
-  const bool scale = p.alpha != 1.0f;
-  if (epi & kBias) {
-    ptx::mbar_wait(&e.xbar[kMaxNx], (e.xph >> kMaxNx) & 1);
-    e.xph ^= 1u << kMaxNx;
-  }
-  const float* bias_s = epi_bias(p, e) - col0;  // indexed by global column
-  uint32_t raw[64];
-  ptx::tmem_ld_32x32b_x32(tbase + half * 64, *reinterpret_cast<uint32_t(*)[32]>(raw));
-  ptx::tmem_ld_32x32b_x32(tbase + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
-#pragma unroll 1
-  for (int j = 0; j < kGroups; ++j) {
-    const int g = half + 2 * j;
-    const int n0 = col0 + g * 64;
-    ptx::tmem_wait_ld();
-    float v[64];
-#pragma unroll
-    for (int k = 0; k < 64; ++k) v[k] = __uint_as_float(raw[k]);
-    if (j + 1 < kGroups) {  // the next group streams out of TMEM while this one is processed
-      ptx::tmem_ld_32x32b_x32(tbase + (g + 2) * 64, *reinterpret_cast<uint32_t(*)[32]>(raw));
-      ptx::tmem_ld_32x32b_x32(tbase + (g + 2) * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
-    }
-    if (n0 >= p.N) {  // group entirely right of the matrix
-      ++e.seq;
-      continue;
-    }
-    if (scale) {
-#pragma unroll
-      for (int k = 0; k < 64; ++k) v[k] *= p.alpha;
-    }
-    if (epi & kBias) {  // smem broadcast reads (columns past N hold junk; clipped on store)
-      const float4* b4 = reinterpret_cast<const float4*>(bias_s + n0);
-#pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const float4 bb = b4[q];
-        v[4 * q] += bb.x;
-        v[4 * q + 1] += bb.y;
-        v[4 * q + 2] += bb.z;
-        v[4 * q + 3] += bb.w;
-      }
-    }
-    if (x_in) {
-      const int xb = e.seq % p.epi_nx;
-      uint8_t* xbuf = epi_gxbuf(p, e, xb);
-      ptx::mbar_wait(&e.xbar[xb], (e.xph >> xb) & 1);
-      e.xph ^= 1u << xb;
-      // 8 columns at a time (keeps the register footprint at raw + v)
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        float xv[8];
-        unpack_bf16x8(*reinterpret_cast<const uint4*>(xbuf + lane * 128 + ((q ^ (lane & 7)) << 4)), xv);
-        if (epi & kResid) {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) v[8 * q + k] += xv[k];
-        } else if (epi & kDGelu) {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) v[8 * q + k] *= dgelu_f(xv[k]);
-        } else {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) v[8 * q + k] *= xv[k] > 0.f ? 1.f : 0.f;
-        }
-      }
-      if (j + p.epi_nx < kGroups) {  // refill only when a warp has more groups than buffers
-        ptx::fence_proxy_async_smem();
-        __syncwarp();
-        const int n2 = col0 + (g + 2 * p.epi_nx) * 64;
-        if (lane == 0 && n2 < p.N) epi_issue_gx(p, e, xb, z, row0, n2);
-      }
-    }
-    // the single staging buffer (and the aux buffer) were last read by the
-    // previous group's bulk store
-    if (lane == 0) ptx::bulk_wait_read<0>();
-    __syncwarp();
-    uint8_t* obuf = e.region;
-    if (epi & kAuxOut) {
-      uint8_t* abuf = epi_gxbuf(p, e, 0);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        uint4 w;
-        pack_bf16x8(v + 8 * q, w);
-        *reinterpret_cast<uint4*>(abuf + lane * 128 + ((q ^ (lane & 7)) << 4)) = w;
-      }
-    }
-    if (epi & kGelu) {
-#pragma unroll
-      for (int k = 0; k < 64; ++k) v[k] = gelu_f(v[k]);
-    } else if (epi & kRelu) {
-#pragma unroll
-      for (int k = 0; k < 64; ++k) v[k] = fmaxf(v[k], 0.f);
-    }
-    if (f32) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          *reinterpret_cast<float4*>(obuf + h * kGroupBytes + lane * 128 + ((q ^ (lane & 7)) << 4)) =
-              make_float4(v[32 * h + 4 * q], v[32 * h + 4 * q + 1], v[32 * h + 4 * q + 2], v[32 * h + 4 * q + 3]);
-    } else {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        uint4 w;
-        pack_bf16x8(v + 8 * q, w);
-        *reinterpret_cast<uint4*>(obuf + lane * 128 + ((q ^ (lane & 7)) << 4)) = w;
-      }
-    }
-    if ((epi & kColSum) && !f32) {
-      // column sums of the staged bf16 group: lane j sums columns j and j + 32 over the valid rows
-      __syncwarp();
-      const int rows = min(32, p.M - row0);
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        const int c = static_cast<int>(lane) + 32 * hh;
-        const int q = c >> 3, el = c & 7;
-        float cs = 0.f;
-        for (int r = 0; r < rows; ++r)
-          cs += __bfloat162float(
-              *reinterpret_cast<const __nv_bfloat16*>(obuf + r * 128 + ((q ^ (r & 7)) << 4) + el * 2));
-        if (n0 + c < p.N) atomicAdd(p.colsum + n0 + c, cs);
-      }
-    }
-    ptx::fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) {
-      int cc[5];
-      epi_coords_g(p, z, row0, n0, cc);
-      if (!f32) {
-        ptx::tma_store_5d(&p.tma_c, obuf, cc[0], cc[1], cc[2], cc[3], cc[4]);
-      } else {
-        int cc2[5];
-        epi_coords_g(p, z, row0, n0 + 32, cc2);
-        if (kind == kOutF32Acc) {
-          ptx::tma_reduce_add_5d(&p.tma_c, obuf, cc[0], cc[1], cc[2], cc[3], cc[4]);
-          if (n0 + 32 < p.N) ptx::tma_reduce_add_5d(&p.tma_c, obuf + kGroupBytes, cc2[0], cc2[1], cc2[2], cc2[3], cc2[4]);
-        } else {
-          ptx::tma_store_5d(&p.tma_c, obuf, cc[0], cc[1], cc[2], cc[3], cc[4]);
-          if (n0 + 32 < p.N) ptx::tma_store_5d(&p.tma_c, obuf + kGroupBytes, cc2[0], cc2[1], cc2[2], cc2[3], cc2[4]);
-        }
-      }
-      if (epi & kAuxOut) ptx::tma_store_5d(&p.tma_x, epi_gxbuf(p, e, 0), cc[0], cc[1], cc[2], cc[3], cc[4]);
-      ptx::bulk_commit();
-    }
     ++e.seq;
   }
 }
 
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_constant__ GemmParams p) {
-  if (threadIdx.x == 0) trace_entry(p);
+  if (threadIdx.x == 0) trace_mark(p, 0);
   using C = Cfg<BN>;
   const int S = p.stages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -860,8 +605,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      int jt = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++jt) {
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
         const int ks = t % p.k_splits;
         const int kb0 = ks * p.kb_per_split;
         const int kb1 = min(p.num_k_blocks, kb0 + p.kb_per_split);
@@ -872,7 +616,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
           if (t == static_cast<int>(blockIdx.x) && kb == kb0) trace_mark(p, 3);
-          if (kb == kb0) trace_tile(p, jt, 0);
           const uint32_t sa = ptx::smem_addr(smem_a + stage * C::kABytes);
           const uint32_t sb = ptx::smem_addr(smem_b + stage * C::kBBytes);
 #pragma unroll
@@ -889,7 +632,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
         }
         ptx::mma_commit(&tmem_full[acc]);
         trace_mark(p, 4);
-        trace_tile(p, jt, 1);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -903,28 +645,20 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
     EpiTma e{smem_epi + (warp - 4) * p.epi_warp_bytes, xbar + kEpiBars * (warp - 4), 0, 0};
     int acc = 0;
     uint32_t acc_phase = 0;
-    int jt = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++jt) {
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
       const int tt = t / p.k_splits;
       const int z = tt / tiles_per_z;
       const int r = tt % tiles_per_z;
       const int mb = r % p.num_m_blocks;
       const int nb = r / p.num_m_blocks;
       const int row0 = mb * kBM + quad * 32;
-      if (BN >= 128 && p.epi_groups) epi_tile_prefetch_g<(BN >= 128 ? BN / 128 : 1)>(p, e, z, row0, nb * BN, half);
-      else epi_tile_prefetch<BN / 64>(p, e, z, row0, nb * BN, half);
+      epi_tile_prefetch<BN / 64>(p, e, z, row0, nb * BN, half);
       ptx::mbar_wait(&tmem_full[acc], acc_phase);
       ptx::tc_fence_after();
       if (warp == 4 && ptx::lane_id() == 0 && t == static_cast<int>(blockIdx.x)) trace_mark(p, 5);
-      if (warp == 4 && ptx::lane_id() == 0) trace_tile(p, jt, 2);
-      if (BN >= 128 && p.epi_groups)
-        epi_tile_tma_g<(BN >= 128 ? BN / 128 : 1)>(p, e, tmem_base + ((quad * 32) << 16) + acc * BN, z, row0,
-                                                   nb * BN, half);
-      else
-        epi_tile_tma<BN / 64>(p, e, tmem_base + ((quad * 32) << 16) + acc * BN, z, row0, nb * BN, half);
+      epi_tile_tma<BN / 64>(p, e, tmem_base + ((quad * 32) << 16) + acc * BN, z, row0, nb * BN, half);
       ptx::tc_fence_before();
       if (warp == 4 && ptx::lane_id() == 0) trace_mark(p, 6);
-      if (warp == 4 && ptx::lane_id() == 0) trace_tile(p, jt, 3);
       ptx::mbar_arrive(&tmem_empty[acc]);
       if (++acc == 2) {
         acc = 0;
@@ -992,7 +726,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
     ptx::tc_fence_after();
     ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
   }
-  if (threadIdx.x == 0) trace_exit(p);
+  if (threadIdx.x == 0) trace_mark(p, 7);
 }
 
 
@@ -1021,7 +755,7 @@ constexpr int kSmem = kSmemBudget;
 
 template <int BN2>
 __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __grid_constant__ GemmParams p) {
-  if (threadIdx.x == 0) trace_entry(p);
+  if (threadIdx.x == 0) trace_mark(p, 0);
   using Pc = PairCfg<BN2>;
   constexpr int kBN = Pc::kBN, kABytes = Pc::kABytes, kBBytes = Pc::kBBytes, kStageBytes = Pc::kStageBytes;
   const int S = p.stages;
@@ -1127,8 +861,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      int jt = 0;
-      for (int t = pair_id; t < p.num_tiles; t += n_pairs, ++jt) {
+      for (int t = pair_id; t < p.num_tiles; t += n_pairs) {
         const int ks = t % p.k_splits;
         const int kb0 = ks * p.kb_per_split;
         const int kb1 = min(p.num_k_blocks, kb0 + p.kb_per_split);
@@ -1139,7 +872,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
           if (t == pair_id && kb == kb0) trace_mark(p, 3);
-          if (kb == kb0) trace_tile(p, jt, 0);
           const uint32_t sa = ptx::smem_addr(smem_a + stage * kABytes);
           const uint32_t sb = ptx::smem_addr(smem_b + stage * kBBytes);
 #pragma unroll
@@ -1156,7 +888,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
         }
         ptx::mma_commit_2sm(&tmem_full[acc]);
         trace_mark(p, 4);
-        trace_tile(p, jt, 1);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -1169,28 +900,21 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
     EpiTma e{smem_epi + (warp - 4) * p.epi_warp_bytes, xbar + kEpiBars * (warp - 4), 0, 0};
     int acc = 0;
     uint32_t acc_phase = 0;
-    int jt = 0;
-    for (int t = pair_id; t < p.num_tiles; t += n_pairs, ++jt) {
+    for (int t = pair_id; t < p.num_tiles; t += n_pairs) {
       const int tt = t / p.k_splits;
       const int z = tt / tiles_per_z;
       const int r = tt % tiles_per_z;
       const int mb = r % p.num_m_blocks;
       const int nb = r / p.num_m_blocks;
       const int row0 = mb * 256 + rank * 128 + quad * 32;
-      if (p.epi_groups) epi_tile_prefetch_g<kBN / 128>(p, e, z, row0, nb * kBN, half);
-      else epi_tile_prefetch<kBN / 64>(p, e, z, row0, nb * kBN, half);
+      epi_tile_prefetch<kBN / 64>(p, e, z, row0, nb * kBN, half);
       ptx::mbar_wait(&tmem_full[acc], acc_phase);
       ptx::tc_fence_after();
       if (warp == 4 && lane == 0 && t == pair_id) trace_mark(p, 5);
-      if (warp == 4 && lane == 0) trace_tile(p, jt, 2);
-      if (p.epi_groups)
-        epi_tile_tma_g<kBN / 128>(p, e, tmem_base + ((quad * 32) << 16) + acc * kBN, z, row0, nb * kBN, half);
-      else
-        epi_tile_tma<kBN / 64>(p, e, tmem_base + ((quad * 32) << 16) + acc * kBN, z, row0, nb * kBN, half);
+      epi_tile_tma<kBN / 64>(p, e, tmem_base + ((quad * 32) << 16) + acc * kBN, z, row0, nb * kBN, half);
       ptx::tc_fence_before();
       __syncwarp();
       if (warp == 4 && lane == 0) trace_mark(p, 6);
-      if (warp == 4 && lane == 0) trace_tile(p, jt, 3);
       if (lane == 0) {
         if (leader) ptx::mbar_arrive(&tmem_empty[acc]);
         else ptx::mbar_arrive_cluster(&tmem_empty[acc], 0);
@@ -1260,7 +984,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
     ptx::tc_fence_after();
     ptx::tmem_dealloc_2sm<Pc::kTmemCols>(tmem_base);
   }
-  if (threadIdx.x == 0) trace_exit(p);
+  if (threadIdx.x == 0) trace_mark(p, 7);
 }
 
 // ---------------------------------------------------------------- host side
@@ -1304,7 +1028,7 @@ CUtensorMap make_map(const void* base, long long inner, long long outer, long lo
 // 5-D map over the epilogue addressing of C (gemm.h):
 //   [n % inner][m][n / inner][z % zdiv][z / zdiv], box 32 columns x 32 rows.
 // Size-1 dimensions get a consistent non-zero stride.
-CUtensorMap make_epi_map(const void* base, bool f32, const GemmDesc& d, int inner, int nhi, bool wide = false) {
+CUtensorMap make_epi_map(const void* base, bool f32, const GemmDesc& d, int inner, int nhi) {
   const long long esz = f32 ? 4 : 2;
   const long long zhi = d.batch / d.zdiv;
   const long long s1 = d.ldc;
@@ -1316,14 +1040,11 @@ CUtensorMap make_epi_map(const void* base, bool f32, const GemmDesc& d, int inne
                         static_cast<cuuint64_t>(d.zdiv), static_cast<cuuint64_t>(zhi)};
   cuuint64_t strides[4] = {static_cast<cuuint64_t>(s1 * esz), static_cast<cuuint64_t>(s2 * esz),
                            static_cast<cuuint64_t>(s3 * esz), static_cast<cuuint64_t>(s4 * esz)};
-  // 32 x 32 boxes (64- / 128-byte rows), or for the 64-column-group epilogue
-  // 64 bf16 columns (128-byte rows); every 128-byte row is SWIZZLE_128B
-  cuuint32_t box[5] = {static_cast<cuuint32_t>(wide && !f32 ? 64 : 32), 32, 1, 1, 1};
+  cuuint32_t box[5] = {32, 32, 1, 1, 1};
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-  const bool sw128 = f32 || wide;
   const CUresult rc = encode_fn()(&map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5,
                                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                  sw128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                                  f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (rc != CUDA_SUCCESS) throw std::runtime_error("dpl gemm: epilogue tensor map failed (" + std::to_string(rc) + ")");
   return map;
@@ -1517,42 +1238,8 @@ void GemmOp::prepare(const GemmDesc& d) {
     if ((d.epi & kBias) && (d.N % 4 != 0 || reinterpret_cast<uintptr_t>(d.bias) % 16 != 0)) ok = false;
     const int stage_bytes = two_sm ? (kBM + bn / 2) * kBK * 2 : (kBM + bn) * kBK * 2;
     const int ring = kSmemBudget - 2048;
-    static const bool groups_enabled = [] {  // DPL_GEMM_EPI64=0: the 32-column-chunk TMA epilogue
-      const char* e = std::getenv("DPL_GEMM_EPI64");
-      return !(e && e[0] == '0');
-    }();
-    const int c_inner = d.ndiv >= d.N ? d.N : d.ndiv;
-    // a 64-column box must not straddle a column split of the output addressing
-    // 64-column groups pay off for bf16 outputs without an extra tensor (qkv,
-    // plain dgrads: fewer, larger stores); the residual / activation-input /
-    // aux-output and fp32 paths keep the 32-column chunks, whose smaller
-    // staging leaves the ring a stage deeper (tools/gemm_graph_bench.py, r02)
-    const bool groups = groups_enabled && bn >= 128 && (c_inner == d.N || c_inner % 64 == 0) && kind == kOutBf16 &&
-                        !x_in && !aux;
     p.stages = std::min(kMaxStages, ring / stage_bytes);
-    static const int max_stages = [] {  // DPL_GEMM_MAX_STAGES: diagnostic cap on the ring depth
-      const char* e = std::getenv("DPL_GEMM_MAX_STAGES");
-      return e ? std::max(2, std::atoi(e)) : kMaxStages;
-    }();
-    if (ok && groups) {
-      // 64-column groups: one staging buffer (4 KB bf16 / 8 KB fp32), up to two
-      // extra-tensor group buffers (or one aux-out buffer), the bias slice
-      const int per_warp = bn / 128;
-      p.epi_groups = 1;
-      p.epi_out_bytes = kind == kOutBf16 ? kGroupBytes : 2 * kGroupBytes;
-      p.epi_nx = x_in ? std::min(2, per_warp) : (aux ? 1 : 0);
-      p.epi_tile_cols = bn;
-      const int bias_bytes = (d.epi & kBias) ? p.epi_tile_cols * 4 : 0;
-      for (;;) {
-        p.epi_warp_bytes = (p.epi_out_bytes + p.epi_nx * kGroupBytes + bias_bytes + 1023) & ~1023;
-        p.stages = std::min(kMaxStages, (ring - kEpiWarps * p.epi_warp_bytes) / stage_bytes);
-        if (p.stages >= 3 || p.epi_nx <= 1) break;
-        p.epi_nx = 1;
-      }
-      if (p.epi_nx == 0) p.epi_nx = 1;  // modulo base for the group index (no buffer is addressed)
-      if (p.stages < 3) p.epi_groups = 0;  // fall back to 32-column chunks
-    }
-    if (ok && !p.epi_groups) {
+    if (ok) {
       // carve the staging out of the ring, keeping >= 4 stages
       const int per_warp = bn / 64;  // chunks per epilogue warp per tile
       p.epi_out_bytes = kind == kOutBf16 ? 2048 : 4096;
@@ -1570,17 +1257,15 @@ void GemmOp::prepare(const GemmDesc& d) {
     }
     if (!ok) {
       p.epi_warp_bytes = 0;
-      p.epi_groups = 0;
       p.stages = std::min(kMaxStages, ring / stage_bytes);
     }
-    p.stages = std::min(p.stages, max_stages);
     if (ok) {
-      const int nhi = d.N / c_inner;
-      p.c_inner = c_inner;
-      p.epi_plain = c_inner == d.N && d.zdiv == 1;
-      p.tma_c = make_epi_map(d.C, kind != kOutBf16, d, c_inner, nhi, p.epi_groups != 0);
+      const int inner = d.ndiv >= d.N ? d.N : d.ndiv;
+      const int nhi = d.N / inner;
+      p.c_inner = inner;
+      p.tma_c = make_epi_map(d.C, kind != kOutBf16, d, inner, nhi);
       const void* x = x_in ? ((d.epi & kResid) ? d.resid : d.aux_in) : (aux ? d.aux_out : nullptr);
-      if (x) p.tma_x = make_epi_map(x, false, d, c_inner, nhi, p.epi_groups != 0);
+      if (x) p.tma_x = make_epi_map(x, false, d, inner, nhi);
       p.tma_epi = 1;
     }
     // without the TMA epilogue the column sums run as a separate pass
