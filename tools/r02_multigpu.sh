@@ -5,7 +5,7 @@
 # and the C5 XLNet-36 stand-in on the planner's plans.
 out=gpurun_out/r2mg; mkdir -p $out
 nvidia-smi topo -m > $out/topo.txt 2>&1
-timeout 1500 python -m pytest tests/test_executor_multigpu.py tests/test_cpp_executor_gpu.py -q --timeout 600 --timeout-method thread -p no:cacheprovider -rf > $out/pytest_mgpu.txt 2>&1
+timeout 1800 python -m pytest tests -m gpu -q --timeout 600 --timeout-method thread -p no:cacheprovider -rf > $out/pytest_mgpu.txt 2>&1
 tail -5 $out/pytest_mgpu.txt
 run() { # n tag args...
   local n=$1 tag=$2; shift 2
