@@ -602,6 +602,7 @@ def main():
     if not args.no_profile or args.plan == "planner":
         profiles[mb] = profile_model(model, mb) if rank == 0 else None
     if args.plan == "planner":
+        plan = None
         if rank == 0:
             plan, planner_info = plan_fixed_point(model, profiles, mb, cluster, M)
         plan = broadcast(plan, world)
