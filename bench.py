@@ -91,37 +91,54 @@ DEFAULTS = {"bert48": dict(micro_batches=8, slice=8, straight=False, global_batc
             "vgg19": dict(micro_batches=8, slice=24, straight=False)}
 
 
-def plan_fixed_point(model: dict, profiles: dict, mb: int, cluster: dict, m: int, max_iter: int = 4):
+def plan_fixed_point(model: dict, profiles: dict, mb: int, cluster: dict, m: int, max_iter: int = 5):
     """The host planner's plan (pipeplan.plan, bit-exact to the reference's
     planner.cpp:306-421) on B200 layer profiles taken at the plan's OWN
-    replica slice sizes: the reference cost model divides a stage's time by r
-    (model.cpp:228-230), which assumes perfect strong scaling of a layer over
-    smaller slices; so profile at mb, plan, profile every layer at the slice
-    its stage runs (times x r, slice_profile), re-plan, until the plan stops
-    changing.  At the fixed point the planner's est / sim L for its own plan
-    are computed from the times its replicas actually run at."""
+    replica slice sizes.  The reference cost model divides a stage's time by
+    r (model.cpp:228-230), i.e. assumes perfect strong scaling of a layer over
+    smaller slices, so: profile at mb and plan; profile every layer at the
+    slice its stage runs (times x r, slice_profile) and evaluate the plan on
+    that, its own profile (simulate_plan, planner.cpp:491-514); re-plan on
+    it; stop when the planner proposes a plan already evaluated.  Among the
+    proposals the one with the lowest self-consistent simulated L is run; its
+    est / sim L are the planner's model evaluated at the times its replicas
+    actually run at."""
     from paper_2007_01045_b200 import pipeplan
+
+    def key(pl):
+        return json.dumps([[s["layers"], s["gpus"]] for s in pl["stages"]])
+
     prof = profiles[mb]
+    cands = {}
     history = []
-    plan = None
-    for it in range(max_iter):
+    for _ in range(max_iter):
         res = pipeplan.plan(prof, cluster, m)["plan"]
-        history.append({"stages": [[s["layers"], s["gpus"]] for s in res["stages"]], "phi": res.get("phi"),
-                        "est_ms": res.get("est_latency_us", 0) / 1e3, "sim_ms": res.get("sim_latency_us", 0) / 1e3})
-        if plan is not None and [s["layers"] for s in res["stages"]] == [s["layers"] for s in plan["stages"]] and \
-                [s["gpus"] for s in res["stages"]] == [s["gpus"] for s in plan["stages"]]:
-            plan = res
+        k = key(res)
+        seen = k in cands
+        if not seen:
+            for st in res["stages"]:
+                size = -(-mb // len(st["gpus"]))
+                if size not in profiles:
+                    profiles[size] = profile_model(model, size)
+            own = slice_profile(profiles, res, mb)
+            seq = pipeplan.build_stage_sequence(res, own, cluster)
+            est = pipeplan.estimate_latency(seq, m)["total"]
+            sim = pipeplan.simulate_plan(res, own, cluster, m)["latency"]
+            cands[k] = (res, own, est, sim)
+        history.append({"stages": json.loads(k), "phi": res.get("phi"),
+                        "planner_est_ms": res.get("est_latency_us", 0) / 1e3,
+                        "planner_sim_ms": res.get("sim_latency_us", 0) / 1e3,
+                        "own_profile_est_ms": cands[k][2] * 1e3, "own_profile_sim_ms": cands[k][3] * 1e3})
+        if seen:
             break
-        plan = res
-        for st in plan["stages"]:
-            size = -(-mb // len(st["gpus"]))
-            if size not in profiles:
-                profiles[size] = profile_model(model, size)
-        prof = slice_profile(profiles, plan, mb)
+        prof = cands[k][1]
+    best = min(cands.values(), key=lambda c: c[3])
+    plan, own, est, sim = best
     fixed = len(history) >= 2 and history[-1]["stages"] == history[-2]["stages"]
-    return plan, {"iterations": history, "fixed_point": fixed, "per_gpu_memory_gb": cluster["per_gpu_memory_gb"],
-                  "est_latency_ms": plan.get("est_latency_us", 0) / 1e3,
-                  "sim_latency_ms": plan.get("sim_latency_us", 0) / 1e3}
+    return plan, {"iterations": history, "fixed_point": fixed, "candidates": len(cands),
+                  "per_gpu_memory_gb": cluster["per_gpu_memory_gb"],
+                  "est_latency_ms": est * 1e3, "sim_latency_ms": sim * 1e3,
+                  "profile": "B200 layer profiles at the plan's own replica slice sizes"}
 
 
 def make_plan(n: int, layers: int, straight: bool = False, kind: str = "") -> dict:

@@ -1,6 +1,6 @@
 // In-stage replica gradient AllReduce over peer memory (N4; PAPER.md:1248-1252,
-// cost model costmodel.cpp:41-50) and the flag signal used by every
-// cross-rank dependency of the step.
+// cost model costmodel.cpp:41-50).  The flag rounds around it are stream
+// memory operations issued by the executor (executor.cu signal / wait_flag).
 //
 // Replica j of an r-way stage owns chunk j of every parameter block.  When
 // all r replicas have signalled that a block's gradients are final, replica j
@@ -68,14 +68,6 @@ __global__ void __launch_bounds__(256) replica_sum_kernel(ReplicaPtrs ptrs, int 
   }
 }
 
-__global__ void signal_peers_kernel(FlagPtrs flags, int n, uint32_t value) {
-  // the stream's earlier work (a peer-memory kernel or copy) is complete;
-  // make it visible system-wide before each release store
-  __threadfence_system();
-  for (int i = 0; i < n; ++i)
-    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flags.f[i]), "r"(value) : "memory");
-}
-
 }  // namespace
 
 long long replica_chunk_lo(long long n, int j, int r) {
@@ -93,15 +85,6 @@ void replica_allreduce_chunk(const ReplicaPtrs& ptrs, int r, long long n, int j,
   const long long vec = (hi - lo + 3) / 4;
   const int blocks = static_cast<int>(std::min<long long>(64, std::max<long long>(1, (vec + 1023) / 1024)));
   launch_pdl(replica_sum_kernel, dim3(blocks), dim3(256), 0, s, ptrs, r, lo, hi);
-}
-
-void signal_peers(const FlagPtrs& flags, int n, uint32_t value, cudaStream_t s) {
-  if (n <= 0) return;
-  if (n > kMaxFlags) throw std::invalid_argument("dpl: too many flags in one signal");
-  count_launch();
-  signal_peers_kernel<<<1, 1, 0, s>>>(flags, n, value);
-  const cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) throw std::runtime_error(std::string("dpl: signal launch failed: ") + cudaGetErrorString(e));
 }
 
 }  // namespace dpl

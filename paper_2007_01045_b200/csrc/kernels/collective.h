@@ -1,4 +1,4 @@
-// Peer-memory replica AllReduce and flag signalling (collective.cu).
+// Peer-memory replica AllReduce (collective.cu).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -10,7 +10,6 @@
 namespace dpl {
 
 constexpr int kMaxReplicas = 16;
-constexpr int kMaxFlags = 32;
 
 // fp32 gradient buffers of the r replicas (replica order), each at the same
 // parameter-block offset; peers' buffers are peer mappings (CUDA IPC, or plain
@@ -18,17 +17,11 @@ constexpr int kMaxFlags = 32;
 struct ReplicaPtrs {
   float* g[kMaxReplicas];
 };
-struct FlagPtrs {
-  uint32_t* f[kMaxFlags];
-};
 
 // first element of replica j's chunk of an n-element block (256-byte aligned)
 long long replica_chunk_lo(long long n, int j, int r);
 // sum chunk j of the block over the r buffers (replica order) and store the
 // sum into all of them
 void replica_allreduce_chunk(const ReplicaPtrs& ptrs, int r, long long n, int j, cudaStream_t s);
-// one thread: system-scope release store of `value` into each flag, after the
-// stream's earlier work
-void signal_peers(const FlagPtrs& flags, int n, uint32_t value, cudaStream_t s);
 
 }  // namespace dpl

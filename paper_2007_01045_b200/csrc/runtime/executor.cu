@@ -69,6 +69,21 @@ using json::Value;
 
 typedef CUresult (*StreamValueFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 
+// cuStreamWriteValue32: the flag store of a hand-off as a stream memory
+// operation -- executed in stream order by the GPU front end, no SM needed
+// (a one-thread signal kernel can wait a whole persistent GEMM for a free SM)
+StreamValueFn write_value_fn() {
+  static StreamValueFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<StreamValueFn>(p);
+  }();
+  return fn;
+}
+
 StreamValueFn wait_value_fn() {
   static StreamValueFn fn = [] {
     void* p = nullptr;
@@ -922,6 +937,15 @@ void Executor::wait_flag(cudaStream_t s, uint32_t* flag, uint32_t value) {
 }
 
 void Executor::signal(cudaStream_t s, uint32_t* remote_flag, uint32_t value) {
+  // default flags (0): the write is ordered after the stream's earlier work
+  // and that work's memory writes (the hand-off copy) are visible first
+  if (memops_ok()) {
+    if (StreamValueFn fn = write_value_fn()) {
+      const CUresult rc =
+          fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(remote_flag), value, 0x0 /*DEFAULT*/);
+      if (rc == CUDA_SUCCESS) return;
+    }
+  }
   count_launch();
   signal_kernel<<<1, 1, 0, s>>>(remote_flag, value);
 }
@@ -1082,11 +1106,8 @@ void Executor::peer_allreduce(float* mine, const std::vector<float*>& peers, siz
   }
   for (int round = 0; round < 2; ++round) {
     if (round == 1) replica_allreduce_chunk(rp, r_, static_cast<long long>(n), rep_, reduce_);
-    FlagPtrs fp{};
-    int nf = 0;
     for (int p : group_)
-      if (p != rank_) fp.f[nf++] = flag_at(peer_recv_[p], p, ar_word(round, blk, rank_));
-    signal_peers(fp, nf, 1u, reduce_);
+      if (p != rank_) signal(reduce_, flag_at(peer_recv_[p], p, ar_word(round, blk, rank_)), 1u);
     for (int p : group_)
       if (p != rank_) wait_flag(reduce_, flags() + ar_word(round, blk, p), 1u);
   }

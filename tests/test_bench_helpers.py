@@ -125,3 +125,28 @@ def test_plan_fixed_point_replans_on_slice_profiles(monkeypatch):
     assert info["sim_latency_ms"] > 0
     for st in plan["stages"]:
         assert -(-8 // len(st["gpus"])) in profiles
+
+
+def test_plan_fixed_point_picks_the_self_consistent_best(monkeypatch):
+    """When re-planning on a plan's own slice profile proposes a different
+    plan (the ÷r model flatters small slices), the loop stops at the first
+    repeat and runs the proposal with the lowest L evaluated on its OWN slice
+    profile -- the L it reports."""
+    from paper_2007_01045_b200 import pipeplan
+
+    def fake_profile(model, samples, reps=5):
+        # strongly sub-linear: a 1-sample slice costs 60% of an 8-sample one
+        t = 100.0 * (0.55 + 0.45 * samples / 8)
+        return {"profile_batch_size": samples, "layers": [
+            {"fwd_time_us": t, "bwd_time_us": 2 * t, "activation_bytes": samples << 20, "param_bytes": 50 << 20}
+            for _ in range(24)]}
+
+    monkeypatch.setattr(bench, "profile_model", fake_profile)
+    profiles = {8: fake_profile(None, 8)}
+    cl = bench.b200_cluster(4, 180.0)
+    plan, info = bench.plan_fixed_point({"layers": 24}, profiles, 8, cl, 8)
+    sims = [it["own_profile_sim_ms"] for it in info["iterations"]]
+    assert info["sim_latency_ms"] == pytest.approx(min(sims))
+    own = bench.slice_profile(profiles, plan, 8)
+    assert pipeplan.simulate_plan(plan, own, cl, 8)["latency"] * 1e3 == pytest.approx(info["sim_latency_ms"])
+    assert len(info["iterations"]) <= 5
