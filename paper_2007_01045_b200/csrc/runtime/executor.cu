@@ -945,6 +945,7 @@ void Executor::signal(cudaStream_t s, uint32_t* remote_flag, uint32_t value) {
           fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(remote_flag), value, 0x0 /*DEFAULT*/);
       if (rc == CUDA_SUCCESS) return;
     }
+    memops_flag() = false;  // not available / not capturable: the capture is retried with kernels
   }
   count_launch();
   signal_kernel<<<1, 1, 0, s>>>(remote_flag, value);
