@@ -45,6 +45,12 @@ MODELS = {
     # a BERT-style encoder of that depth; its plans come from the host planner
     # on this model's own B200 profile (--plan planner), measured L vs est / sim L
     "xlnet36": dict(kind="bert", layers=36, hidden=1024, heads=16, ffn=4096, seq=512),
+    # C5's AmoebaNet-36 (Table I: 36 conv cells in 3 resolution
+    # stages, activations shrinking and parameters growing with depth) as a
+    # 36-layer conv net of the VGG family: 12 + 12 + 11 3x3 convs at widths
+    # 128 / 256 / 512 with a 2x2 pool after each stage, then the classifier
+    "amoebanet36": dict(kind="vgg", layers=36, image=128, width=128, fc=4096, classes=1000,
+                        convs=[12, 12, 11], mults=[1, 2, 4], fcs=1),
     # C3: VGG-19 on 224x224 images, 1000-class cross-entropy (convs as im2col + tcgen05 GEMM)
     "vgg19": dict(kind="vgg", layers=19, image=224, width=64, fc=4096, classes=1000),
 }
@@ -53,16 +59,19 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 
 
 def vgg_shapes(m: dict) -> list:
-    """The 19 VGG profile layers (csrc/runtime/layers.cu vgg_layer)."""
+    """The conv net's profile layers (csrc/runtime/layers.cu vgg_layer):
+    VGG-19 by default, or the groups / multipliers / FC count given."""
     out, hw, cin = [], m["image"], 3
-    for convs, mult in zip((2, 2, 4, 4, 4), (1, 2, 4, 8, 8)):
+    for convs, mult in zip(m.get("convs", (2, 2, 4, 4, 4)), m.get("mults", (1, 2, 4, 8, 8))):
         for c in range(convs):
             cout = m["width"] * mult
             out.append(dict(conv=True, h=hw, w=hw, cin=cin, cout=cout, pool=c == convs - 1))
             cin = cout
         hw //= 2
-    for fin, fout in ((hw * hw * cin, m["fc"]), (m["fc"], m["fc"]), (m["fc"], m["classes"])):
-        out.append(dict(conv=False, fin=fin, fout=fout))
+    fcs = m.get("fcs", 3)
+    for f in range(fcs):
+        out.append(dict(conv=False, fin=hw * hw * cin if f == 0 else m["fc"],
+                        fout=m["classes"] if f == fcs - 1 else m["fc"]))
     return out
 
 
@@ -88,6 +97,7 @@ DEFAULTS = {"bert48": dict(micro_batches=8, slice=8, straight=False, global_batc
             "gpt2-1.5b": dict(micro_batches=32, slice=1, straight=True),
             "mlp16": dict(micro_batches=8, slice=8, straight=False),
             "xlnet36": dict(micro_batches=16, slice=8, straight=False, global_batch=128),
+            "amoebanet36": dict(micro_batches=16, slice=8, straight=False, global_batch=128),
             "vgg19": dict(micro_batches=8, slice=24, straight=False)}
 
 
@@ -141,13 +151,13 @@ def plan_fixed_point(model: dict, profiles: dict, mb: int, cluster: dict, m: int
                   "profile": "B200 layer profiles at the plan's own replica slice sizes"}
 
 
-def make_plan(n: int, layers: int, straight: bool = False, kind: str = "") -> dict:
+def make_plan(n: int, layers: int, straight: bool = False, kind: str = "", conv_layers: int = 16) -> dict:
     if n == 1:
         return {"stages": [{"layers": [0, layers], "gpus": [0], "replication": 1}]}
     if kind == "vgg":  # C3: conv stage on N - N/4 GPUs, FC stage on N/4 (6 + 2 at N = 8)
         fc = max(1, n // 4)
-        return {"stages": [{"layers": [0, 16], "gpus": list(range(n - fc)), "replication": n - fc},
-                           {"layers": [16, layers], "gpus": list(range(n - fc, n)), "replication": fc}]}
+        return {"stages": [{"layers": [0, conv_layers], "gpus": list(range(n - fc)), "replication": n - fc},
+                           {"layers": [conv_layers, layers], "gpus": list(range(n - fc, n)), "replication": fc}]}
     if straight:
         cuts = [layers * k // n for k in range(n + 1)]
         return {"stages": [{"layers": [cuts[k], cuts[k + 1]], "gpus": [k], "replication": 1} for k in range(n)]}
@@ -624,7 +634,7 @@ def main():
             plan, planner_info = plan_fixed_point(model, profiles, mb, cluster, M)
         plan = broadcast(plan, world)
     else:
-        plan = make_plan(world, model["layers"], straight, model["kind"])
+        plan = make_plan(world, model["layers"], straight, model["kind"], sum(model.get("convs", [16])))
     if profiles and rank == 0:
         for st in plan["stages"]:
             size = -(-mb // len(st["gpus"]))

@@ -98,13 +98,19 @@ class Model:
     width: int = 64
     fc: int = 4096
     classes: int = 1000
+    # conv-net family (layers.h ModelSpec): convs per pool group, width multipliers, 3 FCs or the classifier only
+    convs: tuple = (2, 2, 4, 4, 4)
+    mults: tuple = (1, 2, 4, 8, 8)
+    fcs: int = 3
 
     @staticmethod
     def from_dict(d: dict) -> "Model":
         m = Model(kind=d["kind"], layers=d["layers"], hidden=d.get("hidden", 8), heads=d.get("heads", 16),
                   ffn=d.get("ffn", 4 * d.get("hidden", 8)), seq=d.get("seq", 1), causal=d.get("causal", False),
                   vocab=d.get("vocab", 0), image=d.get("image", 224), width=d.get("width", 64),
-                  fc=d.get("fc", 4096), classes=d.get("classes", 1000))
+                  fc=d.get("fc", 4096), classes=d.get("classes", 1000),
+                  convs=tuple(d.get("convs", (2, 2, 4, 4, 4))), mults=tuple(d.get("mults", (1, 2, 4, 8, 8))),
+                  fcs=d.get("fcs", 3))
         if m.kind == "mlp":
             m.seq = 1
         if m.kind == "gpt":
@@ -117,15 +123,18 @@ class Model:
 def vgg_layer(model: Model, l: int) -> dict:
     """Shape of VGG profile layer l (csrc/runtime/layers.cu vgg_layer)."""
     hw, cin, idx = model.image, 3, 0
-    for g, (convs, mult) in enumerate(zip((2, 2, 4, 4, 4), (1, 2, 4, 8, 8))):
+    for g, (convs, mult) in enumerate(zip(model.convs, model.mults)):
         for c in range(convs):
             cout = model.width * mult
             if idx == l:
                 return dict(conv=True, h=hw, w=hw, cin=cin, cout=cout, kp=(9 * cin + 7) // 8 * 8, pool=c == convs - 1)
             cin, idx = cout, idx + 1
         hw //= 2
-    fins, fouts = (hw * hw * cin, model.fc, model.fc), (model.fc, model.fc, model.classes)
-    return dict(conv=False, fin=fins[l - 16], fout=fouts[l - 16], relu=l != 18)
+    f = l - sum(model.convs)  # FC index
+    if not 0 <= f < model.fcs:
+        raise IndexError("vgg_layer: layer index")
+    return dict(conv=False, fin=hw * hw * cin if f == 0 else model.fc,
+                fout=model.classes if f == model.fcs - 1 else model.fc, relu=f != model.fcs - 1)
 
 
 def elems_per_sample(model: Model, l: int) -> int:

@@ -420,9 +420,16 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
   if (m.contains("width")) spec_.width = static_cast<int>(m.at("width").as_int());
   if (m.contains("fc")) spec_.fc = static_cast<int>(m.at("fc").as_int());
   if (m.contains("classes")) spec_.classes = static_cast<int>(m.at("classes").as_int());
+  if (m.contains("convs")) spec_.convs = m.at("convs").as_int_vector();
+  if (m.contains("mults")) spec_.mults = m.at("mults").as_int_vector();
+  if (m.contains("fcs")) spec_.fcs = static_cast<int>(m.at("fcs").as_int());
   if (spec_.kind == "vgg") {
-    if (spec_.layers != 19 || spec_.image % 32 || spec_.width % 8 || spec_.classes % 8 || spec_.fc % 8)
-      throw std::invalid_argument("dpl exec: vgg needs 19 layers, image % 32 == 0, width / fc / classes % 8 == 0");
+    const int pools = static_cast<int>(spec_.convs.size());
+    if (spec_.convs.size() != spec_.mults.size() || spec_.convs.empty() || (spec_.fcs != 1 && spec_.fcs != 3) ||
+        spec_.layers != spec_.conv_layers() + spec_.fcs || spec_.image % (1 << pools) || spec_.width % 8 ||
+        spec_.classes % 8 || spec_.fc % 8)
+      throw std::invalid_argument("dpl exec: conv net needs layers == sum(convs) + fcs (1 or 3), image divisible by "
+                                  "2^groups, width / fc / classes % 8 == 0");
     spec_.seq = 1;
     spec_.hidden = spec_.classes;
   }

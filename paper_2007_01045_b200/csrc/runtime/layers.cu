@@ -356,32 +356,30 @@ class TransformerLayer final : public Layer {
 // Gradient contract: every VGG layer takes dL/d(its output) and returns
 // dL/d(its input) (ReLU' and the pool backward are applied inside).
 VggLayerShape vgg_layer(const ModelSpec& spec, int l) {
-  static const int kConvs[5] = {2, 2, 4, 4, 4};
-  static const int kMult[5] = {1, 2, 4, 8, 8};
   VggLayerShape v;
   int idx = 0, hw = spec.image, cin = 3;
-  for (int g = 0; g < 5; ++g) {
-    for (int c = 0; c < kConvs[g]; ++c, ++idx) {
-      const int cout = spec.width * kMult[g];
+  for (size_t g = 0; g < spec.convs.size(); ++g) {
+    for (int c = 0; c < spec.convs[g]; ++c, ++idx) {
+      const int cout = spec.width * spec.mults[g];
       if (idx == l) {
         v.conv = true;
         v.h = v.w = hw;
         v.cin = cin;
         v.cout = cout;
         v.kp = (9 * cin + 7) / 8 * 8;
-        v.pool = c == kConvs[g] - 1;
+        v.pool = c == spec.convs[g] - 1;
         return v;
       }
       cin = cout;
     }
     hw /= 2;
   }
-  const int flat = hw * hw * cin;
-  const int fins[3] = {flat, spec.fc, spec.fc}, fouts[3] = {spec.fc, spec.fc, spec.classes};
-  if (l < 16 || l > 18) throw std::out_of_range("vgg_layer: layer index");
-  v.fin = fins[l - 16];
-  v.fout = fouts[l - 16];
-  v.relu = l != 18;
+  const int flat = hw * hw * cin, nc = spec.conv_layers();
+  if (l < nc || l >= nc + spec.fcs) throw std::out_of_range("vgg_layer: layer index");
+  const int f = l - nc;  // FC index
+  v.fin = f == 0 ? flat : spec.fc;
+  v.fout = f == spec.fcs - 1 ? spec.classes : spec.fc;
+  v.relu = f != spec.fcs - 1;
   return v;
 }
 
@@ -557,7 +555,7 @@ std::unique_ptr<Layer> make_layer(const ModelSpec& spec, int global_index) {
   if (spec.kind == "mlp") return std::make_unique<MlpLayer>(spec, global_index);
   if (spec.kind == "bert" || spec.kind == "gpt") return std::make_unique<TransformerLayer>(spec, global_index);
   if (spec.kind == "vgg") {
-    if (global_index < 16) return std::make_unique<ConvLayer>(spec, global_index);
+    if (global_index < spec.conv_layers()) return std::make_unique<ConvLayer>(spec, global_index);
     return std::make_unique<FcLayer>(spec, global_index);
   }
   throw std::invalid_argument("dpl: unknown model kind '" + spec.kind + "'");

@@ -37,8 +37,18 @@ struct ModelSpec {
   int vocab = 0;  // > 0: GPT language model (token ids in, cross-entropy out)
   // VGG-19 (kind "vgg", config C3): NHWC images image x image x 3, conv
   // widths width x {1, 2, 4, 8, 8} (2, 2, 4, 4, 4 convs, 2x2 max pool after
-  // each group), FC fc -> fc -> classes; cross-entropy over classes
+  // each group), FC fc -> fc -> classes; cross-entropy over classes.
+  // The same family with other groups ("convs" per group, width "mults",
+  // "fcs" = 3: fc, fc, classes or 1: classes only) gives the deeper conv
+  // stand-ins (C5's AmoebaNet-36 shape: 12 + 12 + 11 convs + classifier).
   int image = 224, width = 64, fc = 4096, classes = 1000;
+  std::vector<int> convs = {2, 2, 4, 4, 4}, mults = {1, 2, 4, 8, 8};
+  int fcs = 3;
+  int conv_layers() const {
+    int n = 0;
+    for (int c : convs) n += c;
+    return n;
+  }
 };
 
 // One VGG profile layer: a 3x3 conv (+ReLU, + optional 2x2 pool) or an FC.

@@ -25,7 +25,7 @@ def test_flops_per_sample_match_survey():
 def test_plans_cover_the_layers(n):
     for name, model in bench.MODELS.items():
         straight = bench.DEFAULTS[name]["straight"]
-        plan = bench.make_plan(n, model["layers"], straight, model["kind"])
+        plan = bench.make_plan(n, model["layers"], straight, model["kind"], sum(model.get("convs", [16])))
         gpus = [g for s in plan["stages"] for g in s["gpus"]]
         assert sorted(gpus) == list(range(n))
         assert plan["stages"][0]["layers"][0] == 0 and plan["stages"][-1]["layers"][1] == model["layers"]
@@ -150,3 +150,22 @@ def test_plan_fixed_point_picks_the_self_consistent_best(monkeypatch):
     own = bench.slice_profile(profiles, plan, 8)
     assert pipeplan.simulate_plan(plan, own, cl, 8)["latency"] * 1e3 == pytest.approx(info["sim_latency_ms"])
     assert len(info["iterations"]) <= 5
+
+
+def test_amoebanet_stand_in_shapes():
+    """C5's AmoebaNet-36 stand-in: 36 profile layers, 3 resolution stages with
+    growing channels (parameters grow, activations shrink with depth)."""
+    m = bench.MODELS["amoebanet36"]
+    v = bench.vgg_shapes(m)
+    assert len(v) == m["layers"] == 36 and sum(x["conv"] for x in v) == 35
+    assert [v[i]["cout"] for i in (0, 12, 24)] == [128, 256, 512]
+    assert v[11]["pool"] and v[23]["pool"] and v[34]["pool"]
+    assert v[35] == dict(conv=False, fin=16 * 16 * 512, fout=1000)
+    from oracle.executor_ref import Model, vgg_layer
+    om = Model.from_dict(m)
+    for l in range(36):
+        o = vgg_layer(om, l)
+        if v[l]["conv"]:
+            assert (o["h"], o["cin"], o["cout"], o["pool"]) == (v[l]["h"], v[l]["cin"], v[l]["cout"], v[l]["pool"])
+        else:
+            assert (o["fin"], o["fout"], o["relu"]) == (v[l]["fin"], v[l]["fout"], False)

@@ -131,30 +131,45 @@ def test_scheduled_equals_full_batch_vgg(plan):
         assert np.allclose(b.grads[key], g, rtol=1e-9, atol=1e-13), key
 
 
-def test_vgg_manual_backward_matches_autograd():
+# the conv-net family with other groups (C5's AmoebaNet-36 stand-in shape, small)
+CONV36 = dict(kind="vgg", layers=8, image=16, width=8, fc=32, classes=16, convs=[3, 2, 2], mults=[1, 2, 4], fcs=1)
+
+
+def test_scheduled_equals_full_batch_conv_family():
+    plan = {"stages": [{"layers": [0, 4], "gpus": [0, 1]}, {"layers": [4, 8], "gpus": [2]}]}
+    a = full_batch_step(CONV36, 8)
+    b = scheduled_step(CONV36, plan, 2, 8)
+    assert abs(a.loss - b.loss) <= 1e-12 * abs(a.loss)
+    for key, g in a.grads.items():
+        assert np.allclose(b.grads[key], g, rtol=1e-9, atol=1e-13), key
+
+
+@pytest.mark.parametrize("cfg", [VGG, CONV36], ids=["vgg19", "conv-family"])
+def test_vgg_manual_backward_matches_autograd(cfg):
     """The oracle's conv (im2col, (kh, kw, c) order, zero-padded K), pool
     (first max), ReLU and FC backward equal torch autograd in fp64."""
     import torch
     import torch.nn.functional as F
     from oracle.executor_ref import class_ce, layer_backward, vgg_batch, vgg_layer
-    m = Model.from_dict(VGG)
+    m = Model.from_dict(cfg)
     n = 2
+    L = m.layers
     x0, lab = vgg_batch(m, 5, 0, n)
-    params = {l: {k: v.astype(np.float64) for k, v in init_layer(m, l, 5).items()} for l in range(19)}
+    params = {l: {k: v.astype(np.float64) for k, v in init_layer(m, l, 5).items()} for l in range(L)}
     x = x0.astype(np.float64)
     caches = []
-    for l in range(19):
+    for l in range(L):
         x, c = layer_forward(m, l, params[l], x, n)
         caches.append(c)
     lsum, dy = class_ce(x, lab, 1.0 / n, lambda a: a)
     grads = {}
-    for l in reversed(range(19)):
+    for l in reversed(range(L)):
         dy, g = layer_backward(m, l, params[l], caches[l], dy, n, need_dx=l > 0)
         grads[l] = g
     # torch reference in NCHW
-    tp = {l: {k: torch.tensor(v, requires_grad=True) for k, v in params[l].items()} for l in range(19)}
-    t = torch.tensor(x0, dtype=torch.float64).view(n, 32, 32, 3).permute(0, 3, 1, 2)
-    for l in range(19):
+    tp = {l: {k: torch.tensor(v, requires_grad=True) for k, v in params[l].items()} for l in range(L)}
+    t = torch.tensor(x0, dtype=torch.float64).view(n, m.image, m.image, 3).permute(0, 3, 1, 2)
+    for l in range(L):
         v = vgg_layer(m, l)
         if v["conv"]:
             w = tp[l]["W"][:, :9 * v["cin"]].view(v["cout"], 3, 3, v["cin"]).permute(0, 3, 1, 2)
@@ -170,7 +185,7 @@ def test_vgg_manual_backward_matches_autograd():
     loss = F.cross_entropy(t, torch.tensor(lab), reduction="mean")
     loss.backward()
     assert abs(loss.item() - lsum / n) < 1e-10
-    for l in range(19):
+    for l in range(L):
         for k in ("W", "b"):
             got = grads[l][k]
             want = tp[l][k].grad.numpy()

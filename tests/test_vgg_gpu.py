@@ -51,3 +51,33 @@ def test_vgg_profile_and_width64(cuda):
     # with 4 samples a few ReLU sign flips in the 128-wide FCs give ~4% there
     check_grads(ex, emu, exact, range(19), "vgg", 19, depth_rtol=0.02, base_rtol=0.05)
     ex.close()
+
+
+# the conv-net family beyond VGG-19's group table (C5's AmoebaNet-36 stand-in
+# shape, small): 3 + 2 + 2 convs at 64 / 128 / 256 channels, classifier only
+CONV = dict(kind="vgg", layers=8, image=16, width=64, fc=32, classes=16, convs=[3, 2, 2], mults=[1, 2, 4], fcs=1)
+
+
+@pytest.mark.parametrize("plan", [
+    {"stages": [{"layers": [0, 8], "gpus": [0], "replication": 1}]},
+    {"stages": [{"layers": [0, 5], "gpus": [0, 1]}, {"layers": [5, 8], "gpus": [2]}]},
+], ids=["one-gpu", "2x1-ranks-on-one-gpu"])
+def test_conv_family_step_matches_oracle(cuda, plan):
+    from paper_2007_01045_b200.runtime import Executor, LocalRanks
+    exact = full_batch_step(CONV, 8)
+    emu = full_batch_step(CONV, 8, bf16=True)
+    if len(plan["stages"]) == 1:
+        ranks = [Executor(CONV, plan, 2, 8, apply=False)]
+        losses = [ranks[0].step()]
+        close = ranks[0].close
+    else:
+        group = LocalRanks(CONV, plan, 2, 8, apply=False)
+        ranks, losses, close = group.ranks, group.step(), group.close
+    try:
+        check_loss(losses[-1], emu, exact)
+        for rank, ex in enumerate(ranks):
+            stage = next(s for s in plan["stages"] if rank in s["gpus"])
+            # pool-argmax flips toward the input, as for the wide VGG above
+            check_grads(ex, emu, exact, range(*stage["layers"]), "vgg", 8, depth_rtol=0.02, base_rtol=0.05)
+    finally:
+        close()
