@@ -362,7 +362,7 @@ class Executor {
   // the replica group and apply on the reduce stream
   void reduce_apply(cudaEvent_t ready, size_t off, size_t n, int blk);
   // peer-memory AllReduce of one block over the replica group on the reduce stream
-  void peer_allreduce(float* mine, const std::vector<float*>& peers, size_t n, int blk);
+  void peer_allreduce(const std::vector<float*>& peers, size_t n, int blk);
   double flops_per_step_ = 0.0;
 
   // --- helpers
@@ -1091,7 +1091,7 @@ void Executor::reduce_apply(cudaEvent_t ready, size_t off, size_t n, int blk) {
   if (r_ > 1 && peer_ar_) {
     std::vector<float*> peers(r_);
     for (int j = 0; j < r_; ++j) peers[j] = peer_g32_[group_[j]] + off;
-    peer_allreduce(g32_ + off, peers, n, blk);
+    peer_allreduce(peers, n, blk);
   } else if (r_ > 1) {
     if (!comm_) throw std::runtime_error("dpl exec: replicated stage without an NCCL communicator");
     DPL_NCCL(ncclAllReduce(g32_ + off, g32_ + off, n, ncclFloat, ncclSum, comm_, reduce_));
@@ -1104,8 +1104,7 @@ void Executor::reduce_apply(cudaEvent_t ready, size_t off, size_t n, int blk) {
 // that its block is final, replica j reduces chunk j across the group and
 // stores the sum into every replica, and each replica waits until all
 // chunks have landed before anything (SGD) reads the block.
-void Executor::peer_allreduce(float* mine, const std::vector<float*>& peers, size_t n, int blk) {
-  (void)mine;
+void Executor::peer_allreduce(const std::vector<float*>& peers, size_t n, int blk) {
   if (static_cast<int>(peers.size()) != r_) throw std::logic_error("dpl exec: replica pointers");
   ReplicaPtrs rp{};
   for (int j = 0; j < r_; ++j) {
@@ -1198,7 +1197,7 @@ void Executor::enqueue_step(const void* host_input, const void* host_target) {
       for (int j = 0; j < r_; ++j)
         peers[j] = group_[j] == rank_ ? loss_acc_
                                       : reinterpret_cast<float*>(peer_recv_[group_[j]] + loss_off(group_[j]));
-      peer_allreduce(loss_acc_, peers, 1, L() + 2);
+      peer_allreduce(peers, 1, L() + 2);
     } else {
       if (!comm_) throw std::runtime_error("dpl exec: replicated stage without an NCCL communicator");
       DPL_NCCL(ncclAllReduce(loss_acc_, loss_acc_, 1, ncclFloat, ncclSum, comm_, reduce_));
