@@ -739,6 +739,8 @@ def main():
             if k["kernel"] == "gemm_bf16_tcgen05":
                 g_flops += k.get("flops", 0.0) or k.get("tflops", 0.0) * 1e12 * k["seconds"]
                 g_secs += k["seconds"]
+            elif k["kernel"] == "gemm_split_epilogue":  # the bf16 epilogue pass of split-K GEMMs is GEMM time
+                g_secs += k["seconds"]
     if g_secs == 0.0:
         g_flops = sum(p["prof"]["flops"] for p in profs)
         g_secs = sum(p["prof"]["seconds"] for p in profs)

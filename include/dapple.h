@@ -82,6 +82,12 @@ typedef struct dpl_gemm_desc {
    * MN-major (K = n*h*w, N = 9c); loaded by TMA in im2col mode, no column matrix */
   const void* conv_x;
   int conv_operand, conv_n, conv_h, conv_w, conv_c;
+  /* optional zeroed fp32 scratch (>= M*N*4 bytes, left zeroed): a bf16-output
+   * GEMM that would leave most CTA pairs idle runs as split-K fp32 reduce-add
+   * into it plus a bf16 epilogue pass (bias / residual / gelu' only).
+   * NULL = never split (the executor passes its stage scratch). */
+  float* split_ws;
+  size_t split_ws_bytes;
 } dpl_gemm_desc;
 
 #define DPL_EPI_OUT_BF16 0u

@@ -33,6 +33,7 @@ class GemmDesc(ctypes.Structure):
         ("trace", ctypes.c_void_p), ("colsum", ctypes.c_void_p),
         ("conv_x", ctypes.c_void_p), ("conv_operand", ctypes.c_int), ("conv_n", ctypes.c_int),
         ("conv_h", ctypes.c_int), ("conv_w", ctypes.c_int), ("conv_c", ctypes.c_int),
+        ("split_ws", ctypes.c_void_p), ("split_ws_bytes", ctypes.c_size_t),
     ]
 
 

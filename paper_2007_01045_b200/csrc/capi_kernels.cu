@@ -89,6 +89,8 @@ int dpl_k_gemm(const dpl_gemm_desc* d, void* stream) {
     g.conv_h = d->conv_h;
     g.conv_w = d->conv_w;
     g.conv_c = d->conv_c;
+    g.split_ws = d->split_ws;
+    g.split_ws_bytes = d->split_ws_bytes;
     dpl::GemmOp op;
     op.prepare(g);
     op.launch(static_cast<cudaStream_t>(stream));

@@ -442,6 +442,59 @@ __global__ void __launch_bounds__(256, 4) colsum_acc_kernel(const __nv_bfloat16*
   }
 }
 
+// ------------------------------------------------------------ split-K epilogue
+// The same GELU derivative as the GEMM epilogue (gemm_tcgen05.cu dgelu_f:
+// tanh form, tanh on the SFU), so a split GEMM rounds like an unsplit one.
+__device__ __forceinline__ float split_dgelu(float x) {
+  constexpr float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  const float x2 = x * x;
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(k0 * fmaf(k1 * x, x2, x)));
+  return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * k0 * fmaf(3.0f * k1, x2, 1.0f);
+}
+
+template <bool kBiasT, bool kResidT, bool kDGeluT>
+__global__ void __launch_bounds__(256) split_epilogue_kernel(float* __restrict__ acc, __nv_bfloat16* __restrict__ c,
+                                                             long long ldc, int m, int n, float alpha,
+                                                             const float* __restrict__ bias,
+                                                             const __nv_bfloat16* __restrict__ resid,
+                                                             const __nv_bfloat16* __restrict__ aux_in) {
+  ptx::pdl_wait();
+  const int nv = n / 8;
+  const long long total = static_cast<long long>(m) * nv;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int row = static_cast<int>(i / nv), col = static_cast<int>(i % nv) * 8;
+    float* a = acc + static_cast<long long>(row) * n + col;
+    float v[8];
+    load8(a, v);
+    *reinterpret_cast<float4*>(a) = make_float4(0.f, 0.f, 0.f, 0.f);  // scratch left zero
+    *reinterpret_cast<float4*>(a + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+    const long long off = static_cast<long long>(row) * ldc + col;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] *= alpha;
+    if (kBiasT) {
+      float b[8];
+      ldg8(bias + col, b);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] += b[e];
+    }
+    if (kResidT) {
+      float r[8];
+      load8(resid + off, r);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] += r[e];
+    }
+    if (kDGeluT) {
+      float z[8];
+      load8(aux_in + off, z);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] *= split_dgelu(z[e]);
+    }
+    store8(c + off, v);
+  }
+}
+
 // ------------------------------------------------------------ loss
 // loss_acc += sum (y - t)^2 ; dy = (y - t) * grad_scale  (grad_scale = 2/numel)
 __global__ void mse_kernel(const __nv_bfloat16* __restrict__ y, const __nv_bfloat16* __restrict__ t,
@@ -626,6 +679,29 @@ void colsum_acc(const void* dy, float* db, int rows, int cols, cudaStream_t s) {
   const int rpb = (rows + gy - 1) / gy;
   gy = (rows + rpb - 1) / rpb;
   launch_pdl(colsum_acc_kernel, dim3(gx, gy), dim3(256), 0, s, static_cast<const __nv_bfloat16*>(dy), db, rows, cols, rpb);
+}
+
+void split_epilogue(float* acc, void* c, long long ldc, int m, int n, float alpha, const float* bias,
+                    const void* resid, const void* aux_in, uint32_t epi, cudaStream_t s) {
+  constexpr uint32_t kB = 1u << 2, kR = 1u << 8, kDG = 1u << 6;  // gemm.h kBias / kResid / kDGelu
+  if (n % 8 || ldc % 8) throw std::invalid_argument("split_epilogue: N and ldc must be multiples of 8");
+  if (epi & ~(kB | kR | kDG)) throw std::invalid_argument("split_epilogue: unsupported epilogue flags");
+  count_launch();
+  TimedLaunch timed_("gemm_split_epilogue", s);
+  const int grid = grid_for(static_cast<long long>(m) * n / 8, 256);
+  auto* pc = static_cast<__nv_bfloat16*>(c);
+  const auto* pr = static_cast<const __nv_bfloat16*>(resid);
+  const auto* pa = static_cast<const __nv_bfloat16*>(aux_in);
+  auto go = [&](auto kernel) { launch_pdl(kernel, dim3(grid), dim3(256), 0, s, acc, pc, ldc, m, n, alpha, bias, pr, pa); };
+  const bool b = epi & kB, r = epi & kR, dg = epi & kDG;
+  if (!b && !r && !dg) go(split_epilogue_kernel<false, false, false>);
+  else if (b && !r && !dg) go(split_epilogue_kernel<true, false, false>);
+  else if (b && r && !dg) go(split_epilogue_kernel<true, true, false>);
+  else if (!b && r && !dg) go(split_epilogue_kernel<false, true, false>);
+  else if (!b && !r && dg) go(split_epilogue_kernel<false, false, true>);
+  else if (b && !r && dg) go(split_epilogue_kernel<true, false, true>);
+  else if (!b && r && dg) go(split_epilogue_kernel<false, true, true>);
+  else go(split_epilogue_kernel<true, true, true>);
 }
 
 void mse_loss(const void* y, const void* t, void* dy, float* loss_acc, long long n, float grad_scale, cudaStream_t s) {

@@ -65,6 +65,10 @@ struct GemmDesc {
   //   conv_operand 2: B[K = n*h*w][N = 9c] are its im2col columns (MN-major, B unused)
   const void* conv_x = nullptr;
   int conv_operand = 0, conv_n = 0, conv_h = 0, conv_w = 0, conv_c = 0;
+  // fp32 scratch for split-K of bf16-output GEMMs with too few tiles (host
+  // side only; the GemmCache fills it in): zero on entry and left zero
+  float* split_ws = nullptr;
+  size_t split_ws_bytes = 0;
 };
 
 // Device-visible launch parameters (one per prepared GEMM).
@@ -117,10 +121,15 @@ class GemmOp {
   double flops() const { return 2.0 * params_.M * params_.N * static_cast<double>(params_.K) * params_.batch; }
   const GemmParams& params() const { return params_; }
   bool ready() const { return bn_ != 0; }
+  bool split_bf16() const { return split_ != nullptr; }
 
  private:
   GemmParams params_{};
   bool colsum_fallback_ = false;
+  // split-K of a bf16-output GEMM: the fp32 reduce-add GEMM into the cache's
+  // scratch, then split_epilogue (bias / residual / act' -> bf16, scratch zeroed)
+  std::shared_ptr<GemmOp> split_;
+  GemmDesc split_desc_{};
   int bn_ = 0;
   int grid_ = 0;
   size_t smem_ = 0;
@@ -183,6 +192,10 @@ class GemmCache {
   GemmProfile profile;
   size_t size() const;
   double flops_run = 0.0;  // flops launched through run() (accounting)
+  // zero-initialised fp32 scratch shared by this cache's split-K bf16 GEMMs
+  // (they all run on one stream, one after another); null disables them
+  float* split_ws = nullptr;
+  size_t split_ws_bytes = 0;
 
  private:
   struct Impl;

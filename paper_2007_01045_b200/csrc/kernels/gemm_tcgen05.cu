@@ -1101,8 +1101,52 @@ int num_sms() {
   return n;
 }
 
+// Split-K for a bf16-output GEMM that leaves most CTA pairs idle (e.g. the
+// N = 1024 / 1600 GEMMs of 1024- and 2048-row replica slices: 16-32 pair
+// tiles for 74 pairs): the fp32 reduce-add GEMM (the wgrad path, split-K
+// built in) accumulates into the cache's zeroed scratch, then
+// split_epilogue applies bias / residual / act' and writes bf16.
+static bool split_bf16_candidate(const GemmDesc& d) {
+  static const bool enabled = [] {  // DPL_GEMM_SPLIT_BF16=0: never
+    const char* e = std::getenv("DPL_GEMM_SPLIT_BF16");
+    return !(e && e[0] == '0');
+  }();
+  if (!enabled || !d.split_ws || (d.epi & kOutMask) != kOutBf16 || d.batch != 1 || d.zdiv != 1 ||
+      d.ndiv < d.N || d.conv_operand || d.trace || d.force_bn || d.force_1sm)
+    return false;
+  if (d.epi & ~static_cast<uint32_t>(kBias | kResid | kDGelu)) return false;
+  if (d.N % 8 || d.ldc % 8 || static_cast<size_t>(d.M) * d.N * 4 > d.split_ws_bytes) return false;
+  if (d.M < 256 || d.N <= 128) return false;  // the CTA-pair kernel's shapes only
+  const long long pair_tiles = static_cast<long long>((d.M + 255) / 256) * ((d.N + 255) / 256);
+  const int kblocks = (d.K + 63) / 64;
+  const int pairs = num_sms() / 2;
+  // at most half the pairs busy, and enough K to split in >= 2 x 8 blocks
+  return pair_tiles * 2 <= pairs && kblocks >= 16;
+}
+
 void GemmOp::prepare(const GemmDesc& d) {
   if (d.M <= 0 || d.N <= 0 || d.K <= 0 || d.batch <= 0) throw std::invalid_argument("dpl gemm: empty problem");
+  if (split_bf16_candidate(d)) {
+    GemmDesc inner = d;
+    inner.C = d.split_ws;
+    inner.ldc = d.N;
+    inner.epi = kOutF32Acc;
+    inner.alpha = 1.0f;
+    inner.bias = nullptr;
+    inner.resid = nullptr;
+    inner.aux_in = nullptr;
+    inner.aux_out = nullptr;
+    inner.colsum = nullptr;
+    inner.split_ws = nullptr;
+    split_ = std::make_shared<GemmOp>();
+    split_->prepare(inner);
+    split_desc_ = d;
+    params_ = split_->params_;
+    bn_ = split_->bn_;
+    grid_ = split_->grid_;
+    smem_ = split_->smem_;
+    return;
+  }
   if (d.ndiv % 32 != 0) throw std::invalid_argument("dpl gemm: ndiv must be a multiple of 32");
   int bn = d.force_bn;
   if (bn == 0 && (d.epi & kOutMask) == kOutF32Acc && d.N > 128) bn = 256;  // split-K fills the machine
@@ -1304,8 +1348,11 @@ struct GemmCache::Impl {
   std::unordered_map<std::string, std::unique_ptr<GemmOp>> ops;
 };
 
-const GemmOp& GemmCache::get(const GemmDesc& d) {
+const GemmOp& GemmCache::get(const GemmDesc& dd) {
   if (!impl_) impl_ = std::make_shared<Impl>();
+  GemmDesc d = dd;  // this cache's split-K scratch (not part of the key: one per cache)
+  d.split_ws = split_ws;
+  d.split_ws_bytes = split_ws_bytes;
   // explicit field-wise key: no padding bytes
   const long long f[] = {d.M, d.N, d.K, d.batch,
                          static_cast<long long>(reinterpret_cast<uintptr_t>(d.A)), d.lda, d.a_batch_stride,
@@ -1371,6 +1418,12 @@ void GemmCache::run(const GemmDesc& d, cudaStream_t s) {
 }
 
 void GemmOp::launch(cudaStream_t stream) const {
+  if (split_) {
+    split_->launch_kernel(stream);
+    const GemmDesc& d = split_desc_;
+    split_epilogue(d.split_ws, d.C, d.ldc, d.M, d.N, d.alpha, d.bias, d.resid, d.aux_in, d.epi, stream);
+    return;
+  }
   launch_kernel(stream);
   if (colsum_fallback_)  // kColSum without the TMA epilogue: a column-sum pass over C
     colsum_acc(params_.C, params_.colsum, params_.M, params_.N, stream);

@@ -605,6 +605,13 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
     ctx_.t_qkv = static_cast<bf16*>(mem_.alloc(RH * 3 * 2));
     ctx_.t_f = static_cast<bf16*>(mem_.alloc(static_cast<size_t>(ctx_.rows) * spec_.ffn * 2));
   }
+  if (spec_.kind != "vgg") {
+    // scratch for the split-K bf16 GEMMs of small replica slices (gemm_tcgen05.cu
+    // split_bf16_candidate): one [rows][widest layer output] fp32 buffer, zero
+    const int widest = spec_.kind == "mlp" ? spec_.hidden : std::max(spec_.hidden, spec_.ffn);
+    ctx_.gemms.split_ws_bytes = static_cast<size_t>(ctx_.rows) * widest * 4;
+    ctx_.gemms.split_ws = static_cast<float*>(mem_.alloc(ctx_.gemms.split_ws_bytes));
+  }
   for (auto& layer : layers_) layer->alloc_stash(ctx_);
   act_.assign(L(), {});
   // activation buffers sized per boundary: layer l's input is samples x elems(l)

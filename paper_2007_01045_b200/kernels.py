@@ -20,7 +20,8 @@ def _stream():
 
 def gemm(A, B, C, M, N, K, *, lda, ldb, ldc, a_mn_major=False, b_mn_major=False, batch=1, a_batch_stride=0,
          b_batch_stride=0, epi=EPI_OUT_BF16, alpha=1.0, bias=None, aux_in=None, resid=None, aux_out=None, zdiv=1,
-         s_zo=None, s_zi=0, ndiv=1 << 30, s_no=0, force_bn=0, force_1sm=False, trace=None, colsum=None, conv=None):
+         s_zo=None, s_zi=0, ndiv=1 << 30, s_no=0, force_bn=0, force_1sm=False, trace=None, colsum=None, conv=None,
+         split_ws=None):
     """C[z,m,n] = epi(alpha * sum_k A[z,m,k] * B[z,n,k]) (see csrc/kernels/gemm.h)."""
     d = GemmDesc()
     d.M, d.N, d.K, d.batch = M, N, K, batch
@@ -38,6 +39,8 @@ def gemm(A, B, C, M, N, K, *, lda, ldb, ldc, a_mn_major=False, b_mn_major=False,
     d.force_1sm = int(force_1sm)
     d.trace = None if trace is None else trace.data_ptr()
     d.colsum = None if colsum is None else colsum.data_ptr()
+    if split_ws is not None:  # zeroed fp32 scratch: split-K for bf16 outputs with few tiles
+        d.split_ws, d.split_ws_bytes = split_ws.data_ptr(), split_ws.numel() * split_ws.element_size()
     if conv is not None:  # (operand 1|2, x NHWC tensor, n, h, w, c): implicit-GEMM convolution
         d.conv_operand, x, d.conv_n, d.conv_h, d.conv_w, d.conv_c = conv
         d.conv_x = x.data_ptr()

@@ -139,3 +139,42 @@ def test_gemm_colsum_epilogue(cuda, m, n, k, one_sm):
     ref = c.float().sum(0) + 0.5
     assert torch.allclose(c.float(), a.float() @ b.float().T, rtol=2e-2, atol=2e-2)
     assert torch.allclose(cs, ref, rtol=1e-4, atol=1e-2 * m ** 0.5 * 0.01)
+
+
+@pytest.mark.parametrize("M,N,Kd,epi", [
+    (1024, 1600, 6400, "bias+resid"),   # GPT-2 ffn2 at one sample per micro-batch (28 pair tiles)
+    (2048, 1024, 4096, "plain"),        # BERT dgrad at a 4-sample replica slice (32 pair tiles)
+    (1024, 1024, 1024, "dgelu"),        # 16 pair tiles, act' epilogue
+    (1000, 1600, 1600, "bias"),         # ragged M
+])
+def test_gemm_split_k_bf16(cuda, M, N, Kd, epi):
+    """bf16-output GEMMs that would leave most CTA pairs idle run as split-K
+    fp32 reduce-add into a zeroed scratch + a bf16 epilogue pass; the result
+    matches the unsplit GEMM and torch, and the scratch is left zero."""
+    A = _rand(M, Kd, dev=cuda, seed=11)
+    B = _rand(N, Kd, dev=cuda, seed=12)
+    bias = _rand(N, dev=cuda, seed=13, dtype=torch.float32)
+    res = _rand(M, N, dev=cuda, seed=14)
+    z = _rand(M, N, dev=cuda, seed=15, scale=3.0)
+    flags = {"plain": 0, "bias": K.EPI_BIAS, "bias+resid": K.EPI_BIAS | K.EPI_RESID, "dgelu": K.EPI_DGELU}[epi]
+    kw = dict(lda=Kd, ldb=Kd, ldc=N, epi=flags, bias=bias if flags & K.EPI_BIAS else None,
+              resid=res if flags & K.EPI_RESID else None, aux_in=z if flags & K.EPI_DGELU else None)
+    ws = torch.zeros(M * N, dtype=torch.float32, device=cuda)
+    C1 = torch.zeros(M, N, dtype=torch.bfloat16, device=cuda)
+    C2 = torch.zeros(M, N, dtype=torch.bfloat16, device=cuda)
+    K.gemm(A, B, C1, M, N, Kd, **kw)
+    for _ in range(2):  # twice: the scratch must come back zeroed
+        K.gemm(A, B, C2, M, N, Kd, split_ws=ws, **kw)
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float().T
+    if flags & K.EPI_BIAS:
+        ref = ref + bias
+    if flags & K.EPI_RESID:
+        ref = ref + res.float()
+    if flags & K.EPI_DGELU:
+        zf = z.float()
+        t = torch.tanh(0.7978845608028654 * (zf + 0.044715 * zf ** 3))
+        ref = ref * (0.5 * (1 + t) + 0.5 * zf * (1 - t * t) * 0.7978845608028654 * (1 + 3 * 0.044715 * zf * zf))
+    _close(C2, ref, 2e-2)
+    _close(C2, C1.float(), 2e-2)
+    assert int((ws != 0).sum()) == 0
