@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <sstream>
@@ -299,6 +300,8 @@ class Executor {
   std::vector<int> peer_stage_;      // stage of each rank
 
   cudaStream_t compute_ = nullptr, send_act_ = nullptr, send_grad_s_ = nullptr, reduce_ = nullptr;
+  cudaStream_t wgrad_ = nullptr;  // transformer weight gradients (StageContext::wstream)
+  cudaEvent_t ev_wg_done_ = nullptr;
   ncclComm_t comm_ = nullptr;
   cudaEvent_t ev_begin_ = nullptr, ev_end_ = nullptr, ev_reduce_done_ = nullptr;
   cudaEvent_t ev_sa_done_ = nullptr, ev_sg_done_ = nullptr, ev_fork_ = nullptr, ev_last_bwd_ = nullptr;
@@ -556,6 +559,16 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
   DPL_CUDA(cudaStreamCreateWithFlags(&send_grad_s_, cudaStreamNonBlocking));
   DPL_CUDA(cudaStreamCreateWithFlags(&reduce_, cudaStreamNonBlocking));
   ctx_.stream = compute_;
+  {  // weight-gradient side stream of the transformer backward (DPL_WGRAD_STREAM=0: off)
+    const char* e = std::getenv("DPL_WGRAD_STREAM");
+    const bool on = cfg.contains("wgrad_stream") ? cfg.at("wgrad_stream").as_bool() : !(e && e[0] == '0');
+    if (on && (spec_.kind == "bert" || spec_.kind == "gpt")) {
+      DPL_CUDA(cudaStreamCreateWithFlags(&wgrad_, cudaStreamNonBlocking));
+      DPL_CUDA(cudaEventCreateWithFlags(&ctx_.ev_fork, cudaEventDisableTiming));
+      DPL_CUDA(cudaEventCreateWithFlags(&ctx_.ev_join, cudaEventDisableTiming));
+      ctx_.wstream = wgrad_;
+    }
+  }
 
   for (int l = lo_; l < hi_; ++l) layers_.push_back(make_layer(spec_, l));
   for (auto& layer : layers_) {
@@ -689,6 +702,7 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
   mk_nt(&ev_sg_done_);
   mk_nt(&ev_fork_);
   mk_nt(&ev_last_bwd_);
+  mk_nt(&ev_wg_done_);
   fwd_ev_.resize(M_);
   bwd_ev_.resize(M_);
   send_fwd_ev_.resize(M_);
@@ -761,7 +775,7 @@ Executor::~Executor() {
   for (void* p : staging_)
     if (p) cudaFreeHost(p);
   for (cudaEvent_t e : {ev_begin_, ev_end_, ev_reduce_done_, ev_sa_done_, ev_sg_done_, ev_fork_, ev_last_bwd_,
-                        emb_done_, head_done_})
+                        emb_done_, head_done_, ev_wg_done_, ctx_.ev_fork, ctx_.ev_join})
     if (e) cudaEventDestroy(e);
   for (auto* v : {&fwd_ev_, &bwd_ev_, &send_fwd_ev_, &send_bwd_ev_, &ar_ev_})
     for (BlockEvents& b : *v) {
@@ -771,7 +785,7 @@ Executor::~Executor() {
   for (auto* v : {&layer_done_, &fwd_done_, &bwd_done_})
     for (cudaEvent_t e : *v)
       if (e) cudaEventDestroy(e);
-  for (cudaStream_t s : {compute_, send_act_, send_grad_s_, reduce_})
+  for (cudaStream_t s : {compute_, send_act_, send_grad_s_, reduce_, wgrad_})
     if (s) cudaStreamDestroy(s);
 }
 
@@ -1135,7 +1149,8 @@ void Executor::enqueue_step(const void* host_input, const void* host_target) {
   // fork every side stream from the compute stream (they join again at the
   // end), so a captured step always has one origin and one sink
   DPL_CUDA(cudaEventRecord(ev_fork_, compute_));
-  for (cudaStream_t side : {send_act_, send_grad_s_, reduce_}) DPL_CUDA(cudaStreamWaitEvent(side, ev_fork_, 0));
+  for (cudaStream_t side : {send_act_, send_grad_s_, reduce_, wgrad_})
+    if (side) DPL_CUDA(cudaStreamWaitEvent(side, ev_fork_, 0));
   DPL_CUDA(cudaMemsetAsync(loss_acc_, 0, 4, compute_));
 
   // sample rows [row0, row0 + samples) of micro-batch i owned by this replica
@@ -1216,6 +1231,10 @@ void Executor::enqueue_step(const void* host_input, const void* host_target) {
   DPL_CUDA(cudaStreamWaitEvent(compute_, ev_reduce_done_, 0));
   DPL_CUDA(cudaStreamWaitEvent(compute_, ev_sa_done_, 0));
   DPL_CUDA(cudaStreamWaitEvent(compute_, ev_sg_done_, 0));
+  if (wgrad_) {  // joined after every layer already; a step without transformer work still rejoins it
+    DPL_CUDA(cudaEventRecord(ev_wg_done_, wgrad_));
+    DPL_CUDA(cudaStreamWaitEvent(compute_, ev_wg_done_, 0));
+  }
   record(ev_end_, compute_);
   if (k_ == S_ - 1) DPL_CUDA(cudaMemcpyAsync(loss_host_, loss_acc_, 4, cudaMemcpyDeviceToHost, compute_));
   // clear this step's flag bank (signalled again two steps from now)
@@ -1682,6 +1701,7 @@ std::string Executor::info() const {
   v["input_dtype"] = emb_ ? "int32" : "bfloat16";
   v["target_dtype"] = (head_ || classify()) ? "int32" : "bfloat16";
   v["graphs"] = graph_count();
+  v["wgrad_stream"] = wgrad_ != nullptr;
   Value chain = Value::array();
   for (const auto& c : chain_) chain.push_back(std::string(c.kind == pipeplan::BlockKind::forward ? "F" : "B") +
                                                std::to_string(c.micro_batch));

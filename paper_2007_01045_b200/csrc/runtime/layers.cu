@@ -255,8 +255,14 @@ class TransformerLayer final : public Layer {
     bf16* dctx_h = ctx.t_h3;
     bf16* dqkv = ctx.t_qkv;
 
+    // Weight gradients go to the side stream (ctx.on_side) beside the dgrad
+    // chain; each reads only buffers the chain does not write before the
+    // join at the end of this layer, and they accumulate into W* gradients
+    // the chain never touches.
     // FFN2: dW2 += dy^T g ; db2 ; dz1 = (dy W2) * gelu'(z1)
-    ctx.gemms.run(plain(H_, F_, R, dy, H_, true, st.g, F_, true, g32_ + w2_, F_, kOutF32Acc), str);
+    ctx.on_side([&](cudaStream_t s) {
+      ctx.gemms.run(plain(H_, F_, R, dy, H_, true, st.g, F_, true, g32_ + w2_, F_, kOutF32Acc), s);
+    });
     {
       // db1 = colsum(dz1) accumulated by the epilogue from the staged chunks
       GemmDesc d = plain(R, F_, H_, dy, H_, false, w16_ + w2_, F_, true, dz1, F_, kDGelu | kColSum);
@@ -265,14 +271,18 @@ class TransformerLayer final : public Layer {
       ctx.gemms.run(d, str);
     }
     // FFN1: dW1 += dz1^T ln2 ; dln2 = dz1 W1
-    ctx.gemms.run(plain(F_, H_, R, dz1, F_, true, st.ln2, H_, true, g32_ + w1_, H_, kOutF32Acc), str);
+    ctx.on_side([&](cudaStream_t s) {
+      ctx.gemms.run(plain(F_, H_, R, dz1, F_, true, st.ln2, H_, true, g32_ + w1_, H_, kOutF32Acc), s);
+    });
     ctx.gemms.run(plain(R, H_, F_, dz1, F_, false, w16_ + w1_, H_, true, dln, H_, kOutBf16), str);
     // LN2 backward (+ residual gradient dy); also db2 = colsum(dy) and
     // dbo = colsum(dh) from the rows it already holds
     layernorm_bwd(dln, st.h, st.mean2, st.rstd2, w32_ + ln2g_, dy, dh, g32_ + ln2g_, g32_ + ln2b_, R, H_, str,
                   ctx.ln_ws, g32_ + b2_, g32_ + bo_);
     // O projection: dWo += dh^T ctx ; dbo ; dctx = dh Wo (head-split store)
-    ctx.gemms.run(plain(H_, H_, R, dh, H_, true, st.ctx, H_, true, g32_ + wo_, H_, kOutF32Acc), str);
+    ctx.on_side([&](cudaStream_t s) {
+      ctx.gemms.run(plain(H_, H_, R, dh, H_, true, st.ctx, H_, true, g32_ + wo_, H_, kOutF32Acc), s);
+    });
     {
       GemmDesc d = plain(R, H_, H_, dh, H_, false, w16_ + wo_, H_, true, dctx_h, d_, kOutBf16);
       d.ndiv = d_;
@@ -282,13 +292,18 @@ class TransformerLayer final : public Layer {
     // fused flash attention backward -> dQ, dK, dV head-merged into dqkv
     attention(ctx, slot).backward(str);
     // QKV: dWqkv += dqkv^T ln1 ; dbqkv ; dln1 = dqkv Wqkv
-    ctx.gemms.run(plain(3 * H_, H_, R, dqkv, 3 * H_, true, st.ln1, H_, true, g32_ + wqkv_, H_, kOutF32Acc), str);
-    colsum_acc(dqkv, g32_ + bqkv_, R, 3 * H_, str);
+    ctx.on_side([&](cudaStream_t s) {
+      ctx.gemms.run(plain(3 * H_, H_, R, dqkv, 3 * H_, true, st.ln1, H_, true, g32_ + wqkv_, H_, kOutF32Acc), s);
+      colsum_acc(dqkv, g32_ + bqkv_, R, 3 * H_, s);
+    });
     ctx.gemms.run(plain(R, H_, 3 * H_, dqkv, 3 * H_, false, w16_ + wqkv_, H_, true, dln, H_, kOutBf16), str);
     // LN1 backward (+ residual gradient dh); the model's first layer still
     // needs gamma/beta grads, its dx goes to scratch
     layernorm_bwd(dln, x, st.mean1, st.rstd1, w32_ + ln1g_, dh, dx ? dx : dctx_h, g32_ + ln1g_, g32_ + ln1b_, R, H_,
                   str, ctx.ln_ws);
+    // the layer's weight gradients are final (and its scratch free) when the
+    // next layer's backward starts
+    ctx.join_side();
   }
 
   double flops_fwd(const StageContext& ctx) const override {

@@ -84,6 +84,28 @@ struct StageContext {
   int samples = 0;  // samples per micro-batch slice
   int slots = 1;    // activation stash depth (phi of this stage)
   cudaStream_t stream = nullptr;
+  // Weight-gradient side stream (transformer backward): the wgrad GEMMs of a
+  // layer run there beside the dgrad chain on `stream`, forked and joined
+  // with the two events below inside the layer (null: everything on stream)
+  cudaStream_t wstream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // run f(stream) on the side stream after everything issued so far on `stream`
+  template <typename F>
+  void on_side(F&& f) {
+    if (!wstream) {
+      f(stream);
+      return;
+    }
+    cudaEventRecord(ev_fork, stream);
+    cudaStreamWaitEvent(wstream, ev_fork, 0);
+    f(wstream);
+  }
+  // `stream` waits for the side stream's work so far
+  void join_side() {
+    if (!wstream) return;
+    cudaEventRecord(ev_join, wstream);
+    cudaStreamWaitEvent(stream, ev_join, 0);
+  }
   GemmCache gemms;
   DeviceMemory* mem = nullptr;
   // shared scratch (transformer backward / attention)
