@@ -1646,14 +1646,18 @@ std::string Executor::gemm_profile_json() const {
   }
   out["shapes"] = std::move(shapes);
   // every libdapple kernel of the profiled step, grouped by kernel
+  // "seconds" sums each launch's own duration; "busy_seconds" is the union of
+  // the launches' intervals on the step's timeline (launches on the compute
+  // and weight-gradient streams overlap, so the sum double-counts)
   struct K {
     std::string name;
     long long launches = 0;
     double seconds = 0, flops = 0;
+    std::vector<std::pair<float, float>> spans;  // ms from the step's first event
   };
   std::vector<K> ks;
   for (const auto& r : kernel_timer().recs) {
-    float ms = 0.f;
+    float ms = 0.f, a = 0.f, b = 0.f;
     cudaEventElapsedTime(&ms, r.start, r.end);
     auto it = std::find_if(ks.begin(), ks.end(), [&](const K& k) { return k.name == r.name; });
     if (it == ks.end()) {
@@ -1663,14 +1667,32 @@ std::string Executor::gemm_profile_json() const {
     it->launches++;
     it->seconds += ms * 1e-3;
     it->flops += r.flops;
+    if (cudaEventElapsedTime(&a, ev_begin_, r.start) == cudaSuccess &&
+        cudaEventElapsedTime(&b, ev_begin_, r.end) == cudaSuccess)
+      it->spans.push_back({a, b});
+    cudaGetLastError();
   }
   Value kernels = Value::array();
-  for (const K& k : ks) {
+  for (K& k : ks) {
     Value e = Value::object();
     e["kernel"] = k.name;
     e["launches"] = k.launches;
     e["seconds"] = k.seconds;
     if (k.flops > 0) e["tflops"] = k.flops / k.seconds * 1e-12;
+    std::sort(k.spans.begin(), k.spans.end());
+    double busy = 0.0, lo = -1.0, hi = -1.0;
+    for (const auto& [a, b] : k.spans) {
+      if (a > hi) {
+        if (hi > lo) busy += hi - lo;
+        lo = a;
+        hi = b;
+      } else {
+        hi = std::max<double>(hi, b);
+      }
+    }
+    if (hi > lo) busy += hi - lo;
+    e["busy_seconds"] = busy * 1e-3;
+    if (k.flops > 0 && busy > 0) e["busy_tflops"] = k.flops / (busy * 1e-3) * 1e-12;
     kernels.push_back(std::move(e));
   }
   out["kernels"] = std::move(kernels);

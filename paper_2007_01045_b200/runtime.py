@@ -21,7 +21,8 @@ class Executor:
     def __init__(self, model: dict, plan, micro_batches: int, gbs: int, *, lr: float = 1e-3, seed: int = 1234,
                  rank: int = 0, world: int = 1, device: Optional[int] = None, apply: bool = True,
                  timeline: bool = True, schedule: str = "dapple", recompute: bool = False,
-                 allreduce: Optional[str] = None, connect: bool = True, probe: bool = False):
+                 allreduce: Optional[str] = None, connect: bool = True, probe: bool = False,
+                 wgrad_stream: Optional[bool] = None):
         self.plan = json.loads(plan) if isinstance(plan, str) else plan
         self.model, self.M, self.gbs = model, micro_batches, gbs
         self.rank, self.world = rank, world
@@ -31,6 +32,8 @@ class Executor:
                "rank": rank, "world": world, "apply": apply, "timeline": timeline,
                "schedule": schedule, "recompute": recompute, "allreduce": self.allreduce, "probe": probe,
                "graph": os.environ.get("DPL_GRAPH", "1") != "0"}
+        if wgrad_stream is not None:
+            cfg["wgrad_stream"] = wgrad_stream
         h = ctypes.c_void_p()
         check(lib().dpl_exec_create(json.dumps(cfg).encode(), self.device, ctypes.byref(h)))
         self._h = h
@@ -244,6 +247,11 @@ class LocalRanks:
         devices = devices or [0] * world
         if kw.get("allreduce", "peer") != "peer":
             raise ValueError("LocalRanks reduce over shared memory (allreduce='peer')")
+        # The weight-gradient side stream stays off here: with several ranks'
+        # step graphs co-resident in one context, its extra branch can share a
+        # hardware queue with another rank's blocked flag wait (observed as a
+        # hang on one B200); one process per GPU has no such sharing.
+        kw.setdefault("wgrad_stream", False)
         self.ranks = [Executor(model, plan, micro_batches, gbs, rank=r, world=world, device=devices[r],
                                allreduce="peer", connect=False, **kw) for r in range(world)]
         blobs = [ex.export() for ex in self.ranks]
