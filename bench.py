@@ -555,7 +555,8 @@ def run_reference(args, rank, world):
     unit = "samples/s"
     line = {"metric": METRIC, "value": value, "unit": unit, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "strong" if DEFAULTS[args.model]["straight"] or model["kind"] == "vgg" else "weak",
+            "scaling": "strong" if DEFAULTS[args.model]["straight"] or model["kind"] == "vgg" or
+                                   "global_batch" in DEFAULTS[args.model] else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
             "config": {"workload": args.model, **model},
             "cpu_baseline": {"value": value, "unit": unit, "cores": os.cpu_count(), "kind": "port",
