@@ -176,16 +176,55 @@ def load_peaks() -> tuple[dict, str]:
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled during the timed region: NVML
+    polled every 5 ms from a thread (a short timed region -- VGG-19 at N=4 is
+    ~100 ms -- still gets samples), nvidia-smi -lms 200 where NVML is absent."""
+    # nvmlClocksEventReason* bits
+    NVML_BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
+
+    def _nvml_start(self) -> bool:
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            handles = [pynvml.nvmlDeviceGetHandleByIndex(i) for i in range(pynvml.nvmlDeviceGetCount())]
+            reasons_fn = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            smax = [pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM) for h in handles]
+        except Exception:
+            return False
+        self.nvml = True
+        self.stop_evt = threading.Event()
+
+        def poll():
+            while not self.stop_evt.is_set():
+                ts = time.time()
+                for h, cmax in zip(handles, smax):
+                    try:
+                        clk = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        power = pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0
+                        bits = reasons_fn(h)
+                    except Exception:
+                        continue
+                    order = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+                    flags = ["Active" if bits & self.NVML_BITS[n] else "Not Active" for n in order]
+                    self.lines.append((ts, ", ".join(["", "", str(clk), str(cmax), str(power)] + flags)))
+                self.stop_evt.wait(0.005)
+
+        self.thread = threading.Thread(target=poll, daemon=True)
+        self.thread.start()
+        return True
     FIELDS = ["timestamp", "index", "clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
               "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
               "clocks_event_reasons.sw_power_cap"]
 
     def __init__(self):
         self.proc = None
+        self.nvml = False
         self.lines = []
 
     def start(self):
+        if self._nvml_start():
+            return
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "--query-gpu=" + ",".join(self.FIELDS),
                                           "--format=csv,noheader,nounits", "-lms", "200"],
@@ -203,13 +242,17 @@ class ClockSampler:
         setattr(self, name, time.time())
 
     def stop(self) -> dict:
-        if not self.proc:
+        if self.nvml:
+            self.stop_evt.set()
+            self.thread.join(timeout=5)
+        elif not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
+        else:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
         sm, smax, reasons, n_all = [], [], set(), 0
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         t0, t1 = getattr(self, "t_start", 0.0), getattr(self, "t_stop", float("inf"))
@@ -229,7 +272,8 @@ class ClockSampler:
                 sm.append(clk)
                 smax.append(cmax)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples_under_load": len(sm), "samples": n_all}
+                "reasons": sorted(reasons), "samples_under_load": len(sm), "samples": n_all,
+                "source": "nvml 5 ms" if self.nvml else "nvidia-smi 200 ms"}
 
 
 def dist_setup():

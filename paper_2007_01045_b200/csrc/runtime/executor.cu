@@ -300,7 +300,7 @@ class Executor {
   std::vector<int> peer_stage_;      // stage of each rank
 
   cudaStream_t compute_ = nullptr, send_act_ = nullptr, send_grad_s_ = nullptr, reduce_ = nullptr;
-  cudaStream_t wgrad_ = nullptr;  // transformer weight gradients (StageContext::wstream)
+  cudaStream_t wgrad_ = nullptr;  // weight gradients (StageContext::wstream)
   cudaEvent_t ev_wg_done_ = nullptr;
   ncclComm_t comm_ = nullptr;
   cudaEvent_t ev_begin_ = nullptr, ev_end_ = nullptr, ev_reduce_done_ = nullptr;
@@ -559,10 +559,10 @@ Executor::Executor(const Value& cfg, int device) : device_(device) {
   DPL_CUDA(cudaStreamCreateWithFlags(&send_grad_s_, cudaStreamNonBlocking));
   DPL_CUDA(cudaStreamCreateWithFlags(&reduce_, cudaStreamNonBlocking));
   ctx_.stream = compute_;
-  {  // weight-gradient side stream of the transformer backward (DPL_WGRAD_STREAM=0: off)
+  {  // weight-gradient side stream of the backward (DPL_WGRAD_STREAM=0: off)
     const char* e = std::getenv("DPL_WGRAD_STREAM");
     const bool on = cfg.contains("wgrad_stream") ? cfg.at("wgrad_stream").as_bool() : !(e && e[0] == '0');
-    if (on && (spec_.kind == "bert" || spec_.kind == "gpt")) {
+    if (on) {
       DPL_CUDA(cudaStreamCreateWithFlags(&wgrad_, cudaStreamNonBlocking));
       DPL_CUDA(cudaEventCreateWithFlags(&ctx_.ev_fork, cudaEventDisableTiming));
       DPL_CUDA(cudaEventCreateWithFlags(&ctx_.ev_join, cudaEventDisableTiming));

@@ -109,15 +109,19 @@ class MlpLayer final : public Layer {
 
   void backward(StageContext& ctx, int, const bf16* x, const bf16* dz, bf16* dx) override {
     const int R = ctx.rows;
-    // dW += dZ^T X  (both operands read transposed from their row-major forms)
-    ctx.gemms.run(plain(h_, h_, R, dz, h_, true, x, h_, true, g32_, h_, kOutF32Acc), ctx.stream);
-    colsum_acc(dz, g32_ + static_cast<size_t>(h_) * h_, R, h_, ctx.stream);
+    // dW += dZ^T X  (both operands read transposed from their row-major forms),
+    // db: on the weight-gradient side stream, joined below
+    ctx.on_side([&](cudaStream_t s) {
+      ctx.gemms.run(plain(h_, h_, R, dz, h_, true, x, h_, true, g32_, h_, kOutF32Acc), s);
+      colsum_acc(dz, g32_ + static_cast<size_t>(h_) * h_, R, h_, s);
+    });
     if (dx) {
       // dX = dZ W, with the previous layer's relu'(x) fused in the epilogue
       GemmDesc d = plain(R, h_, h_, dz, h_, false, w16_, h_, true, dx, h_, in_relu_ ? kDRelu : 0u);
       d.aux_in = x;
       ctx.gemms.run(d, ctx.stream);
     }
+    ctx.join_side();
   }
 
   double flops_fwd(const StageContext& ctx) const override { return 2.0 * ctx.rows * h_ * h_; }
@@ -457,13 +461,17 @@ class ConvLayer final : public Layer {
     if (v_.pool) maxpool2_relu_bwd(yr_[slot], dy, ctx.conv_dz, n, v_.h, v_.w, v_.cout, ctx.stream);
     else relu_bwd(ctx.cur_y, dy, ctx.conv_dz, static_cast<long long>(rows) * v_.cout, ctx.stream);
     float* gw = g32_;
-    colsum_acc(ctx.conv_dz, gw + static_cast<size_t>(v_.cout) * v_.kp, rows, v_.cout, ctx.stream);
-    // dW += dz^T col: the B tiles are TMA im2col loads of the stashed input
-    // (explicit columns from the forward for the RGB layer)
-    GemmDesc dw = plain(v_.cout, v_.kp, rows, ctx.conv_dz, v_.cout, true, implicit() ? x : col_[slot], v_.kp, true, gw,
-                        v_.kp, kOutF32Acc);
-    if (implicit()) conv_operand(dw, 2, x, n);
-    ctx.gemms.run(dw, ctx.stream);
+    // db and dW += dz^T col (the B tiles are TMA im2col loads of the stashed
+    // input; explicit columns from the forward for the RGB layer) on the
+    // weight-gradient side stream; dz, x and the columns stay untouched until
+    // the join at the end of this layer
+    ctx.on_side([&](cudaStream_t s) {
+      colsum_acc(ctx.conv_dz, gw + static_cast<size_t>(v_.cout) * v_.kp, rows, v_.cout, s);
+      GemmDesc dw = plain(v_.cout, v_.kp, rows, ctx.conv_dz, v_.cout, true, implicit() ? x : col_[slot], v_.kp, true,
+                          gw, v_.kp, kOutF32Acc);
+      if (implicit()) conv_operand(dw, 2, x, n);
+      ctx.gemms.run(dw, s);
+    });
     if (dx && implicit_dgrad()) {
       // backward data as a forward conv of dz with the flipped, transposed
       // weights: dx = im2col(dz) wt^T, the A tiles TMA im2col loads of dz
@@ -483,6 +491,7 @@ class ConvLayer final : public Layer {
                     ctx.stream);
       col2im3x3(ctx.conv_dcol, dx, n, v_.h, v_.w, v_.cin, v_.kp, ctx.stream);
     }
+    ctx.join_side();
   }
   double flops_fwd(const StageContext& ctx) const override { return 2.0 * px(ctx) * v_.cout * 9.0 * v_.cin; }
   double flops_bwd(const StageContext& ctx, bool need_dx) const override {
@@ -544,10 +553,13 @@ class FcLayer final : public Layer {
       relu_bwd(ctx.cur_y, dy, ctx.conv_dz, static_cast<long long>(n) * v_.fout, ctx.stream);
       dz = ctx.conv_dz;
     }
-    ctx.gemms.run(plain(v_.fout, v_.fin, n, dz, v_.fout, true, x, v_.fin, true, g32_, v_.fin, kOutF32Acc), ctx.stream);
-    colsum_acc(dz, g32_ + static_cast<size_t>(v_.fout) * v_.fin, n, v_.fout, ctx.stream);
+    ctx.on_side([&](cudaStream_t s) {
+      ctx.gemms.run(plain(v_.fout, v_.fin, n, dz, v_.fout, true, x, v_.fin, true, g32_, v_.fin, kOutF32Acc), s);
+      colsum_acc(dz, g32_ + static_cast<size_t>(v_.fout) * v_.fin, n, v_.fout, s);
+    });
     if (dx)
       ctx.gemms.run(plain(n, v_.fin, v_.fout, dz, v_.fout, false, w16_, v_.fin, true, dx, v_.fin, kOutBf16), ctx.stream);
+    ctx.join_side();
   }
   double flops_fwd(const StageContext& ctx) const override { return 2.0 * ctx.samples * v_.fin * v_.fout; }
   double flops_bwd(const StageContext& ctx, bool need_dx) const override {
@@ -635,10 +647,13 @@ void LmHead::forward(StageContext& ctx, int slot, const bf16* y, const int* tgt,
 void LmHead::backward(StageContext& ctx, int slot, const bf16* y, bf16* dy) {
   const Slot& st = slots_[slot];
   const int R = ctx.rows;
-  // dWout += dlogits^T xn ; dxn = dlogits Wout
-  ctx.gemms.run(plain(vp_, h_, R, st.dlogits, vp_, true, st.xn, h_, true, g32_ + 2 * h_, h_, kOutF32Acc), ctx.stream);
+  // dWout += dlogits^T xn (side stream) ; dxn = dlogits Wout
+  ctx.on_side([&](cudaStream_t s) {
+    ctx.gemms.run(plain(vp_, h_, R, st.dlogits, vp_, true, st.xn, h_, true, g32_ + 2 * h_, h_, kOutF32Acc), s);
+  });
   ctx.gemms.run(plain(R, h_, vp_, st.dlogits, vp_, false, w16_ + 2 * h_, h_, true, dxn_, h_, kOutBf16), ctx.stream);
   layernorm_bwd(dxn_, y, st.mean, st.rstd, w32_, nullptr, dy, g32_, g32_ + h_, R, h_, ctx.stream, ctx.ln_ws);
+  ctx.join_side();
 }
 
 std::vector<Layer::Named> LmHead::tensors() const {

@@ -84,7 +84,7 @@ struct StageContext {
   int samples = 0;  // samples per micro-batch slice
   int slots = 1;    // activation stash depth (phi of this stage)
   cudaStream_t stream = nullptr;
-  // Weight-gradient side stream (transformer backward): the wgrad GEMMs of a
+  // Weight-gradient side stream of the backward: the wgrad GEMMs of a
   // layer run there beside the dgrad chain on `stream`, forked and joined
   // with the two events below inside the layer (null: everything on stream)
   cudaStream_t wstream = nullptr;
