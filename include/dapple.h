@@ -107,6 +107,10 @@ int dpl_k_gemm(const dpl_gemm_desc* desc, void* stream);
  * ctx head-merged [B*S][ldc], lse [heads*B][S]. */
 int dpl_k_attention_fwd(const void* qkv, void* ctx, long long ldc, float* lse, int samples, int seq, int heads,
                         int causal, void* stream);
+/* Diagnostics: the same forward with 16 %globaltimer / %smid slots per CTA
+ * written to trace (tools/attn_trace.py). */
+int dpl_k_attention_fwd_traced(const void* qkv, void* ctx, long long ldc, float* lse, int samples, int seq,
+                               int heads, int causal, long long* trace, void* stream);
 /* Fused attention backward: recomputes P from lse, dO head-split
  * [heads][B][S][64]; writes dQ/dK/dV head-merged into dqkv [B*S][3H];
  * workspaces dsum [heads*B][S] and dq_acc [heads*B][S][64] fp32. */

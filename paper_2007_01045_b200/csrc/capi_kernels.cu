@@ -97,10 +97,19 @@ int dpl_k_gemm(const dpl_gemm_desc* d, void* stream) {
   });
 }
 
+int dpl_k_attention_fwd_traced(const void* qkv, void* ctx, long long ldc, float* lse, int samples, int seq, int heads,
+                               int causal, long long* trace, void* stream);
+
 int dpl_k_attention_fwd(const void* qkv, void* ctx, long long ldc, float* lse, int samples, int seq, int heads,
                         int causal, void* stream) {
+  return dpl_k_attention_fwd_traced(qkv, ctx, ldc, lse, samples, seq, heads, causal, nullptr, stream);
+}
+
+int dpl_k_attention_fwd_traced(const void* qkv, void* ctx, long long ldc, float* lse, int samples, int seq, int heads,
+                               int causal, long long* trace, void* stream) {
   return guarded([&] {
     dpl::AttentionDesc d;
+    d.trace = trace;
     d.qkv = qkv;
     d.ctx = ctx;
     d.ldc = ldc;

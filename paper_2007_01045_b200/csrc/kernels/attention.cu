@@ -44,7 +44,8 @@ namespace {
 constexpr int kT = 128;           // query / key tile
 constexpr int kD = 64;            // head dim
 constexpr int kTileBytes = kT * kD * 2;  // 16 KB
-constexpr int kFwdThreads = 256;
+constexpr int kFwdThreads = 320;      // warp 0 TMA, warp 1 MMA, warps 2-9 softmax
+constexpr int kSoftmaxThreads = 256;
 
 struct AttnFwdParams {
   CUtensorMap qkv;  // {64, S, 3*heads*B}
@@ -58,6 +59,7 @@ struct AttnFwdParams {
   float* part;    // [z][S/128][2][66][128]: o[64], m, l per row, per half
   int* flags;     // [z][S/128] tickets
   int n_items;
+  long long* trace;  // 16 %globaltimer slots per CTA (diagnostics), or null
   unsigned char it_qt[32], it_lo[32], it_hi[32], it_half[32];
 };
 
@@ -78,32 +80,51 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-// Two CTAs per SM (80 KB smem, 256 TMEM columns each): S single-buffered,
-// O double-buffered; K, V, P single-buffered -- the co-resident CTA fills the
-// gaps this CTA's dependency chain leaves.
+// Two CTAs per SM (96 KB smem, 256 TMEM columns each): S single-buffered,
+// O and V double-buffered (V_{j+1} lands while PV_j runs); K, P single.  Ten warps: warp 0 TMA (and
+// the TMEM allocation), warp 1 MMA, warps 2-9 softmax -- two threads per
+// query row, each owning 64 of the tile's 128 key columns and 32 of the 64
+// output columns, so four softmax warps per SM sub-partition hide each
+// other's TMEM-load / SFU latency.  The row max of a tile is combined
+// through shared memory (a 64-thread named barrier per lane quadrant); the
+// row sums stay per thread until the end.  The MMA warp issues S_{j+1} ahead
+// of PV_j and the softmax releases S_j at its last TMEM load.
 __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_constant__ AttnFwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                // 16 KB
   uint8_t* sK = sQ + kTileBytes;     // 16 KB
-  uint8_t* sV = sK + kTileBytes;     // 16 KB
-  uint8_t* sP = sV + kTileBytes;     // 32 KB (two 64-key halves)
+  uint8_t* sV = sK + kTileBytes;     // 2 x 16 KB
+  uint8_t* sP = sV + 2 * kTileBytes; // 32 KB (two 64-key halves)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * kTileBytes);
   uint64_t* q_full = bars;
   uint64_t* k_full = bars + 1;
   uint64_t* k_empty = bars + 2;
-  uint64_t* v_full = bars + 3;
-  uint64_t* v_empty = bars + 4;
-  uint64_t* s_full = bars + 5;
-  uint64_t* s_empty = bars + 6;
-  uint64_t* p_full = bars + 7;
-  uint64_t* p_empty = bars + 8;
-  uint64_t* o_full = bars + 9;    // [2]
-  uint64_t* o_empty = bars + 11;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
-  int* ticket = reinterpret_cast<int*>(bars + 15);
+  uint64_t* s_full = bars + 3;
+  uint64_t* s_empty = bars + 4;
+  uint64_t* p_full = bars + 5;
+  uint64_t* p_empty = bars + 6;
+  uint64_t* o_full = bars + 7;    // [2]
+  uint64_t* o_empty = bars + 9;   // [2]
+  uint64_t* v_full = bars + 11;   // [2]
+  uint64_t* v_empty = bars + 13;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
+  int* ticket = reinterpret_cast<int*>(bars + 16);
+  float* xch = reinterpret_cast<float*>(bars + 17);  // [2 tiles][2 halves][128 rows] row-max / row-sum exchange
 
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
+  long long* trace = p.trace ? p.trace + 16LL * (blockIdx.x + gridDim.x * blockIdx.y) : nullptr;
+  auto mark = [&](int slot) {
+    if (trace) trace[slot] = static_cast<long long>(ptx::globaltimer_ns());
+  };
+  if (warp == 2 && lane == 0) {
+    mark(0);
+    if (trace) {
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      trace[15] = smid;
+    }
+  }
   int qt, z, kv_lo, half = 0, n_kv;
   if (p.n_items) {
     z = blockIdx.x;
@@ -120,29 +141,35 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
   const int q0 = qt * kT;
   const int zk = p.z_count + z, zv = 2 * p.z_count + z;
 
-  if (warp == 0 && lane == 0) {
-    ptx::tma_prefetch_desc(&p.qkv);
-    ptx::mbar_init(q_full, 1);
-    ptx::mbar_init(k_full, 1);
-    ptx::mbar_init(k_empty, 1);
-    ptx::mbar_init(v_full, 1);
-    ptx::mbar_init(v_empty, 1);
-    ptx::mbar_init(s_full, 1);
-    ptx::mbar_init(s_empty, 128);
-    ptx::mbar_init(p_full, 128);
-    ptx::mbar_init(p_empty, 1);
-    for (int i = 0; i < 2; ++i) {
-      ptx::mbar_init(&o_full[i], 1);
-      ptx::mbar_init(&o_empty[i], 128);
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::tma_prefetch_desc(&p.qkv);
+      ptx::mbar_init(q_full, 1);
+      ptx::mbar_init(k_full, 1);
+      ptx::mbar_init(k_empty, 1);
+      for (int i = 0; i < 2; ++i) {
+        ptx::mbar_init(&v_full[i], 1);
+        ptx::mbar_init(&v_empty[i], 1);
+      }
+      ptx::mbar_init(s_full, 1);
+      ptx::mbar_init(s_empty, kSoftmaxThreads);
+      ptx::mbar_init(p_full, kSoftmaxThreads);
+      ptx::mbar_init(p_empty, 1);
+      for (int i = 0; i < 2; ++i) {
+        ptx::mbar_init(&o_full[i], 1);
+        ptx::mbar_init(&o_empty[i], kSoftmaxThreads);
+      }
+      ptx::fence_barrier_init();
     }
-    ptx::fence_barrier_init();
+    __syncwarp();
+    ptx::tmem_alloc<256>(tmem_slot);
   }
-  if (warp == 2) ptx::tmem_alloc<256>(tmem_slot);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   ptx::pdl_wait();
+  if (warp == 2 && lane == 0) mark(1);
   // TMEM columns: S [0,128), O buffers [128,192) [192,256)
 
   if (warp == 0) {
@@ -150,25 +177,24 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
       ptx::mbar_arrive_expect_tx(q_full, kTileBytes);
       ptx::tma_load_3d(sQ, &p.qkv, q_full, 0, q0, z);
       for (int j = 0; j < n_kv; ++j) {
-        const uint32_t ph = (j & 1) ^ 1;
-        ptx::mbar_wait(k_empty, ph);
+        const int b = j & 1;
+        ptx::mbar_wait(k_empty, (j & 1) ^ 1);  // S_{j-1} done
         ptx::mbar_arrive_expect_tx(k_full, kTileBytes);
         ptx::tma_load_3d(sK, &p.qkv, k_full, 0, (kv_lo + j) * kT, zk);
-        ptx::mbar_wait(v_empty, ph);
-        ptx::mbar_arrive_expect_tx(v_full, kTileBytes);
-        ptx::tma_load_3d(sV, &p.qkv, v_full, 0, (kv_lo + j) * kT, zv);
+        ptx::mbar_wait(&v_empty[b], ((j >> 1) & 1) ^ 1);  // PV_{j-2} done
+        ptx::mbar_arrive_expect_tx(&v_full[b], kTileBytes);
+        ptx::tma_load_3d(sV + b * kTileBytes, &p.qkv, &v_full[b], 0, (kv_lo + j) * kT, zv);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       const uint32_t idesc_s = ptx::idesc_bf16_f32(kT, kT, false, false);  // Q K-major, K K-major
       const uint32_t idesc_o = ptx::idesc_bf16_f32(kT, kD, false, true);   // P K-major, V MN-major
-      const uint32_t aq = ptx::smem_addr(sQ), bk = ptx::smem_addr(sK), bv = ptx::smem_addr(sV);
+      const uint32_t aq = ptx::smem_addr(sQ), bk = ptx::smem_addr(sK);
       const uint32_t ap = ptx::smem_addr(sP);
-      ptx::mbar_wait(q_full, 0);
-      for (int j = 0; j < n_kv; ++j) {
+      // S_j = Q K_j^T once K_j landed and the softmax read S_{j-1}
+      auto issue_s = [&](int j) {
         const uint32_t ph = j & 1;
-        // S_j = Q K_j^T once K_j landed and S_{j-1} was read
         ptx::mbar_wait(k_full, ph);
         ptx::mbar_wait(s_empty, ph ^ 1);
         ptx::tc_fence_after();
@@ -178,8 +204,17 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
                         idesc_s, k > 0);
         ptx::mma_commit(s_full);
         ptx::mma_commit(k_empty);
+      };
+      ptx::mbar_wait(q_full, 0);
+      mark(12);
+      if (n_kv > 0) issue_s(0);
+      for (int j = 0; j < n_kv; ++j) {
+        const uint32_t ph = j & 1;
+        if (j + 1 < n_kv) issue_s(j + 1);
         // O_j = P_j V_j
-        ptx::mbar_wait(v_full, ph);
+        const int vb = j & 1;
+        const uint32_t bv = ptx::smem_addr(sV + vb * kTileBytes);
+        ptx::mbar_wait(&v_full[vb], (j >> 1) & 1);
         ptx::mbar_wait(p_full, ph);
         ptx::mbar_wait(&o_empty[j & 1], ((j >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
@@ -190,19 +225,29 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
                         ptx::smem_desc_sw128(bv + k * 16 * 128, 16, 1024), idesc_o, k > 0);
         }
         ptx::mma_commit(&o_full[j & 1]);
-        ptx::mma_commit(v_empty);
+        ptx::mma_commit(&v_empty[vb]);
         ptx::mma_commit(p_empty);
       }
     }
-  } else if (warp >= 4) {
+  } else {
     const int quad = warp & 3;
+    const int kh = (warp - 2) >> 2;  // key columns [64*kh, 64*kh+64), output columns [32*kh, 32*kh+32)
     const int r = quad * 32 + lane;  // query row within the tile
     const int q = q0 + r;
     const uint32_t trow = (quad * 32) << 16;
     const float c = p.scale_log2;
-    float o[kD];
+    // the two warps of a lane quadrant meet at named barrier 1 + quad
+    auto pair_sync = [&]() {
+      switch (quad) {  // immediate barrier ids (a register id reserves all 16)
+        case 0: asm volatile("bar.sync 1, 64;" ::: "memory"); break;
+        case 1: asm volatile("bar.sync 2, 64;" ::: "memory"); break;
+        case 2: asm volatile("bar.sync 3, 64;" ::: "memory"); break;
+        default: asm volatile("bar.sync 4, 64;" ::: "memory"); break;
+      }
+    };
+    float o[32];
 #pragma unroll
-    for (int i = 0; i < kD; ++i) o[i] = 0.f;
+    for (int i = 0; i < 32; ++i) o[i] = 0.f;
     float m = -INFINITY, l = 0.f;
     float alpha_prev = 0.f;
     for (int j = 0; j <= n_kv; ++j) {
@@ -211,14 +256,15 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
         const uint32_t ph = j & 1;
         ptx::mbar_wait(s_full, ph);
         ptx::tc_fence_after();
+        if (r == 0 && kh == 0 && j < 4) mark(2 + j);
         const bool diag = p.causal && kv_lo + j == qt;
-        const int lim = diag ? r : kT - 1;  // last unmasked key column of this row
-        // pass 1: row max of the raw scores (scale > 0 commutes with max)
+        const int lim = diag ? r - 64 * kh : 63;  // last unmasked key column of this row, in this half
+        // pass 1: row max of the raw scores over this half (scale > 0 commutes with max)
         float mx = -INFINITY;
 #pragma unroll 1
-        for (int cc = 0; cc < kT / 32; ++cc) {
+        for (int cc = 0; cc < 2; ++cc) {
           uint32_t v[32];
-          ptx::tmem_ld_32x32b_x32(tmem + trow + cc * 32, v);
+          ptx::tmem_ld_32x32b_x32(tmem + trow + 64 * kh + cc * 32, v);
           ptx::tmem_wait_ld();
           if (!diag) {
 #pragma unroll
@@ -228,24 +274,43 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
             for (int e = 0; e < 32; ++e) mx = cc * 32 + e <= lim ? fmaxf(mx, __uint_as_float(v[e])) : mx;
           }
         }
+        float* xm = xch + (j & 1) * 256;
+        xm[kh * 128 + r] = mx;
+        pair_sync();
+        mx = fmaxf(mx, xm[(kh ^ 1) * 128 + r]);
         const float m_new = fmaxf(m, mx * c);
         alpha = exp2_fast(m - m_new);
         m = m_new;
         ptx::mbar_wait(p_empty, ph ^ 1);  // PV_{j-1} finished reading P
-        float rs = 0.f;
+        float2 rs2 = make_float2(0.f, 0.f);
+        uint8_t* ph_tile = sP + kh * kTileBytes;  // this half's 64 keys
 #pragma unroll 1
-        for (int cc = 0; cc < kT / 32; ++cc) {
+        for (int cc = 0; cc < 2; ++cc) {
           uint32_t v[32];
-          ptx::tmem_ld_32x32b_x32(tmem + trow + cc * 32, v);
+          ptx::tmem_ld_32x32b_x32(tmem + trow + 64 * kh + cc * 32, v);
           ptx::tmem_wait_ld();
-          float pv[32];
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const float x = exp2_fast(fmaf(__uint_as_float(v[e]), c, -m));
-            pv[e] = (!diag || cc * 32 + e <= lim) ? x : 0.f;
-            rs += pv[e];
+          if (cc == 1) {  // S_j fully read: the MMA may write S_{j+1}
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(s_empty);
           }
-          uint8_t* half = sP + (cc >> 1) * kTileBytes;
+          float pv[32];
+          if (!diag) {  // packed fp32x2 FMA / add: half the scale and row-sum instructions
+            const float2 c2 = make_float2(c, c), nm2 = make_float2(-m, -m);
+#pragma unroll
+            for (int e = 0; e < 32; e += 2) {
+              const float2 x = __ffma2_rn(make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])), c2, nm2);
+              pv[e] = exp2_fast(x.x);
+              pv[e + 1] = exp2_fast(x.y);
+              rs2 = __fadd2_rn(rs2, make_float2(pv[e], pv[e + 1]));
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              const float x = exp2_fast(fmaf(__uint_as_float(v[e]), c, -m));
+              pv[e] = cc * 32 + e <= lim ? x : 0.f;
+              rs2.x += pv[e];
+            }
+          }
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             uint4 w;
@@ -253,33 +318,42 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
             w.y = pack_bf16(pv[8 * u + 2], pv[8 * u + 3]);
             w.z = pack_bf16(pv[8 * u + 4], pv[8 * u + 5]);
             w.w = pack_bf16(pv[8 * u + 6], pv[8 * u + 7]);
-            *reinterpret_cast<uint4*>(half + sw128(r, (cc & 1) * 4 + u)) = w;
+            *reinterpret_cast<uint4*>(ph_tile + sw128(r, cc * 4 + u)) = w;
           }
         }
-        l = l * alpha + rs;
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(s_empty);
+        l = l * alpha + (rs2.x + rs2.y);  // this half's share of the row sum
         fence_async_smem();
         ptx::mbar_arrive(p_full);
+        if (r == 0 && kh == 0 && j < 4) mark(6 + j);
       }
-      if (j > 0) {  // O = O * alpha_{j-1} + O_{j-1}
+      if (j > 0) {  // O = O * alpha_{j-1} + O_{j-1} (this thread's 32 columns)
         const int jj = j - 1;
         ptx::mbar_wait(&o_full[jj & 1], (jj >> 1) & 1);
         ptx::tc_fence_after();
-        const uint32_t to = tmem + trow + 128 + (jj & 1) * kD;
-#pragma unroll
-        for (int cc = 0; cc < kD / 32; ++cc) {
-          uint32_t v[32];
-          ptx::tmem_ld_32x32b_x32(to + cc * 32, v);
-          ptx::tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) o[cc * 32 + e] = fmaf(o[cc * 32 + e], alpha_prev, __uint_as_float(v[e]));
-        }
+        uint32_t v[32];
+        ptx::tmem_ld_32x32b_x32(tmem + trow + 128 + (jj & 1) * kD + 32 * kh, v);
+        ptx::tmem_wait_ld();
         ptx::tc_fence_before();
         ptx::mbar_arrive(&o_empty[jj & 1]);
+        const float2 a2 = make_float2(alpha_prev, alpha_prev);
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const float2 r2 =
+              __ffma2_rn(make_float2(o[e], o[e + 1]), a2, make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])));
+          o[e] = r2.x;
+          o[e + 1] = r2.y;
+        }
       }
       alpha_prev = alpha;
     }
+    // full row sum: the two halves' shares (same max, same rescalings)
+    {
+      float* xl = xch + (n_kv & 1) * 256;
+      xl[kh * 128 + r] = l;
+      pair_sync();
+      l += xl[(kh ^ 1) * 128 + r];
+    }
+    if (r == 0 && kh == 0) mark(10);
     bool write_out = true;
     if (half) {
       // Publish this half's (o, m, l); the CTA that takes ticket 1 merges
@@ -289,17 +363,19 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
       float* mine = p.part + (tile * 2 + (half - 1)) * 66 * kT;
       const float* other = p.part + (tile * 2 + (2 - half)) * 66 * kT;
 #pragma unroll
-      for (int e = 0; e < kD; ++e) __stcg(mine + e * kT + r, o[e]);
-      __stcg(mine + 64 * kT + r, m);
-      __stcg(mine + 65 * kT + r, l);
+      for (int e = 0; e < 32; ++e) __stcg(mine + (32 * kh + e) * kT + r, o[e]);
+      if (kh == 0) {
+        __stcg(mine + 64 * kT + r, m);
+        __stcg(mine + 65 * kT + r, l);
+      }
       __threadfence();
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (quad == 0 && lane == 0) {
+      asm volatile("bar.sync 5, %0;" ::"n"(kSoftmaxThreads) : "memory");
+      if (warp == 2 && lane == 0) {
         const int t = atomicAdd(p.flags + tile, 1);
         if (t == 1) p.flags[tile] = 0;  // both halves in: ready for the next call
         *ticket = t;
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      asm volatile("bar.sync 5, %0;" ::"n"(kSoftmaxThreads) : "memory");
       write_out = *ticket == 1;
       if (write_out) {  // merged in half order (1, 2) whichever CTA runs it: deterministic
         __threadfence();
@@ -310,8 +386,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
         const float mm = fmaxf(m1, m2);
         const float s1 = exp2_fast(m1 - mm), s2 = exp2_fast(m2 - mm);
 #pragma unroll
-        for (int e = 0; e < kD; ++e) {
-          const float ot = __ldcg(other + e * kT + r);
+        for (int e = 0; e < 32; ++e) {
+          const float ot = __ldcg(other + (32 * kh + e) * kT + r);
           o[e] = fmaf(first ? o[e] : ot, s1, (first ? ot : o[e]) * s2);
         }
         l = fmaf(l1, s1, l2 * s2);
@@ -319,26 +395,27 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
       }
     }
     if (write_out) {
-    const float inv = 1.f / l;
-    const int b = z % p.B, h = z / p.B;
-    __nv_bfloat16* out = p.ctx + static_cast<long long>(b * p.S + q) * p.ldc + h * kD;
+      const float inv = 1.f / l;
+      const int b = z % p.B, h = z / p.B;
+      __nv_bfloat16* out = p.ctx + static_cast<long long>(b * p.S + q) * p.ldc + h * kD + 32 * kh;
 #pragma unroll
-    for (int u = 0; u < kD / 8; ++u) {
-      uint4 w;
-      w.x = pack_bf16(o[8 * u + 0] * inv, o[8 * u + 1] * inv);
-      w.y = pack_bf16(o[8 * u + 2] * inv, o[8 * u + 3] * inv);
-      w.z = pack_bf16(o[8 * u + 4] * inv, o[8 * u + 5] * inv);
-      w.w = pack_bf16(o[8 * u + 6] * inv, o[8 * u + 7] * inv);
-      reinterpret_cast<uint4*>(out)[u] = w;
-    }
-    p.lse[static_cast<long long>(z) * p.S + q] = (m + log2f(l)) * 0.69314718055994531f;
+      for (int u = 0; u < 4; ++u) {
+        uint4 w;
+        w.x = pack_bf16(o[8 * u + 0] * inv, o[8 * u + 1] * inv);
+        w.y = pack_bf16(o[8 * u + 2] * inv, o[8 * u + 3] * inv);
+        w.z = pack_bf16(o[8 * u + 4] * inv, o[8 * u + 5] * inv);
+        w.w = pack_bf16(o[8 * u + 6] * inv, o[8 * u + 7] * inv);
+        reinterpret_cast<uint4*>(out)[u] = w;
+      }
+      if (kh == 0) p.lse[static_cast<long long>(z) * p.S + q] = (m + log2f(l)) * 0.69314718055994531f;
     }
   }
 
   ptx::pdl_trigger();
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 2 && lane == 0) mark(11);
+  if (warp == 0) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<256>(tmem);
   }
@@ -468,8 +545,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
         const int st = it & 1, b = it & 1;
         const uint32_t aq = ptx::smem_addr(sQ + st * kTileBytes), ao = ptx::smem_addr(sO + st * kTileBytes);
         const uint32_t ap = ptx::smem_addr(sP + b * 2 * kTileBytes), as = ptx::smem_addr(sS + b * 2 * kTileBytes);
-        ptx::mbar_wait(&pds_full[b], (it >> 1) & 1);  // softmax(it) wrote P / dS (and read S / dP)
-        if (it + 1 < n_iter) mma1(it + 1);            // next tile's scores overlap this tile's gradients
+        // next tile's scores as soon as softmax(it) has S / dP in registers:
+        // they overlap the rest of softmax(it) and this tile's gradients
+        if (it + 1 < n_iter) mma1(it + 1);
+        ptx::mbar_wait(&pds_full[b], (it >> 1) & 1);  // softmax(it) wrote P / dS
         ptx::mbar_wait(dq_empty, (it & 1) ^ 1);       // dQ(it-1) drained
         ptx::tc_fence_after();
 #pragma unroll
@@ -512,11 +591,23 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
         atomicAdd(dst + c * 8 + u, make_float4(__uint_as_float(v[4 * u]), __uint_as_float(v[4 * u + 1]),
                                                __uint_as_float(v[4 * u + 2]), __uint_as_float(v[4 * u + 3])));
     };
+    // lse / D of the next query tile are loaded one iteration ahead
+    float lse_n = 0.f, dsum_n = 0.f;
+    if (n_iter > 0) {
+      const long long idx = static_cast<long long>(z) * p.S + i_first * kT + r;
+      lse_n = p.lse[idx];
+      dsum_n = p.dsum[idx];
+    }
     for (int it = 0; it < n_iter; ++it) {
       const int i = i_first + it, q = i * kT + r;
       const int pb = it & 1;
-      const float lse2 = p.lse[static_cast<long long>(z) * p.S + q] * 1.4426950408889634f;
-      const float dsum = p.dsum[static_cast<long long>(z) * p.S + q];
+      const float lse2 = lse_n * 1.4426950408889634f;
+      const float dsum = dsum_n;
+      if (it + 1 < n_iter) {
+        const long long idx = static_cast<long long>(z) * p.S + q + kT;
+        lse_n = p.lse[idx];
+        dsum_n = p.dsum[idx];
+      }
       const bool diag = p.causal && i == j;
       ptx::mbar_wait(sp_full, it & 1);
       ptx::tc_fence_after();
@@ -536,12 +627,28 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
       for (int cc = 0; cc < 2; ++cc) {
         const int c = 2 * half + cc;
         float pv[32], dv[32];
+        if (!diag) {  // packed fp32x2 arithmetic: one FMA / add / mul per two scores
+          const float2 sl2 = make_float2(p.scale_log2, p.scale_log2), nl2 = make_float2(-lse2, -lse2);
+          const float2 nd2 = make_float2(-dsum, -dsum);
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const bool masked = diag && (k0 + c * 32 + e > q);
-          const float pe = masked ? 0.f : exp2_fast(__uint_as_float(vs[cc][e]) * p.scale_log2 - lse2);
-          pv[e] = pe;
-          dv[e] = pe * (__uint_as_float(vp[cc][e]) - dsum);
+          for (int e = 0; e < 32; e += 2) {
+            const float2 x =
+                __ffma2_rn(make_float2(__uint_as_float(vs[cc][e]), __uint_as_float(vs[cc][e + 1])), sl2, nl2);
+            pv[e] = exp2_fast(x.x);
+            pv[e + 1] = exp2_fast(x.y);
+            const float2 d = __fmul2_rn(make_float2(pv[e], pv[e + 1]),
+                                        __fadd2_rn(make_float2(__uint_as_float(vp[cc][e]), __uint_as_float(vp[cc][e + 1])), nd2));
+            dv[e] = d.x;
+            dv[e + 1] = d.y;
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const bool masked = k0 + c * 32 + e > q;
+            const float pe = masked ? 0.f : exp2_fast(__uint_as_float(vs[cc][e]) * p.scale_log2 - lse2);
+            pv[e] = pe;
+            dv[e] = pe * (__uint_as_float(vp[cc][e]) - dsum);
+          }
         }
         uint8_t* hp = hp0 + (c >> 1) * kTileBytes;
         uint8_t* hs = hs0 + (c >> 1) * kTileBytes;
@@ -675,7 +782,7 @@ CUtensorMap head_map(const void* base, int S, long long mats) {
   return map;
 }
 
-constexpr int kFwdSmem = 1024 + 5 * kTileBytes + 256;
+constexpr int kFwdSmem = 1024 + 6 * kTileBytes + 256 + 2 * 2 * 128 * 4;
 
 }  // namespace
 
@@ -709,6 +816,7 @@ void AttentionOp::forward(cudaStream_t s) const {
   p.part = desc_.fwd_part;
   p.flags = desc_.fwd_flags;
   p.n_items = 0;
+  p.trace = desc_.trace;
   const int nq = desc_.seq / kT;
   static const bool split_on = [] {
     const char* e = std::getenv("DPL_ATTN_SPLIT");

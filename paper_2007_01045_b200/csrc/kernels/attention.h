@@ -27,6 +27,9 @@ struct AttentionDesc {
   // int (zero before the first call; the merging CTA re-zeroes its entry).
   float* fwd_part = nullptr;
   int* fwd_flags = nullptr;
+  // diagnostics (tools/attn_trace.py): per-CTA %globaltimer marks of the
+  // forward, 16 slots per CTA; null in the product path
+  long long* trace = nullptr;
 };
 
 class AttentionOp {

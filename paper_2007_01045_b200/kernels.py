@@ -133,6 +133,12 @@ def attention_fwd(qkv, ctx, lse, samples, seq, heads, ldc, causal=False):
     check(lib().dpl_k_attention_fwd(_ptr(qkv), _ptr(ctx), ldc, _ptr(lse), samples, seq, heads, int(causal), _stream()))
 
 
+def attention_fwd_traced(qkv, ctx, lse, samples, seq, heads, ldc, trace, causal=False):
+    """attention_fwd with per-CTA %globaltimer marks in trace (int64, 16 per CTA)."""
+    check(lib().dpl_k_attention_fwd_traced(_ptr(qkv), _ptr(ctx), ldc, _ptr(lse), samples, seq, heads, int(causal),
+                                           _ptr(trace), _stream()))
+
+
 def attention_bwd(qkv, ctx, lse, dout, dqkv, dsum, dq_acc, samples, seq, heads, ldc, causal=False):
     """Fused flash attention backward (head dim 64)."""
     check(lib().dpl_k_attention_bwd(_ptr(qkv), _ptr(ctx), ldc, _ptr(lse), _ptr(dout), _ptr(dqkv), _ptr(dsum),
