@@ -117,6 +117,11 @@ int dpl_k_attention_fwd_traced(const void* qkv, void* ctx, long long ldc, float*
 int dpl_k_attention_bwd(const void* qkv, const void* ctx, long long ldc, const float* lse, const void* dout,
                         void* dqkv, float* dsum, float* dq_acc, int samples, int seq, int heads, int causal,
                         void* stream);
+/* Diagnostics: the same backward with 16 %globaltimer / %smid slots per CTA
+ * of the main kernel written to trace (tools/attn_trace.py --bwd). */
+int dpl_k_attention_bwd_traced(const void* qkv, const void* ctx, long long ldc, const float* lse, const void* dout,
+                               void* dqkv, float* dsum, float* dq_acc, int samples, int seq, int heads, int causal,
+                               long long* trace, void* stream);
 int dpl_k_layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y, float* mean, float* rstd,
                         int rows, int h, float eps, void* stream);
 int dpl_k_layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd, const float* gamma,

@@ -136,11 +136,23 @@ int dpl_k_attention_fwd_traced(const void* qkv, void* ctx, long long ldc, float*
   });
 }
 
+int dpl_k_attention_bwd_traced(const void* qkv, const void* ctx, long long ldc, const float* lse, const void* dout,
+                               void* dqkv, float* dsum, float* dq_acc, int samples, int seq, int heads, int causal,
+                               long long* trace, void* stream);
+
 int dpl_k_attention_bwd(const void* qkv, const void* ctx, long long ldc, const float* lse, const void* dout,
                         void* dqkv, float* dsum, float* dq_acc, int samples, int seq, int heads, int causal,
                         void* stream) {
+  return dpl_k_attention_bwd_traced(qkv, ctx, ldc, lse, dout, dqkv, dsum, dq_acc, samples, seq, heads, causal, nullptr,
+                                    stream);
+}
+
+int dpl_k_attention_bwd_traced(const void* qkv, const void* ctx, long long ldc, const float* lse, const void* dout,
+                               void* dqkv, float* dsum, float* dq_acc, int samples, int seq, int heads, int causal,
+                               long long* trace, void* stream) {
   return guarded([&] {
     dpl::AttentionDesc d;
+    d.trace = trace;
     d.qkv = qkv;
     d.ctx = const_cast<void*>(ctx);
     d.ldc = ldc;

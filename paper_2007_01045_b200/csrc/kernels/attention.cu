@@ -80,37 +80,42 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-// Two CTAs per SM (96 KB smem, 256 TMEM columns each): S single-buffered,
-// O and V double-buffered (V_{j+1} lands while PV_j runs); K, P single.  Ten warps: warp 0 TMA (and
-// the TMEM allocation), warp 1 MMA, warps 2-9 softmax -- two threads per
-// query row, each owning 64 of the tile's 128 key columns and 32 of the 64
-// output columns, so four softmax warps per SM sub-partition hide each
-// other's TMEM-load / SFU latency.  The row max of a tile is combined
-// through shared memory (a 64-thread named barrier per lane quadrant); the
-// row sums stay per thread until the end.  The MMA warp issues S_{j+1} ahead
-// of PV_j and the softmax releases S_j at its last TMEM load.
+// Two CTAs per SM (~66 KB smem, 256 TMEM columns each).  Ten warps: warp 0
+// TMA (and the TMEM allocation), warp 1 MMA, warps 2-9 softmax -- two threads
+// per query row, each owning 64 of the tile's 128 key columns and 32 of the
+// 64 output columns, so four softmax warps per SM sub-partition hide each
+// other's TMEM-load / SFU latency.
+// TMEM: S [0,128) fp32, P [128,192) bf16 pairs, O [192,256) fp32.  P goes
+// from the softmax registers to tensor memory (tcgen05.st) and the PV MMA
+// reads its A operand from there, and O accumulates in tensor memory across
+// key tiles: shared memory carries only the TMA tiles and the MMAs' Q / K / V
+// operands (80 KB per CTA-tile instead of 144 KB with P staged in smem --
+// the per-SM shared-memory bandwidth is what bounded the smem-P form).
+// O is rescaled only when a row's max grows by more than 2^8 (the stale max
+// keeps every P <= 256); l and the output use the same reference max.
+// The row max of a tile is combined through shared memory (a 64-thread
+// named barrier per lane quadrant); the row sums stay per thread until the
+// end.  The MMA warp issues S_{j+1} ahead of PV_j and the softmax releases
+// S_j at its last TMEM load.
 __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_constant__ AttnFwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                // 16 KB
   uint8_t* sK = sQ + kTileBytes;     // 16 KB
   uint8_t* sV = sK + kTileBytes;     // 2 x 16 KB
-  uint8_t* sP = sV + 2 * kTileBytes; // 32 KB (two 64-key halves)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * kTileBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 2 * kTileBytes);
   uint64_t* q_full = bars;
   uint64_t* k_full = bars + 1;
   uint64_t* k_empty = bars + 2;
   uint64_t* s_full = bars + 3;
   uint64_t* s_empty = bars + 4;
   uint64_t* p_full = bars + 5;
-  uint64_t* p_empty = bars + 6;
-  uint64_t* o_full = bars + 7;    // [2]
-  uint64_t* o_empty = bars + 9;   // [2]
-  uint64_t* v_full = bars + 11;   // [2]
-  uint64_t* v_empty = bars + 13;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
-  int* ticket = reinterpret_cast<int*>(bars + 16);
-  float* xch = reinterpret_cast<float*>(bars + 17);  // [2 tiles][2 halves][128 rows] row-max / row-sum exchange
+  uint64_t* p_empty = bars + 6;   // PV_j done: P free, O holds tiles 0..j
+  uint64_t* v_full = bars + 7;    // [2]
+  uint64_t* v_empty = bars + 9;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
+  int* ticket = reinterpret_cast<int*>(bars + 12);
+  float* xch = reinterpret_cast<float*>(bars + 13);  // [2 tiles][2 halves][128 rows] row-max / row-sum exchange
 
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
   long long* trace = p.trace ? p.trace + 16LL * (blockIdx.x + gridDim.x * blockIdx.y) : nullptr;
@@ -140,6 +145,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
   }
   const int q0 = qt * kT;
   const int zk = p.z_count + z, zv = 2 * p.z_count + z;
+  constexpr uint32_t kColP = 128, kColO = 192;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -155,10 +161,6 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
       ptx::mbar_init(s_empty, kSoftmaxThreads);
       ptx::mbar_init(p_full, kSoftmaxThreads);
       ptx::mbar_init(p_empty, 1);
-      for (int i = 0; i < 2; ++i) {
-        ptx::mbar_init(&o_full[i], 1);
-        ptx::mbar_init(&o_empty[i], kSoftmaxThreads);
-      }
       ptx::fence_barrier_init();
     }
     __syncwarp();
@@ -170,7 +172,6 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
   const uint32_t tmem = *tmem_slot;
   ptx::pdl_wait();
   if (warp == 2 && lane == 0) mark(1);
-  // TMEM columns: S [0,128), O buffers [128,192) [192,256)
 
   if (warp == 0) {
     if (lane == 0) {
@@ -189,9 +190,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
   } else if (warp == 1) {
     if (lane == 0) {
       const uint32_t idesc_s = ptx::idesc_bf16_f32(kT, kT, false, false);  // Q K-major, K K-major
-      const uint32_t idesc_o = ptx::idesc_bf16_f32(kT, kD, false, true);   // P K-major, V MN-major
+      const uint32_t idesc_o = ptx::idesc_bf16_f32(kT, kD, false, true);   // P (TMEM) K-major, V MN-major
       const uint32_t aq = ptx::smem_addr(sQ), bk = ptx::smem_addr(sK);
-      const uint32_t ap = ptx::smem_addr(sP);
       // S_j = Q K_j^T once K_j landed and the softmax read S_{j-1}
       auto issue_s = [&](int j) {
         const uint32_t ph = j & 1;
@@ -211,20 +211,16 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
       for (int j = 0; j < n_kv; ++j) {
         const uint32_t ph = j & 1;
         if (j + 1 < n_kv) issue_s(j + 1);
-        // O_j = P_j V_j
+        // O (+)= P_j V_j, P_j from tensor memory (16 keys = 8 columns per step)
         const int vb = j & 1;
         const uint32_t bv = ptx::smem_addr(sV + vb * kTileBytes);
         ptx::mbar_wait(&v_full[vb], (j >> 1) & 1);
         ptx::mbar_wait(p_full, ph);
-        ptx::mbar_wait(&o_empty[j & 1], ((j >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < kT / 16; ++k) {
-          const uint32_t a_off = (k >> 2) * kTileBytes + (k & 3) * 32;  // 64-key halves 16 KB apart
-          ptx::mma_bf16(tmem + 128 + (j & 1) * kD, ptx::smem_desc_sw128(ap + a_off, 16, 1024),
-                        ptx::smem_desc_sw128(bv + k * 16 * 128, 16, 1024), idesc_o, k > 0);
-        }
-        ptx::mma_commit(&o_full[j & 1]);
+        for (int k = 0; k < kT / 16; ++k)
+          ptx::mma_bf16_ts(tmem + kColO, tmem + kColP + k * 8, ptx::smem_desc_sw128(bv + k * 16 * 128, 16, 1024),
+                           idesc_o, (j | k) != 0);
         ptx::mma_commit(&v_empty[vb]);
         ptx::mma_commit(p_empty);
       }
@@ -236,7 +232,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
     const int q = q0 + r;
     const uint32_t trow = (quad * 32) << 16;
     const float c = p.scale_log2;
-    // the two warps of a lane quadrant meet at named barrier 1 + quad
+    // the two warps of a lane quadrant meet at a named barrier
     auto pair_sync = [&]() {
       switch (quad) {  // immediate barrier ids (a register id reserves all 16)
         case 0: asm volatile("bar.sync 1, 64;" ::: "memory"); break;
@@ -245,108 +241,107 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
         default: asm volatile("bar.sync 4, 64;" ::: "memory"); break;
       }
     };
-    float o[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) o[i] = 0.f;
-    float m = -INFINITY, l = 0.f;
-    float alpha_prev = 0.f;
-    for (int j = 0; j <= n_kv; ++j) {
-      float alpha = 1.f;
-      if (j < n_kv) {
-        const uint32_t ph = j & 1;
-        ptx::mbar_wait(s_full, ph);
-        ptx::tc_fence_after();
-        if (r == 0 && kh == 0 && j < 4) mark(2 + j);
-        const bool diag = p.causal && kv_lo + j == qt;
-        const int lim = diag ? r - 64 * kh : 63;  // last unmasked key column of this row, in this half
-        // pass 1: row max of the raw scores over this half (scale > 0 commutes with max)
-        float mx = -INFINITY;
+    constexpr float kRescale = 8.f;  // log2 headroom of the stale max
+    float m = -INFINITY, l = 0.f;    // reference max (scaled, log2 units) and this half's row sum
+    for (int j = 0; j < n_kv; ++j) {
+      const uint32_t ph = j & 1;
+      ptx::mbar_wait(s_full, ph);
+      ptx::tc_fence_after();
+      if (r == 0 && kh == 0 && j < 4) mark(2 + j);
+      const bool diag = p.causal && kv_lo + j == qt;
+      const int lim = diag ? r - 64 * kh : 63;  // last unmasked key column of this row, in this half
+      // pass 1: row max of the raw scores over this half (scale > 0 commutes with max)
+      float mx = -INFINITY;
 #pragma unroll 1
-        for (int cc = 0; cc < 2; ++cc) {
-          uint32_t v[32];
-          ptx::tmem_ld_32x32b_x32(tmem + trow + 64 * kh + cc * 32, v);
-          ptx::tmem_wait_ld();
-          if (!diag) {
+      for (int cc = 0; cc < 2; ++cc) {
+        uint32_t v[32];
+        ptx::tmem_ld_32x32b_x32(tmem + trow + 64 * kh + cc * 32, v);
+        ptx::tmem_wait_ld();
+        if (!diag) {
 #pragma unroll
-            for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(v[e]));
-          } else {
+          for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(v[e]));
+        } else {
 #pragma unroll
-            for (int e = 0; e < 32; ++e) mx = cc * 32 + e <= lim ? fmaxf(mx, __uint_as_float(v[e])) : mx;
-          }
+          for (int e = 0; e < 32; ++e) mx = cc * 32 + e <= lim ? fmaxf(mx, __uint_as_float(v[e])) : mx;
         }
-        float* xm = xch + (j & 1) * 256;
-        xm[kh * 128 + r] = mx;
-        pair_sync();
-        mx = fmaxf(mx, xm[(kh ^ 1) * 128 + r]);
-        const float m_new = fmaxf(m, mx * c);
-        alpha = exp2_fast(m - m_new);
-        m = m_new;
-        ptx::mbar_wait(p_empty, ph ^ 1);  // PV_{j-1} finished reading P
-        float2 rs2 = make_float2(0.f, 0.f);
-        uint8_t* ph_tile = sP + kh * kTileBytes;  // this half's 64 keys
-#pragma unroll 1
-        for (int cc = 0; cc < 2; ++cc) {
-          uint32_t v[32];
-          ptx::tmem_ld_32x32b_x32(tmem + trow + 64 * kh + cc * 32, v);
-          ptx::tmem_wait_ld();
-          if (cc == 1) {  // S_j fully read: the MMA may write S_{j+1}
-            ptx::tc_fence_before();
-            ptx::mbar_arrive(s_empty);
-          }
-          float pv[32];
-          if (!diag) {  // packed fp32x2 FMA / add: half the scale and row-sum instructions
-            const float2 c2 = make_float2(c, c), nm2 = make_float2(-m, -m);
-#pragma unroll
-            for (int e = 0; e < 32; e += 2) {
-              const float2 x = __ffma2_rn(make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])), c2, nm2);
-              pv[e] = exp2_fast(x.x);
-              pv[e + 1] = exp2_fast(x.y);
-              rs2 = __fadd2_rn(rs2, make_float2(pv[e], pv[e + 1]));
-            }
-          } else {
-#pragma unroll
-            for (int e = 0; e < 32; ++e) {
-              const float x = exp2_fast(fmaf(__uint_as_float(v[e]), c, -m));
-              pv[e] = cc * 32 + e <= lim ? x : 0.f;
-              rs2.x += pv[e];
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            uint4 w;
-            w.x = pack_bf16(pv[8 * u + 0], pv[8 * u + 1]);
-            w.y = pack_bf16(pv[8 * u + 2], pv[8 * u + 3]);
-            w.z = pack_bf16(pv[8 * u + 4], pv[8 * u + 5]);
-            w.w = pack_bf16(pv[8 * u + 6], pv[8 * u + 7]);
-            *reinterpret_cast<uint4*>(ph_tile + sw128(r, cc * 4 + u)) = w;
-          }
-        }
-        l = l * alpha + (rs2.x + rs2.y);  // this half's share of the row sum
-        fence_async_smem();
-        ptx::mbar_arrive(p_full);
-        if (r == 0 && kh == 0 && j < 4) mark(6 + j);
       }
-      if (j > 0) {  // O = O * alpha_{j-1} + O_{j-1} (this thread's 32 columns)
-        const int jj = j - 1;
-        ptx::mbar_wait(&o_full[jj & 1], (jj >> 1) & 1);
+      float* xm = xch + (j & 1) * 256;
+      xm[kh * 128 + r] = mx;
+      pair_sync();
+      mx = fmaxf(mx, xm[(kh ^ 1) * 128 + r]) * c;
+      ptx::mbar_wait(p_empty, ph ^ 1);  // PV_{j-1} done: P free, O current
+      // new reference max where a row's max grew past the headroom (both
+      // halves of a row decide alike); the TMEM rescale of O is warp-wide
+      // (.sync.aligned), with alpha = 1 on the rows that keep theirs
+      const bool need = mx > m + kRescale;
+      const float alpha = need ? exp2_fast(m - mx) : 1.f;
+      if (j > 0 && __any_sync(0xffffffffu, need)) {
         ptx::tc_fence_after();
         uint32_t v[32];
-        ptx::tmem_ld_32x32b_x32(tmem + trow + 128 + (jj & 1) * kD + 32 * kh, v);
+        ptx::tmem_ld_32x32b_x32(tmem + trow + kColO + 32 * kh, v);
         ptx::tmem_wait_ld();
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&o_empty[jj & 1]);
-        const float2 a2 = make_float2(alpha_prev, alpha_prev);
+        uint32_t w[16];
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          const float2 r2 =
-              __ffma2_rn(make_float2(o[e], o[e + 1]), a2, make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])));
-          o[e] = r2.x;
-          o[e + 1] = r2.y;
+        for (int h2 = 0; h2 < 2; ++h2) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) w[e] = __float_as_uint(__uint_as_float(v[16 * h2 + e]) * alpha);
+          ptx::tmem_st_32x32b_x16(tmem + trow + kColO + 32 * kh + 16 * h2, w);
         }
       }
-      alpha_prev = alpha;
+      if (need) {
+        l *= alpha;
+        m = mx;
+      }
+      float2 rs2 = make_float2(0.f, 0.f);
+#pragma unroll 1
+      for (int cc = 0; cc < 2; ++cc) {
+        uint32_t v[32];
+        ptx::tmem_ld_32x32b_x32(tmem + trow + 64 * kh + cc * 32, v);
+        ptx::tmem_wait_ld();
+        if (cc == 1) {  // S_j fully read: the MMA may write S_{j+1}
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(s_empty);
+        }
+        uint32_t pk[16];
+        if (!diag) {  // packed fp32x2 FMA / add: half the scale and row-sum instructions
+          const float2 c2 = make_float2(c, c), nm2 = make_float2(-m, -m);
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            const float2 x = __ffma2_rn(make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])), c2, nm2);
+            const float p0 = exp2_fast(x.x), p1 = exp2_fast(x.y);
+            rs2 = __fadd2_rn(rs2, make_float2(p0, p1));
+            pk[e >> 1] = pack_bf16(p0, p1);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            const float p0 = cc * 32 + e <= lim ? exp2_fast(fmaf(__uint_as_float(v[e]), c, -m)) : 0.f;
+            const float p1 = cc * 32 + e + 1 <= lim ? exp2_fast(fmaf(__uint_as_float(v[e + 1]), c, -m)) : 0.f;
+            rs2.x += p0;
+            rs2.x += p1;
+            pk[e >> 1] = pack_bf16(p0, p1);
+          }
+        }
+        ptx::tmem_st_32x32b_x16(tmem + trow + kColP + 32 * kh + 16 * cc, pk);
+      }
+      l += rs2.x + rs2.y;  // this half's share of the row sum
+      ptx::tmem_wait_st();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(p_full);
+      if (r == 0 && kh == 0 && j < 4) mark(6 + j);
     }
-    // full row sum: the two halves' shares (same max, same rescalings)
+    // O of this thread's 32 columns once the last PV finished
+    float o[32];
+    ptx::mbar_wait(p_empty, (n_kv - 1) & 1);
+    ptx::tc_fence_after();
+    {
+      uint32_t v[32];
+      ptx::tmem_ld_32x32b_x32(tmem + trow + kColO + 32 * kh, v);
+      ptx::tmem_wait_ld();
+#pragma unroll
+      for (int e = 0; e < 32; ++e) o[e] = __uint_as_float(v[e]);
+    }
+    // full row sum: the two halves' shares (same reference max)
     {
       float* xl = xch + (n_kv & 1) * 256;
       xl[kh * 128 + r] = l;
@@ -446,6 +441,7 @@ struct AttnBwdParams {
   __nv_bfloat16* dqkv;  // [B*S][3H]
   long long ld;         // 3H
   int H;
+  long long* trace;     // 16 %globaltimer slots per CTA (diagnostics), or null
 };
 
 __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_constant__ AttnBwdParams p) {
@@ -470,6 +466,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
 
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
+  long long* trace = p.trace ? p.trace + 16LL * (blockIdx.x + gridDim.x * blockIdx.y) : nullptr;
+  auto mark = [&](int slot) {
+    if (trace) trace[slot] = static_cast<long long>(ptx::globaltimer_ns());
+  };
+  if (warp == 4 && lane == 0) {
+    mark(0);
+    if (trace) {
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      trace[15] = smid;
+    }
+  }
   // causal: blockIdx = (z, j) so the block scheduler hands out every head's
   // longest key tile (j = 0 walks all query tiles) first and the short ones
   // fill the tail of the >1-wave grid; non-causal: (j, z)
@@ -503,6 +511,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   ptx::pdl_wait();
+  if (warp == 4 && lane == 0) mark(1);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -611,6 +620,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
       const bool diag = p.causal && i == j;
       ptx::mbar_wait(sp_full, it & 1);
       ptx::tc_fence_after();
+      if (warp == 4 && lane == 0 && it < 4) mark(2 + it);
       uint32_t vs[2][32], vp[2][32];
       ptx::tmem_ld_32x32b_x32(tmem + trow + (2 * half) * 32, vs[0]);
       ptx::tmem_ld_32x32b_x32(tmem + trow + 128 + (2 * half) * 32, vp[0]);
@@ -670,9 +680,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
       }
       fence_async_smem();
       ptx::mbar_arrive(&pds_full[pb]);
+      if (warp == 4 && lane == 0 && it < 4) mark(6 + it);
       if (it > 0) drain_dq(it - 1);
     }
     if (n_iter > 0) drain_dq(n_iter - 1);
+    if (warp == 4 && lane == 0) mark(10);
     // dV, dK of this key tile (all MMAs done once the last dQ arrived)
     const int key = k0 + r;
     __nv_bfloat16* row = p.dqkv + static_cast<long long>(b * p.S + key) * p.ld + h * kD;
@@ -701,6 +713,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
   ptx::pdl_trigger();
   ptx::tc_fence_before();
   __syncthreads();
+  if (warp == 4 && lane == 0) mark(11);
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<512>(tmem);
@@ -782,7 +795,7 @@ CUtensorMap head_map(const void* base, int S, long long mats) {
   return map;
 }
 
-constexpr int kFwdSmem = 1024 + 6 * kTileBytes + 256 + 2 * 2 * 128 * 4;
+constexpr int kFwdSmem = 1024 + 4 * kTileBytes + 256 + 2 * 2 * 128 * 4;
 
 }  // namespace
 
@@ -880,6 +893,7 @@ void AttentionOp::backward(cudaStream_t s) const {
   p.dqkv = static_cast<__nv_bfloat16*>(desc_.dqkv);
   p.ld = 3LL * desc_.heads * kD;
   p.H = desc_.heads * kD;
+  p.trace = desc_.trace;
   const dim3 bgrid = desc_.causal ? dim3(z_count, desc_.seq / kT) : dim3(desc_.seq / kT, z_count);
   launch_pdl(attn_bwd_kernel, bgrid, dim3(kBwdThreads), kBwdSmem, s, p);
   launch_pdl(attn_bwd_dq_kernel, dim3(std::min((rows + 15) / 16, 148 * 16)), dim3(256), 0, s,

@@ -143,3 +143,9 @@ def attention_bwd(qkv, ctx, lse, dout, dqkv, dsum, dq_acc, samples, seq, heads, 
     """Fused flash attention backward (head dim 64)."""
     check(lib().dpl_k_attention_bwd(_ptr(qkv), _ptr(ctx), ldc, _ptr(lse), _ptr(dout), _ptr(dqkv), _ptr(dsum),
                                     _ptr(dq_acc), samples, seq, heads, int(causal), _stream()))
+
+
+def attention_bwd_traced(qkv, ctx, lse, dout, dqkv, dsum, dq_acc, samples, seq, heads, ldc, trace, causal=False):
+    """attention_bwd with per-CTA %globaltimer marks of the main kernel in trace (int64, 16 per CTA)."""
+    check(lib().dpl_k_attention_bwd_traced(_ptr(qkv), _ptr(ctx), ldc, _ptr(lse), _ptr(dout), _ptr(dqkv), _ptr(dsum),
+                                           _ptr(dq_acc), samples, seq, heads, int(causal), _ptr(trace), _stream()))

@@ -3,6 +3,8 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2007_01045_b200/csrc/kernels tools/micro/tmem_bw.cu -o tools/micro/tmem_bw -lcuda
 #include <cstdio>
 #include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include "ptx.cuh"
 
 using namespace dpl;
@@ -66,6 +68,48 @@ __global__ void mufu(long long* out, int iters, float seed) {
   if (s == 1234.5f) out[0] = 0;
 }
 
+__global__ void mufu_bf16x2(long long* out, int iters, float seed) {
+  uint32_t x[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(-seed * (threadIdx.x + e), -seed * e);
+    x[e] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(x[e]));
+  }
+  const long long t1 = clock64();
+  __syncthreads();
+  if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+  uint32_t s = 0;
+  for (int e = 0; e < 8; ++e) s ^= x[e];
+  if (s == 12345u) out[0] = 0;
+}
+
+__global__ void mufu_f16x2(long long* out, int iters, float seed) {
+  uint32_t x[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    __half2 h = __floats2half2_rn(-seed * (threadIdx.x + e), -seed * e);
+    x[e] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(x[e]));
+  }
+  const long long t1 = clock64();
+  __syncthreads();
+  if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+  uint32_t s = 0;
+  for (int e = 0; e < 8; ++e) s ^= x[e];
+  if (s == 12345u) out[0] = 0;
+}
+
 template <typename K>
 void run(const char* name, K kernel, int threads, int iters, double bytes_per_warp_iter) {
   long long* d;
@@ -103,6 +147,18 @@ int main() {
     for (int i = 0; i < 148; ++i) cyc += h[i];
     cyc /= 148;
     printf("ex2 threads %3d: %.2f ex2/cycle/SM\n", threads, threads * 8.0 * 1024 / cyc);
+  }
+  for (int threads : {128, 256, 512}) {
+    for (int kind = 0; kind < 2; ++kind) {
+      if (kind == 0) mufu_bf16x2<<<148, threads>>>(d, 1024, 1e-3f), mufu_bf16x2<<<148, threads>>>(d, 1024, 1e-3f);
+      else mufu_f16x2<<<148, threads>>>(d, 1024, 1e-3f), mufu_f16x2<<<148, threads>>>(d, 1024, 1e-3f);
+      long long h[148];
+      cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+      double cyc = 0;
+      for (int i = 0; i < 148; ++i) cyc += h[i];
+      cyc /= 148;
+      printf("ex2 %s threads %3d: %.2f results/cycle/SM\n", kind ? "f16x2" : "bf16x2", threads, threads * 16.0 * 1024 / cyc);
+    }
   }
   cudaError_t e = cudaDeviceSynchronize();
   printf("status %s\n", cudaGetErrorString(e));
