@@ -187,8 +187,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
         ptx::tma_load_3d(sV + b * kTileBytes, &p.qkv, &v_full[b], 0, (kv_lo + j) * kT, zv);
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {
+  } else if (warp == 1) {  // whole warp: descriptors uniform, one elected lane issues
+    {
       const uint32_t idesc_s = ptx::idesc_bf16_f32(kT, kT, false, false);  // Q K-major, K K-major
       const uint32_t idesc_o = ptx::idesc_bf16_f32(kT, kD, false, true);   // P (TMEM) K-major, V MN-major
       const uint32_t aq = ptx::smem_addr(sQ), bk = ptx::smem_addr(sK);
@@ -200,13 +200,13 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
         ptx::tc_fence_after();
 #pragma unroll
         for (int k = 0; k < kD / 16; ++k)
-          ptx::mma_bf16(tmem, ptx::smem_desc_sw128(aq + k * 32, 16, 1024), ptx::smem_desc_sw128(bk + k * 32, 16, 1024),
+          ptx::mma_bf16_e(tmem, ptx::smem_desc_sw128(aq + k * 32, 16, 1024), ptx::smem_desc_sw128(bk + k * 32, 16, 1024),
                         idesc_s, k > 0);
-        ptx::mma_commit(s_full);
-        ptx::mma_commit(k_empty);
+        ptx::mma_commit_e(s_full);
+        ptx::mma_commit_e(k_empty);
       };
       ptx::mbar_wait(q_full, 0);
-      mark(12);
+      if (lane == 0) mark(12);
       if (n_kv > 0) issue_s(0);
       for (int j = 0; j < n_kv; ++j) {
         const uint32_t ph = j & 1;
@@ -219,10 +219,10 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_kernel(const __grid_c
         ptx::tc_fence_after();
 #pragma unroll
         for (int k = 0; k < kT / 16; ++k)
-          ptx::mma_bf16_ts(tmem + kColO, tmem + kColP + k * 8, ptx::smem_desc_sw128(bv + k * 16 * 128, 16, 1024),
+          ptx::mma_bf16_ts_e(tmem + kColO, tmem + kColP + k * 8, ptx::smem_desc_sw128(bv + k * 16 * 128, 16, 1024),
                            idesc_o, (j | k) != 0);
-        ptx::mma_commit(&v_empty[vb]);
-        ptx::mma_commit(p_empty);
+        ptx::mma_commit_e(&v_empty[vb]);
+        ptx::mma_commit_e(p_empty);
       }
     }
   } else {
@@ -526,8 +526,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
         ptx::tma_load_3d(sO + st * kTileBytes, &p.dout, &qdo_full[st], 0, q0, z);
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {
+  } else if (warp == 1) {  // whole warp: descriptors uniform, one elected lane issues
+    {
       const uint32_t id_sq = ptx::idesc_bf16_f32(kT, kT, false, false);  // S, dP: K-major A and B
       const uint32_t id_tt = ptx::idesc_bf16_f32(kT, kD, true, true);    // dV, dK: A^T, B MN-major
       const uint32_t id_dq = ptx::idesc_bf16_f32(kT, kD, false, true);   // dQ: dS K-major, K MN-major
@@ -541,12 +541,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
         ptx::tc_fence_after();
 #pragma unroll
         for (int k = 0; k < kD / 16; ++k) {
-          ptx::mma_bf16(tmem, ptx::smem_desc_sw128(aq + k * 32, 16, 1024), ptx::smem_desc_sw128(ak + k * 32, 16, 1024),
+          ptx::mma_bf16_e(tmem, ptx::smem_desc_sw128(aq + k * 32, 16, 1024), ptx::smem_desc_sw128(ak + k * 32, 16, 1024),
                         id_sq, k > 0);
-          ptx::mma_bf16(tmem + 128, ptx::smem_desc_sw128(ao + k * 32, 16, 1024),
+          ptx::mma_bf16_e(tmem + 128, ptx::smem_desc_sw128(ao + k * 32, 16, 1024),
                         ptx::smem_desc_sw128(av + k * 32, 16, 1024), id_sq, k > 0);
         }
-        ptx::mma_commit(sp_full);
+        ptx::mma_commit_e(sp_full);
       };
       ptx::mbar_wait(kv_full, 0);
       if (n_iter > 0) mma1(0);
@@ -564,17 +564,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
         for (int k = 0; k < kT / 16; ++k) {
           // A^T views: 64-key halves 16 KB apart (LBO), 16 query rows per K step
           const uint32_t row_step = k * 16 * 128;
-          ptx::mma_bf16(tmem + 256, ptx::smem_desc_sw128(ap + row_step, kTileBytes, 1024),
+          ptx::mma_bf16_e(tmem + 256, ptx::smem_desc_sw128(ap + row_step, kTileBytes, 1024),
                         ptx::smem_desc_sw128(ao + row_step, 16, 1024), id_tt, (it | k) != 0);
-          ptx::mma_bf16(tmem + 320, ptx::smem_desc_sw128(as + row_step, kTileBytes, 1024),
+          ptx::mma_bf16_e(tmem + 320, ptx::smem_desc_sw128(as + row_step, kTileBytes, 1024),
                         ptx::smem_desc_sw128(aq + row_step, 16, 1024), id_tt, (it | k) != 0);
           const uint32_t a_off = (k >> 2) * kTileBytes + (k & 3) * 32;
-          ptx::mma_bf16(tmem + 384, ptx::smem_desc_sw128(as + a_off, 16, 1024),
+          ptx::mma_bf16_e(tmem + 384, ptx::smem_desc_sw128(as + a_off, 16, 1024),
                         ptx::smem_desc_sw128(ak + row_step, 16, 1024), id_dq, k > 0);
         }
-        ptx::mma_commit(&qdo_empty[st]);
-        ptx::mma_commit(&pds_empty[b]);
-        ptx::mma_commit(dq_full);
+        ptx::mma_commit_e(&qdo_empty[st]);
+        ptx::mma_commit_e(&pds_empty[b]);
+        ptx::mma_commit_e(dq_full);
       }
     }
   } else if (warp >= 4) {

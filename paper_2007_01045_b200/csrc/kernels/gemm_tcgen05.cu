@@ -592,7 +592,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // (the whole warp runs the loop; one elected lane issues each MMA)
+    {
       const uint32_t idesc = ptx::idesc_bf16_f32(kBM, BN, p.a_mn_major != 0, p.b_mn_major != 0);
       // K-major: 8-row groups 1024 B apart, advance 32 B per K=16 step.
       // MN-major: 64-wide MN chunks 8 KB apart (LBO), 8-row K groups 1 KB
@@ -615,23 +616,23 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
         for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
-          if (t == static_cast<int>(blockIdx.x) && kb == kb0) trace_mark(p, 3);
+          if (lane == 0 && t == static_cast<int>(blockIdx.x) && kb == kb0) trace_mark(p, 3);
           const uint32_t sa = ptx::smem_addr(smem_a + stage * C::kABytes);
           const uint32_t sb = ptx::smem_addr(smem_b + stage * C::kBBytes);
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
             const uint64_t ad = ptx::smem_desc_sw128(sa + k * a_step, a_lbo, 1024);
             const uint64_t bd = ptx::smem_desc_sw128(sb + k * b_step, b_lbo, 1024);
-            ptx::mma_bf16(tmem_d, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+            ptx::mma_bf16_e(tmem_d, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
           }
-          ptx::mma_commit(&empty[stage]);
+          ptx::mma_commit_e(&empty[stage]);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
         }
-        ptx::mma_commit(&tmem_full[acc]);
-        trace_mark(p, 4);
+        ptx::mma_commit_e(&tmem_full[acc]);
+        if (lane == 0) trace_mark(p, 4);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -851,7 +852,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
       }
     }
   } else if (warp == 1) {
-    if (leader && lane == 0) {
+    if (leader) {  // the whole warp runs the loop; one elected lane issues each MMA
       const uint32_t idesc = ptx::idesc_bf16_f32(256, kBN, p.a_mn_major != 0, p.b_mn_major != 0);
       const uint32_t a_lbo = p.a_mn_major ? 64 * kBK * 2 : 16;
       const uint32_t b_lbo = p.b_mn_major ? 64 * kBK * 2 : 16;
@@ -871,23 +872,23 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
         for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
-          if (t == pair_id && kb == kb0) trace_mark(p, 3);
+          if (lane == 0 && t == pair_id && kb == kb0) trace_mark(p, 3);
           const uint32_t sa = ptx::smem_addr(smem_a + stage * kABytes);
           const uint32_t sb = ptx::smem_addr(smem_b + stage * kBBytes);
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
             const uint64_t ad = ptx::smem_desc_sw128(sa + k * a_step, a_lbo, 1024);
             const uint64_t bd = ptx::smem_desc_sw128(sb + k * b_step, b_lbo, 1024);
-            ptx::mma_bf16_2sm(tmem_d, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+            ptx::mma_bf16_2sm_e(tmem_d, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
           }
-          ptx::mma_commit_2sm(&empty[stage]);
+          ptx::mma_commit_2sm_e(&empty[stage]);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
         }
-        ptx::mma_commit_2sm(&tmem_full[acc]);
-        trace_mark(p, 4);
+        ptx::mma_commit_2sm_e(&tmem_full[acc]);
+        if (lane == 0) trace_mark(p, 4);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
