@@ -69,6 +69,9 @@ struct GemmDesc {
   // side only; the GemmCache fills it in): zero on entry and left zero
   float* split_ws = nullptr;
   size_t split_ws_bytes = 0;
+  // cap on the persistent grid in CTAs (0: one per SM): a GEMM on a side
+  // stream can leave SMs to the critical-path stream (host side only)
+  int max_ctas = 0;
 };
 
 // Device-visible launch parameters (one per prepared GEMM).
@@ -196,6 +199,9 @@ class GemmCache {
   // (they all run on one stream, one after another); null disables them
   float* split_ws = nullptr;
   size_t split_ws_bytes = 0;
+  // nonzero: GemmDesc::max_ctas for every GEMM fetched while it is set
+  // (StageContext::on_side caps the weight-gradient stream's grids)
+  int max_ctas_override = 0;
 
  private:
   struct Impl;

@@ -1326,7 +1326,7 @@ void GemmOp::prepare(const GemmDesc& d) {
     const char* e = std::getenv("DPL_GEMM_MAX_CTAS");
     return e ? std::max(2, std::atoi(e)) : 1 << 30;
   }();
-  const int sms = std::min(num_sms(), max_ctas);
+  const int sms = std::min(num_sms(), d.max_ctas > 1 ? std::min(max_ctas, d.max_ctas) : max_ctas);
   grid_ = two_sm ? 2 * std::min(p.num_tiles, sms / 2) : std::min(p.num_tiles, sms);
   if (two_sm) {
     smem_ = pair::kSmem;
@@ -1354,6 +1354,7 @@ const GemmOp& GemmCache::get(const GemmDesc& dd) {
   GemmDesc d = dd;  // this cache's split-K scratch (not part of the key: one per cache)
   d.split_ws = split_ws;
   d.split_ws_bytes = split_ws_bytes;
+  if (max_ctas_override) d.max_ctas = max_ctas_override;
   // explicit field-wise key: no padding bytes
   const long long f[] = {d.M, d.N, d.K, d.batch,
                          static_cast<long long>(reinterpret_cast<uintptr_t>(d.A)), d.lda, d.a_batch_stride,
@@ -1369,7 +1370,7 @@ const GemmOp& GemmCache::get(const GemmDesc& dd) {
                          static_cast<long long>(reinterpret_cast<uintptr_t>(d.trace)),
                          static_cast<long long>(reinterpret_cast<uintptr_t>(d.colsum)),
                          static_cast<long long>(reinterpret_cast<uintptr_t>(d.conv_x)), d.conv_operand, d.conv_n,
-                         d.conv_h, d.conv_w, d.conv_c};
+                         d.conv_h, d.conv_w, d.conv_c, d.max_ctas};
   std::string key(reinterpret_cast<const char*>(f), sizeof f);
   uint32_t a;
   std::memcpy(&a, &d.alpha, 4);

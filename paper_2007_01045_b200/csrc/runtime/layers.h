@@ -90,6 +90,9 @@ struct StageContext {
   cudaStream_t wstream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // run f(stream) on the side stream after everything issued so far on `stream`
+  // (side-stream GEMM grids capped at wgrad_ctas CTAs when nonzero, so the
+  // critical-path stream keeps SMs)
+  int wgrad_ctas = 0;
   template <typename F>
   void on_side(F&& f) {
     if (!wstream) {
@@ -98,7 +101,9 @@ struct StageContext {
     }
     cudaEventRecord(ev_fork, stream);
     cudaStreamWaitEvent(wstream, ev_fork, 0);
+    gemms.max_ctas_override = wgrad_ctas;
     f(wstream);
+    gemms.max_ctas_override = 0;
   }
   // `stream` waits for the side stream's work so far
   void join_side() {
