@@ -80,6 +80,12 @@ __device__ __forceinline__ void unpack8(const uint4& r, float (&f)[8]) {
     f[2 * e + 1] = x.y;
   }
 }
+__device__ __forceinline__ void lds8(const float* p, float (&f)[8]) {
+  const float4 a = reinterpret_cast<const float4*>(p)[0];
+  const float4 b = reinterpret_cast<const float4*>(p)[1];
+  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+  f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
 __device__ __forceinline__ void ldg8(const float* p, float (&f)[8]) {
   const float4 a = __ldg(reinterpret_cast<const float4*>(p));
   const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
@@ -88,13 +94,23 @@ __device__ __forceinline__ void ldg8(const float* p, float (&f)[8]) {
 }
 
 // One warp per row; the row stays in registers as packed bf16 (4 registers
-// per 8 values) and gamma / beta are re-read through L1, so the kernel fits
-// 64 registers and keeps 32 warps per SM in flight.
+// per 8 values), so the kernel fits 64 registers and keeps 32 warps per SM in
+// flight.  gamma / beta (parameters, not written by the preceding kernel) are
+// staged in shared memory before the programmatic-dependency wait, so their
+// load overlaps the producer's tail instead of following the row load.
 template <int kMaxVec>
 __global__ void __launch_bounds__(256, 4)
     layernorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ gamma,
                          const float* __restrict__ beta, __nv_bfloat16* __restrict__ y, float* __restrict__ mean_out,
                          float* __restrict__ rstd_out, int rows, int h, float eps) {
+  extern __shared__ float4 ln_par[];  // gamma [h], beta [h]
+  float* sg = reinterpret_cast<float*>(ln_par);
+  float* sb = sg + h;
+  for (int i = threadIdx.x; i < h / 4; i += blockDim.x) {
+    reinterpret_cast<float4*>(sg)[i] = __ldg(reinterpret_cast<const float4*>(gamma) + i);
+    reinterpret_cast<float4*>(sb)[i] = __ldg(reinterpret_cast<const float4*>(beta) + i);
+  }
+  __syncthreads();
   ptx::pdl_wait();
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -134,8 +150,8 @@ __global__ void __launch_bounds__(256, 4)
       if (vi < nvec) {
         float v[8], g[8], b[8], o[8];
         unpack8(raw[i], v);
-        ldg8(gamma + vi * 8, g);
-        ldg8(beta + vi * 8, b);
+        lds8(sg + vi * 8, g);
+        lds8(sb + vi * 8, b);
 #pragma unroll
         for (int e = 0; e < 8; ++e) o[e] = (v[e] - mean) * rstd * g[e] + b[e];
         store8(yr + vi * 8, o);
@@ -157,6 +173,11 @@ __global__ void __launch_bounds__(256, kMaxVec > 4 ? 2 : 4)  // h > 1024 (GPT-2)
                               const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
                               const float* __restrict__ gamma, const __nv_bfloat16* __restrict__ dresid,
                               __nv_bfloat16* __restrict__ dx, int rows, int h) {
+  extern __shared__ float4 ln_par[];  // gamma [h], staged before the dependency wait
+  float* sg = reinterpret_cast<float*>(ln_par);
+  for (int i = threadIdx.x; i < h / 4; i += blockDim.x)
+    reinterpret_cast<float4*>(sg)[i] = __ldg(reinterpret_cast<const float4*>(gamma) + i);
+  __syncthreads();
   ptx::pdl_wait();
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -182,7 +203,7 @@ __global__ void __launch_bounds__(256, kMaxVec > 4 ? 2 : 4)  // h > 1024 (GPT-2)
         float xv[8], dv[8], g[8];
         unpack8(rx[i], xv);
         unpack8(rd[i], dv);
-        ldg8(gamma + vi * 8, g);
+        lds8(sg + vi * 8, g);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const float gd = dv[e] * g[e];
@@ -200,7 +221,7 @@ __global__ void __launch_bounds__(256, kMaxVec > 4 ? 2 : 4)  // h > 1024 (GPT-2)
         float xv[8], dv[8], g[8], rr[8], o[8];
         unpack8(rx[i], xv);
         unpack8(rd[i], dv);
-        ldg8(gamma + vi * 8, g);
+        lds8(sg + vi * 8, g);
         if (dresid) {
           load8(dresid + base + vi * 8, rr);
         } else {
@@ -613,7 +634,7 @@ void layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y
   const int warps = 8;
   const int grid = std::max(1, std::min((rows + warps - 1) / warps, 148 * 8));
   dispatch_vec(h, [&](auto v) {
-    launch_pdl(layernorm_fwd_kernel<decltype(v)::value>, dim3(grid), dim3(warps * 32), 0, s, 
+    launch_pdl(layernorm_fwd_kernel<decltype(v)::value>, dim3(grid), dim3(warps * 32), 2 * h * sizeof(float), s, 
         static_cast<const __nv_bfloat16*>(x), gamma, beta, static_cast<__nv_bfloat16*>(y), mean, rstd, rows, h, eps);
   });
 }
@@ -633,7 +654,7 @@ void layernorm_bwd(const void* dy, const void* x, const float* mean, const float
   const auto* pr = static_cast<const __nv_bfloat16*>(dresid);
   auto* pdx = static_cast<__nv_bfloat16*>(dx);
   dispatch_vec(h, [&](auto v) {
-    launch_pdl(layernorm_bwd_rows_kernel<decltype(v)::value>, dim3(grid), dim3(warps * 32), 0, s, pdy, px, mean, rstd, gamma, pr, pdx,
+    launch_pdl(layernorm_bwd_rows_kernel<decltype(v)::value>, dim3(grid), dim3(warps * 32), h * sizeof(float), s, pdy, px, mean, rstd, gamma, pr, pdx,
                                                                               rows, h);
   });
   const int nred = dx_colsum ? 4 : (dresid_colsum ? 3 : 2);
