@@ -71,7 +71,8 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
 // waiting thread sleeps in hardware until the phase completes instead of
 // spinning -- a spinning producer / MMA lane otherwise takes issue slots from
 // the softmax / epilogue warps on its SM sub-partition.  Traps after 20 s (a
-// deadlock, not a slow phase).
+// deadlock, not a slow phase).  Build with -DDPL_MBAR_SPIN for the plain
+// spinning wait (the A/B in profiles/r02/SUMMARY.md).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_addr(bar);
   uint32_t done = 0;
