@@ -118,33 +118,46 @@ def plan_fixed_point(model: dict, profiles: dict, mb: int, cluster: dict, m: int
     def key(pl):
         return json.dumps([[s["layers"], s["gpus"]] for s in pl["stages"]])
 
-    prof = profiles[mb]
     cands = {}
     history = []
-    for _ in range(max_iter):
-        res = pipeplan.plan(prof, cluster, m)["plan"]
-        k = key(res)
-        seen = k in cands
-        if not seen:
-            for st in res["stages"]:
-                size = -(-mb // len(st["gpus"]))
-                if size not in profiles:
-                    profiles[size] = profile_model(model, size)
-            own = slice_profile(profiles, res, mb)
-            seq = pipeplan.build_stage_sequence(res, own, cluster)
-            est = pipeplan.estimate_latency(seq, m)["total"]
-            sim = pipeplan.simulate_plan(res, own, cluster, m)["latency"]
-            cands[k] = (res, own, est, sim)
-        history.append({"stages": json.loads(k), "phi": res.get("phi"),
-                        "planner_est_ms": res.get("est_latency_us", 0) / 1e3,
-                        "planner_sim_ms": res.get("sim_latency_us", 0) / 1e3,
-                        "own_profile_est_ms": cands[k][2] * 1e3, "own_profile_sim_ms": cands[k][3] * 1e3})
-        if seen:
-            break
-        prof = cands[k][1]
+    # Start from the full micro-batch profile and, so the choice does not hinge
+    # on which proposals one chain happens to visit, also from the profile at
+    # the slice of every replication factor r <= the GPU count (a plan whose
+    # stages run r-way replicas is priced at the time they really take).
+    n_gpus = sum(cluster.get("seps", [1]))
+    starts = [mb] + sorted({-(-mb // r) for r in range(2, n_gpus + 1)} - {mb}, reverse=True)
+    fixed = False
+    for start in starts:
+        if start not in profiles:
+            profiles[start] = profile_model(model, start)
+        prof = profiles[start]
+        chain = []
+        for _ in range(max_iter):
+            res = pipeplan.plan(prof, cluster, m)["plan"]
+            k = key(res)
+            seen = k in cands
+            if not seen:
+                for st in res["stages"]:
+                    size = -(-mb // len(st["gpus"]))
+                    if size not in profiles:
+                        profiles[size] = profile_model(model, size)
+                own = slice_profile(profiles, res, mb)
+                seq = pipeplan.build_stage_sequence(res, own, cluster)
+                est = pipeplan.estimate_latency(seq, m)["total"]
+                sim = pipeplan.simulate_plan(res, own, cluster, m)["latency"]
+                cands[k] = (res, own, est, sim)
+            chain.append({"start_slice": start, "stages": json.loads(k), "phi": res.get("phi"),
+                          "planner_est_ms": res.get("est_latency_us", 0) / 1e3,
+                          "planner_sim_ms": res.get("sim_latency_us", 0) / 1e3,
+                          "own_profile_est_ms": cands[k][2] * 1e3, "own_profile_sim_ms": cands[k][3] * 1e3})
+            if seen:
+                break
+            prof = cands[k][1]
+        if start == mb:
+            fixed = len(chain) >= 2 and chain[-1]["stages"] == chain[-2]["stages"]
+        history += chain
     best = min(cands.values(), key=lambda c: c[3])
     plan, own, est, sim = best
-    fixed = len(history) >= 2 and history[-1]["stages"] == history[-2]["stages"]
     return plan, {"iterations": history, "fixed_point": fixed, "candidates": len(cands),
                   "per_gpu_memory_gb": cluster["per_gpu_memory_gb"],
                   "est_latency_ms": est * 1e3, "sim_latency_ms": sim * 1e3,

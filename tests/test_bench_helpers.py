@@ -120,9 +120,12 @@ def test_plan_fixed_point_replans_on_slice_profiles(monkeypatch):
     profiles = {8: fake_profile(None, 8)}
     plan, info = bench.plan_fixed_point({"layers": 24}, profiles, 8, bench.b200_cluster(4, 6.0), 8)
     assert info["fixed_point"]
-    last = info["iterations"][-1]
-    assert last["stages"] == [[s["layers"], s["gpus"]] for s in plan["stages"]]
+    chosen = [[s["layers"], s["gpus"]] for s in plan["stages"]]
+    assert any(it["stages"] == chosen for it in info["iterations"])
     assert info["sim_latency_ms"] > 0
+    # every chain starts from the full micro-batch or a replica slice of it
+    assert {it["start_slice"] for it in info["iterations"]} <= {8, 4, 3, 2}
+    assert info["iterations"][0]["start_slice"] == 8
     for st in plan["stages"]:
         assert -(-8 // len(st["gpus"])) in profiles
 
@@ -149,7 +152,8 @@ def test_plan_fixed_point_picks_the_self_consistent_best(monkeypatch):
     assert info["sim_latency_ms"] == pytest.approx(min(sims))
     own = bench.slice_profile(profiles, plan, 8)
     assert pipeplan.simulate_plan(plan, own, cl, 8)["latency"] * 1e3 == pytest.approx(info["sim_latency_ms"])
-    assert len(info["iterations"]) <= 5
+    starts = {it["start_slice"] for it in info["iterations"]}
+    assert all(sum(it["start_slice"] == st for it in info["iterations"]) <= 5 for st in starts)
 
 
 def test_amoebanet_stand_in_shapes():

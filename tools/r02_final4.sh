@@ -1,6 +1,6 @@
 #!/bin/bash
 # Final 4-GPU confirmation of the round-2 tree.
-out=gpurun_out/r2f5; mkdir -p $out
+out=${OUT:-gpurun_out/r2f6}; mkdir -p $out
 timeout 1800 python -m pytest tests -m gpu -q --timeout 600 --timeout-method thread -p no:cacheprovider -rf > $out/pytest_4gpu.txt 2>&1
 tail -3 $out/pytest_4gpu.txt
 run() { # n tag args...
