@@ -318,12 +318,12 @@ __device__ __forceinline__ float* epi_bias(const GemmParams& p, const EpiTma& e)
   return reinterpret_cast<float*>(e.region + p.epi_warp_bytes - p.epi_tile_cols * 4);
 }
 
-// lane 0: bulk-load the extra input of the chunk at (row0, n0) into x buffer b
+// whole warp (one elected lane issues): bulk-load the extra input of the
+// chunk at (row0, n0) into x buffer b
 __device__ __forceinline__ void epi_issue_x(const GemmParams& p, EpiTma& e, int b, int z, int row0, int n0) {
   int c[5];
   epi_coords(p, z, row0, n0, c);
-  ptx::mbar_arrive_expect_tx(&e.xbar[b], kXBytes);
-  ptx::tma_load_5d(epi_xbuf(p, e, b), &p.tma_x, &e.xbar[b], c[0], c[1], c[2], c[3], c[4]);
+  ptx::tma_load_5d_e(epi_xbuf(p, e, b), &p.tma_x, &e.xbar[b], kXBytes, c[0], c[1], c[2], c[3], c[4]);
 }
 
 // Before the tile's accumulator is ready: prefetch up to epi_nx input chunks
@@ -336,12 +336,10 @@ __device__ __forceinline__ void epi_tile_prefetch(const GemmParams& p, EpiTma& e
   // the previous tile's generic reads of these buffers precede the new bulk loads
   ptx::fence_proxy_async_smem();
   __syncwarp();
-  if (lane != 0) return;
   if (bias) {
     const int cols = min(p.epi_tile_cols, p.N - col0);
     const uint32_t bytes = static_cast<uint32_t>((cols * 4 + 15) & ~15);
-    ptx::mbar_arrive_expect_tx(&e.xbar[kMaxNx], bytes);
-    ptx::bulk_load(epi_bias(p, e), p.bias + col0, bytes, &e.xbar[kMaxNx]);
+    ptx::bulk_load_e(epi_bias(p, e), p.bias + col0, bytes, &e.xbar[kMaxNx]);
   }
   if (!epi_has_x_in(p)) return;
 #pragma unroll
@@ -412,7 +410,7 @@ __device__ __forceinline__ void epi_tile_tma(const GemmParams& p, EpiTma& e, uin
         ptx::fence_proxy_async_smem();
         __syncwarp();
         const int n2 = col0 + (c + 2 * p.epi_nx) * 32;
-        if (lane == 0 && n2 < p.N) epi_issue_x(p, e, xb, z, row0, n2);
+        if (n2 < p.N) epi_issue_x(p, e, xb, z, row0, n2);
       }
       if (epi & kResid) {
 #pragma unroll
@@ -427,7 +425,7 @@ __device__ __forceinline__ void epi_tile_tma(const GemmParams& p, EpiTma& e, uin
     }
     EPI_MARK(j, 1);
     // output buffer ob (and the aux buffer) were last read by the bulk store two chunks ago
-    if (lane == 0) ptx::bulk_wait_read<1>();
+    ptx::bulk_wait_read<1>();
     __syncwarp();
     if (epi & kAuxOut) {
       uint8_t* abuf = epi_xbuf(p, e, ob);
@@ -484,13 +482,11 @@ __device__ __forceinline__ void epi_tile_tma(const GemmParams& p, EpiTma& e, uin
     }
     ptx::fence_proxy_async_smem();
     __syncwarp();
-    if (lane == 0) {
+    {
       int cc[5];
       epi_coords(p, z, row0, n0, cc);
-      if (kind == kOutF32Acc) ptx::tma_reduce_add_5d(&p.tma_c, obuf, cc[0], cc[1], cc[2], cc[3], cc[4]);
-      else ptx::tma_store_5d(&p.tma_c, obuf, cc[0], cc[1], cc[2], cc[3], cc[4]);
-      if (epi & kAuxOut) ptx::tma_store_5d(&p.tma_x, epi_xbuf(p, e, ob), cc[0], cc[1], cc[2], cc[3], cc[4]);
-      ptx::bulk_commit();
+      ptx::tma_store_chunk_e(&p.tma_c, obuf, kind == kOutF32Acc, &p.tma_x,
+                             (epi & kAuxOut) ? epi_xbuf(p, e, ob) : nullptr, cc);
     }
     ++e.seq;
   }
@@ -666,7 +662,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05(const __grid_co
         acc_phase ^= 1;
       }
     }
-    if (ptx::lane_id() == 0) ptx::bulk_wait<0>();
+    ptx::bulk_wait<0>();
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const uint32_t quad = warp & 3;          // TMEM lane quadrant this warp may access
@@ -925,7 +921,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
         acc_phase ^= 1;
       }
     }
-    if (lane == 0) ptx::bulk_wait<0>();
+    ptx::bulk_wait<0>();
   } else if (warp >= 4) {
     const uint32_t quad = warp & 3;
     const int half = (warp - 4) >> 2;

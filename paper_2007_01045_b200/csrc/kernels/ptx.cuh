@@ -160,6 +160,56 @@ template <int N>
 __device__ __forceinline__ void bulk_wait() {
   asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
+// Elected-lane forms for a converged warp (see mma_bf16_e): the whole warp
+// executes them with warp-uniform operands and one elect.sync lane issues,
+// so ptxas does not wrap the uniform-datapath TMA instruction in a per-lane
+// loop.  Waits on bulk groups are then executed by every lane (a lane with
+// no groups of its own returns at once).
+// expect_tx + 5-D tensor load of one box onto bar
+__device__ __forceinline__ void tma_load_5d_e(void* dst, const CUtensorMap* map, uint64_t* bar, uint32_t bytes,
+                                              int c0, int c1, int c2, int c3, int c4) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%2], %8;\n\t"
+      "@e cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], "
+      "[%2];\n\t}" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_addr(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bytes)
+      : "memory");
+}
+// expect_tx + 1-D bulk copy onto bar
+__device__ __forceinline__ void bulk_load_e(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%3], %2;\n\t"
+      "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n\t}" ::"r"(
+          smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+// one output chunk: store (or fp32 reduce-add) src1 through map1, plus the
+// same box of src2 through map2 when src2 is set, as one bulk group
+__device__ __forceinline__ void tma_store_chunk_e(const CUtensorMap* map1, const void* src1, bool reduce_add,
+                                                  const CUtensorMap* map2, const void* src2, const int (&c)[5]) {
+  asm volatile(
+      "{\n\t.reg .pred e, r, a, er, es, ea;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 r, %7, 0;\n\t"
+      "setp.ne.b32 a, %8, 0;\n\t"
+      "and.pred er, e, r;\n\t"
+      "not.pred r, r;\n\t"
+      "and.pred es, e, r;\n\t"
+      "and.pred ea, e, a;\n\t"
+      "@er cp.reduce.async.bulk.tensor.5d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];\n\t"
+      "@es cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];\n\t"
+      "@ea cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%9, {%2, %3, %4, %5, %6}], [%8];\n\t"
+      "@e cp.async.bulk.commit_group;\n\t}" ::"l"(reinterpret_cast<uint64_t>(map1)),
+      "r"(smem_addr(src1)), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(reduce_add ? 1u : 0u),
+      "r"(src2 ? smem_addr(src2) : 0u), "l"(reinterpret_cast<uint64_t>(map2))
+      : "memory");
+}
+
 // order this thread's generic-proxy smem accesses before later async-proxy (TMA) ones
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
