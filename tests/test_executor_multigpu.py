@@ -42,6 +42,13 @@ CASES += [
     (2, VGGS, {"stages": [{"layers": [0, 10], "gpus": [0]}, {"layers": [10, 19], "gpus": [1]}]}, 2, 8),
     (4, VGGS, {"stages": [{"layers": [0, 16], "gpus": [0, 1, 2]}, {"layers": [16, 19], "gpus": [3]}]}, 2, 12),
 ]
+# eight ranks: C2's structure (2 stages x 4 replicas: Split-Concat 4 -> 4, a
+# 4-way replica AllReduce) and C4's (a straight 8-stage LM pipeline)
+C2_8 = {"stages": [{"layers": [0, 2], "gpus": [0, 1, 2, 3]}, {"layers": [2, 4], "gpus": [4, 5, 6, 7]}]}
+LMGPT8 = dict(LMGPT, layers=8)
+C4_8 = {"stages": [{"layers": [k, k + 1], "gpus": [k]} for k in range(8)]}
+CASES8 = [(8, BERT, C2_8, 4, 32), (8, LMGPT8, C4_8, 8, 8)]
+CASES += CASES8
 TWO = {"stages": [{"layers": [0, 2], "gpus": [0]}, {"layers": [2, 4], "gpus": [1]}]}
 # GPipe / re-computation on the device (the schedules of the paper's Table VI)
 SCHED_CASES = [
