@@ -74,6 +74,23 @@ __device__ __forceinline__ float dgelu_f(float x) {
   const float t = tanh_fast(kGeluK0 * fmaf(kGeluK1 * x, x2, x));
   return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * kGeluK0 * fmaf(3.0f * kGeluK1, x2, 1.0f);
 }
+// the same two functions on packed fp32x2 operands (FMUL2 / FFMA2 / FADD2:
+// half the FMA-pipe instructions of the TMA epilogue's activation math)
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 gelu2(float2 x) {
+  const float2 c = __ffma2_rn(__fmul2_rn(f2(kGeluK1), x), __fmul2_rn(x, x), x);
+  const float2 g = __fmul2_rn(f2(kGeluK0), c);
+  const float2 t = make_float2(tanh_fast(g.x), tanh_fast(g.y));
+  return __fmul2_rn(__fmul2_rn(f2(0.5f), x), __fadd2_rn(f2(1.0f), t));
+}
+__device__ __forceinline__ float2 dgelu2(float2 x) {
+  const float2 x2 = __fmul2_rn(x, x);
+  const float2 g = __fmul2_rn(f2(kGeluK0), __ffma2_rn(__fmul2_rn(f2(kGeluK1), x), x2, x));
+  const float2 t = make_float2(tanh_fast(g.x), tanh_fast(g.y));
+  const float2 one_m_tt = __ffma2_rn(make_float2(-t.x, -t.y), t, f2(1.0f));
+  const float2 a = __fmul2_rn(__fmul2_rn(__fmul2_rn(f2(0.5f), x), one_m_tt), f2(kGeluK0));
+  return __ffma2_rn(a, __ffma2_rn(f2(3.0f * kGeluK1), x2, f2(1.0f)), __fmul2_rn(f2(0.5f), __fadd2_rn(f2(1.0f), t)));
+}
 
 // Implicit-GEMM convolution: load the im2col tile whose first pixel (output
 // position, row-major n, h, w) is `pixel` and whose 64 channels start at
@@ -380,17 +397,26 @@ __device__ __forceinline__ void epi_tile_tma(const GemmParams& p, EpiTma& e, uin
     const int ob = e.seq & 1;
     const int xb = e.seq % p.epi_nx;
     float v[32];
+    {
+      const float2 al = make_float2(p.alpha, p.alpha);
 #pragma unroll
-    for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(raw[k]) * p.alpha;
+      for (int k = 0; k < 32; k += 2) {
+        const float2 r = __fmul2_rn(make_float2(__uint_as_float(raw[k]), __uint_as_float(raw[k + 1])), al);
+        v[k] = r.x;
+        v[k + 1] = r.y;
+      }
+    }
     if (epi & kBias) {  // smem broadcast reads (columns past N hold junk; they are clipped on store)
       const float4* b4 = reinterpret_cast<const float4*>(bias_s + n0);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const float4 bb = b4[q];
-        v[4 * q] += bb.x;
-        v[4 * q + 1] += bb.y;
-        v[4 * q + 2] += bb.z;
-        v[4 * q + 3] += bb.w;
+        const float2 lo = __fadd2_rn(make_float2(v[4 * q], v[4 * q + 1]), make_float2(bb.x, bb.y));
+        const float2 hi = __fadd2_rn(make_float2(v[4 * q + 2], v[4 * q + 3]), make_float2(bb.z, bb.w));
+        v[4 * q] = lo.x;
+        v[4 * q + 1] = lo.y;
+        v[4 * q + 2] = hi.x;
+        v[4 * q + 3] = hi.y;
       }
     }
     uint8_t* xbuf = epi_xbuf(p, e, xb);
@@ -414,10 +440,18 @@ __device__ __forceinline__ void epi_tile_tma(const GemmParams& p, EpiTma& e, uin
       }
       if (epi & kResid) {
 #pragma unroll
-        for (int k = 0; k < 32; ++k) v[k] += xv[k];
+        for (int k = 0; k < 32; k += 2) {
+          const float2 r = __fadd2_rn(make_float2(v[k], v[k + 1]), make_float2(xv[k], xv[k + 1]));
+          v[k] = r.x;
+          v[k + 1] = r.y;
+        }
       } else if (epi & kDGelu) {
 #pragma unroll
-        for (int k = 0; k < 32; ++k) v[k] *= dgelu_f(xv[k]);
+        for (int k = 0; k < 32; k += 2) {
+          const float2 r = __fmul2_rn(make_float2(v[k], v[k + 1]), dgelu2(make_float2(xv[k], xv[k + 1])));
+          v[k] = r.x;
+          v[k + 1] = r.y;
+        }
       } else {
 #pragma unroll
         for (int k = 0; k < 32; ++k) v[k] *= xv[k] > 0.f ? 1.f : 0.f;
@@ -443,7 +477,11 @@ __device__ __forceinline__ void epi_tile_tma(const GemmParams& p, EpiTma& e, uin
     }
     if (epi & kGelu) {
 #pragma unroll
-      for (int k = 0; k < 32; ++k) v[k] = gelu_f(v[k]);
+      for (int k = 0; k < 32; k += 2) {
+        const float2 r = gelu2(make_float2(v[k], v[k + 1]));
+        v[k] = r.x;
+        v[k + 1] = r.y;
+      }
     } else if (epi & kRelu) {
 #pragma unroll
       for (int k = 0; k < 32; ++k) v[k] = fmaxf(v[k], 0.f);
