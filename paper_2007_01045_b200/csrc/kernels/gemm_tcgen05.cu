@@ -1322,14 +1322,23 @@ void GemmOp::prepare(const GemmDesc& d) {
       // carve the staging out of the ring, keeping >= 4 stages
       const int per_warp = bn / 64;  // chunks per epilogue warp per tile
       p.epi_out_bytes = kind == kOutBf16 ? 2048 : 4096;
-      p.epi_nx = x_in ? std::min(kMaxNx, per_warp) : (aux ? 2 : 1);
+      // prefetched residual / activation-input chunks per warp: one, so the
+      // ring keeps a fifth stage -- the mainloop gains more from the deeper
+      // ring than the epilogue loses to the exposed input loads (BERT-48
+      // ffn2 34.8 -> 31.0 us, ffn2 dgrad 46.2 -> 43.5, o 15.9 -> 15.4;
+      // DPL_GEMM_X_BUFS=2 restores the previous carve-out)
+      static const int max_nx = [] {
+        const char* e = std::getenv("DPL_GEMM_X_BUFS");
+        return e ? std::max(1, std::min(kMaxNx, std::atoi(e))) : 1;
+      }();
+      p.epi_nx = x_in ? std::min(max_nx, per_warp) : (aux ? 2 : 1);
       p.epi_tile_cols = bn;
       const int bias_bytes = (d.epi & kBias) ? p.epi_tile_cols * 4 : 0;
       for (;;) {
         // 1 KB multiple: every warp's chunk buffers stay swizzle-atom aligned
         p.epi_warp_bytes = (2 * p.epi_out_bytes + (x_in || aux ? p.epi_nx * kXBytes : 0) + bias_bytes + 1023) & ~1023;
         p.stages = std::min(kMaxStages, (ring - kEpiWarps * p.epi_warp_bytes) / stage_bytes);
-        if (p.stages >= 4 || !x_in || p.epi_nx <= 2) break;
+        if (p.stages >= 4 || !x_in || p.epi_nx <= std::min(2, max_nx)) break;
         p.epi_nx /= 2;
       }
       ok = p.stages >= 4;
