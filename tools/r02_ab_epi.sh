@@ -3,11 +3,11 @@
 # vs lane-0 divergent issue (old), same box
 out=gpurun_out/r2abepi; mkdir -p $out
 cp abtmp/libdapple_new.so paper_2007_01045_b200/libdapple.so
-timeout 900 python -m pytest tests/test_gemm_gpu.py tests/test_vgg_gpu.py tests/test_lm_gpu.py tests/test_executor_gpu.py -m gpu -q -x --timeout 300 --timeout-method thread -p no:cacheprovider > $out/pytest.txt 2>&1; tail -1 $out/pytest.txt
+timeout 900 python -m pytest tests/test_gemm_gpu.py tests/test_vgg_gpu.py tests/test_lm_gpu.py tests/test_executor_gpu.py tests/test_baseline_shapes_gpu.py -m gpu -q -x --timeout 300 --timeout-method thread -p no:cacheprovider > $out/pytest.txt 2>&1; tail -1 $out/pytest.txt
 for r in 1 2; do
 for v in old new; do
   cp abtmp/libdapple_$v.so paper_2007_01045_b200/libdapple.so
-  timeout 200 python tools/gemm_graph_bench.py > $out/gg_${v}_$r.txt 2>&1; echo "$v gg: $(grep -i 'sum\|total' $out/gg_${v}_$r.txt | tail -2 | tr '\n' ' ')"
+  timeout 200 python tools/gemm_graph_bench.py > $out/gg_${v}_$r.txt 2>&1; echo "$v gg:"; python tools/gg_summary.py $out/gg_${v}_$r.txt
   for m in bert48 gpt2-1.5b; do
     timeout 600 python bench.py --model $m --steps 5 --warmup 3 --no-cpu > $out/${v}_${m}_$r.json 2>/dev/null
     echo "$v $m $(python -c "import json; d=json.load(open('$out/${v}_${m}_$r.json')); print(round(d['value'],2), d['clocks']['sm_mhz'], round(d['roofline']['achieved']))" 2>&1 | tail -1)"
