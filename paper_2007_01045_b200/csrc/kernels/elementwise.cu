@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(256, kMaxVec > 4 ? 2 : 4)  // h > 1024 (GPT-2)
                               const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
                               const float* __restrict__ gamma, const __nv_bfloat16* __restrict__ dresid,
                               __nv_bfloat16* __restrict__ dx, int rows, int h) {
-  extern __shared__ float4 ln_par[];  // gamma [h], staged before the dependency wait
+  extern __shared__ float4 ln_par[];  // gamma [h] (staged before the dependency wait), then a bf16 row per warp
   float* sg = reinterpret_cast<float*>(ln_par);
   for (int i = threadIdx.x; i < h / 4; i += blockDim.x)
     reinterpret_cast<float4*>(sg)[i] = __ldg(reinterpret_cast<const float4*>(gamma) + i);
@@ -187,14 +187,23 @@ __global__ void __launch_bounds__(256, kMaxVec > 4 ? 2 : 4)  // h > 1024 (GPT-2)
     const float mean = mean_in[row];
     const float rstd = rstd_in[row];
     uint4 rx[kMaxVec], rd[kMaxVec];
+    // the residual gradient is fetched with x and dy -- asynchronously into
+    // this warp's shared-memory row (cp.async: no registers held), so its
+    // latency overlaps theirs instead of following the row reductions
+    __nv_bfloat16* srow = reinterpret_cast<__nv_bfloat16*>(sg + h) + (threadIdx.x >> 5) * h;
 #pragma unroll
     for (int i = 0; i < kMaxVec; ++i) {
       const int vi = lane + 32 * i;
       if (vi < nvec) {
         rx[i] = *reinterpret_cast<const uint4*>(x + base + vi * 8);
         rd[i] = *reinterpret_cast<const uint4*>(dy + base + vi * 8);
+        if (dresid)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ptx::smem_addr(srow + vi * 8)),
+                       "l"(dresid + base + vi * 8)
+                       : "memory");
       }
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int i = 0; i < kMaxVec; ++i) {
@@ -214,22 +223,23 @@ __global__ void __launch_bounds__(256, kMaxVec > 4 ? 2 : 4)  // h > 1024 (GPT-2)
     }
     const float m1 = warp_sum(s1) / h;
     const float m2 = warp_sum(s2) / h;
+    asm volatile("cp.async.wait_group 0;" ::: "memory");  // this thread's own residual chunks
 #pragma unroll
     for (int i = 0; i < kMaxVec; ++i) {
       const int vi = lane + 32 * i;
       if (vi < nvec) {
-        float xv[8], dv[8], g[8], rr[8], o[8];
+        float xv[8], dv[8], g[8], rv[8], o[8];
         unpack8(rx[i], xv);
         unpack8(rd[i], dv);
         lds8(sg + vi * 8, g);
         if (dresid) {
-          load8(dresid + base + vi * 8, rr);
+          unpack8(*reinterpret_cast<const uint4*>(srow + vi * 8), rv);
         } else {
 #pragma unroll
-          for (int e = 0; e < 8; ++e) rr[e] = 0.f;
+          for (int e = 0; e < 8; ++e) rv[e] = 0.f;
         }
 #pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = rstd * (dv[e] * g[e] - m1 - ((xv[e] - mean) * rstd) * m2) + rr[e];
+        for (int e = 0; e < 8; ++e) o[e] = rstd * (dv[e] * g[e] - m1 - ((xv[e] - mean) * rstd) * m2) + rv[e];
         store8(dx + base + vi * 8, o);
       }
     }
@@ -654,7 +664,8 @@ void layernorm_bwd(const void* dy, const void* x, const float* mean, const float
   const auto* pr = static_cast<const __nv_bfloat16*>(dresid);
   auto* pdx = static_cast<__nv_bfloat16*>(dx);
   dispatch_vec(h, [&](auto v) {
-    launch_pdl(layernorm_bwd_rows_kernel<decltype(v)::value>, dim3(grid), dim3(warps * 32), h * sizeof(float), s, pdy, px, mean, rstd, gamma, pr, pdx,
+    launch_pdl(layernorm_bwd_rows_kernel<decltype(v)::value>, dim3(grid), dim3(warps * 32),
+               h * sizeof(float) + (pr ? warps * h * sizeof(__nv_bfloat16) : 0), s, pdy, px, mean, rstd, gamma, pr, pdx,
                                                                               rows, h);
   });
   const int nred = dx_colsum ? 4 : (dresid_colsum ? 3 : 2);
@@ -695,8 +706,9 @@ void colsum_acc(const void* dy, float* db, int rows, int cols, cudaStream_t s) {
   count_launch();
   TimedLaunch timed_("colsum_acc", s);
   const int gx = (cols + 255) / 256;
-  // about two blocks per SM, at least 64 rows per block
-  int gy = std::max(1, std::min((rows + 63) / 64, (148 * 2 + gx - 1) / gx));
+  // about four blocks per SM (the occupancy the kernel's launch bounds
+  // allow: 32 warps x 64 bytes in flight per lane), at least 64 rows per block
+  int gy = std::max(1, std::min((rows + 63) / 64, (148 * 4 + gx - 1) / gx));
   const int rpb = (rows + gy - 1) / gy;
   gy = (rows + rpb - 1) / rpb;
   launch_pdl(colsum_acc_kernel, dim3(gx, gy), dim3(256), 0, s, static_cast<const __nv_bfloat16*>(dy), db, rows, cols, rpb);
