@@ -1155,8 +1155,15 @@ static bool split_bf16_candidate(const GemmDesc& d) {
   const long long pair_tiles = static_cast<long long>((d.M + 255) / 256) * ((d.N + 255) / 256);
   const int kblocks = (d.K + 63) / 64;
   const int pairs = num_sms() / 2;
-  // at most half the pairs busy, and enough K to split in >= 2 x 8 blocks
-  return pair_tiles * 2 <= pairs && kblocks >= 16;
+  // at most half the pairs busy, and enough K for the split to pay for the
+  // fp32 round trip of the separate epilogue pass: K >= 3072 (GPT-2 N=1
+  // 55.2-55.5 samples/s at >= 48 K blocks, 54.7-55.0 at >= 16, 53.9 off;
+  // DPL_GEMM_SPLIT_MIN_KB overrides)
+  static const int min_kb = [] {
+    const char* e = std::getenv("DPL_GEMM_SPLIT_MIN_KB");
+    return e ? std::max(16, std::atoi(e)) : 48;
+  }();
+  return pair_tiles * 2 <= pairs && kblocks >= min_kb;
 }
 
 void GemmOp::prepare(const GemmDesc& d) {
