@@ -126,6 +126,11 @@ int dpl_k_layernorm_fwd(const void* x, const float* gamma, const float* beta, vo
                         int rows, int h, float eps, void* stream);
 int dpl_k_layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd, const float* gamma,
                         const void* dresid, void* dx, float* dgamma, float* dbeta, int rows, int h, void* stream);
+/* The same, also accumulating the column sums of dresid and (if dx_colsum)
+ * of dx -- the bias gradients the executor folds into LayerNorm backward. */
+int dpl_k_layernorm_bwd_colsum(const void* dy, const void* x, const float* mean, const float* rstd, const float* gamma,
+                               const void* dresid, void* dx, float* dgamma, float* dbeta, float* dresid_colsum,
+                               float* dx_colsum, int rows, int h, void* stream);
 int dpl_k_softmax_fwd(const float* s, void* p, int rows, int len, int q_len, int causal, void* stream);
 int dpl_k_softmax_bwd(const void* p, const float* dp, void* ds, int rows, int len, void* stream);
 int dpl_k_colsum_acc(const void* dy, float* db, int rows, int cols, void* stream);

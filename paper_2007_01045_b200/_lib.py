@@ -55,6 +55,7 @@ _PROTOS = {
     "dpl_k_attention_bwd_traced": (_I, [_VP, _VP, _LL, _VP, _VP, _VP, _VP, _VP, _I, _I, _I, _I, _VP, _VP]),
     "dpl_k_layernorm_fwd": (_I, [_VP, _VP, _VP, _VP, _VP, _VP, _I, _I, _F, _VP]),
     "dpl_k_layernorm_bwd": (_I, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I, _I, _VP]),
+    "dpl_k_layernorm_bwd_colsum": (_I, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I, _I, _VP]),
     "dpl_k_softmax_fwd": (_I, [_VP, _VP, _I, _I, _I, _I, _VP]),
     "dpl_k_softmax_bwd": (_I, [_VP, _VP, _VP, _I, _I, _VP]),
     "dpl_k_colsum_acc": (_I, [_VP, _VP, _I, _I, _VP]),

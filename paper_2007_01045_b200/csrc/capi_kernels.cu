@@ -189,6 +189,20 @@ int dpl_k_layernorm_bwd(const void* dy, const void* x, const float* mean, const 
   });
 }
 
+int dpl_k_layernorm_bwd_colsum(const void* dy, const void* x, const float* mean, const float* rstd, const float* gamma,
+                               const void* dresid, void* dx, float* dgamma, float* dbeta, float* dresid_colsum,
+                               float* dx_colsum, int rows, int h, void* stream) {
+  return guarded([&] {
+    float* ws = nullptr;
+    const size_t bytes = static_cast<size_t>(dpl::kLnBwdBlocks) * 4 * h * sizeof(float);
+    if (cudaMallocAsync(reinterpret_cast<void**>(&ws), bytes, static_cast<cudaStream_t>(stream)) != cudaSuccess)
+      throw std::runtime_error("layernorm_bwd: workspace allocation failed");
+    dpl::layernorm_bwd(dy, x, mean, rstd, gamma, dresid, dx, dgamma, dbeta, rows, h, static_cast<cudaStream_t>(stream),
+                       ws, dresid_colsum, dx_colsum);
+    cudaFreeAsync(ws, static_cast<cudaStream_t>(stream));
+  });
+}
+
 int dpl_k_softmax_fwd(const float* s, void* p, int rows, int len, int q_len, int causal, void* stream) {
   return guarded([&] { dpl::softmax_fwd(s, p, rows, len, q_len, causal, static_cast<cudaStream_t>(stream)); });
 }

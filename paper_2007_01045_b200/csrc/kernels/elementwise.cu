@@ -8,6 +8,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <mutex>
 #include <stdexcept>
 #include <cstdint>
 #include <type_traits>
@@ -278,6 +280,167 @@ __global__ void __launch_bounds__(256, kMaxVec > 4 ? 2 : 4)  // h > 1024 (GPT-2)
   }
 }
 
+// Fused LayerNorm backward: the dx rows AND the per-block column partials of
+// dgamma = sum dy*xhat, dbeta = sum dy [, sum dresid [, sum dx]] in one pass
+// over x / dy / dresid (the three-launch form re-read all of them, and dx, in
+// a column kernel).  A row is spread over kTPR threads (one 8-column vector
+// each, so every thread owns the same columns for the whole block and keeps
+// their partials in registers); 512 / kTPR row groups per block take kR rows
+// at a time, the row statistics meet in shared memory across the row group's
+// warps (named barrier per group, double-buffered by iteration parity).  One
+// block per SM; ws[block][k][h] partials are summed by ln_param_reduce_kernel
+// in block order (deterministic).
+constexpr int kLnFusedR = 4;
+template <int kThreads, int kTPR, int kRed>
+__global__ void __launch_bounds__(kThreads, 512 / kThreads)
+    ln_bwd_fused_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+                        const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
+                        const float* __restrict__ gamma, const __nv_bfloat16* __restrict__ dresid,
+                        __nv_bfloat16* __restrict__ dx, float* __restrict__ ws, int rows, int h, int rows_per_block) {
+  constexpr int kRG = kThreads / kTPR;
+  constexpr int kWPR = kTPR / 32;
+  constexpr int kR = kLnFusedR;
+  extern __shared__ float4 ln_fused_smem[];
+  float* sg = reinterpret_cast<float*>(ln_fused_smem);                 // gamma [h]
+  float* red = sg + h;                                                  // [2][kRG][kWPR][kR][2]
+  float* part = red + 2 * kRG * kWPR * kR * 2;                          // [kRG][kRed][h]
+  __nv_bfloat16* sres = reinterpret_cast<__nv_bfloat16*>(part + kRG * kRed * h);  // [kRG][kR][h]
+  for (int i = threadIdx.x; i < h / 4; i += blockDim.x)
+    reinterpret_cast<float4*>(sg)[i] = __ldg(reinterpret_cast<const float4*>(gamma) + i);
+  __syncthreads();
+  ptx::pdl_wait();
+  const int rg = threadIdx.x / kTPR;
+  const int vi = threadIdx.x % kTPR;  // this thread's 8-column vector
+  const int wr = vi >> 5, lane = threadIdx.x & 31;
+  const int nvec = h / 8;
+  const bool act = vi < nvec;
+  const float inv_h = 1.0f / h;
+  float2 g[4];
+  if (act) {
+    const float2* g2 = reinterpret_cast<const float2*>(sg + vi * 8);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) g[e] = g2[e];
+  }
+  float2 acc[kRed][4];
+#pragma unroll
+  for (int k = 0; k < kRed; ++k)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[k][e] = ff2(0.f);
+  __nv_bfloat16* my_res = sres + rg * kR * h;
+  const int r0 = blockIdx.x * rows_per_block;
+  const int r1 = min(rows, r0 + rows_per_block);
+  int par = 0;
+  for (int rb = r0 + rg * kR; rb - rg * kR < r1; rb += kRG * kR, par ^= 1) {
+    // every row group runs the same number of iterations (named barriers)
+    uint4 rx[kR], rd[kR];
+    float mean[kR], rstd[kR];
+#pragma unroll
+    for (int j = 0; j < kR; ++j) {
+      const int r = rb + j;
+      mean[j] = 0.f;
+      rstd[j] = 0.f;
+      if (r < r1) {
+        mean[j] = mean_in[r];
+        rstd[j] = rstd_in[r];
+        if (act) {
+          const long long off = static_cast<long long>(r) * h + vi * 8;
+          rx[j] = *reinterpret_cast<const uint4*>(x + off);
+          rd[j] = *reinterpret_cast<const uint4*>(dy + off);
+          if (dresid)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ptx::smem_addr(my_res + j * h + vi * 8)),
+                         "l"(dresid + off)
+                         : "memory");
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    float st[kR][2];
+#pragma unroll
+    for (int j = 0; j < kR; ++j) {
+      float2 s1 = ff2(0.f), s2 = ff2(0.f);
+      if (rb + j < r1 && act) {
+        const float2 r2 = ff2(rstd[j]), c2 = ff2(-mean[j] * rstd[j]);
+        const uint32_t* wx = reinterpret_cast<const uint32_t*>(&rx[j]);
+        const uint32_t* wd = reinterpret_cast<const uint32_t*>(&rd[j]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 gd = __fmul2_rn(bf2f(wd[e]), g[e]);
+          s1 = __fadd2_rn(s1, gd);
+          s2 = __ffma2_rn(gd, __ffma2_rn(bf2f(wx[e]), r2, c2), s2);
+        }
+      }
+      st[j][0] = warp_sum(s1.x + s1.y);
+      st[j][1] = warp_sum(s2.x + s2.y);
+    }
+    if constexpr (kWPR > 1) {
+      float* rr = red + ((par * kRG + rg) * kWPR) * kR * 2;
+      if (lane == 0) {
+#pragma unroll
+        for (int j = 0; j < kR; ++j) {
+          rr[(wr * kR + j) * 2] = st[j][0];
+          rr[(wr * kR + j) * 2 + 1] = st[j][1];
+        }
+      }
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + rg), "r"(kTPR) : "memory");
+#pragma unroll
+      for (int j = 0; j < kR; ++j) {
+        float a = 0.f, b = 0.f;
+#pragma unroll
+        for (int w = 0; w < kWPR; ++w) {
+          a += rr[(w * kR + j) * 2];
+          b += rr[(w * kR + j) * 2 + 1];
+        }
+        st[j][0] = a;
+        st[j][1] = b;
+      }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");  // this thread's own residual chunks
+#pragma unroll
+    for (int j = 0; j < kR; ++j) {
+      if (rb + j < r1 && act) {
+        const float2 r2 = ff2(rstd[j]), c2 = ff2(-mean[j] * rstd[j]);
+        const float2 nm1 = ff2(-st[j][0] * inv_h), nm2 = ff2(-st[j][1] * inv_h);
+        const uint32_t* wx = reinterpret_cast<const uint32_t*>(&rx[j]);
+        const uint32_t* wd = reinterpret_cast<const uint32_t*>(&rd[j]);
+        uint4 rr4 = make_uint4(0u, 0u, 0u, 0u);
+        if (dresid) rr4 = *reinterpret_cast<const uint4*>(my_res + j * h + vi * 8);
+        const uint32_t* wres = reinterpret_cast<const uint32_t*>(&rr4);
+        uint4 o;
+        uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 dv = bf2f(wd[e]);
+          const float2 xh = __ffma2_rn(bf2f(wx[e]), r2, c2);
+          const float2 t = __fadd2_rn(__ffma2_rn(xh, nm2, __fmul2_rn(dv, g[e])), nm1);
+          const float2 rv = bf2f(wres[e]);
+          ow[e] = f2bf(__ffma2_rn(t, r2, rv));
+          acc[0][e] = __ffma2_rn(dv, xh, acc[0][e]);
+          acc[1][e] = __fadd2_rn(acc[1][e], dv);
+          if constexpr (kRed > 2) acc[2][e] = __fadd2_rn(acc[2][e], rv);
+          if constexpr (kRed > 3) acc[3][e] = __fadd2_rn(acc[3][e], bf2f(ow[e]));  // the stored (bf16) dx
+        }
+        *reinterpret_cast<uint4*>(dx + static_cast<long long>(rb + j) * h + vi * 8) = o;
+      }
+    }
+  }
+  // row groups meet in shared memory; one ws row per reduction per block
+  if (act) {
+#pragma unroll
+    for (int k = 0; k < kRed; ++k) {
+      float4* d = reinterpret_cast<float4*>(part + (rg * kRed + k) * h + vi * 8);
+      d[0] = make_float4(acc[k][0].x, acc[k][0].y, acc[k][1].x, acc[k][1].y);
+      d[1] = make_float4(acc[k][2].x, acc[k][2].y, acc[k][3].x, acc[k][3].y);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kRed * h; i += blockDim.x) {
+    float sum = 0.f;
+#pragma unroll
+    for (int q = 0; q < kRG; ++q) sum += part[q * kRed * h + i];
+    ws[static_cast<long long>(blockIdx.x) * kRed * h + i] = sum;
+  }
+}
+
 // Column reductions over a slab of 64 rows (block = 32 column vectors x 8
 // row phases):
 //   0: sum dy*xhat (dgamma)  1: sum dy (dbeta)  2: sum dresid  3: sum dx
@@ -355,24 +518,34 @@ __global__ void __launch_bounds__(256, 4)
 }
 
 // dst_k[c] += sum_b ws[b][k][c] for each of the nred column reductions.
-// Block: 32 columns x 8 slab groups; each thread sums every 8th slab (loads
-// independent, so they overlap), then the 8 groups meet in smem.
-__global__ void __launch_bounds__(256) ln_param_reduce_kernel(const float* __restrict__ ws, float* d0, float* d1,
+// Block: 32 columns x 16 slab groups; each thread sums every 16th slab with
+// eight loads in flight at a time (the partials are L2-resident: the sum is
+// latency-bound, so the loads must overlap), then the 16 groups meet in smem.
+__global__ void __launch_bounds__(512) ln_param_reduce_kernel(const float* __restrict__ ws, float* d0, float* d1,
                                                               float* d2, float* d3, int blocks, int nred, int h) {
   ptx::pdl_wait();
-  __shared__ float part[8][33];
+  __shared__ float part[16][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int i = blockIdx.x * 32 + tx;  // (k, c) flattened
+  const long long stride = static_cast<long long>(nred) * h;
   float s = 0.f;
   if (i < nred * h) {
-#pragma unroll 4
-    for (int b = ty; b < blocks; b += 8) s += ws[static_cast<long long>(b) * nred * h + i];
+    for (int b0 = ty; b0 < blocks; b0 += 16 * 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int b = b0 + 16 * u;
+        v[u] = b < blocks ? ws[b * stride + i] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += v[u];
+    }
   }
   part[ty][tx] = s;
   __syncthreads();
   if (ty == 0 && i < nred * h) {
 #pragma unroll
-    for (int y = 1; y < 8; ++y) s += part[y][tx];
+    for (int y = 1; y < 16; ++y) s += part[y][tx];
     const int k = i / h, c = i % h;
     float* d = k == 0 ? d0 : k == 1 ? d1 : k == 2 ? d2 : d3;
     d[c] += s;
@@ -691,23 +864,71 @@ void layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y
 void layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd, const float* gamma,
                    const void* dresid, void* dx, float* dgamma, float* dbeta, int rows, int h, cudaStream_t s,
                    float* ws, float* dresid_colsum, float* dx_colsum) {
-  count_launch(3);
   TimedLaunch timed_("layernorm_bwd", s);
   if (!ws) throw std::invalid_argument("layernorm_bwd: workspace required");
   if (dx_colsum && !dresid_colsum) throw std::invalid_argument("layernorm_bwd: dx_colsum needs dresid_colsum");
   if (dresid_colsum && !dresid) throw std::invalid_argument("layernorm_bwd: dresid_colsum needs dresid");
-  const int warps = 8;
-  const int grid = std::max(1, std::min((rows + warps - 1) / warps, 148 * 8));
   const auto* pdy = static_cast<const __nv_bfloat16*>(dy);
   const auto* px = static_cast<const __nv_bfloat16*>(x);
   const auto* pr = static_cast<const __nv_bfloat16*>(dresid);
   auto* pdx = static_cast<__nv_bfloat16*>(dx);
+  const int nred = dx_colsum ? 4 : (dresid_colsum ? 3 : 2);
+  static const bool fused = [] {
+    const char* e = std::getenv("DPL_LN_BWD_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  if (fused && h <= 2048) {
+    count_launch(2);
+    // blocks per SM (A/B knob): 1 x 512 threads (default; 13.1 vs 13.5 us at 4096 x 1024) or 2 x 256
+    static const int bps = [] {
+      const char* e = std::getenv("DPL_LN_FUSED_BPS");
+      return e && e[0] == '2' ? 2 : 1;
+    }();
+    const int threads = 512 / bps;
+    const int nvec = h / 8;
+    const int tpr = std::min(threads, nvec <= 32 ? 32 : nvec <= 64 ? 64 : nvec <= 128 ? 128 : 256);
+    const int rg = threads / tpr;
+    const int grid = std::max(1, std::min(148 * bps, (rows + rg * kLnFusedR - 1) / (rg * kLnFusedR)));
+    const int rpb = (rows + grid - 1) / grid;
+    const size_t smem = h * sizeof(float) + 2 * (threads / 32) * kLnFusedR * 2 * sizeof(float) +
+                        static_cast<size_t>(rg) * nred * h * sizeof(float) +
+                        (pr ? static_cast<size_t>(rg) * kLnFusedR * h * sizeof(__nv_bfloat16) : 0);
+    auto go = [&](auto thr_c, auto tpr_c, auto red_c) {
+      constexpr int N = decltype(thr_c)::value, T = decltype(tpr_c)::value, R = decltype(red_c)::value;
+      if constexpr (T <= N) {
+        static std::once_flag once;  // one per instantiation
+        std::call_once(once, [] {
+          cudaFuncSetAttribute(ln_bwd_fused_kernel<N, T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
+        });
+        launch_pdl(ln_bwd_fused_kernel<N, T, R>, dim3(grid), dim3(N), smem, s, pdy, px, mean, rstd, gamma, pr, pdx, ws,
+                   rows, h, rpb);
+      }
+    };
+    auto by_red = [&](auto thr_c, auto tpr_c) {
+      if (nred == 2) go(thr_c, tpr_c, std::integral_constant<int, 2>{});
+      else if (nred == 3) go(thr_c, tpr_c, std::integral_constant<int, 3>{});
+      else go(thr_c, tpr_c, std::integral_constant<int, 4>{});
+    };
+    auto by_tpr = [&](auto thr_c) {
+      if (tpr == 32) by_red(thr_c, std::integral_constant<int, 32>{});
+      else if (tpr == 64) by_red(thr_c, std::integral_constant<int, 64>{});
+      else if (tpr == 128) by_red(thr_c, std::integral_constant<int, 128>{});
+      else by_red(thr_c, std::integral_constant<int, 256>{});
+    };
+    if (threads == 512) by_tpr(std::integral_constant<int, 512>{});
+    else by_tpr(std::integral_constant<int, 256>{});
+    launch_pdl(ln_param_reduce_kernel, dim3((nred * h + 31) / 32), dim3(512), 0, s, ws, dgamma, dbeta, dresid_colsum,
+               dx_colsum, grid, nred, h);
+    return;
+  }
+  count_launch(3);
+  const int warps = 8;
+  const int grid = std::max(1, std::min((rows + warps - 1) / warps, 148 * 8));
   dispatch_vec(h, [&](auto v) {
     launch_pdl(layernorm_bwd_rows_kernel<decltype(v)::value>, dim3(grid), dim3(warps * 32),
                h * sizeof(float) + (pr ? warps * h * sizeof(__nv_bfloat16) : 0), s, pdy, px, mean, rstd, gamma, pr, pdx,
                                                                               rows, h);
   });
-  const int nred = dx_colsum ? 4 : (dresid_colsum ? 3 : 2);
   const int slabs = (rows + 63) / 64;
   if (static_cast<long long>(slabs) * nred * h > static_cast<long long>(kLnBwdBlocks) * 4 * h)
     throw std::invalid_argument("layernorm_bwd: too many rows for the workspace");
@@ -715,7 +936,7 @@ void layernorm_bwd(const void* dy, const void* x, const float* mean, const float
   if (nred == 2) launch_pdl(ln_bwd_cols_kernel<2>, dim3(cg), dim3(256), 0, s, pdy, px, mean, rstd, pr, pdx, ws, rows, h);
   else if (nred == 3) launch_pdl(ln_bwd_cols_kernel<3>, dim3(cg), dim3(256), 0, s, pdy, px, mean, rstd, pr, pdx, ws, rows, h);
   else launch_pdl(ln_bwd_cols_kernel<4>, dim3(cg), dim3(256), 0, s, pdy, px, mean, rstd, pr, pdx, ws, rows, h);
-  launch_pdl(ln_param_reduce_kernel, dim3((nred * h + 31) / 32), dim3(256), 0, s, ws, dgamma, dbeta, dresid_colsum,
+  launch_pdl(ln_param_reduce_kernel, dim3((nred * h + 31) / 32), dim3(512), 0, s, ws, dgamma, dbeta, dresid_colsum,
              dx_colsum, slabs, nred, h);
 }
 

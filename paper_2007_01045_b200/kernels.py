@@ -57,6 +57,12 @@ def layernorm_bwd(dy, x, mean, rstd, gamma, dresid, dx, dgamma, dbeta, rows, h):
                                     _ptr(dgamma), _ptr(dbeta), rows, h, _stream()))
 
 
+def layernorm_bwd_colsum(dy, x, mean, rstd, gamma, dresid, dx, dgamma, dbeta, dresid_colsum, dx_colsum, rows, h):
+    check(lib().dpl_k_layernorm_bwd_colsum(_ptr(dy), _ptr(x), _ptr(mean), _ptr(rstd), _ptr(gamma), _ptr(dresid),
+                                           _ptr(dx), _ptr(dgamma), _ptr(dbeta), _ptr(dresid_colsum), _ptr(dx_colsum),
+                                           rows, h, _stream()))
+
+
 def softmax_fwd(s, p, rows, length, q_len, causal=False):
     check(lib().dpl_k_softmax_fwd(_ptr(s), _ptr(p), rows, length, q_len, int(causal), _stream()))
 

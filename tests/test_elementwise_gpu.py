@@ -40,6 +40,42 @@ def test_layernorm_fwd_bwd(cuda, rows, h):
     assert torch.allclose(dbeta, gb, rtol=1e-3, atol=1e-2)
 
 
+@pytest.mark.parametrize("rows,h,with_dx", [(4096, 1024, True), (4096, 1024, False), (1024, 1600, True),
+                                            (333, 2048, True), (70, 256, False), (5, 512, True)])
+def test_layernorm_bwd_column_sums(cuda, rows, h, with_dx):
+    """LayerNorm backward with the neighbouring layers' bias gradients folded in
+    (sum dresid, sum dx) against torch fp32, at the BERT / GPT-2 slice shapes
+    and ragged row counts (partial row groups, idle blocks)."""
+    x = _rand(rows, h, dev=cuda, seed=11, scale=3.0)
+    gamma = 1 + _rand(h, dev=cuda, seed=12, dtype=torch.float32, scale=0.5)
+    beta = _rand(h, dev=cuda, seed=13, dtype=torch.float32, scale=0.5)
+    y = torch.empty_like(x)
+    mean = torch.empty(rows, device=cuda)
+    rstd = torch.empty(rows, device=cuda)
+    K.layernorm_fwd(x, gamma, beta, y, mean, rstd, rows, h, 1e-5)
+    dy = _rand(rows, h, dev=cuda, seed=14)
+    dres = _rand(rows, h, dev=cuda, seed=15)
+    dx = torch.empty_like(x)
+    dgamma = torch.full((h,), 0.25, device=cuda)  # accumulates into existing gradients
+    dbeta = torch.full((h,), -0.5, device=cuda)
+    drs = torch.full((h,), 1.0, device=cuda)
+    dxs = torch.full((h,), 2.0, device=cuda) if with_dx else None
+    K.layernorm_bwd_colsum(dy, x, mean, rstd, gamma, dres, dx, dgamma, dbeta, drs, dxs, rows, h)
+    xr = x.float().requires_grad_(True)
+    g_, b_ = gamma.clone().requires_grad_(True), beta.clone().requires_grad_(True)
+    yr = torch.nn.functional.layer_norm(xr, (h,), g_, b_, 1e-5)
+    gx, gg, gb = torch.autograd.grad(yr, (xr, g_, b_), dy.float())
+    torch.cuda.synchronize()
+    ref_dx = gx + dres.float()
+    assert (dx.float() - ref_dx).abs().max().item() < 0.02 * ref_dx.abs().max().item() + 0.02
+    tol = dict(rtol=1e-3, atol=1e-2 * max(1.0, rows / 512))
+    assert torch.allclose(dgamma, gg + 0.25, **tol)
+    assert torch.allclose(dbeta, gb - 0.5, **tol)
+    assert torch.allclose(drs, dres.float().sum(0) + 1.0, **tol)
+    if with_dx:
+        assert torch.allclose(dxs, dx.float().sum(0) + 2.0, **tol)
+
+
 @pytest.mark.parametrize("causal", [False, True])
 def test_softmax(cuda, causal):
     z, L = 8, 512
