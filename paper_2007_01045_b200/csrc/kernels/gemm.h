@@ -96,6 +96,7 @@ struct alignas(64) GemmParams {
   int num_m_blocks, num_n_blocks, num_k_blocks, num_tiles;
   int k_splits, kb_per_split;  // split-K (fp32-accumulate outputs only)
   int two_sm;                  // cta_group::2 pair kernel (256 x 256 tiles)
+  int split_tail;              // pair kernel: the last split_tail tiles run as two 256 x 128 halves each
   uint32_t epi;
   float alpha;
   void* C;

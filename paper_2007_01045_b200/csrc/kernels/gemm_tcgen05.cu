@@ -788,6 +788,18 @@ namespace pair {
 constexpr int kSmem = kSmemBudget;
 }  // namespace pair
 
+// Work units of the pair kernel: tiles [0, num_tiles - split_tail) whole,
+// then each of the last split_tail tiles as two 256 x BN2/2 halves (hh 0 / 1),
+// so a last wave that would leave most pairs idle finishes in half the time.
+struct PairUnit {
+  int t, hh;  // tile, half (-1: whole tile)
+};
+__device__ __forceinline__ PairUnit pair_unit(const GemmParams& p, int u) {
+  const int whole = p.num_tiles - p.split_tail;
+  if (u < whole) return {u, -1};
+  return {whole + ((u - whole) >> 1), (u - whole) & 1};
+}
+
 template <int BN2>
 __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __grid_constant__ GemmParams p) {
   if (threadIdx.x == 0) trace_mark(p, 0);
@@ -835,13 +847,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
   ptx::pdl_trigger();
   if (threadIdx.x == 0) trace_mark(p, 1);
   const int tiles_per_z = p.num_m_blocks * p.num_n_blocks;
+  const int n_units = p.num_tiles + p.split_tail;
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       const int first_tile = pair_id;
-      for (int t = pair_id; t < p.num_tiles; t += n_pairs) {
+      for (int u = pair_id; u < n_units; u += n_pairs) {
+        const PairUnit un = pair_unit(p, u);
+        const int t = un.t;
         const int ks = t % p.k_splits;
         const int tt = t / p.k_splits;
         const int z = tt / tiles_per_z;
@@ -851,7 +866,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
         const int kb0 = ks * p.kb_per_split;
         const int kb1 = min(p.num_k_blocks, kb0 + p.kb_per_split);
         const int m0 = mb * 256 + rank * 128;
-        const int n0 = nb * kBN + rank * (kBN / 2);
+        // a half unit loads the same boxes from its half's start (the second
+        // 64 rows of each CTA's B box are not read by the N = BN2/2 MMA)
+        const int n0 = nb * kBN + (un.hh < 0 ? rank * (kBN / 2) : un.hh * (kBN / 2) + rank * (kBN / 4));
         for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
@@ -877,7 +894,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
             for (int j = 0; j < kBN / 128; ++j)
               ptx::tma_load_3d_2sm(sb + j * 64 * kBK * 2, &p.tma_b, &full[stage], n0 + j * 64, kb * kBK, z);
           }
-          if (t == first_tile && kb == kb0) trace_mark(p, 2);
+          if (u == first_tile && kb == kb0) trace_mark(p, 2);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -887,7 +904,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
     }
   } else if (warp == 1) {
     if (leader) {  // the whole warp runs the loop; one elected lane issues each MMA
-      const uint32_t idesc = ptx::idesc_bf16_f32(256, kBN, p.a_mn_major != 0, p.b_mn_major != 0);
+      const uint32_t idesc_whole = ptx::idesc_bf16_f32(256, kBN, p.a_mn_major != 0, p.b_mn_major != 0);
+      const uint32_t idesc_half = ptx::idesc_bf16_f32(256, kBN / 2, p.a_mn_major != 0, p.b_mn_major != 0);
       const uint32_t a_lbo = p.a_mn_major ? 64 * kBK * 2 : 16;
       const uint32_t b_lbo = p.b_mn_major ? 64 * kBK * 2 : 16;
       const uint32_t a_step = p.a_mn_major ? 16 * 128 : 32;
@@ -896,8 +914,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = pair_id; t < p.num_tiles; t += n_pairs) {
-        const int ks = t % p.k_splits;
+      for (int u = pair_id; u < n_units; u += n_pairs) {
+        const PairUnit un = pair_unit(p, u);
+        const uint32_t idesc = un.hh < 0 ? idesc_whole : idesc_half;
+        const int ks = un.t % p.k_splits;
         const int kb0 = ks * p.kb_per_split;
         const int kb1 = min(p.num_k_blocks, kb0 + p.kb_per_split);
         ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
@@ -906,7 +926,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
         for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
-          if (lane == 0 && t == pair_id && kb == kb0) trace_mark(p, 3);
+          if (lane == 0 && u == pair_id && kb == kb0) trace_mark(p, 3);
           const uint32_t sa = ptx::smem_addr(smem_a + stage * kABytes);
           const uint32_t sb = ptx::smem_addr(smem_b + stage * kBBytes);
 #pragma unroll
@@ -935,18 +955,28 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
     EpiTma e{smem_epi + (warp - 4) * p.epi_warp_bytes, xbar + kEpiBars * (warp - 4), 0, 0};
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = pair_id; t < p.num_tiles; t += n_pairs) {
-      const int tt = t / p.k_splits;
+    for (int u = pair_id; u < n_units; u += n_pairs) {
+      const PairUnit un = pair_unit(p, u);
+      const int tt = un.t / p.k_splits;
       const int z = tt / tiles_per_z;
       const int r = tt % tiles_per_z;
       const int mb = r % p.num_m_blocks;
       const int nb = r / p.num_m_blocks;
       const int row0 = mb * 256 + rank * 128 + quad * 32;
-      epi_tile_prefetch<kBN / 64>(p, e, z, row0, nb * kBN, half);
-      ptx::mbar_wait(&tmem_full[acc], acc_phase);
-      ptx::tc_fence_after();
-      if (warp == 4 && lane == 0 && t == pair_id) trace_mark(p, 5);
-      epi_tile_tma<kBN / 64>(p, e, tmem_base + ((quad * 32) << 16) + acc * kBN, z, row0, nb * kBN, half);
+      const uint32_t taddr = tmem_base + ((quad * 32) << 16) + acc * kBN;
+      if (un.hh < 0) {
+        epi_tile_prefetch<kBN / 64>(p, e, z, row0, nb * kBN, half);
+        ptx::mbar_wait(&tmem_full[acc], acc_phase);
+        ptx::tc_fence_after();
+        if (warp == 4 && lane == 0 && u == pair_id) trace_mark(p, 5);
+        epi_tile_tma<kBN / 64>(p, e, taddr, z, row0, nb * kBN, half);
+      } else if constexpr (kBN == 256) {
+        const int col0 = nb * kBN + un.hh * (kBN / 2);
+        epi_tile_prefetch<kBN / 128>(p, e, z, row0, col0, half);
+        ptx::mbar_wait(&tmem_full[acc], acc_phase);
+        ptx::tc_fence_after();
+        epi_tile_tma<kBN / 128>(p, e, taddr, z, row0, col0, half);
+      }
       ptx::tc_fence_before();
       __syncwarp();
       if (warp == 4 && lane == 0) trace_mark(p, 6);
@@ -966,7 +996,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16_tcgen05_2sm(const __gri
     constexpr int kChunks = kBN / 32;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = pair_id; t < p.num_tiles; t += n_pairs) {
+    for (int u = pair_id; u < n_units; u += n_pairs) {  // whole tiles only (split_tail needs the TMA epilogue)
+      const int t = pair_unit(p, u).t;
       const int tt = t / p.k_splits;
       const int z = tt / tiles_per_z;
       const int r = tt % tiles_per_z;
@@ -1378,6 +1409,21 @@ void GemmOp::prepare(const GemmDesc& d) {
   }();
   const int sms = std::min(num_sms(), d.max_ctas > 1 ? std::min(max_ctas, d.max_ctas) : max_ctas);
   grid_ = two_sm ? 2 * std::min(p.num_tiles, sms / 2) : std::min(p.num_tiles, sms);
+  // a last wave of at most half the pairs runs as 256 x 128 halves (two per
+  // tile): e.g. 4096 x 4096 has 256 tiles on 74 pairs = 3 waves + 34 tiles.
+  // Only for full-machine grids with >= 2 whole waves: GPT-2's 1.0-1.4-wave
+  // 1024-row GEMMs and the capped side-stream grids measured slower with it
+  // (GPT-2 N=1 54.8 vs 56.1 samples/s), the side stream already fills idle pairs
+  static const bool split_tail = [] {  // DPL_GEMM_SPLIT_TAIL=0: whole last wave (A/B)
+    const char* e = std::getenv("DPL_GEMM_SPLIT_TAIL");
+    return !(e && e[0] == '0');
+  }();
+  p.split_tail = 0;
+  if (split_tail && two_sm && bn == 256 && p.tma_epi && !p.conv_operand && p.k_splits == 1) {
+    const int pairs = grid_ / 2;
+    const int rem = p.num_tiles % pairs;
+    if (pairs * 2 >= num_sms() - 1 && p.num_tiles >= 2 * pairs && rem > 0 && 2 * rem <= pairs) p.split_tail = rem;
+  }
   if (two_sm) {
     smem_ = pair::kSmem;
     static std::once_flag once;

@@ -178,3 +178,55 @@ def test_gemm_split_k_bf16(cuda, M, N, Kd, epi):
     _close(C2, ref, 2e-2)
     _close(C2, C1.float(), 2e-2)
     assert int((ws != 0).sum()) == 0
+
+
+@pytest.mark.parametrize("M,N,Kd,epi,mn", [
+    (4096, 4096, 1024, "bias+gelu+aux", False),  # BERT ffn1: 256 pair tiles = 3 waves + 34 -> 68 halves
+    (4096, 4096, 1024, "dgelu", False),          # BERT ffn2 dgrad
+    (4096, 4096, 1024, "resid", False),
+    (2048, 6400, 1600, "bias+gelu+aux", False),  # 200 tiles -> 2 waves + 52 -> 104 halves (no split: > 74)
+    (3072, 4096, 1600, "bias", False),           # 192 tiles -> 148 whole + 44 -> 88 halves (no split)
+    (4096, 4608, 520, "bias+gelu+aux", False),   # 288 tiles -> 3 waves + 66 (no split: 132 > 74)
+    (4096, 4352, 520, "resid", False),           # 272 tiles -> 3 waves + 50 (no split) ; sanity of the rule
+    (6144, 4096, 1024, "bias+gelu+aux", False),  # 384 tiles -> 5 waves + 14 -> 28 halves
+    (4096, 4096, 1024, "f32acc", True),          # weight-gradient form: MN-major operands, fp32 reduce-add
+    (4000, 4000, 520, "bias", False),            # ragged edges in the split tail
+])
+def test_gemm_split_tail_halves(cuda, M, N, Kd, epi, mn):
+    """Pair-kernel GEMMs whose last wave fills at most half the CTA pairs run
+    that wave's tiles as two 256 x 128 halves each (GemmParams.split_tail);
+    every output element, bias / activation / aux / residual / fp32
+    accumulation included, matches torch fp32."""
+    A = _rand(M, Kd, dev=cuda, seed=31)
+    B = _rand(N, Kd, dev=cuda, seed=32, scale=0.2)
+    bias = _rand(N, dev=cuda, seed=33, dtype=torch.float32)
+    z = _rand(M, N, dev=cuda, seed=34, scale=2.0)
+    res = _rand(M, N, dev=cuda, seed=35)
+    ref = A.float() @ B.float().T
+    if epi == "f32acc":
+        At, Bt = A.T.contiguous(), B.T.contiguous()
+        C = torch.full((M, N), 0.5, dtype=torch.float32, device=cuda)
+        K.gemm(At, Bt, C, M, N, Kd, lda=M, ldb=N, ldc=N, a_mn_major=True, b_mn_major=True, epi=K.EPI_OUT_F32_ACC)
+        torch.cuda.synchronize()
+        _close(C, ref + 0.5, 1e-3)
+        return
+    flags = {"bias": K.EPI_BIAS, "bias+gelu+aux": K.EPI_BIAS | K.EPI_GELU | K.EPI_AUX_OUT, "dgelu": K.EPI_DGELU,
+             "resid": K.EPI_RESID}[epi]
+    C = torch.zeros(M, N, dtype=torch.bfloat16, device=cuda)
+    Z = torch.zeros(M, N, dtype=torch.bfloat16, device=cuda)
+    K.gemm(A, B, C, M, N, Kd, lda=Kd, ldb=Kd, ldc=N, epi=flags, bias=bias if flags & K.EPI_BIAS else None,
+           aux_in=z if flags & K.EPI_DGELU else None, resid=res if flags & K.EPI_RESID else None,
+           aux_out=Z if flags & K.EPI_AUX_OUT else None)
+    torch.cuda.synchronize()
+    if flags & K.EPI_BIAS:
+        ref = ref + bias
+    if flags & K.EPI_AUX_OUT:
+        _close(Z, ref, 2e-2)
+    if flags & K.EPI_GELU:
+        ref = torch.nn.functional.gelu(ref, approximate="tanh")
+    if flags & K.EPI_RESID:
+        ref = ref + res.float()
+    if flags & K.EPI_DGELU:
+        zf = z.float().requires_grad_(True)
+        ref = ref * torch.autograd.grad(torch.nn.functional.gelu(zf, approximate="tanh").sum(), zf)[0]
+    _close(C, ref, 2e-2)
