@@ -1304,6 +1304,22 @@ void GemmOp::prepare(const GemmDesc& d) {
     const int tiles = p.num_m_blocks * p.num_n_blocks * d.batch;
     int splits = 1;
     while (tiles * splits * 2 <= sms && p.num_k_blocks / (splits * 2) >= 8) splits *= 2;
+    // a non-power-of-two split when it fills the waves much better: e.g. the
+    // 3072 x 1024 QKV weight gradient (48 pair tiles, K = 4096) at 3 splits
+    // runs 144 units in 2 waves = 2/3 of the unsplit mainloop per pair
+    static const bool any_split = [] {  // DPL_GEMM_SPLIT_ANY=0: powers of two only (A/B)
+      const char* e = std::getenv("DPL_GEMM_SPLIT_ANY");
+      return !(e && e[0] == '0');
+    }();
+    if (any_split) {
+      auto cost = [&](int sp) {  // mainloop waves per K, plus ~8% per extra fp32 reduce-add pass
+        return static_cast<double>(ceil_div(tiles * sp, sms)) / sp * (1.0 + 0.08 * (sp - 1));
+      };
+      int best = splits;
+      for (int sp = 2; sp <= 8; ++sp)
+        if (p.num_k_blocks / sp >= 8 && cost(sp) < 0.8 * cost(best)) best = sp;
+      splits = best;
+    }
     p.kb_per_split = ceil_div(p.num_k_blocks, splits);
     p.k_splits = ceil_div(p.num_k_blocks, p.kb_per_split);
   }

@@ -46,7 +46,8 @@ def test_gemm_mn_major(cuda, a_mn, b_mn, M, N, Kd, bn):
     _close(C, A.float() @ B.float().T, 1e-3)
 
 
-@pytest.mark.parametrize("T,n_out,k_in", [(1024, 768, 512), (4096, 1024, 1024), (4096, 1000, 520)])
+@pytest.mark.parametrize("T,n_out,k_in", [(1024, 768, 512), (4096, 1024, 1024), (4096, 1000, 520), (4096, 3072, 1024),
+                                          (4096, 2816, 1024)])
 def test_gemm_wgrad_accumulates(cuda, T, n_out, k_in):
     # dW[N_out, K_in] += dY^T X over two micro-batches (both operands MN-major;
     # few output tiles -> split-K with atomic fp32 accumulation)
