@@ -782,7 +782,7 @@ struct PairCfg {
   static constexpr int kABytes = kBM * kBK * 2;        // 16 KB: this CTA's 128 rows of A
   static constexpr int kBBytes = (kBN / 2) * kBK * 2;  // this CTA's half of B
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kTmemCols = 2 * kBN;            // double-buffered accumulator
+  static constexpr int kTmemCols = kBN == 192 ? 512 : 2 * kBN;  // double-buffered accumulator (power of two)
 };
 namespace pair {
 constexpr int kSmem = kSmemBudget;
@@ -1238,10 +1238,21 @@ void GemmOp::prepare(const GemmDesc& d) {
         const char* e = std::getenv("DPL_GEMM_BN128_COST");
         return e ? std::atof(e) : 1.4;
       }();
+      // 256 x 192 pair tiles (K-major B only: an MN-major B tile is loaded in
+      // 64-column boxes) for shapes whose 256-wide last wave is ragged, e.g.
+      // GPT-2's 1024 x 1600 / 1024 x 4800 / 1024 x 6400 or BERT's 2048-row
+      // replica slices (DPL_GEMM_BN192_COST: A/B knob, 0 disables)
+      static const double mid_cost = [] {
+        const char* e = std::getenv("DPL_GEMM_BN192_COST");
+        return e ? std::atof(e) : 1.1;
+      }();
+      const bool allow192 = mid_cost > 0 && !d.b_mn_major && !d.conv_operand && d.M >= 256 && !d.force_1sm;
       double best = -1;
-      for (int cand : {256, 128}) {
+      for (int cand : {256, 192, 128}) {
+        if (cand == 192 && !allow192) continue;
         const long long tiles = static_cast<long long>(ceil_div(d.M, kBM)) * ceil_div(d.N, cand) * d.batch;
-        const double cost = static_cast<double>((tiles + sms - 1) / sms) * cand * (cand == 128 ? narrow_cost : 1.0);
+        const double cost = static_cast<double>((tiles + sms - 1) / sms) * cand *
+                            (cand == 128 ? narrow_cost : cand == 192 ? mid_cost : 1.0);
         if (best < 0 || cost < best) {
           best = cost;
           bn = cand;
@@ -1260,8 +1271,10 @@ void GemmOp::prepare(const GemmDesc& d) {
   // 256x128 pairs help the 1024-row transformer GEMMs but not the implicit
   // convolutions (VGG-19 N=1: 3719 vs 3889 samples/s with them), which keep
   // the 1-SM 128x128 tile
+  if (bn == 192 && (d.b_mn_major || d.conv_operand || d.M < 256 || d.force_1sm || !pair_enabled))
+    throw std::invalid_argument("dpl gemm: BN 192 needs the pair kernel with a K-major B");
   const bool two_sm = pair_enabled && !d.force_1sm && d.M >= 256 &&
-                      (bn == 256 || (bn == 128 && pair128 && !d.conv_operand));
+                      (bn == 256 || bn == 192 || (bn == 128 && pair128 && !d.conv_operand));
   const int bm = two_sm ? 256 : kBM;
   GemmParams& p = params_;
   p = GemmParams{};
@@ -1446,6 +1459,7 @@ void GemmOp::prepare(const GemmDesc& d) {
     std::call_once(once, [] {
       cudaFuncSetAttribute(gemm_bf16_tcgen05_2sm<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, pair::kSmem);
       cudaFuncSetAttribute(gemm_bf16_tcgen05_2sm<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, pair::kSmem);
+      cudaFuncSetAttribute(gemm_bf16_tcgen05_2sm<192>, cudaFuncAttributeMaxDynamicSharedMemorySize, pair::kSmem);
     });
     return;
   }
@@ -1561,8 +1575,9 @@ void GemmOp::launch_kernel(cudaStream_t stream) const {
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    const cudaError_t e = bn_ == 256 ? cudaLaunchKernelEx(&cfg, gemm_bf16_tcgen05_2sm<256>, params_)
-                                     : cudaLaunchKernelEx(&cfg, gemm_bf16_tcgen05_2sm<128>, params_);
+    const cudaError_t e = bn_ == 256   ? cudaLaunchKernelEx(&cfg, gemm_bf16_tcgen05_2sm<256>, params_)
+                          : bn_ == 192 ? cudaLaunchKernelEx(&cfg, gemm_bf16_tcgen05_2sm<192>, params_)
+                                       : cudaLaunchKernelEx(&cfg, gemm_bf16_tcgen05_2sm<128>, params_);
     if (e != cudaSuccess) throw std::runtime_error(std::string("dpl gemm: pair launch failed: ") + cudaGetErrorString(e));
     return;
   }

@@ -231,3 +231,38 @@ def test_gemm_split_tail_halves(cuda, M, N, Kd, epi, mn):
         zf = z.float().requires_grad_(True)
         ref = ref * torch.autograd.grad(torch.nn.functional.gelu(zf, approximate="tanh").sum(), zf)[0]
     _close(C, ref, 2e-2)
+
+
+@pytest.mark.parametrize("M,N,Kd,epi", [
+    (1024, 4800, 1600, "bias"),            # GPT-2 qkv (default choice: 256 x 192 pairs)
+    (1024, 6400, 1600, "bias+gelu+aux"),   # GPT-2 ffn1: ragged last n-block (6400 = 33 x 192 + 64)
+    (2048, 3072, 1024, "bias"),            # BERT qkv at a 4-sample replica slice
+    (300, 1000, 520, "resid"),             # ragged M and N
+    (512, 192, 64, "plain"),               # one n-block
+])
+@pytest.mark.parametrize("forced", [True, False])
+def test_gemm_pair_bn192(cuda, M, N, Kd, epi, forced):
+    """256 x 192 CTA-pair tiles (K-major B): every epilogue against torch fp32,
+    forced and as the default tile choice."""
+    A = _rand(M, Kd, dev=cuda, seed=41)
+    B = _rand(N, Kd, dev=cuda, seed=42, scale=0.2)
+    bias = _rand(N, dev=cuda, seed=43, dtype=torch.float32)
+    res = _rand(M, N, dev=cuda, seed=44)
+    flags = {"plain": 0, "bias": K.EPI_BIAS, "bias+gelu+aux": K.EPI_BIAS | K.EPI_GELU | K.EPI_AUX_OUT,
+             "resid": K.EPI_RESID}[epi]
+    C = torch.zeros(M, N, dtype=torch.bfloat16, device=cuda)
+    Z = torch.zeros(M, N, dtype=torch.bfloat16, device=cuda)
+    K.gemm(A, B, C, M, N, Kd, lda=Kd, ldb=Kd, ldc=N, epi=flags, bias=bias if flags & K.EPI_BIAS else None,
+           resid=res if flags & K.EPI_RESID else None, aux_out=Z if flags & K.EPI_AUX_OUT else None,
+           force_bn=192 if forced else 0)
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float().T
+    if flags & K.EPI_BIAS:
+        ref = ref + bias
+    if flags & K.EPI_AUX_OUT:
+        _close(Z, ref, 2e-2)
+    if flags & K.EPI_GELU:
+        ref = torch.nn.functional.gelu(ref, approximate="tanh")
+    if flags & K.EPI_RESID:
+        ref = ref + res.float()
+    _close(C, ref, 2e-2)
