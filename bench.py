@@ -132,20 +132,31 @@ def plan_fixed_point(model: dict, profiles: dict, mb: int, cluster: dict, m: int
             profiles[start] = profile_model(model, start)
         prof = profiles[start]
         chain = []
-        for _ in range(max_iter):
-            res = pipeplan.plan(prof, cluster, m)["plan"]
-            k = key(res)
-            seen = k in cands
-            if not seen:
-                for st in res["stages"]:
+        def evaluate(pl):
+            k = key(pl)
+            if k not in cands:
+                for st in pl["stages"]:
                     size = -(-mb // len(st["gpus"]))
                     if size not in profiles:
                         profiles[size] = profile_model(model, size)
-                own = slice_profile(profiles, res, mb)
-                seq = pipeplan.build_stage_sequence(res, own, cluster)
+                own = slice_profile(profiles, pl, mb)
+                seq = pipeplan.build_stage_sequence(pl, own, cluster)
                 est = pipeplan.estimate_latency(seq, m)["total"]
-                sim = pipeplan.simulate_plan(res, own, cluster, m)["latency"]
-                cands[k] = (res, own, est, sim)
+                sim = pipeplan.simulate_plan(pl, own, cluster, m)["latency"]
+                cands[k] = (pl, own, est, sim)
+            return k
+
+        for _ in range(max_iter):
+            rep = pipeplan.plan(prof, cluster, m, report=True)
+            res = rep["plan"]
+            k = key(res)
+            seen = k in cands
+            evaluate(res)
+            # the planner's runners-up (its top-k) are priced on their own
+            # slice profiles too: which plan wins on the self-consistent
+            # profile should not hinge on profile noise steering the chain
+            for alt in (rep.get("report") or {}).get("top", []):
+                evaluate(alt["plan"])
             chain.append({"start_slice": start, "stages": json.loads(k), "phi": res.get("phi"),
                           "planner_est_ms": res.get("est_latency_us", 0) / 1e3,
                           "planner_sim_ms": res.get("sim_latency_us", 0) / 1e3,
@@ -158,7 +169,11 @@ def plan_fixed_point(model: dict, profiles: dict, mb: int, cluster: dict, m: int
         history += chain
     best = min(cands.values(), key=lambda c: c[3])
     plan, own, est, sim = best
-    return plan, {"iterations": history, "fixed_point": fixed, "candidates": len(cands),
+    visited = {json.dumps(it["stages"]) for it in history}
+    alternatives = [{"stages": json.loads(k), "own_profile_est_ms": c[2] * 1e3, "own_profile_sim_ms": c[3] * 1e3}
+                    for k, c in cands.items() if k not in visited]
+    return plan, {"iterations": history, "alternatives": alternatives, "fixed_point": fixed,
+                  "candidates": len(cands),
                   "per_gpu_memory_gb": cluster["per_gpu_memory_gb"],
                   "est_latency_ms": est * 1e3, "sim_latency_ms": sim * 1e3,
                   "profile": "B200 layer profiles at the plan's own replica slice sizes"}
