@@ -726,6 +726,7 @@ __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ dout, con
                                      long long ldo, float* __restrict__ dsum, float* __restrict__ dq_acc, int S, int B,
                                      int rows) {
   ptx::pdl_wait();
+  ptx::pdl_trigger();
   const int lane = threadIdx.x & 31, sub = lane >> 3, l8 = lane & 7;
   const int groups = (blockDim.x >> 5) * 4;
   for (int row = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 4 + sub; row < rows;
@@ -755,6 +756,7 @@ __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ dout, con
 __global__ void attn_bwd_dq_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv, long long ld,
                                    float scale, int S, int B, int rows) {
   ptx::pdl_wait();
+  ptx::pdl_trigger();
   const int lane = threadIdx.x & 31, sub = lane >> 4, l16 = lane & 15;
   const int groups = (blockDim.x >> 5) * 2;
   for (int row = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 2 + sub; row < rows;

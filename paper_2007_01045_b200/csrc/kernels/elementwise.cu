@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(256, 4)
   }
   __syncthreads();
   ptx::pdl_wait();
+  ptx::pdl_trigger();  // dependents (GEMMs) may start their prologue; they wait for our completion
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nvec = h / 8;
@@ -309,6 +310,7 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads)
     reinterpret_cast<float4*>(sg)[i] = __ldg(reinterpret_cast<const float4*>(gamma) + i);
   __syncthreads();
   ptx::pdl_wait();
+  ptx::pdl_trigger();  // dependents (GEMMs) may start their prologue; they wait for our completion
   const int rg = threadIdx.x / kTPR;
   const int vi = threadIdx.x % kTPR;  // this thread's 8-column vector
   const int wr = vi >> 5, lane = threadIdx.x & 31;
@@ -452,6 +454,7 @@ __global__ void __launch_bounds__(256, 4)
                        const __nv_bfloat16* __restrict__ dresid, const __nv_bfloat16* __restrict__ dx,
                        float* __restrict__ ws, int rows, int h) {
   ptx::pdl_wait();
+  ptx::pdl_trigger();  // dependents (GEMMs) may start their prologue; they wait for our completion
   __shared__ float part[8][kRed][257];
   const int vx = threadIdx.x & 31, ry = threadIdx.x >> 5;
   const int vi = blockIdx.x * 32 + vx;
@@ -524,6 +527,7 @@ __global__ void __launch_bounds__(256, 4)
 __global__ void __launch_bounds__(512) ln_param_reduce_kernel(const float* __restrict__ ws, float* d0, float* d1,
                                                               float* d2, float* d3, int blocks, int nred, int h) {
   ptx::pdl_wait();
+  ptx::pdl_trigger();  // dependents (GEMMs) may start their prologue; they wait for our completion
   __shared__ float part[16][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int i = blockIdx.x * 32 + tx;  // (k, c) flattened
@@ -649,6 +653,7 @@ __global__ void softmax_bwd_kernel(const __nv_bfloat16* __restrict__ p, const fl
 __global__ void __launch_bounds__(256, 4) colsum_acc_kernel(const __nv_bfloat16* __restrict__ dy, float* __restrict__ db, int rows, int cols,
                                   int rows_per_block) {
   ptx::pdl_wait();
+  ptx::pdl_trigger();  // dependents (GEMMs) may start their prologue; they wait for our completion
   __shared__ float part[8][256 + 1];
   const int vx = threadIdx.x & 31, ry = threadIdx.x >> 5;
   const int vi = blockIdx.x * 32 + vx;
@@ -703,6 +708,7 @@ __global__ void __launch_bounds__(256) split_epilogue_kernel(float* __restrict__
                                                              const __nv_bfloat16* __restrict__ resid,
                                                              const __nv_bfloat16* __restrict__ aux_in) {
   ptx::pdl_wait();
+  ptx::pdl_trigger();  // dependents (GEMMs) may start their prologue; they wait for our completion
   const int nv = n / 8;
   const long long total = static_cast<long long>(m) * nv;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
