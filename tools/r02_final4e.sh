@@ -7,7 +7,7 @@ run() { # n tag args...
   local n=$1 tag=$2; shift 2
   timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29611 \
     bench.py --gpus $n --steps 5 --warmup 3 "$@" > $out/$tag.json 2> $out/$tag.err
-  echo "$tag rc=$? $(python -c "import json; d=json.load(open('$out/$tag.json')); print(round(d['value'],2), round(d['e2e']['value'],2), d['clocks']['sm_mhz'], round(d['roofline']['frac'],4), d.get('bubble'), ((d.get('latency') or {}).get('planner') or {}).get('measured_over_planner_sim'))" 2>&1 | tail -1)"
+  echo "$tag rc=$? $(python -c "import json; d=json.load(open('$out/$tag.json')); print(round(d['value'],2), round(d['e2e']['value'],2), d['clocks']['sm_mhz'], round(d['roofline']['frac'],4), d['config']['plan'], round(d.get('bubble') or 0,3), ((d.get('latency') or {}).get('planner') or {}).get('measured_over_planner_sim'))" 2>&1 | tail -1)"
 }
 run 2 bert_n2
 run 4 bert_n4
