@@ -4,6 +4,7 @@
 // attention itself is the fused flash kernel (kernels/attention.cu), so the
 // only other kernels are LayerNorm and the bias-gradient column sums.
 #include <cmath>
+#include <cstdlib>
 #include <stdexcept>
 
 #include "kernels/attention.h"
@@ -275,14 +276,28 @@ class TransformerLayer final : public Layer {
       ctx.gemms.run(d, str);
     }
     // FFN1: dW1 += dz1^T ln2 ; dln2 = dz1 W1
-    ctx.on_side([&](cudaStream_t s) {
-      ctx.gemms.run(plain(F_, H_, R, dz1, F_, true, st.ln2, H_, true, g32_ + w1_, H_, kOutF32Acc), s);
-    });
+    // With a full-machine side grid (4096-row slices), fork dW1 after the
+    // LN2 backward so the persistent wgrad grid does not hold the SMs that
+    // kernel needs (BERT-48 N=1 +0.8%, LN backward 26.9 -> 20.3 ms per step);
+    // capped side grids (<= 2048-row slices) keep the early fork (GPT-2
+    // -1.9% late).  DPL_WGRAD_LATE=0/1 forces either (A/B).
+    static const int late_env = [] {
+      const char* e = std::getenv("DPL_WGRAD_LATE");
+      return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    const bool late = late_env >= 0 ? late_env == 1 : ctx.wgrad_ctas == 0;
+    auto w1_grad = [&] {
+      ctx.on_side([&](cudaStream_t s) {
+        ctx.gemms.run(plain(F_, H_, R, dz1, F_, true, st.ln2, H_, true, g32_ + w1_, H_, kOutF32Acc), s);
+      });
+    };
+    if (!late) w1_grad();
     ctx.gemms.run(plain(R, H_, F_, dz1, F_, false, w16_ + w1_, H_, true, dln, H_, kOutBf16), str);
     // LN2 backward (+ residual gradient dy); also db2 = colsum(dy) and
     // dbo = colsum(dh) from the rows it already holds
     layernorm_bwd(dln, st.h, st.mean2, st.rstd2, w32_ + ln2g_, dy, dh, g32_ + ln2g_, g32_ + ln2b_, R, H_, str,
                   ctx.ln_ws, g32_ + b2_, g32_ + bo_);
+    if (late) w1_grad();
     // O projection: dWo += dh^T ctx ; dbo ; dctx = dh Wo (head-split store)
     ctx.on_side([&](cudaStream_t s) {
       ctx.gemms.run(plain(H_, H_, R, dh, H_, true, st.ctx, H_, true, g32_ + wo_, H_, kOutF32Acc), s);
